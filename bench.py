@@ -1,0 +1,523 @@
+#!/usr/bin/env python
+"""Headline benchmark: lambda(omega) gasket passes on B200 (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload write16|write16-i32|stencil17|stencil17-nsum4]
+                    [--no-sweep] [--no-e2e] [--no-cpu]
+
+Default workload (BASELINE configs[1]): the n = 2^16 write pass ("write a
+constant value on all the elements") on int8 cells, lambda
+map, tuned strategy.  One step = one launch over the whole gasket
+(3^16 = 43,046,721 cells).  Each timed step is bracketed by CUDA events on
+the launching stream, and the L2 is flushed (a 4x-L2 read) before every step,
+outside the events.  value = gasket cells/s over all ranks (every rank runs
+its own independent grid: weak scaling, no collective on the data path).
+
+Extras on the same JSON line: the rho sweep of lambda vs bounding box at the
+headline size (paper-literal SUBBOX/TABLE/UNROLL and tuned lambda, paper-
+literal and block-early-exit BB) with the best-vs-best speedup; `roofline`
+(sector-minimum bytes / event time vs the measured HBM peak); `cpu_baseline`
+(the C/OpenMP port of the reference numba kernels, all host threads, bounded
+sample); `e2e` (the reference-facing call with host numpy buffers); `clocks`
+(NVML sampled during the timed region); `gpu_launches`.
+
+`--impl reference` times the reference algorithm's CPU implementation (the
+oracle port of backends.py:143-222, the reference itself being pure
+Python/numba that does not travel to the GPU box) on the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    # name: (r, cell dtype name, kind, rho, description)
+    "write16": (16, "int8", 0, 32, "n=2^16 gasket write pass (const 1), int8 cells, lambda map"),
+    "write16-i32": (16, "int32", 0, 32, "n=2^16 gasket write pass (const 1), int32 cells, lambda map"),
+    "stencil17": (17, "int8", 2, 64, "n=2^17 8-neighbour CA step, int8 states, lambda map"),
+    "stencil17-nsum4": (17, "int8", 1, 64, "n=2^17 4-neighbour CA step, int8 states, lambda map"),
+}
+FALLBACK_HBM_GBS = 6650.0
+
+
+def _peaks() -> tuple[float, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (NVML in-process sampler)
+# ---------------------------------------------------------------------------
+
+_REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+            0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle", 0x2: "applications_clocks_setting"}
+
+
+class ClockSampler:
+    def __init__(self, index: int, period_s: float = 0.005) -> None:
+        self.index, self.period = index, period_s
+        self.samples: list[tuple[int, int]] = []
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._thr = None
+        self.error = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = int(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+
+            def loop():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append((int(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)),
+                                             int(get_reasons(h))))
+                    except Exception as e:  # pragma: no cover
+                        self.error = repr(e)
+                    time.sleep(self.period)
+
+            self._thr = threading.Thread(target=loop, daemon=True)
+            self._thr.start()
+        except Exception as e:  # pragma: no cover
+            self.error = repr(e)
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._thr is not None:
+            self._thr.join()
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0, "error": self.error}
+        mhz = [s[0] for s in self.samples]
+        bits = 0
+        for _, r in self.samples:
+            bits |= r
+        reasons = sorted(v for k, v in _REASONS.items() if bits & k and v != "gpu_idle")
+        return {"sm_mhz": statistics.median(mhz), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(mhz), "sm_mhz_min": min(mhz)}
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+# ---------------------------------------------------------------------------
+
+def _dist_init(ngpus: int):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        if torch.cuda.is_available():
+            torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def _barrier(world: int) -> None:
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def _max_over_ranks(v: float, world: int) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def _traffic_from_profiles(workload: str) -> float | None:
+    p = ROOT / "profiles" / "traffic.json"
+    try:
+        return float(json.loads(p.read_text())[workload]["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
+def _make_step(workload: str, grid, src, rho: int, flags: int):
+    from paper_1706_04552_b200 import backends
+    from paper_1706_04552_b200.geometry import IntraStrategy
+
+    r, _, kind, _, _ = WORKLOADS[workload]
+    r_b = r - (rho.bit_length() - 1)
+    bufs = [grid, src]
+    state = {"i": 0}
+
+    def step():
+        if kind == 0:
+            backends.run_block_space(grid, grid, rho, r_b, IntraStrategy.TUNED, kind=0, param=1)
+        else:
+            # CA ping-pong: read bufs[i], write bufs[1-i]; both agree off the gasket
+            i = state["i"]
+            backends.run_block_space(bufs[1 - i], bufs[i], rho, r_b, IntraStrategy.TUNED, kind=kind, param=1,
+                                     flags=flags)
+            state["i"] = 1 - i
+
+    return step
+
+
+def _time_steps(step, flusher, steps: int) -> list[float]:
+    import torch
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for a, b in ev:
+        flusher()
+        a.record()
+        step()
+        b.record()
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in ev]
+
+
+def _sweep(r: int, dtype, flusher, budget_s: float = 3.0) -> dict:
+    """rho sweep at the headline size: lambda (literal strategies + tuned) vs BB."""
+    import torch
+
+    from paper_1706_04552_b200 import backends
+    from paper_1706_04552_b200.geometry import IntraStrategy
+
+    n = 1 << r
+    cells = 3**r
+    grid = torch.zeros((n, n), dtype=dtype, device="cuda")
+    out: dict = {}
+
+    def timed(fn) -> float:
+        fn()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        fn()
+        torch.cuda.synchronize()
+        one = time.perf_counter() - t0
+        reps = int(max(2, min(20, budget_s / max(one, 1e-6))))
+        ts = _time_steps(fn, flusher, reps)
+        return statistics.fmean(ts)
+
+    for rho in (1, 2, 4, 8, 16, 32):
+        r_b = r - (rho.bit_length() - 1)
+        row = {}
+        row["bb"] = timed(lambda: backends.run_bounding_box(grid, grid, rho, 0, 1))
+        row["bb-exit"] = timed(lambda: backends.run_bounding_box(grid, grid, rho, 0, 1, early_exit=True))
+        for s in (IntraStrategy.SUBBOX, IntraStrategy.TABLE, IntraStrategy.UNROLL, IntraStrategy.TUNED):
+            row[s.value] = timed(lambda: backends.run_block_space(grid, grid, rho, r_b, s, kind=0, param=1))
+        out[str(rho)] = {k: {"ms": round(v, 5), "cells_per_s": cells / (v * 1e-3)} for k, v in row.items()}
+    del grid
+    torch.cuda.empty_cache()
+
+    def best(keys):
+        return min(((float(out[rho][k]["ms"]), rho, k) for rho in out for k in keys))
+
+    bb = best(["bb"])
+    bbx = best(["bb", "bb-exit"])
+    lit = best(["subbox", "table", "unroll"])
+    tun = best(["subbox", "table", "unroll", "tuned"])
+    summary = {
+        "best_bb_paper": {"rho": bb[1], "ms": bb[0]},
+        "best_bb_any": {"rho": bbx[1], "variant": bbx[2], "ms": bbx[0]},
+        "best_lambda_paper": {"rho": lit[1], "strategy": lit[2], "ms": lit[0]},
+        "best_lambda_any": {"rho": tun[1], "strategy": tun[2], "ms": tun[0]},
+        "speedup_paper_literal_best_vs_best": bb[0] / lit[0],
+        "speedup_best_lambda_vs_best_bb_paper": bb[0] / tun[0],
+        "speedup_best_lambda_vs_best_bb_any": bbx[0] / tun[0],
+        "speedup_rho32_subbox_vs_bb": float(out["32"]["bb"]["ms"]) / float(out["32"]["subbox"]["ms"]),
+        "speedup_rho1_subbox_vs_bb": float(out["1"]["bb"]["ms"]) / float(out["1"]["subbox"]["ms"]),
+    }
+    return {"per_rho_ms": {rho: {k: v["ms"] for k, v in row.items()} for rho, row in out.items()},
+            "summary": summary}
+
+
+def _e2e(workload: str, rho: int, steps: int) -> dict:
+    """The reference-facing call (backends.run_block_space on host numpy grids)."""
+    import numpy as np
+    import torch
+
+    from paper_1706_04552_b200 import backends, device
+    from paper_1706_04552_b200 import roofline as R
+    from paper_1706_04552_b200.geometry import IntraStrategy
+
+    r, dname, kind, _, _ = WORKLOADS[workload]
+    n = 1 << r
+    c = np.dtype(dname).itemsize
+    r_b = r - (rho.bit_length() - 1)
+    res = {}
+    # pinned host grid (the contract's "pinned host memory"); numpy view for the public API
+    host = torch.zeros((n, n), dtype=getattr(torch, dname), pin_memory=True)
+    g = host.numpy()
+    src = None
+    if kind != 0:
+        srct = torch.empty((n, n), dtype=getattr(torch, dname), pin_memory=True)
+        device.fill_hash(n, getattr(torch, dname), 1, 0, out=None)  # warm the module
+        srct.copy_(device.fill_hash(n, getattr(torch, dname), 1, 0).cpu())
+        src = srct.numpy()
+        g[...] = src
+    for transport in ("mapped", "copy"):
+        os.environ[device.HOST_TRANSPORT_ENV] = transport
+        call = (lambda: backends.run_block_space(g, g if src is None else src, rho, r_b, IntraStrategy.TUNED,
+                                                 kind=kind, param=1))
+        call()  # warm-up (page-locks and maps the buffer once for "mapped")
+        k = steps if transport == "mapped" else max(2, min(steps, 3))
+        t0 = time.perf_counter()
+        for _ in range(k):
+            call()
+        dt = (time.perf_counter() - t0) / k
+        if transport == "mapped":
+            seg_total = (16 // c) * 3 ** (r - (16 // c).bit_length() + 1) if kind == 0 else None
+            if kind == 0:
+                full = 3 ** (r - (16 // c).bit_length() + 1)
+                h2d = (seg_total - full) * 16  # partial segments are read for the blend
+                d2h = seg_total * 16
+            else:
+                h2d = R.stencil_read_bytes(r, c, kind == 2) + R.write_bytes(r, c)
+                d2h = R.write_bytes(r, c)
+        else:
+            h2d = n * n * c * (1 if kind == 0 else 2)
+            d2h = n * n * c
+        res[transport] = {"s_per_step": dt, "cells_per_s": 3**r / dt, "h2d_bytes_per_step": int(h2d),
+                          "d2h_bytes_per_step": int(d2h), "steps": k}
+        if transport == "mapped":
+            device.unmap_host(g)
+            if src is not None:
+                device.unmap_host(src)
+    os.environ.pop(device.HOST_TRANSPORT_ENV, None)
+    best = min(res.values(), key=lambda v: v["s_per_step"])
+    which = [k for k, v in res.items() if v is best][0]
+    return {"value": best["cells_per_s"], "unit": "cells/s", "h2d_bytes_per_step": best["h2d_bytes_per_step"],
+            "d2h_bytes_per_step": best["d2h_bytes_per_step"], "transport": which, "api": "backends.run_block_space(numpy)",
+            "timer": "host wall clock around the synchronous call", "variants": res}
+
+
+def _cpu_baseline(workload: str, budget_s: float = 12.0) -> dict:
+    """The reference algorithm on the host cores (oracle = C/OpenMP port of the numba kernels)."""
+    import numpy as np
+
+    import oracle
+
+    r, dname, kind, _, _ = WORKLOADS[workload]
+    if r >= 17:
+        r_s = 16  # bounded sample: one 2^16 tile-equivalent of the same pass
+    else:
+        r_s = r
+    n = 1 << r_s
+    rho = 16
+    g = np.zeros((n, n), dtype=np.dtype(dname))
+    src = oracle.fill_hash(n, np.dtype(dname), 1, 0) if kind else g
+    lx, ly = oracle.local_cells(oracle.STRAT_TABLE, rho)
+    oracle.run_block_space(g, src, rho, r_s - 4, oracle.STRAT_TABLE, lx, ly, kind, 1)  # warm
+    times = []
+    t_end = time.perf_counter() + budget_s
+    while time.perf_counter() < t_end or len(times) < 3:
+        t0 = time.perf_counter()
+        oracle.run_block_space(g, src, rho, r_s - 4, oracle.STRAT_TABLE, lx, ly, kind, 1)
+        times.append(time.perf_counter() - t0)
+    mean = statistics.fmean(times)
+    return {"value": 3**r_s / mean, "unit": "cells/s", "cores": oracle.max_threads(), "kind": "port",
+            "sample": f"{len(times)} x lambda TABLE rho=16 pass over n=2^{r_s} {dname} "
+                      f"({['write', 'nsum4', 'nsum8'][kind]}), oracle/gasket_oracle.c (OpenMP)",
+            "s_per_pass": mean}
+
+
+def run_ours(args) -> None:
+    import numpy as np
+    import torch
+
+    from paper_1706_04552_b200 import device, native
+    from paper_1706_04552_b200 import roofline as R
+
+    world, rank, local = _dist_init(args.gpus)
+    workload = args.workload
+    r, dname, kind, rho, desc = WORKLOADS[workload]
+    if args.rho:
+        rho = args.rho
+    n = 1 << r
+    c = np.dtype(dname).itemsize
+    tdt = getattr(torch, dname)
+    native.lib()
+    flusher = device.L2Flusher()
+
+    grid = torch.zeros((n, n), dtype=tdt, device="cuda")
+    src = None
+    flags = 0
+    if kind != 0:
+        src = device.fill_hash(n, tdt, 1 + rank, 0)
+        grid.copy_(src)
+        flags = native.FLAG_DST_FROM_SRC
+    step = _make_step(workload, grid, src, rho, flags)
+    for _ in range(args.warmup):
+        flusher()
+        step()
+    torch.cuda.synchronize()
+
+    _barrier(world)
+    torch.cuda.synchronize()
+    launches0 = native.launch_count()
+    with ClockSampler(local) as clk:
+        t_wall0 = time.perf_counter()
+        ms = _time_steps(step, flusher, args.steps)
+        t_wall = time.perf_counter() - t_wall0
+    torch.cuda.synchronize()
+    _barrier(world)
+    launches = native.launch_count() - launches0
+    total_ms = _max_over_ranks(sum(ms), world)
+    ms_per_step = total_ms / args.steps
+    cells = 3**r
+    value = world * cells / (ms_per_step * 1e-3)
+
+    peak, peak_src = _peaks()
+    alg_bytes = R.pass_bytes(r, c, kind)
+    achieved = alg_bytes / (statistics.fmean(ms) * 1e-3) / 1e9
+    traffic = _traffic_from_profiles(workload)
+    line = {
+        "metric": "gasket cells/s (lambda map), n=2^%d %s; lambda-vs-BB speedup and %% HBM roofline alongside" % (r, desc.split(',')[1].strip() if ',' in desc else ''),
+        "value": value,
+        "unit": "cells/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": {"int8": "i8", "int32": "i32"}[dname],
+        "data": "synthetic (zero grid, param=1)" if kind == 0 else "synthetic (splitmix64 hash states, all cells)",
+        "config": {"workload": workload, "description": desc, "n": n, "rho": rho, "mapping": "lambda",
+                   "strategy": "tuned", "kind": ["const", "nsum4", "nsum8"][kind], "cells_per_step": cells,
+                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "l2": "flushed before every timed step (4x L2 read, outside the events)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_source": peak_src, "algorithmic_bytes_per_launch": alg_bytes,
+                     "bytes_model": "exact 32-byte-sector minimum on the dense row-major grid (SURVEY §8d)",
+                     "element_bytes_frac": R.element_bytes(r, c, kind) / (statistics.fmean(ms) * 1e-3) / 1e9 / peak},
+        "clocks": clk.summary(),
+        "gpu_launches": int(launches),
+        "timed_region_wall_s": t_wall,
+    }
+    del grid, src
+    torch.cuda.empty_cache()
+    if rank == 0 and world == 1:
+        if not args.no_sweep and kind == 0:
+            line["sweep"] = _sweep(r, tdt, flusher)
+        if not args.no_e2e:
+            line["e2e"] = _e2e(workload, rho, steps=max(3, min(args.steps, 10)))
+        if not args.no_cpu:
+            line["cpu_baseline"] = _cpu_baseline(workload)
+    if rank == 0:
+        if "e2e" not in line:
+            line["e2e"] = None
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def run_reference(args) -> None:
+    """Reference arm: the reference algorithm's CPU path (C/OpenMP port of its
+    numba kernels, all host threads), rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    import numpy as np
+
+    import oracle
+
+    workload = args.workload
+    r, dname, kind, _, desc = WORKLOADS[workload]
+    # bounded sample: one pass at n=2^16 for 2^17 workloads (cells/s is size-independent here)
+    r_s = min(r, 16)
+    n = 1 << r_s
+    rho = 16  # the reference's best lambda configuration on CPU
+    g = np.zeros((n, n), dtype=np.dtype(dname))
+    src = oracle.fill_hash(n, np.dtype(dname), 1, 0) if kind else g
+    lx, ly = oracle.local_cells(oracle.STRAT_TABLE, rho)
+    for _ in range(max(1, args.warmup)):
+        oracle.run_block_space(g, src, rho, r_s - 4, oracle.STRAT_TABLE, lx, ly, kind, 1)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.run_block_space(g, src, rho, r_s - 4, oracle.STRAT_TABLE, lx, ly, kind, 1)
+        times.append(time.perf_counter() - t0)
+    sec = statistics.fmean(times)
+    value = 3**r_s / sec
+    line = {
+        "impl": "reference",
+        "metric": "gasket cells/s (lambda map)",
+        "value": value,
+        "unit": "cells/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": sec * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": {"int8": "i8", "int32": "i32"}[dname],
+        "data": "synthetic",
+        "config": {"workload": workload, "description": desc, "sample_n": n, "rho": rho, "strategy": "table"},
+        "cpu_baseline": {"value": value, "unit": "cells/s", "cores": oracle.max_threads(), "kind": "port",
+                         "sample": f"lambda TABLE rho=16 pass over n=2^{r_s} {dname} per step"},
+        "e2e": {"value": value, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--warmup", type=int, default=None)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", choices=tuple(WORKLOADS), default="write16")
+    ap.add_argument("--rho", type=int, default=None)
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        args.steps = args.steps or 10
+        args.warmup = args.warmup if args.warmup is not None else 3
+        run_reference(args)
+    else:
+        args.steps = args.steps or 500
+        args.warmup = max(3, args.warmup if args.warmup is not None else 10)
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,128 @@
+/*
+ * gasket_b200.h -- C ABI of libgasket_b200.so, the sm_100a implementation of
+ * the block-space map lambda(omega) and the embedded-gasket kernels it drives.
+ *
+ * Drop-in boundary.  Each entry point replaces one reference interface
+ * (paths relative to /root/reference/pkg/src/gasketmap/):
+ *
+ *   gm_run_bounding_box  <- backends.run_bounding_box   backends.py:225-231
+ *                           (numba kernel _bounding_box_nb, backends.py:143-156)
+ *   gm_run_block_space   <- backends.run_block_space    backends.py:234-272
+ *                           (numba kernel _block_space_nb, backends.py:158-222)
+ *   gm_map_blocks        <- blockmap.map_blocks_array   blockmap.py:91-108
+ *   gm_map_rectangle     <- the idx%W, idx//W call sites of map_blocks_array
+ *                           (blockmap.py:140-141, engine.py:233-235, backends.py:103-105)
+ *   gm_coverage          <- engine.verify_coverage      engine.py:214-258 (counting leg)
+ *   gm_coverage_blocks   <- engine.verify_coverage with a map_fn  engine.py:236-251
+ *   gm_bijection_check   <- blockmap.verify_bijection   blockmap.py:123-166
+ *
+ * Conventions (mirroring backends.py): grids are dense row-major n x n arrays
+ * of 1/2/4/8-byte integer cells; `grid` is mutated in place and only gasket
+ * cells are written; `src` is the read-only pre-launch snapshot and may alias
+ * `grid` only for GM_KIND_CONST.  Pointers are device pointers or mapped
+ * pinned-host pointers (cudaHostRegisterMapped / cudaHostAlloc(Mapped)).
+ * Every launch is asynchronous on `stream` (a cudaStream_t, NULL = legacy
+ * default stream).  Results: 0 on success, otherwise a GM_E* code, with a
+ * message in gm_last_error() (thread-local).  No entry point falls back to
+ * the CPU.
+ */
+#ifndef GASKET_B200_H
+#define GASKET_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* backends.py:30-34 integer tags, extended. */
+#define GM_KIND_CONST 0   /* KERNEL_CONST */
+#define GM_KIND_NSUM4 1   /* KERNEL_NEIGHBOR_SUM (4-neighbour) */
+#define GM_KIND_NSUM8 2   /* 8-neighbour extension (no reference implementation) */
+#define GM_KIND_COUNT 3   /* coverage audit: atomic per-cell uint32 counters */
+
+#define GM_STRAT_UNROLL 0 /* STRAT_UNROLL */
+#define GM_STRAT_TABLE 1  /* STRAT_TABLE */
+#define GM_STRAT_SUBBOX 2 /* STRAT_SUBBOX */
+#define GM_STRAT_TUNED 3  /* B200 row-segment kernel (same index set) */
+
+#define GM_MAP_BB 0       /* engine.Mapping.BOUNDING_BOX (paper-literal) */
+#define GM_MAP_LAMBDA 1   /* engine.Mapping.BLOCK_SPACE */
+#define GM_MAP_BB_EXIT 2  /* bounding box with block-level early exit */
+
+#define GM_FLAG_OMEGA_ORDER 1  /* tuned: visit tiles in b = wy*W + wx order */
+#define GM_FLAG_DST_FROM_SRC 2 /* stencil: grid == copy of src off-gasket (engine.py:201) */
+
+#define GM_OK 0
+#define GM_EINVAL 1  /* bad shape / size / tag (the reference's ValueError) */
+#define GM_ECUDA 2   /* CUDA runtime error */
+#define GM_ENOMEM 3
+
+typedef struct gm_cfg {
+    int64_t n;          /* grid edge, power of two */
+    int32_t rho;        /* block edge, power of two, rho <= n */
+    int32_t mapping;    /* GM_MAP_* */
+    int32_t strategy;   /* GM_STRAT_* (ignored for bounding-box maps) */
+    int32_t kind;       /* GM_KIND_* */
+    int32_t cell_bytes; /* 1, 2, 4 or 8 */
+    int32_t param;      /* CellKernel.param (engine.py:35-41); int32 like np.int32(param) */
+    int32_t flags;      /* GM_FLAG_* */
+    int32_t reserved;
+} gm_cfg_t;
+
+/* backends.py:225-231.  grid/src: n*n cells. */
+int gm_run_bounding_box(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t rho,
+                        int32_t kind, int32_t param, int32_t early_exit, void* stream);
+
+/* backends.py:234-272.  tab_x/tab_y: device int32[ntab] local offsets (TABLE only;
+ * intra.build_lookup_table order), ignored by the other strategies. */
+int gm_run_block_space(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t rho,
+                       int32_t r_b, int32_t strategy, const int32_t* tab_x, const int32_t* tab_y,
+                       int32_t ntab, int32_t kind, int32_t param, int32_t flags, void* stream);
+
+/* Generic launch through a config struct (engine.LaunchPlan.run, engine.py:159-178). */
+int gm_launch(const gm_cfg_t* cfg, void* grid, const void* src, const int32_t* tab_x,
+              const int32_t* tab_y, int32_t ntab, void* stream);
+
+/* blockmap.py:91-108: (lx, ly) = lambda(wx, wy) element-wise, int64, floor semantics. */
+int gm_map_blocks(const int64_t* wx, const int64_t* wy, int64_t count, int32_t r_b, int64_t* lx,
+                  int64_t* ly, void* stream);
+
+/* lambda over the whole packed rectangle in b = wy*W + wx order (3^r_b entries). */
+int gm_map_rectangle(int32_t r_b, int64_t* lx, int64_t* ly, void* stream);
+
+/* engine.py:214-258 counting leg: counts (uint32, n*n, zeroed by the caller)
+ * += 1 per cell the launch shape of `cfg` writes, using the real kernels. */
+int gm_coverage(const gm_cfg_t* cfg, uint32_t* counts, const int32_t* tab_x, const int32_t* tab_y,
+                int32_t ntab, void* stream);
+
+/* engine.py:245-251 with explicit block coordinates (map_fn given): counts +=1 at
+ * (bx*rho+lx, by*rho+ly) for every block and local cell; off-grid writes dropped. */
+int gm_coverage_blocks(const int64_t* bx, const int64_t* by, int64_t nblocks, const int32_t* lx,
+                       const int32_t* ly, int32_t nlocal, int32_t rho, int64_t n, uint32_t* counts,
+                       void* stream);
+
+/* blockmap.py:123-166 on the device.  Maps coordinates (cx, cy) (e.g. from
+ * gm_map_rectangle, row-major omega order) of nblocks blocks onto the edge-n_b
+ * gasket; owner must be n_b*n_b int64 scratch.  Writes result[0] = first bad
+ * omega index (or -1), result[1] = number of distinct gasket cells hit. */
+int gm_bijection_check(const int64_t* cx, const int64_t* cy, int64_t nblocks, int64_t n_b,
+                       int64_t* owner, int64_t* result, void* stream);
+
+/* Synthetic inputs / checks shared with the CPU oracle (oracle/gasket_oracle.c). */
+int gm_fill_hash(void* buf, int64_t n, int32_t cell_bytes, uint64_t seed, int32_t mode, void* stream);
+int gm_checksum(const void* buf, int64_t count, int32_t cell_bytes, uint64_t* out_dev, void* stream);
+int gm_count_equal(const void* a, const void* b, int64_t count, int32_t cell_bytes,
+                   unsigned long long* out_dev, void* stream);
+/* Reads `bytes` of `buf` (bigger than L2) so the next kernel starts cold. */
+int gm_l2_flush(const void* buf, int64_t bytes, uint64_t* sink_dev, void* stream);
+
+/* Number of kernels this library has launched (all entry points). */
+uint64_t gm_launch_count(void);
+const char* gm_last_error(void);
+const char* gm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GASKET_B200_H */

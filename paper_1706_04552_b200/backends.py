@@ -1,0 +1,232 @@
+"""The drop-in boundary: ``run_bounding_box`` / ``run_block_space`` on the B200.
+
+Same call signatures, integer tags and conventions as the reference plugin
+point (``gasketmap/backends.py:225-272``; tags ``:30-34``; backend selection
+``:20, 39-59``), but every launch goes through the C ABI of
+``libgasket_b200.so`` (include/gasket_b200.h).  There is exactly one backend,
+the sm_100a library; asking for the reference's CPU backends raises instead of
+silently falling back.
+
+Grids may be
+  * CUDA tensors (int8/uint8/int16/uint16/int32/uint32/int64, n x n,
+    contiguous): launched asynchronously on the current torch stream, or
+  * numpy arrays: synchronous, like the reference (see device.py for the
+    "copy" and "mapped" host transports).
+``grid`` is mutated in place and only gasket cells are written; ``src`` is the
+pre-launch snapshot.  If a neighbour-sum launch passes ``src`` aliasing
+``grid`` (racy in the reference) it is snapshotted first, which is exactly the
+``engine.launch`` semantics (engine.py:201).
+"""
+
+from __future__ import annotations
+
+import os
+from typing import Any, Optional
+
+import numpy as np
+import torch
+
+from . import device, native
+from .geometry import IntraStrategy, local_cells, packing_dims, scale_level
+
+BACKEND_ENV = "GASKETMAP_BACKEND"
+BACKEND = "cuda"
+HAVE_NUMBA = False  # kept for import compatibility: no CPU kernels exist here
+
+KERNEL_CONST = native.KIND_CONST
+KERNEL_NEIGHBOR_SUM = native.KIND_NSUM4
+KERNEL_NEIGHBOR_SUM8 = native.KIND_NSUM8
+STRAT_UNROLL = native.STRAT_UNROLL
+STRAT_TABLE = native.STRAT_TABLE
+STRAT_SUBBOX = native.STRAT_SUBBOX
+STRAT_TUNED = native.STRAT_TUNED
+
+_STRAT_TAG = {
+    IntraStrategy.UNROLL: STRAT_UNROLL,
+    IntraStrategy.TABLE: STRAT_TABLE,
+    IntraStrategy.SUBBOX: STRAT_SUBBOX,
+    IntraStrategy.TUNED: STRAT_TUNED,
+}
+
+_EMPTY = np.empty(0, dtype=np.int64)
+
+
+def resolve_backend(name: str | None = None) -> str:
+    """'auto' / 'cuda' (or the env flag) -> 'cuda'.  The CPU backends do not exist here."""
+    choice = (name or os.environ.get(BACKEND_ENV, "") or "auto").strip().lower()
+    if choice in ("auto", "cuda", "b200", "sm_100a"):
+        return BACKEND
+    if choice in ("numba", "numpy"):
+        raise RuntimeError(
+            f"{choice} backend requested, but this package runs the gasket kernels only on the "
+            "B200 (sm_100a); there is no CPU backend")
+    raise ValueError(f"unknown backend {choice!r} (expected cuda or auto)")
+
+
+def set_workers(workers: int | None) -> None:
+    """Accepted for API compatibility; device launches size themselves to the SMs."""
+    return None
+
+
+def local_cell_arrays(strategy: IntraStrategy, rho: int) -> tuple[np.ndarray, np.ndarray]:
+    cells = local_cells(strategy, rho)
+    lx = np.array([c.x for c in cells], dtype=np.int64)
+    ly = np.array([c.y for c in cells], dtype=np.int64)
+    return lx, ly
+
+
+# ---------------------------------------------------------------------------
+# argument plumbing
+# ---------------------------------------------------------------------------
+
+_table_cache: dict[tuple, tuple[torch.Tensor, torch.Tensor]] = {}
+
+
+def _device_table(local_x, local_y, rho: int) -> tuple[int, int, int]:
+    """Upload a TABLE lookup table once (cached by content); returns (px, py, count)."""
+    lx = np.ascontiguousarray(local_x, dtype=np.int64).reshape(-1)
+    ly = np.ascontiguousarray(local_y, dtype=np.int64).reshape(-1)
+    if lx.shape != ly.shape:
+        raise ValueError("local_x and local_y must have the same length")
+    if lx.size and (lx.min() < 0 or ly.min() < 0 or lx.max() >= rho or ly.max() >= rho):
+        raise ValueError(f"lookup table entries must lie inside the {rho}x{rho} tile")
+    key = (torch.cuda.current_device(), rho, lx.tobytes(), ly.tobytes())
+    hit = _table_cache.get(key)
+    if hit is None:
+        hit = (torch.from_numpy(lx.astype(np.int32)).cuda(), torch.from_numpy(ly.astype(np.int32)).cuda())
+        if len(_table_cache) > 64:
+            _table_cache.clear()
+        _table_cache[key] = hit
+    return int(hit[0].data_ptr()), int(hit[1].data_ptr()), int(lx.size)
+
+
+def _param32(param) -> int:
+    return int(np.int32(param))  # OverflowError for out-of-range, like np.int32(param) at backends.py:229
+
+
+def _strategy_tag(strategy) -> int:
+    if isinstance(strategy, IntraStrategy):
+        return _STRAT_TAG[strategy]
+    tag = int(strategy)
+    if tag not in (STRAT_UNROLL, STRAT_TABLE, STRAT_SUBBOX, STRAT_TUNED):
+        raise ValueError(f"unknown intra-block strategy {strategy!r}")
+    return tag
+
+
+def _shares_memory(a: Any, b: Any) -> bool:
+    if a is b:
+        return True
+    if isinstance(a, torch.Tensor) and isinstance(b, torch.Tensor):
+        return a.data_ptr() == b.data_ptr()
+    if isinstance(a, np.ndarray) and isinstance(b, np.ndarray):
+        return np.shares_memory(a, b)
+    return False
+
+
+def _run(grid: Any, src: Any, kind: int, launch, *, mapped_ok: bool) -> None:
+    """Route one launch: device tensors directly, numpy through a host transport.
+
+    ``launch(grid_ptr, src_ptr, n, cell_bytes, stream)`` issues the C-ABI call."""
+    device.require_cuda()
+    n = device.check_square(grid)
+    c = device.cell_bytes_of(grid)
+    reads_src = kind in (KERNEL_NEIGHBOR_SUM, KERNEL_NEIGHBOR_SUM8)
+    if src is None:
+        src = grid
+    if reads_src:
+        if tuple(src.shape) != tuple(grid.shape) or device.cell_bytes_of(src) != c:
+            raise ValueError("src must have the grid's shape and dtype")
+    stream = device.stream_handle()
+
+    if device.is_device(grid):
+        src_dev = src
+        if reads_src:
+            if not device.is_device(src):
+                src_dev = torch.from_numpy(np.ascontiguousarray(src)).to(grid.device, non_blocking=True)
+            elif _shares_memory(src, grid):
+                snap = device.scratch.get("snapshot", grid.numel(), grid.dtype, grid.device).view(n, n)
+                snap.copy_(grid)
+                src_dev = snap
+            else:
+                device.check_square(src, "src")
+        launch(device.data_ptr(grid), device.data_ptr(src_dev) if reads_src else 0, n, c, stream)
+        return
+
+    if not isinstance(grid, np.ndarray):
+        raise TypeError(f"grid must be a CUDA tensor or a numpy array, got {type(grid).__name__}")
+    if not grid.flags.writeable:
+        raise ValueError("grid is read-only")
+    mode = device.host_transport()
+    if mode == "mapped" and mapped_ok and not (reads_src and _shares_memory(src, grid)):
+        gptr = device.map_host(grid)
+        sptr = device.map_host(np.ascontiguousarray(src)) if reads_src else 0
+        launch(gptr, sptr, n, c, stream)
+        torch.cuda.current_stream().synchronize()
+        return
+
+    tdtype = device._torch_dtype(grid.dtype)
+    dev_grid = device.scratch.get("host_grid", n * n, tdtype).view(n, n)
+    host_grid = torch.from_numpy(grid)
+    dev_grid.copy_(host_grid, non_blocking=True)
+    src_ptr = 0
+    if reads_src:
+        dev_src = device.scratch.get("host_src", n * n, tdtype).view(n, n)
+        if _shares_memory(src, grid):
+            dev_src.copy_(dev_grid)
+        else:
+            dev_src.copy_(torch.from_numpy(np.ascontiguousarray(src)), non_blocking=True)
+        src_ptr = dev_src.data_ptr()
+    launch(dev_grid.data_ptr(), src_ptr, n, c, stream)
+    host_grid.copy_(dev_grid, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+
+
+# ---------------------------------------------------------------------------
+# the reference plugin API
+# ---------------------------------------------------------------------------
+
+def run_bounding_box(grid, src, rho: int, kind: int, param: int, backend: str = BACKEND, *,
+                     early_exit: bool = False) -> None:
+    """backends.py:225-231: identity map over n_b x n_b blocks of rho x rho threads,
+    each thread testing x & (n-1-y) (``early_exit``: whole tiles off the gasket exit first)."""
+    resolve_backend(backend)
+    p = _param32(param)
+    kind = int(kind)
+
+    def launch(gp, sp, n, c, stream):
+        native.call("gm_run_bounding_box", gp, sp, n, c, int(rho), kind, p, 1 if early_exit else 0, stream)
+
+    _run(grid, src, kind, launch, mapped_ok=False)
+
+
+def run_block_space(grid, src, rho: int, r_b: int, strategy, local_x: Optional[np.ndarray] = None,
+                    local_y: Optional[np.ndarray] = None, kind: int = KERNEL_CONST, param: int = 1,
+                    backend: str = BACKEND, *, flags: int = 0) -> None:
+    """backends.py:234-272: lambda over the packed rectangle of level r_b, then the
+    intra-block strategy.  ``local_x/local_y`` are the TABLE lookup table
+    (ignored by the other strategies, as in the numba leg)."""
+    resolve_backend(backend)
+    tag = _strategy_tag(strategy)
+    p = _param32(param)
+    kind = int(kind)
+    packing_dims(int(r_b))  # level range check
+    tx = ty = 0
+    ntab = 0
+    if tag == STRAT_TABLE:
+        if local_x is None or local_y is None:
+            local_x, local_y = local_cell_arrays(IntraStrategy.TABLE, int(rho))
+        device.require_cuda()
+        tx, ty, ntab = _device_table(local_x, local_y, int(rho))
+
+    def launch(gp, sp, n, c, stream):
+        native.call("gm_run_block_space", gp, sp, n, c, int(rho), int(r_b), tag, tx, ty, ntab, kind, p,
+                    int(flags), stream)
+
+    _run(grid, src, kind, launch, mapped_ok=(tag == STRAT_TUNED))
+
+
+__all__ = [
+    "BACKEND_ENV", "HAVE_NUMBA", "KERNEL_CONST", "KERNEL_NEIGHBOR_SUM", "KERNEL_NEIGHBOR_SUM8",
+    "STRAT_UNROLL", "STRAT_TABLE", "STRAT_SUBBOX", "STRAT_TUNED", "resolve_backend", "set_workers",
+    "local_cell_arrays", "run_bounding_box", "run_block_space", "scale_level",
+]

@@ -1,0 +1,233 @@
+// capi.cu -- extern "C" drop-in boundary (include/gasket_b200.h).
+//
+// Validation mirrors the reference's ValueError conditions (core.py:40-41,
+// 46-47, 121-124; engine.py:53-54, 198-199) so the Python layer can re-raise
+// them with the reference's messages; no entry point falls back to the CPU.
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/gasket_b200.h"
+#include "gasket.cuh"
+#include "launch.h"
+
+namespace gm {
+cudaError_t launch_map_blocks(const int64_t*, const int64_t*, int64_t, int, int64_t*, int64_t*, cudaStream_t);
+cudaError_t launch_map_rectangle(int, int64_t*, int64_t*, cudaStream_t);
+cudaError_t launch_bijection(const int64_t*, const int64_t*, int64_t, int64_t, int64_t*, int64_t*, cudaStream_t);
+cudaError_t launch_coverage_blocks(const int64_t*, const int64_t*, int64_t, const int32_t*, const int32_t*, int, int,
+                                   int64_t, uint32_t*, cudaStream_t);
+cudaError_t launch_fill_hash(void*, int64_t, int, uint64_t, int, cudaStream_t);
+cudaError_t launch_checksum(const void*, int64_t, int, uint64_t*, cudaStream_t);
+cudaError_t launch_count_equal(const void*, const void*, int64_t, unsigned long long*, cudaStream_t);
+cudaError_t launch_l2_flush(const void*, int64_t, uint64_t*, cudaStream_t);
+
+static std::atomic<uint64_t> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace gm
+
+namespace {
+thread_local std::string t_err;
+
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    t_err = buf;
+    return code;
+}
+
+int cuda_rc(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return GM_OK;
+    return fail(GM_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+bool pow2(int64_t v) { return v >= 1 && (v & (v - 1)) == 0; }
+int log2i(int64_t v) {
+    int r = 0;
+    while ((int64_t(1) << r) < v) ++r;
+    return r;
+}
+
+int check_common(int64_t n, int32_t cell_bytes, int32_t rho, int32_t kind) {
+    if (!pow2(n)) return fail(GM_EINVAL, "edge length must be a power of two >= 1, got %lld", (long long)n);
+    if (log2i(n) > 40) return fail(GM_EINVAL, "scale level must be in [0, 40], got %d", log2i(n));
+    if (rho < 1 || (rho & (rho - 1))) return fail(GM_EINVAL, "block edge must be a power of two >= 1, got %d", rho);
+    if (rho > n) return fail(GM_EINVAL, "block edge %d exceeds grid edge %lld", rho, (long long)n);
+    if (cell_bytes != 1 && cell_bytes != 2 && cell_bytes != 4 && cell_bytes != 8)
+        return fail(GM_EINVAL, "cell width must be 1, 2, 4 or 8 bytes, got %d", cell_bytes);
+    if (kind < GM_KIND_CONST || kind > GM_KIND_COUNT) return fail(GM_EINVAL, "unknown kernel kind %d", kind);
+    return GM_OK;
+}
+
+int run(const gm::LaunchArgs& a) {
+    cudaError_t e;
+    if (a.mapping == GM_MAP_LAMBDA && a.strategy == GM_STRAT_TUNED)
+        e = gm::launch_tuned(a);
+    else
+        e = gm::launch_literal(a);
+    return cuda_rc(e, "kernel launch");
+}
+
+gm::LaunchArgs make_args(const gm_cfg_t* c, void* grid, const void* src, const int32_t* tx, const int32_t* ty,
+                         int32_t ntab, void* stream) {
+    gm::LaunchArgs a{};
+    a.grid = grid;
+    a.src = src;
+    a.n = c->n;
+    a.rho = c->rho;
+    a.r_b = log2i(c->n / c->rho);
+    a.width = 1;
+    a.height = 1;
+    for (int i = 0; i < a.r_b / 2; ++i) a.width *= 3;
+    for (int i = 0; i < (a.r_b + 1) / 2; ++i) a.height *= 3;
+    a.mapping = c->mapping;
+    a.strategy = c->strategy;
+    a.kind = c->kind;
+    a.cell_bytes = c->cell_bytes;
+    a.param = (uint64_t)(int64_t)c->param;
+    a.tab_x = tx;
+    a.tab_y = ty;
+    a.ntab = ntab;
+    a.flags = c->flags;
+    a.stream = reinterpret_cast<cudaStream_t>(stream);
+    return a;
+}
+
+int launch_cfg(const gm_cfg_t* c, void* grid, const void* src, const int32_t* tx, const int32_t* ty, int32_t ntab,
+               void* stream) {
+    if (!c) return fail(GM_EINVAL, "null config");
+    if (int rc = check_common(c->n, c->cell_bytes, c->rho, c->kind)) return rc;
+    if (!grid) return fail(GM_EINVAL, "null grid");
+    if (c->kind != GM_KIND_CONST && c->kind != GM_KIND_COUNT) {
+        if (!src) return fail(GM_EINVAL, "neighbour kernels need a src snapshot");
+        if (src == grid)
+            return fail(GM_EINVAL, "neighbour kernels read the pre-launch snapshot: src must not alias grid");
+    }
+    if (c->mapping != GM_MAP_BB && c->mapping != GM_MAP_LAMBDA && c->mapping != GM_MAP_BB_EXIT)
+        return fail(GM_EINVAL, "unknown mapping %d", c->mapping);
+    const int r_b = log2i(c->n / c->rho);
+    if (c->mapping == GM_MAP_LAMBDA) {
+        if (c->strategy < GM_STRAT_UNROLL || c->strategy > GM_STRAT_TUNED)
+            return fail(GM_EINVAL, "block-space launches need an intra-block strategy (got %d)", c->strategy);
+        if (r_b > 20) return fail(GM_EINVAL, "block-space level r_b=%d exceeds the device limit 20", r_b);
+        if (c->strategy == GM_STRAT_TABLE && ntab > 0 && (!tx || !ty))
+            return fail(GM_EINVAL, "TABLE strategy needs the lookup table");
+    } else {
+        if (log2i(c->n) > 31) return fail(GM_EINVAL, "bounding-box grid edge 2^%d exceeds the device limit", log2i(c->n));
+    }
+    return run(make_args(c, grid, src, tx, ty, ntab, stream));
+}
+
+}  // namespace
+
+extern "C" {
+
+int gm_launch(const gm_cfg_t* cfg, void* grid, const void* src, const int32_t* tab_x, const int32_t* tab_y,
+              int32_t ntab, void* stream) {
+    return launch_cfg(cfg, grid, src, tab_x, tab_y, ntab, stream);
+}
+
+int gm_run_bounding_box(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t rho, int32_t kind,
+                        int32_t param, int32_t early_exit, void* stream) {
+    gm_cfg_t c{};
+    c.n = n;
+    c.rho = rho;
+    c.mapping = early_exit ? GM_MAP_BB_EXIT : GM_MAP_BB;
+    c.strategy = GM_STRAT_SUBBOX;
+    c.kind = kind;
+    c.cell_bytes = cell_bytes;
+    c.param = param;
+    return launch_cfg(&c, grid, src, nullptr, nullptr, 0, stream);
+}
+
+int gm_run_block_space(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t rho, int32_t r_b,
+                       int32_t strategy, const int32_t* tab_x, const int32_t* tab_y, int32_t ntab, int32_t kind,
+                       int32_t param, int32_t flags, void* stream) {
+    if (pow2(n) && pow2(rho) && rho <= n && log2i(n / rho) != r_b)
+        return fail(GM_EINVAL, "r_b=%d does not match n=%lld, rho=%d", r_b, (long long)n, rho);
+    gm_cfg_t c{};
+    c.n = n;
+    c.rho = rho;
+    c.mapping = GM_MAP_LAMBDA;
+    c.strategy = strategy;
+    c.kind = kind;
+    c.cell_bytes = cell_bytes;
+    c.param = param;
+    c.flags = flags;
+    return launch_cfg(&c, grid, src, tab_x, tab_y, ntab, stream);
+}
+
+int gm_map_blocks(const int64_t* wx, const int64_t* wy, int64_t count, int32_t r_b, int64_t* lx, int64_t* ly,
+                  void* stream) {
+    if (count < 0) return fail(GM_EINVAL, "negative count");
+    if (r_b < 0 || r_b > 62) return fail(GM_EINVAL, "scale level r_b must be in [0, 62], got %d", r_b);
+    if (count && (!wx || !wy || !lx || !ly)) return fail(GM_EINVAL, "null array");
+    return cuda_rc(gm::launch_map_blocks(wx, wy, count, r_b, lx, ly, reinterpret_cast<cudaStream_t>(stream)),
+                   "map_blocks");
+}
+
+int gm_map_rectangle(int32_t r_b, int64_t* lx, int64_t* ly, void* stream) {
+    if (r_b < 0 || r_b > 40) return fail(GM_EINVAL, "scale level must be in [0, 40], got %d", r_b);
+    if (!lx || !ly) return fail(GM_EINVAL, "null array");
+    return cuda_rc(gm::launch_map_rectangle(r_b, lx, ly, reinterpret_cast<cudaStream_t>(stream)), "map_rectangle");
+}
+
+int gm_coverage(const gm_cfg_t* cfg, uint32_t* counts, const int32_t* tab_x, const int32_t* tab_y, int32_t ntab,
+                void* stream) {
+    if (!cfg) return fail(GM_EINVAL, "null config");
+    gm_cfg_t c = *cfg;
+    c.kind = GM_KIND_COUNT;
+    c.cell_bytes = 4;
+    return launch_cfg(&c, counts, nullptr, tab_x, tab_y, ntab, stream);
+}
+
+int gm_coverage_blocks(const int64_t* bx, const int64_t* by, int64_t nblocks, const int32_t* lx, const int32_t* ly,
+                       int32_t nlocal, int32_t rho, int64_t n, uint32_t* counts, void* stream) {
+    if (nblocks < 0 || nlocal < 0 || rho < 1 || n < 1) return fail(GM_EINVAL, "bad coverage shape");
+    return cuda_rc(gm::launch_coverage_blocks(bx, by, nblocks, lx, ly, nlocal, rho, n, counts,
+                                              reinterpret_cast<cudaStream_t>(stream)),
+                   "coverage_blocks");
+}
+
+int gm_bijection_check(const int64_t* cx, const int64_t* cy, int64_t nblocks, int64_t n_b, int64_t* owner,
+                       int64_t* result, void* stream) {
+    if (!pow2(n_b)) return fail(GM_EINVAL, "n_b must be a power of two");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (int rc = cuda_rc(gm::launch_bijection(cx, cy, nblocks, n_b, owner, result, s), "bijection")) return rc;
+    return GM_OK;
+}
+
+int gm_fill_hash(void* buf, int64_t n, int32_t cell_bytes, uint64_t seed, int32_t mode, void* stream) {
+    if (n < 1) return fail(GM_EINVAL, "bad edge");
+    return cuda_rc(gm::launch_fill_hash(buf, n, cell_bytes, seed, mode, reinterpret_cast<cudaStream_t>(stream)),
+                   "fill_hash");
+}
+
+int gm_checksum(const void* buf, int64_t count, int32_t cell_bytes, uint64_t* out_dev, void* stream) {
+    return cuda_rc(gm::launch_checksum(buf, count, cell_bytes, out_dev, reinterpret_cast<cudaStream_t>(stream)),
+                   "checksum");
+}
+
+int gm_count_equal(const void* a, const void* b, int64_t count, int32_t cell_bytes, unsigned long long* out_dev,
+                   void* stream) {
+    const int64_t bytes = count * cell_bytes;
+    if (bytes % 16) return fail(GM_EINVAL, "count_equal needs a multiple of 16 bytes");
+    return cuda_rc(gm::launch_count_equal(a, b, bytes, out_dev, reinterpret_cast<cudaStream_t>(stream)),
+                   "count_equal");
+}
+
+int gm_l2_flush(const void* buf, int64_t bytes, uint64_t* sink_dev, void* stream) {
+    return cuda_rc(gm::launch_l2_flush(buf, bytes, sink_dev, reinterpret_cast<cudaStream_t>(stream)), "l2_flush");
+}
+
+uint64_t gm_launch_count(void) { return gm::g_launches.load(); }
+const char* gm_last_error(void) { return t_err.c_str(); }
+const char* gm_version(void) { return "gasket_b200 0.1.0 sm_100a"; }
+
+}  // extern "C"

@@ -1,0 +1,289 @@
+// maps.cu -- lambda index-set kernels, coverage/bijection audits, synthetic
+// inputs and checksums.
+//   map_blocks_kernel     <- blockmap.py:91-108 map_blocks_array (any int64
+//                            input, Python floor semantics, r_b levels)
+//   map_rectangle_kernel  <- the b -> (b % W, b // W) call sites
+//                            (blockmap.py:140-141, engine.py:233-235)
+//   bijection kernels     <- blockmap.py:123-166 verify_bijection (first bad
+//                            omega in row-major order = the scalar-scan witness)
+//   coverage_blocks       <- engine.py:236-251 (np.add.at counting leg)
+#include "gasket.cuh"
+#include "launch.h"
+
+namespace gm {
+
+static int grid_for(int64_t items, int threads = 256) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t blocks = (items + threads - 1) / threads;
+    const int64_t cap = (int64_t)sms * 16;
+    if (blocks > cap) blocks = cap;
+    return blocks < 1 ? 1 : (int)blocks;
+}
+
+__global__ void map_blocks_kernel(const int64_t* __restrict__ wx, const int64_t* __restrict__ wy, int64_t count,
+                                  int r_b, int64_t* __restrict__ lx, int64_t* __restrict__ ly) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t ax, ay;
+        lambda_loop64(__ldg(wx + i), __ldg(wy + i), r_b, ax, ay);
+        lx[i] = ax;
+        ly[i] = ay;
+    }
+}
+
+// Rectangle in b order; closed form via the digit table (r_b <= 40 => wx, wy < 3^20).
+__global__ void map_rectangle_kernel(int r_b, uint64_t W, uint64_t total, int64_t* __restrict__ lx,
+                                     int64_t* __restrict__ ly) {
+    __shared__ uint16_t tab[243];
+    digit_table_init(tab);
+    __syncthreads();
+    for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < total; b += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t wy = b / W, wx = b - wy * W;
+        uint32_t nzx, twx, nzy, twy;
+        digit_masks((uint32_t)wx, tab, nzx, twx);
+        digit_masks((uint32_t)wy, tab, nzy, twy);
+        // 20 digits per axis -> 40 interleaved bits
+        const uint64_t ey = (uint64_t)spread_even(nzy & 0xffffu) | ((uint64_t)spread_even(nzy >> 16) << 32);
+        const uint64_t ex = (uint64_t)spread_even(nzx & 0xffffu) | ((uint64_t)spread_even(nzx >> 16) << 32);
+        const uint64_t fy = (uint64_t)spread_even(twy & 0xffffu) | ((uint64_t)spread_even(twy >> 16) << 32);
+        const uint64_t fx = (uint64_t)spread_even(twx & 0xffffu) | ((uint64_t)spread_even(twx >> 16) << 32);
+        ly[b] = (int64_t)(ey | (ex << 1));
+        lx[b] = (int64_t)(fy | (fx << 1));
+    }
+}
+
+__global__ void bijection_owner_kernel(const int64_t* __restrict__ cx, const int64_t* __restrict__ cy, int64_t nblocks,
+                                       int64_t n_b, unsigned long long* __restrict__ owner) {
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nblocks; b += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t x = cx[b], y = cy[b];
+        if (x < 0 || x >= n_b || y < 0 || y >= n_b) continue;
+        if ((x & (n_b - 1 - y)) != 0) continue;
+        atomicMin(owner + (y * n_b + x), (unsigned long long)b);
+    }
+}
+
+__global__ void bijection_witness_kernel(const int64_t* __restrict__ cx, const int64_t* __restrict__ cy, int64_t nblocks,
+                                         int64_t n_b, const unsigned long long* __restrict__ owner,
+                                         unsigned long long* __restrict__ first_bad) {
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nblocks; b += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t x = cx[b], y = cy[b];
+        bool bad = x < 0 || x >= n_b || y < 0 || y >= n_b;
+        bad = bad || ((x & (n_b - 1 - y)) != 0);
+        bad = bad || owner[y * n_b + x] != (unsigned long long)b;
+        if (bad) atomicMin(first_bad, (unsigned long long)b);
+    }
+}
+
+__global__ void coverage_blocks_kernel(const int64_t* __restrict__ bx, const int64_t* __restrict__ by, int64_t nblocks,
+                                       const int32_t* __restrict__ lx, const int32_t* __restrict__ ly, int nlocal,
+                                       int rho, int64_t n, unsigned int* __restrict__ counts) {
+    const int64_t total = nblocks * nlocal;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = i / nlocal;
+        const int j = (int)(i - b * nlocal);
+        const int64_t x = bx[b] * rho + lx[j], y = by[b] * rho + ly[j];
+        if (x >= 0 && x < n && y >= 0 && y < n) atomicAdd(counts + (y * n + x), 1u);
+    }
+}
+
+// --- synthetic inputs ---------------------------------------------------------
+
+template <int C>
+__global__ void fill_hash_kernel(uint8_t* __restrict__ buf, int64_t n, uint64_t seed, int mode) {
+    // one thread per 16-byte vector (n*C is a multiple of 16 when n*C >= 16)
+    constexpr int V = 16 / C;
+    const int64_t per_row = (n * C) / 16;
+    const int64_t total = per_row * n;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < total; v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t y = v / per_row;
+        const int64_t x0 = (v - y * per_row) * V;
+        const int64_t m = n - 1 - y;
+        uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            const int64_t x = x0 + j;
+            uint64_t h = splitmix64(seed ^ (((uint64_t)y << 32) | (uint64_t)x));
+            if (mode == 1 && (x & m) != 0) h = 0;
+            if constexpr (C == 8) {
+                w[2 * j] = (uint32_t)h;
+                w[2 * j + 1] = (uint32_t)(h >> 32);
+            } else {
+                const int bit = j * C * 8;
+                const uint32_t cell = C == 4 ? (uint32_t)h : (uint32_t)(h & ((1u << (8 * C)) - 1u));
+                w[bit >> 5] |= cell << (bit & 31);
+            }
+        }
+        *reinterpret_cast<uint4*>(buf + (y * n + x0) * C) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+}
+
+template <int C>
+__global__ void fill_hash_small_kernel(uint8_t* __restrict__ buf, int64_t n, uint64_t seed, int mode) {
+    const int64_t total = n * n;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t y = i / n, x = i - y * n;
+        uint64_t h = splitmix64(seed ^ (((uint64_t)y << 32) | (uint64_t)x));
+        if (mode == 1 && (x & (n - 1 - y)) != 0) h = 0;
+        st_cell<C>(buf, i, h);
+    }
+}
+
+// H = sum_i ((2i+1) K) v_i mod 2^64 (same as oracle go_checksum)
+template <int C>
+__global__ void checksum_kernel(const uint8_t* __restrict__ buf, int64_t count, unsigned long long* __restrict__ out) {
+    const uint64_t K = 0x9E3779B97F4A7C15ull;
+    uint64_t h = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+        h += ((2 * (uint64_t)i + 1) * K) * ld_cell<C>(buf, i);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, (unsigned long long)h);
+}
+
+// 16-byte-vector checksum for byte grids (bandwidth path).
+__global__ void checksum16_kernel(const uint8_t* __restrict__ buf, int64_t count, unsigned long long* __restrict__ out) {
+    const uint64_t K = 0x9E3779B97F4A7C15ull;
+    uint64_t h = 0;
+    const int64_t nv = count / 16;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
+        const uint4 q = __ldg(reinterpret_cast<const uint4*>(buf) + v);
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+        const uint64_t i0 = (uint64_t)v * 16;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) h += ((2 * (i0 + j) + 1) * K) * (uint64_t)((w[j >> 2] >> (8 * (j & 3))) & 0xffu);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, (unsigned long long)h);
+}
+
+__global__ void count_equal_kernel(const uint4* __restrict__ a, const uint4* __restrict__ b, int64_t nvec,
+                                   unsigned long long* __restrict__ out) {
+    unsigned long long bad = 0;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
+        const uint4 p = __ldg(a + v), q = __ldg(b + v);
+        bad += (p.x != q.x) + (p.y != q.y) + (p.z != q.z) + (p.w != q.w);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    if ((threadIdx.x & 31) == 0 && bad) atomicAdd(out, bad);
+}
+
+__global__ void l2_flush_kernel(const uint4* __restrict__ buf, int64_t nvec, unsigned long long* __restrict__ sink) {
+    uint32_t acc = 0;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
+        uint4 q;
+        asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w) : "l"(buf + v));
+        acc ^= q.x ^ q.y ^ q.z ^ q.w;
+    }
+    if (acc == 0x9E3779B9u) atomicAdd(sink, 1ull);  // practically never; keeps the loads live
+}
+
+// --- launchers (called from capi.cu) ------------------------------------------
+
+cudaError_t launch_map_blocks(const int64_t* wx, const int64_t* wy, int64_t count, int r_b, int64_t* lx, int64_t* ly,
+                              cudaStream_t s) {
+    if (count == 0) return cudaSuccess;
+    map_blocks_kernel<<<grid_for(count), 256, 0, s>>>(wx, wy, count, r_b, lx, ly);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_map_rectangle(int r_b, int64_t* lx, int64_t* ly, cudaStream_t s) {
+    uint64_t W = 1, total = 1;
+    for (int i = 0; i < r_b / 2; ++i) W *= 3;
+    for (int i = 0; i < r_b; ++i) total *= 3;
+    map_rectangle_kernel<<<grid_for((int64_t)total), 256, 0, s>>>(r_b, W, total, lx, ly);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bijection(const int64_t* cx, const int64_t* cy, int64_t nblocks, int64_t n_b, int64_t* owner,
+                             int64_t* result, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(owner, 0xff, (size_t)(n_b * n_b) * sizeof(int64_t), s);
+    if (e) return e;
+    e = cudaMemsetAsync(result, 0xff, sizeof(int64_t), s);
+    if (e) return e;
+    auto* own = reinterpret_cast<unsigned long long*>(owner);
+    bijection_owner_kernel<<<grid_for(nblocks), 256, 0, s>>>(cx, cy, nblocks, n_b, own);
+    note_launch();
+    bijection_witness_kernel<<<grid_for(nblocks), 256, 0, s>>>(cx, cy, nblocks, n_b, own,
+                                                                reinterpret_cast<unsigned long long*>(result));
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_coverage_blocks(const int64_t* bx, const int64_t* by, int64_t nblocks, const int32_t* lx,
+                                   const int32_t* ly, int nlocal, int rho, int64_t n, uint32_t* counts, cudaStream_t s) {
+    if (nblocks == 0 || nlocal == 0) return cudaSuccess;
+    coverage_blocks_kernel<<<grid_for(nblocks * nlocal), 256, 0, s>>>(bx, by, nblocks, lx, ly, nlocal, rho, n, counts);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill_hash(void* buf, int64_t n, int c, uint64_t seed, int mode, cudaStream_t s) {
+    uint8_t* b = reinterpret_cast<uint8_t*>(buf);
+    if (n * c >= 16) {
+        const int64_t total = n * n * c / 16;
+        switch (c) {
+        case 1: fill_hash_kernel<1><<<grid_for(total), 256, 0, s>>>(b, n, seed, mode); break;
+        case 2: fill_hash_kernel<2><<<grid_for(total), 256, 0, s>>>(b, n, seed, mode); break;
+        case 4: fill_hash_kernel<4><<<grid_for(total), 256, 0, s>>>(b, n, seed, mode); break;
+        case 8: fill_hash_kernel<8><<<grid_for(total), 256, 0, s>>>(b, n, seed, mode); break;
+        default: return cudaErrorInvalidValue;
+        }
+    } else {
+        switch (c) {
+        case 1: fill_hash_small_kernel<1><<<grid_for(n * n), 256, 0, s>>>(b, n, seed, mode); break;
+        case 2: fill_hash_small_kernel<2><<<grid_for(n * n), 256, 0, s>>>(b, n, seed, mode); break;
+        case 4: fill_hash_small_kernel<4><<<grid_for(n * n), 256, 0, s>>>(b, n, seed, mode); break;
+        case 8: fill_hash_small_kernel<8><<<grid_for(n * n), 256, 0, s>>>(b, n, seed, mode); break;
+        default: return cudaErrorInvalidValue;
+        }
+    }
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_checksum(const void* buf, int64_t count, int c, uint64_t* out, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(uint64_t), s);
+    if (e) return e;
+    auto* o = reinterpret_cast<unsigned long long*>(out);
+    const uint8_t* b = reinterpret_cast<const uint8_t*>(buf);
+    if (count == 0) return cudaSuccess;
+    if (c == 1 && count % 16 == 0 && (reinterpret_cast<uintptr_t>(buf) & 15) == 0) {
+        checksum16_kernel<<<grid_for(count / 16), 256, 0, s>>>(b, count, o);
+    } else {
+        switch (c) {
+        case 1: checksum_kernel<1><<<grid_for(count), 256, 0, s>>>(b, count, o); break;
+        case 2: checksum_kernel<2><<<grid_for(count), 256, 0, s>>>(b, count, o); break;
+        case 4: checksum_kernel<4><<<grid_for(count), 256, 0, s>>>(b, count, o); break;
+        case 8: checksum_kernel<8><<<grid_for(count), 256, 0, s>>>(b, count, o); break;
+        default: return cudaErrorInvalidValue;
+        }
+    }
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_count_equal(const void* a, const void* b, int64_t bytes, unsigned long long* out, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(unsigned long long), s);
+    if (e) return e;
+    if (bytes % 16 != 0) return cudaErrorInvalidValue;
+    if (bytes == 0) return cudaSuccess;
+    count_equal_kernel<<<grid_for(bytes / 16), 256, 0, s>>>(reinterpret_cast<const uint4*>(a),
+                                                              reinterpret_cast<const uint4*>(b), bytes / 16, out);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_l2_flush(const void* buf, int64_t bytes, uint64_t* sink, cudaStream_t s) {
+    l2_flush_kernel<<<grid_for(bytes / 16, 512), 512, 0, s>>>(reinterpret_cast<const uint4*>(buf), bytes / 16,
+                                                               reinterpret_cast<unsigned long long*>(sink));
+    note_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace gm

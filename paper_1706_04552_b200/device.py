@@ -1,0 +1,229 @@
+"""Device plumbing: torch tensors as device buffers, numpy host buffers, streams.
+
+PyTorch is used only for memory, streams and (multi-GPU) torch.distributed;
+every computation is a call into libgasket_b200.so through ``native``.
+
+Host (numpy) arrays follow the reference's synchronous semantics: the call
+returns after the result is back in the caller's array.  Two host transports:
+  * "copy"   (default): H2D of the needed inputs into a cached device buffer,
+               kernel, D2H of the grid;
+  * "mapped": the numpy buffer is page-locked and mapped once
+               (cudaHostRegister, cached per buffer) and the kernel reads and
+               writes it in place over PCIe, so only the 16-byte row segments
+               the gasket touches cross the bus (tuned strategy only).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from typing import Any
+
+import numpy as np
+import torch
+
+from . import native
+
+_TORCH_CELL = {
+    torch.int8: 1, torch.uint8: 1, torch.int16: 2, torch.uint16: 2,
+    torch.int32: 4, torch.uint32: 4, torch.int64: 8,
+}
+_NUMPY_CELL = {
+    np.dtype(np.int8): 1, np.dtype(np.uint8): 1, np.dtype(np.int16): 2, np.dtype(np.uint16): 2,
+    np.dtype(np.int32): 4, np.dtype(np.uint32): 4, np.dtype(np.int64): 8,
+}
+
+HOST_TRANSPORT_ENV = "GASKET_HOST_TRANSPORT"
+
+
+def require_cuda() -> None:
+    if not torch.cuda.is_available():
+        raise native.GasketError("no CUDA device: the gasket kernels run only on the GPU (no CPU fallback)")
+    native.lib()
+
+
+def stream_handle(stream: torch.cuda.Stream | None = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def is_device(a: Any) -> bool:
+    return isinstance(a, torch.Tensor) and a.is_cuda
+
+
+def cell_bytes_of(a: Any) -> int:
+    if isinstance(a, torch.Tensor):
+        if a.dtype not in _TORCH_CELL:
+            raise ValueError(f"unsupported cell dtype {a.dtype} (integer cells of 1, 2, 4 or 8 bytes)")
+        return _TORCH_CELL[a.dtype]
+    if isinstance(a, np.ndarray):
+        if a.dtype not in _NUMPY_CELL:
+            raise ValueError(f"unsupported cell dtype {a.dtype} (integer cells of 1, 2, 4 or 8 bytes)")
+        return _NUMPY_CELL[a.dtype]
+    raise TypeError(f"grid must be a torch tensor or a numpy array, got {type(a).__name__}")
+
+
+def check_square(a: Any, what: str = "grid") -> int:
+    shape = tuple(a.shape)
+    if len(shape) != 2 or shape[0] != shape[1]:
+        raise ValueError(f"{what} must be a square n x n array, got shape {shape}")
+    contiguous = a.is_contiguous() if isinstance(a, torch.Tensor) else a.flags.c_contiguous
+    if not contiguous:
+        raise ValueError(f"{what} must be C-contiguous")
+    return shape[0]
+
+
+def data_ptr(a: Any) -> int:
+    if isinstance(a, torch.Tensor):
+        return int(a.data_ptr())
+    return int(a.ctypes.data)
+
+
+def _torch_dtype(np_dtype: np.dtype) -> torch.dtype:
+    return torch.from_numpy(np.zeros(1, dtype=np_dtype)).dtype
+
+
+# ---------------------------------------------------------------------------
+# scratch buffers (cached per device / size)
+# ---------------------------------------------------------------------------
+
+class _Scratch:
+    def __init__(self) -> None:
+        self._bufs: dict[tuple, torch.Tensor] = {}
+        self._lock = threading.Lock()
+
+    def get(self, key: str, numel: int, dtype: torch.dtype, device: torch.device | None = None) -> torch.Tensor:
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        k = (key, dev, dtype)
+        with self._lock:
+            t = self._bufs.get(k)
+            if t is None or t.numel() < numel:
+                self._bufs.pop(k, None)
+                t = torch.empty(max(numel, 1), dtype=dtype, device=dev)
+                self._bufs[k] = t
+            return t[:numel]
+
+    def clear(self) -> None:
+        with self._lock:
+            self._bufs.clear()
+
+
+scratch = _Scratch()
+
+
+# ---------------------------------------------------------------------------
+# mapped (zero-copy) host buffers
+# ---------------------------------------------------------------------------
+
+_registered: dict[int, int] = {}
+_reg_lock = threading.Lock()
+CUDA_HOST_REGISTER_MAPPED = 2
+CUDA_HOST_REGISTER_PORTABLE = 1
+
+
+def map_host(a: np.ndarray) -> int:
+    """Page-lock and map a numpy buffer once; return its device-visible address."""
+    ptr, nbytes = int(a.ctypes.data), int(a.nbytes)
+    with _reg_lock:
+        have = _registered.get(ptr)
+        if have is not None and have >= nbytes:
+            return ptr
+        if have is not None:
+            torch.cuda.cudart().cudaHostUnregister(ptr)
+        rc = torch.cuda.cudart().cudaHostRegister(ptr, nbytes, CUDA_HOST_REGISTER_MAPPED | CUDA_HOST_REGISTER_PORTABLE)
+        if int(rc) != 0:
+            raise native.GasketError(f"cudaHostRegister failed ({rc}) for a {nbytes}-byte host grid")
+        _registered[ptr] = nbytes
+    return ptr  # UVA: the registered host address is valid in kernels
+
+
+def unmap_host(a: np.ndarray) -> None:
+    ptr = int(a.ctypes.data)
+    with _reg_lock:
+        if _registered.pop(ptr, None) is not None:
+            torch.cuda.cudart().cudaHostUnregister(ptr)
+
+
+def host_transport() -> str:
+    mode = os.environ.get(HOST_TRANSPORT_ENV, "copy").strip().lower()
+    if mode not in ("copy", "mapped"):
+        raise ValueError(f"{HOST_TRANSPORT_ENV} must be 'copy' or 'mapped', got {mode!r}")
+    return mode
+
+
+# ---------------------------------------------------------------------------
+# lambda index sets on the device
+# ---------------------------------------------------------------------------
+
+def map_blocks_array(wx, wy, r_b: int):
+    """blockmap.map_blocks_array (blockmap.py:91-108) on the GPU.
+
+    Accepts numpy arrays (returns numpy int64, like the reference) or CUDA
+    tensors (returns CUDA int64 tensors, no host round trip)."""
+    require_cuda()
+    host = not is_device(wx)
+    twx = torch.as_tensor(np.ascontiguousarray(wx, dtype=np.int64)) if host else wx.to(torch.int64).contiguous()
+    twy = torch.as_tensor(np.ascontiguousarray(wy, dtype=np.int64)) if host else wy.to(torch.int64).contiguous()
+    if tuple(twx.shape) != tuple(twy.shape):
+        raise ValueError("wx and wy must have the same shape")
+    if host:
+        twx, twy = twx.cuda(), twy.cuda()
+    lx = torch.empty_like(twx)
+    ly = torch.empty_like(twy)
+    native.call("gm_map_blocks", twx.data_ptr(), twy.data_ptr(), twx.numel(), int(r_b), lx.data_ptr(),
+                ly.data_ptr(), stream_handle())
+    if host:
+        return lx.cpu().numpy(), ly.cpu().numpy()
+    return lx, ly
+
+
+def map_rectangle(r_b: int) -> tuple[torch.Tensor, torch.Tensor]:
+    """lambda over the whole packed rectangle (b = wy*W + wx order), CUDA int64."""
+    require_cuda()
+    total = 3 ** r_b
+    lx = torch.empty(total, dtype=torch.int64, device="cuda")
+    ly = torch.empty(total, dtype=torch.int64, device="cuda")
+    native.call("gm_map_rectangle", int(r_b), lx.data_ptr(), ly.data_ptr(), stream_handle())
+    return lx, ly
+
+
+def fill_hash(n: int, dtype: torch.dtype, seed: int, mode: int = 0, out: torch.Tensor | None = None) -> torch.Tensor:
+    """splitmix64(seed ^ (y<<32 | x)) truncated to the cell width; mode 1 zeroes off-gasket cells."""
+    require_cuda()
+    t = out if out is not None else torch.empty((n, n), dtype=dtype, device="cuda")
+    native.call("gm_fill_hash", t.data_ptr(), n, _TORCH_CELL[t.dtype], seed & (2**64 - 1), mode, stream_handle())
+    return t
+
+
+def checksum(t: torch.Tensor) -> int:
+    """Position-weighted 64-bit checksum (same formula as the oracle's)."""
+    require_cuda()
+    out = scratch.get("checksum", 1, torch.int64)
+    native.call("gm_checksum", t.data_ptr(), t.numel(), _TORCH_CELL[t.dtype], out.data_ptr(), stream_handle())
+    return int(out.item()) & (2**64 - 1)
+
+
+def count_mismatch(a: torch.Tensor, b: torch.Tensor) -> int:
+    """Number of differing 32-bit words between two equal-size device buffers."""
+    require_cuda()
+    out = scratch.get("mismatch", 1, torch.int64)
+    native.call("gm_count_equal", a.data_ptr(), b.data_ptr(), a.numel(), _TORCH_CELL[a.dtype], out.data_ptr(),
+                stream_handle())
+    return int(out.item())
+
+
+class L2Flusher:
+    """Reads a buffer of 4x the L2 size so the next timed kernel starts cold
+    (and every dirty line of the previous launch has been written back)."""
+
+    def __init__(self, nbytes: int | None = None) -> None:
+        require_cuda()
+        props = torch.cuda.get_device_properties(torch.cuda.current_device())
+        l2 = int(getattr(props, "L2_cache_size", 126 * 2**20) or 126 * 2**20)
+        self.nbytes = nbytes or max(4 * l2, 256 * 2**20)
+        self.buf = torch.zeros(self.nbytes // 4, dtype=torch.int32, device="cuda")
+        self.sink = torch.zeros(1, dtype=torch.int64, device="cuda")
+
+    def __call__(self) -> None:
+        native.call("gm_l2_flush", self.buf.data_ptr(), self.nbytes, self.sink.data_ptr(), stream_handle())

@@ -1,0 +1,112 @@
+"""ctypes binding of libgasket_b200.so (include/gasket_b200.h).
+
+The library is the product: there is no CPU fallback.  If the in-tree
+``_lib/libgasket_b200.so`` is missing this module raises on first use
+(run ``python -m paper_1706_04552_b200._build`` or ``__graft_entry__.build()``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+from . import _build
+
+LIB_PATH: Path = _build.LIB
+
+GM_OK, GM_EINVAL, GM_ECUDA, GM_ENOMEM = 0, 1, 2, 3
+
+KIND_CONST, KIND_NSUM4, KIND_NSUM8, KIND_COUNT = 0, 1, 2, 3
+STRAT_UNROLL, STRAT_TABLE, STRAT_SUBBOX, STRAT_TUNED = 0, 1, 2, 3
+MAP_BB, MAP_LAMBDA, MAP_BB_EXIT = 0, 1, 2
+FLAG_OMEGA_ORDER, FLAG_DST_FROM_SRC = 1, 2
+
+
+class GmCfg(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_int64),
+        ("rho", ctypes.c_int32),
+        ("mapping", ctypes.c_int32),
+        ("strategy", ctypes.c_int32),
+        ("kind", ctypes.c_int32),
+        ("cell_bytes", ctypes.c_int32),
+        ("param", ctypes.c_int32),
+        ("flags", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+    ]
+
+
+_lib: ctypes.CDLL | None = None
+
+_vp = ctypes.c_void_p
+_i32 = ctypes.c_int32
+_i64 = ctypes.c_int64
+_u64 = ctypes.c_uint64
+
+_SIGS = {
+    "gm_run_bounding_box": [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _vp],
+    "gm_run_block_space": [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _i32, _i32, _i32, _i32, _vp],
+    "gm_launch": [ctypes.POINTER(GmCfg), _vp, _vp, _vp, _vp, _i32, _vp],
+    "gm_map_blocks": [_vp, _vp, _i64, _i32, _vp, _vp, _vp],
+    "gm_map_rectangle": [_i32, _vp, _vp, _vp],
+    "gm_coverage": [ctypes.POINTER(GmCfg), _vp, _vp, _vp, _i32, _vp],
+    "gm_coverage_blocks": [_vp, _vp, _i64, _vp, _vp, _i32, _i32, _i64, _vp, _vp],
+    "gm_bijection_check": [_vp, _vp, _i64, _i64, _vp, _vp, _vp],
+    "gm_fill_hash": [_vp, _i64, _i32, _u64, _i32, _vp],
+    "gm_checksum": [_vp, _i64, _i32, _vp, _vp],
+    "gm_count_equal": [_vp, _vp, _i64, _i32, _vp, _vp],
+    "gm_l2_flush": [_vp, _i64, _vp, _vp],
+}
+
+# Every symbol include/gasket_b200.h declares (checked by tests/test_native_abi.py).
+EXPORTED = tuple(_SIGS) + ("gm_launch_count", "gm_last_error", "gm_version")
+OPTIONAL = ("gm_part_halo_plan",)
+
+
+class GasketError(RuntimeError):
+    pass
+
+
+def lib() -> ctypes.CDLL:
+    """Load the sm_100a library; raise loudly if it has not been built."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise GasketError(
+                f"{LIB_PATH} is missing: build the sm_100a library first "
+                "(python -m paper_1706_04552_b200._build); there is no CPU fallback")
+        L = ctypes.CDLL(str(LIB_PATH))
+        for name, args in _SIGS.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = ctypes.c_int
+        L.gm_launch_count.restype = ctypes.c_uint64
+        L.gm_launch_count.argtypes = []
+        L.gm_last_error.restype = ctypes.c_char_p
+        L.gm_last_error.argtypes = []
+        L.gm_version.restype = ctypes.c_char_p
+        L.gm_version.argtypes = []
+        _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    """Map a GM_E* return code onto the reference's exception types."""
+    if rc == GM_OK:
+        return
+    msg = lib().gm_last_error().decode(errors="replace")
+    if rc == GM_EINVAL:
+        raise ValueError(msg)
+    raise GasketError(msg)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(lib(), name)(*args))
+
+
+def launch_count() -> int:
+    return int(lib().gm_launch_count())
+
+
+def version() -> str:
+    return lib().gm_version().decode()

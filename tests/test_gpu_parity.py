@@ -1,0 +1,328 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) vs the CPU oracle.
+
+Bit-exact for every integer result: index sets element-wise, grids cell by
+cell at sizes the oracle finishes in seconds, and -- at the BASELINE sizes --
+checksums against the oracle plus size-independent properties (every
+strategy agrees with every other, writes land exactly on the gasket, wrap
+arithmetic is linear).
+"""
+
+import itertools
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+DTYPES = {np.int8: torch.int8, np.int16: torch.int16, np.int32: torch.int32, np.int64: torch.int64,
+          np.uint8: torch.uint8}
+KINDS = (0, 1, 2)  # CONST, NSUM4, NSUM8 (ours)
+
+
+def _to_dev(a: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(a.copy()).cuda()
+
+
+def _strategies(gm):
+    S = gm.geometry.IntraStrategy
+    return [S.UNROLL, S.TABLE, S.SUBBOX, S.TUNED]
+
+
+# ---------------------------------------------------------------------------
+# lambda index sets
+# ---------------------------------------------------------------------------
+
+def test_lambda_rectangle_elementwise(gpu, oracle):
+    for r_b in range(0, 17):
+        lx, ly = gpu.device.map_rectangle(r_b)
+        ox, oy = oracle.map_rectangle(r_b)
+        assert np.array_equal(lx.cpu().numpy(), ox), r_b
+        assert np.array_equal(ly.cpu().numpy(), oy), r_b
+
+
+def test_lambda_rectangle_golden_checksums(gpu, golden):
+    meta, _ = golden
+    for r_b, (cx, cy) in meta["lambda_checksum"].items():
+        lx, ly = gpu.device.map_rectangle(int(r_b))
+        assert gpu.device.checksum(lx) == cx and gpu.device.checksum(ly) == cy, r_b
+
+
+def test_lambda_sampled_levels_17_18(gpu, oracle):
+    rng = np.random.default_rng(17)
+    for r_b in (17, 18, 19, 20):
+        w, h = oracle.packing_dims(r_b)
+        idx = rng.integers(0, w * h, size=200_000, dtype=np.int64)
+        lx, ly = gpu.device.map_rectangle(r_b)
+        ox, oy = oracle.map_blocks(idx % w, idx // w, r_b)
+        t = torch.from_numpy(idx).cuda()
+        assert np.array_equal(lx[t].cpu().numpy(), ox)
+        assert np.array_equal(ly[t].cpu().numpy(), oy)
+        del lx, ly
+
+
+def test_map_blocks_array_arbitrary_inputs(gpu, golden):
+    _, arr = golden
+    wx, wy = arr["lambda_rand_wx"], arr["lambda_rand_wy"]
+    for r_b in (0, 1, 7, 20, 33):
+        lx, ly = gpu.blockmap.map_blocks_array(wx, wy, r_b)
+        assert lx.dtype == np.int64
+        assert np.array_equal(lx, arr[f"lambda_rand_lx_{r_b}"])
+        assert np.array_equal(ly, arr[f"lambda_rand_ly_{r_b}"])
+    # device in, device out
+    lx, ly = gpu.blockmap.map_blocks_array(torch.from_numpy(wx).cuda(), torch.from_numpy(wy).cuda(), 7)
+    assert lx.is_cuda and np.array_equal(lx.cpu().numpy(), arr["lambda_rand_lx_7"])
+
+
+def test_verify_bijection_matches_reference(gpu, golden):
+    meta, _ = golden
+    bm = gpu.blockmap
+    for key, (ok, witness, size) in meta["verify_bijection"].items():
+        defect, r_b = key.rsplit("_", 1)
+        fn = None if defect == "None" else bm.corrupted_map_fn(defect)
+        rep = bm.verify_bijection(int(r_b), fn)
+        assert rep.ok == ok, key
+        assert (None if rep.witness is None else list(rep.witness)) == witness, key
+        assert rep.image_size == size, key
+    for r_b in (13, 14, 15, 16):  # beyond the reference's host cap of 12
+        assert bm.verify_bijection(r_b).ok
+
+
+# ---------------------------------------------------------------------------
+# grids: every mapping x strategy x kernel x dtype vs the oracle
+# ---------------------------------------------------------------------------
+
+def _oracle_result(oracle, grid0, src, rho, kind, param):
+    g = grid0.copy()
+    oracle.run_bounding_box(g, src, rho, kind, param)
+    return g
+
+
+def _gpu_all(gpu, grid0, src, rho, kind, param):
+    """Yield (label, result) for every launch shape the device offers."""
+    be = gpu.backends
+    n = grid0.shape[0]
+    r_b = (n // rho).bit_length() - 1
+    sdev = _to_dev(src)
+    for early in (False, True):
+        g = _to_dev(grid0)
+        be.run_bounding_box(g, sdev, rho, kind, param, early_exit=early)
+        yield ("bb-exit" if early else "bb"), g
+    for strat in _strategies(gpu):
+        for flags in ((0, 1) if strat.value == "tuned" else (0,)):
+            g = _to_dev(grid0)
+            lx, ly = be.local_cell_arrays(strat, rho)
+            be.run_block_space(g, sdev, rho, r_b, strat, lx, ly, kind, param, flags=flags)
+            yield f"{strat.value}/f{flags}", g
+
+
+@pytest.mark.parametrize("dtype", list(DTYPES))
+def test_grids_small_exhaustive(gpu, oracle, dtype):
+    for n in (1, 2, 4, 8, 16, 32, 64, 128):
+        for rho in (1, 2, 4, 8, 16, 32, 64):
+            if rho > n:
+                continue
+            for kind in KINDS:
+                for param in (1, -3, 2**31 - 1):
+                    grid0 = oracle.fill_hash(n, dtype, 11, 0)
+                    src = oracle.fill_hash(n, dtype, 22, 0)
+                    want = _oracle_result(oracle, grid0, src, rho, kind, param)
+                    for label, got in _gpu_all(gpu, grid0, src, rho, kind, param):
+                        ok = np.array_equal(got.cpu().numpy(), want)
+                        assert ok, (np.dtype(dtype).name, n, rho, kind, param, label)
+
+
+@pytest.mark.parametrize("dtype", [np.int8, np.int32])
+@pytest.mark.parametrize("n", [1 << 10, 1 << 12])
+def test_grids_medium(gpu, oracle, dtype, n):
+    for kind in KINDS:
+        grid0 = oracle.fill_hash(n, dtype, 5, 1)
+        src = oracle.fill_hash(n, dtype, 6, 0)
+        want = _oracle_result(oracle, grid0, src, 8, kind, 7)
+        for rho in (1, 8, 32, 128):
+            for label, got in _gpu_all(gpu, grid0, src, rho, kind, 7):
+                assert np.array_equal(got.cpu().numpy(), want), (n, rho, kind, label)
+
+
+def test_golden_kernel_checksums_on_device(gpu, oracle, golden):
+    """Reference (numba) checksums reproduced by the device kernels directly."""
+    meta, _ = golden
+    be = gpu.backends
+    S = gpu.geometry.IntraStrategy
+    for row in meta["kernels_big"]:
+        dt = {"int8": torch.int8, "int32": torch.int32}[row["dtype"]]
+        src = gpu.device.fill_hash(row["n"], dt, row["seed"], row["mode"])
+        assert gpu.device.checksum(src) == row["src_checksum"]
+        for strat in (S.TABLE, S.SUBBOX, S.TUNED, S.UNROLL):
+            g = src.clone()
+            be.run_block_space(g, src.clone(), row["rho"], (row["n"] // row["rho"]).bit_length() - 1, strat,
+                               kind=row["kind"], param=row["param"])
+            assert gpu.device.checksum(g) == row["out"], (row, strat)
+
+
+# ---------------------------------------------------------------------------
+# BASELINE sizes: n = 2^16 (checksum vs oracle) and n = 2^17 (properties)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_n16_int8_vs_oracle_checksum(gpu, oracle, kind):
+    n = 1 << 16
+    src_np = oracle.fill_hash(n, np.int8, 3, 0)
+    want = src_np.copy()
+    oracle.run_block_space(want, src_np, 16, 12, 2, None, None, kind, 1)
+    ck = oracle.checksum(want)
+    del want
+    src = gpu.device.fill_hash(n, torch.int8, 3, 0)
+    assert gpu.device.checksum(src) == oracle.checksum(src_np)
+    del src_np
+    S = gpu.geometry.IntraStrategy
+    g = torch.empty_like(src)
+    for rho, strat in [(16, S.TUNED), (32, S.TUNED), (64, S.TUNED), (8, S.TUNED), (16, S.SUBBOX), (32, S.TABLE)]:
+        g.copy_(src)
+        gpu.backends.run_block_space(g, src, rho, 16 - rho.bit_length() + 1, strat, kind=kind, param=1)
+        assert gpu.device.checksum(g) == ck, (rho, strat, kind)
+    g.copy_(src)
+    gpu.backends.run_bounding_box(g, src, 32, kind, 1, early_exit=True)
+    assert gpu.device.checksum(g) == ck
+
+
+def test_n16_int32_const_write_counts(gpu):
+    """Write pass at 2^16 int32 on a sentinel background: exactly 3^16 cells change."""
+    n = 1 << 16
+    S = gpu.geometry.IntraStrategy
+    for rho, strat in [(16, S.TUNED), (32, S.SUBBOX)]:
+        g = torch.full((n, n), -5, dtype=torch.int32, device="cuda")
+        gpu.backends.run_block_space(g, g, rho, 16 - rho.bit_length() + 1, strat, kind=0, param=7)
+        assert int((g == 7).sum()) == 3**16
+        assert int((g == -5).sum()) == n * n - 3**16
+        del g
+
+
+@pytest.mark.parametrize("kind", [1, 2])
+def test_n17_int8_stencil_properties(gpu, kind):
+    """2^17 int8 (16 GiB per grid): tuned == paper-literal SUBBOX bit for bit, and
+    linearity: out(param=a) - out(param=b) == a-b on gasket cells, 0 elsewhere."""
+    n = 1 << 17
+    S = gpu.geometry.IntraStrategy
+    src = gpu.device.fill_hash(n, torch.int8, 9, 0)
+    a = src.clone()
+    gpu.backends.run_block_space(a, src, 32, 12, S.TUNED, kind=kind, param=1, flags=2)
+    b = src.clone()
+    gpu.backends.run_block_space(b, src, 32, 12, S.SUBBOX, kind=kind, param=1)
+    assert gpu.device.count_mismatch(a, b) == 0
+    b.copy_(src)
+    gpu.backends.run_block_space(b, src, 64, 11, S.TUNED, kind=kind, param=4)
+    # (b - a) on gasket cells == 3 (mod 256), elsewhere 0; counted in row chunks
+    threes = zeros = 0
+    for y in range(0, n, 8192):
+        d = b[y:y + 8192].view(torch.uint8) - a[y:y + 8192].view(torch.uint8)
+        threes += int((d == 3).sum())
+        zeros += int((d == 0).sum())
+    assert threes == 3**17
+    assert zeros == n * n - 3**17
+
+
+# ---------------------------------------------------------------------------
+# engine API, coverage, host transports
+# ---------------------------------------------------------------------------
+
+def test_launch_examples_match_reference(gpu, golden):
+    meta, _ = golden
+    eng = gpu.engine
+    from tests.golden.make_golden import hash_grid
+    for ex in meta["launch_examples"]:
+        spec = gpu.geometry.FractalSpec(n=ex["n"], rho=ex["rho"])
+        cfg = eng.LaunchConfig(spec=spec, mapping=eng.Mapping(ex["mapping"]),
+                               strategy=gpu.geometry.IntraStrategy(ex["strategy"]) if ex["strategy"] else None,
+                               kernel=eng.CellKernel(eng.KernelKind(ex["kind"]), ex["param"]), verify_coverage=True)
+        for as_device in (True, False):
+            g = hash_grid(ex["n"], np.int32, 3, 0) if ex["kind"] != "const" else np.zeros((ex["n"],) * 2, np.int32)
+            if as_device:
+                g = torch.from_numpy(g).cuda()
+            m = eng.launch(cfg, g)
+            gn = g.cpu().numpy() if as_device else g
+            from tests.golden.make_golden import checksum
+            assert checksum(gn) == ex["grid"], ex
+            assert [m.blocks_launched, m.threads_launched, m.threads_useful, m.map_ops, m.reduction_depth,
+                    m.simulated_cost] == ex["metrics"]
+
+
+def test_coverage_reports_match_reference(gpu, golden):
+    meta, _ = golden
+    eng = gpu.engine
+    from tests.golden.make_golden import checksum
+    for row in meta["coverage"]:
+        spec = gpu.geometry.FractalSpec(n=row["n"], rho=row["rho"])
+        cfg = eng.LaunchConfig(spec=spec, mapping=eng.Mapping.BLOCK_SPACE,
+                               strategy=gpu.geometry.IntraStrategy(row["strategy"]))
+        fn = None if row["defect"] is None else gpu.blockmap.corrupted_map_fn(row["defect"])
+        rep = eng.verify_coverage(cfg, fn)
+        assert rep.exact == row["exact"], row
+        assert checksum(rep.counts) == row["counts"], row
+        assert len(rep.duplicates) == row["ndups"] and len(rep.misses) == row["nmisses"]
+        assert [list(c) for c in rep.duplicates[:50]] == row["dups"]
+        assert [list(c) for c in rep.misses[:50]] == row["misses"]
+
+
+def test_coverage_real_kernels_exact_large(gpu):
+    eng = gpu.engine
+    S = gpu.geometry.IntraStrategy
+    for n, rho in ((1 << 12, 8), (1 << 14, 32), (1 << 14, 1)):
+        spec = gpu.geometry.FractalSpec(n=n, rho=rho)
+        for mapping, strat in [(eng.Mapping.BOUNDING_BOX, None), (eng.Mapping.BOUNDING_BOX_EXIT, None)] + \
+                [(eng.Mapping.BLOCK_SPACE, s) for s in S]:
+            rep = eng.verify_coverage(eng.LaunchConfig(spec=spec, mapping=mapping, strategy=strat))
+            assert rep.exact, (n, rho, mapping, strat)
+
+
+@pytest.mark.parametrize("transport", ["copy", "mapped"])
+def test_numpy_host_path(gpu, oracle, monkeypatch, transport):
+    monkeypatch.setenv("GASKET_HOST_TRANSPORT", transport)
+    S = gpu.geometry.IntraStrategy
+    for n, dtype, kind in itertools.product((64, 1024), (np.int8, np.int32), KINDS):
+        grid0 = oracle.fill_hash(n, dtype, 1, 0)
+        src = oracle.fill_hash(n, dtype, 2, 0)
+        want = _oracle_result(oracle, grid0, src, 16, kind, 9)
+        for strat in (S.TUNED, S.SUBBOX):
+            g = grid0.copy()
+            gpu.backends.run_block_space(g, src, 16, (n // 16).bit_length() - 1, strat, kind=kind, param=9)
+            assert np.array_equal(g, want), (transport, n, dtype, kind, strat)
+        g = grid0.copy()
+        gpu.backends.run_bounding_box(g, src, 16, kind, 9)
+        assert np.array_equal(g, want)
+        gpu.device.unmap_host(g)
+
+
+def test_src_alias_is_snapshotted(gpu, oracle):
+    n = 256
+    grid0 = oracle.fill_hash(n, np.int32, 4, 0)
+    want = grid0.copy()
+    oracle.run_bounding_box(want, grid0.copy(), 4, 1, 1)
+    g = torch.from_numpy(grid0.copy()).cuda()
+    gpu.backends.run_block_space(g, g, 4, 6, gpu.geometry.IntraStrategy.TUNED, kind=1, param=1)
+    assert np.array_equal(g.cpu().numpy(), want)
+
+
+def test_errors_are_loud(gpu):
+    be = gpu.backends
+    g = torch.zeros((64, 64), dtype=torch.int32, device="cuda")
+    with pytest.raises(ValueError):
+        be.run_block_space(g, g, 128, 0, gpu.geometry.IntraStrategy.SUBBOX)
+    with pytest.raises(ValueError):
+        be.run_block_space(g, g, 8, 4, gpu.geometry.IntraStrategy.SUBBOX)  # r_b mismatch (64/8 = 2^3)
+    with pytest.raises(ValueError):
+        be.run_bounding_box(torch.zeros((64, 32), dtype=torch.int32, device="cuda"), None, 8, 0, 1)
+    with pytest.raises(ValueError):
+        be.run_bounding_box(torch.zeros((64, 64), dtype=torch.float32, device="cuda"), None, 8, 0, 1)
+    with pytest.raises(RuntimeError):
+        be.resolve_backend("numba")
+    with pytest.raises(OverflowError):
+        be.run_bounding_box(g, g, 8, 0, 2**31)
+
+
+def test_launch_counter_moves(gpu):
+    before = gpu.native.launch_count()
+    g = torch.zeros((64, 64), dtype=torch.int8, device="cuda")
+    gpu.backends.run_block_space(g, g, 8, 3, gpu.geometry.IntraStrategy.TUNED)
+    torch.cuda.synchronize()
+    assert gpu.native.launch_count() == before + 1

@@ -1,0 +1,57 @@
+"""The C-ABI library builds for sm_100a, loads without a GPU and exports every
+symbol include/gasket_b200.h declares (no compute calls here)."""
+
+import re
+import subprocess
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def _declared_symbols() -> set[str]:
+    text = (ROOT / "include" / "gasket_b200.h").read_text()
+    return set(re.findall(r"^\s*(?:int|uint64_t|const char\*)\s+(gm_\w+)\s*\(", text, flags=re.M))
+
+
+def test_header_declares_expected_surface():
+    syms = _declared_symbols()
+    assert {"gm_run_bounding_box", "gm_run_block_space", "gm_map_blocks", "gm_launch"} <= syms
+
+
+def test_library_loads_and_exports_header_symbols():
+    from paper_1706_04552_b200 import _build, native
+
+    _build.build()
+    lib = native.lib()
+    for name in _declared_symbols():
+        assert hasattr(lib, name), name
+    assert set(native.EXPORTED) == _declared_symbols()
+    assert native.version().startswith("gasket_b200")
+    assert native.launch_count() == 0  # nothing ran in this CPU process
+
+
+def test_library_is_sm100a_cubin():
+    from paper_1706_04552_b200 import _build
+
+    lib = _build.build()
+    out = subprocess.run(["cuobjdump", "-lelf", str(lib)], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+def test_errors_without_gpu_are_loud():
+    """Product entry points refuse to run (no CPU fallback) when there is no GPU."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import numpy as np
+
+    from paper_1706_04552_b200 import backends, native
+
+    g = np.zeros((8, 8), dtype=np.int32)
+    with pytest.raises(native.GasketError):
+        backends.run_bounding_box(g, g, 2, 0, 1)
