@@ -52,6 +52,7 @@ extern "C" {
 
 #define GM_FLAG_OMEGA_ORDER 1  /* tuned: visit tiles in b = wy*W + wx order */
 #define GM_FLAG_DST_FROM_SRC 2 /* stencil: grid == copy of src off-gasket (engine.py:201) */
+#define GM_FLAG_EXPLICIT_RMW 4 /* tuned write: load partial sectors, store whole sectors */
 
 #define GM_OK 0
 #define GM_EINVAL 1  /* bad shape / size / tag (the reference's ValueError) */
@@ -116,6 +117,14 @@ int gm_count_equal(const void* a, const void* b, int64_t count, int32_t cell_byt
                    unsigned long long* out_dev, void* stream);
 /* Reads `bytes` of `buf` (bigger than L2) so the next kernel starts cold. */
 int gm_l2_flush(const void* buf, int64_t bytes, uint64_t* sink_dev, void* stream);
+
+/* Host buffers for the zero-copy transport: returns the device-visible address
+ * of a page-locked host range, page-locking and mapping it first when
+ * register_if_needed != 0 (cudaHostRegisterMapped); *registered = 1 when this
+ * call did the registration (the caller then owns a gm_host_unmap). */
+int gm_host_map(void* host, int64_t bytes, int32_t register_if_needed, void** dev_ptr,
+                int32_t* registered);
+int gm_host_unmap(void* host);
 
 /* Number of kernels this library has launched (all entry points). */
 uint64_t gm_launch_count(void);

@@ -158,10 +158,14 @@ def _run(grid: Any, src: Any, kind: int, launch, *, mapped_ok: bool) -> None:
         raise ValueError("grid is read-only")
     mode = device.host_transport()
     if mode == "mapped" and mapped_ok and not (reads_src and _shares_memory(src, grid)):
-        gptr = device.map_host(grid)
-        sptr = device.map_host(np.ascontiguousarray(src)) if reads_src else 0
-        launch(gptr, sptr, n, c, stream)
-        torch.cuda.current_stream().synchronize()
+        src_host = np.ascontiguousarray(src) if reads_src else None
+        with device.MappedHost(grid) as gptr:
+            if src_host is None:
+                launch(gptr, 0, n, c, stream)
+            else:
+                with device.MappedHost(src_host) as sptr:
+                    launch(gptr, sptr, n, c, stream)
+            torch.cuda.current_stream().synchronize()
         return
 
     tdtype = device._torch_dtype(grid.dtype)

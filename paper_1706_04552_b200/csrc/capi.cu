@@ -226,6 +226,37 @@ int gm_l2_flush(const void* buf, int64_t bytes, uint64_t* sink_dev, void* stream
     return cuda_rc(gm::launch_l2_flush(buf, bytes, sink_dev, reinterpret_cast<cudaStream_t>(stream)), "l2_flush");
 }
 
+int gm_host_map(void* host, int64_t bytes, int32_t register_if_needed, void** dev_ptr, int32_t* registered) {
+    if (!host || !dev_ptr || bytes <= 0) return fail(GM_EINVAL, "bad host buffer");
+    if (registered) *registered = 0;
+    cudaPointerAttributes at{};
+    cudaError_t e = cudaPointerGetAttributes(&at, host);
+    if (e == cudaSuccess && at.type == cudaMemoryTypeHost && at.devicePointer) {
+        *dev_ptr = at.devicePointer;  // already page-locked (e.g. torch pin_memory) and mapped
+        return GM_OK;
+    }
+    cudaGetLastError();
+    if (!register_if_needed) return fail(GM_EINVAL, "host buffer is not page-locked");
+    e = cudaHostRegister(host, (size_t)bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
+    if (e == cudaErrorHostMemoryAlreadyRegistered) {
+        cudaGetLastError();
+    } else if (e != cudaSuccess) {
+        return cuda_rc(e, "cudaHostRegister");
+    } else if (registered) {
+        *registered = 1;
+    }
+    return cuda_rc(cudaHostGetDevicePointer(dev_ptr, host, 0), "cudaHostGetDevicePointer");
+}
+
+int gm_host_unmap(void* host) {
+    cudaError_t e = cudaHostUnregister(host);
+    if (e == cudaErrorHostMemoryNotRegistered) {
+        cudaGetLastError();
+        return GM_OK;
+    }
+    return cuda_rc(e, "cudaHostUnregister");
+}
+
 uint64_t gm_launch_count(void) { return gm::g_launches.load(); }
 const char* gm_last_error(void) { return t_err.c_str(); }
 const char* gm_version(void) { return "gasket_b200 0.1.0 sm_100a"; }

@@ -28,5 +28,7 @@ void note_launch();
 
 cudaError_t launch_literal(const LaunchArgs& a);
 cudaError_t launch_tuned(const LaunchArgs& a);
+cudaError_t launch_stream(const LaunchArgs& a);
+cudaError_t launch_stencil_tile(const LaunchArgs& a);
 
 }  // namespace gm

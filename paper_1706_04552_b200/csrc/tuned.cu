@@ -260,6 +260,16 @@ static cudaError_t launch_c(const LaunchArgs& a) {
 }
 
 cudaError_t launch_tuned(const LaunchArgs& a) {
+    // neighbour sums on grids at least one 128-byte tile wide: shared-memory tiles (stencil.cu)
+    if (a.kind == KIND_NSUM4 || a.kind == KIND_NSUM8) {
+        const cudaError_t es = launch_stencil_tile(a);
+        if (es != cudaErrorNotSupported) return es;
+        cudaGetLastError();
+    }
+    // otherwise the warp-per-tile-band kernel (stream.cu)
+    const cudaError_t e = launch_stream(a);
+    if (e != cudaErrorNotSupported) return e;
+    cudaGetLastError();
     switch (a.cell_bytes) {
     case 1: return launch_c<1>(a);
     case 2: return launch_c<2>(a);

@@ -116,33 +116,31 @@ scratch = _Scratch()
 # mapped (zero-copy) host buffers
 # ---------------------------------------------------------------------------
 
-_registered: dict[int, int] = {}
-_reg_lock = threading.Lock()
-CUDA_HOST_REGISTER_MAPPED = 2
-CUDA_HOST_REGISTER_PORTABLE = 1
+class MappedHost:
+    """Device-visible view of a numpy buffer for one call (context manager).
 
+    Already page-locked memory (e.g. a view of a torch ``pin_memory`` tensor,
+    the fast path) is used in place; pageable memory is page-locked and mapped
+    for the duration of the call and released afterwards, so no registration
+    outlives the array it belongs to."""
 
-def map_host(a: np.ndarray) -> int:
-    """Page-lock and map a numpy buffer once; return its device-visible address."""
-    ptr, nbytes = int(a.ctypes.data), int(a.nbytes)
-    with _reg_lock:
-        have = _registered.get(ptr)
-        if have is not None and have >= nbytes:
-            return ptr
-        if have is not None:
-            torch.cuda.cudart().cudaHostUnregister(ptr)
-        rc = torch.cuda.cudart().cudaHostRegister(ptr, nbytes, CUDA_HOST_REGISTER_MAPPED | CUDA_HOST_REGISTER_PORTABLE)
-        if int(rc) != 0:
-            raise native.GasketError(f"cudaHostRegister failed ({rc}) for a {nbytes}-byte host grid")
-        _registered[ptr] = nbytes
-    return ptr  # UVA: the registered host address is valid in kernels
+    def __init__(self, a: np.ndarray) -> None:
+        self.host = int(a.ctypes.data)
+        self.nbytes = int(a.nbytes)
+        self.ptr = 0
+        self._owned = False
 
+    def __enter__(self) -> int:
+        out = ctypes.c_void_p()
+        reg = ctypes.c_int32(0)
+        native.call("gm_host_map", self.host, self.nbytes, 1, ctypes.byref(out), ctypes.byref(reg))
+        self.ptr, self._owned = int(out.value), bool(reg.value)
+        return self.ptr
 
-def unmap_host(a: np.ndarray) -> None:
-    ptr = int(a.ctypes.data)
-    with _reg_lock:
-        if _registered.pop(ptr, None) is not None:
-            torch.cuda.cudart().cudaHostUnregister(ptr)
+    def __exit__(self, *exc) -> None:
+        if self._owned:
+            torch.cuda.current_stream().synchronize()
+            native.call("gm_host_unmap", self.host)
 
 
 def host_transport() -> str:

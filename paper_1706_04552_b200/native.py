@@ -19,7 +19,7 @@ GM_OK, GM_EINVAL, GM_ECUDA, GM_ENOMEM = 0, 1, 2, 3
 KIND_CONST, KIND_NSUM4, KIND_NSUM8, KIND_COUNT = 0, 1, 2, 3
 STRAT_UNROLL, STRAT_TABLE, STRAT_SUBBOX, STRAT_TUNED = 0, 1, 2, 3
 MAP_BB, MAP_LAMBDA, MAP_BB_EXIT = 0, 1, 2
-FLAG_OMEGA_ORDER, FLAG_DST_FROM_SRC = 1, 2
+FLAG_OMEGA_ORDER, FLAG_DST_FROM_SRC, FLAG_EXPLICIT_RMW = 1, 2, 4
 
 
 class GmCfg(ctypes.Structure):
@@ -56,6 +56,8 @@ _SIGS = {
     "gm_checksum": [_vp, _i64, _i32, _vp, _vp],
     "gm_count_equal": [_vp, _vp, _i64, _i32, _vp, _vp],
     "gm_l2_flush": [_vp, _i64, _vp, _vp],
+    "gm_host_map": [_vp, _i64, _i32, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_int32)],
+    "gm_host_unmap": [_vp],
 }
 
 # Every symbol include/gasket_b200.h declares (checked by tests/test_native_abi.py).

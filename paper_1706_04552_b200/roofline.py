@@ -16,10 +16,20 @@ element-byte figure (c bytes per cell read + written) is reported beside them.
 from __future__ import annotations
 
 import functools
+import json
+from pathlib import Path
 
 import numpy as np
 
 SECTOR = 32
+# stencil_read_sectors(r, c, eight) precomputed with this module's counter
+# (keys "r,c,eight"); tests/test_roofline.py re-derives entries and checks
+# small levels against a brute-force neighbour scan.
+_TABLE_PATH = Path(__file__).with_name("stencil_sectors.json")
+try:
+    _TABLE = json.loads(_TABLE_PATH.read_text())
+except (OSError, ValueError):  # pragma: no cover
+    _TABLE = {}
 
 
 def _k(c: int) -> int:
@@ -91,7 +101,8 @@ def stencil_read_sectors(r: int, c: int, eight: bool, chunk: int = 2048) -> int:
 
 
 def stencil_read_bytes(r: int, c: int, eight: bool) -> int:
-    return SECTOR * stencil_read_sectors(r, c, eight)
+    hit = _TABLE.get(f"{r},{c},{int(eight)}")
+    return SECTOR * (int(hit) if hit is not None else stencil_read_sectors(r, c, eight))
 
 
 def pass_bytes(r: int, c: int, kind: int) -> int:

@@ -1,0 +1,28 @@
+# usage: bash scripts/gpu_round.sh TAG [tests] [bench] [stencil] [ncu] [ncufull]
+TAG=$1; shift
+mkdir -p gpurun_out/$TAG
+for step in "$@"; do
+case $step in
+tests)
+  timeout 300 python __graft_entry__.py smoke > gpurun_out/$TAG/smoke.log 2>&1; echo smoke_rc=$?
+  timeout 1800 python -m pytest tests -m gpu -q -p no:cacheprovider -x > gpurun_out/$TAG/pytest_gpu.log 2>&1; echo pytest_rc=$?
+  tail -3 gpurun_out/$TAG/pytest_gpu.log ;;
+bench)
+  timeout 900 python bench.py > gpurun_out/$TAG/bench_write16.json 2> gpurun_out/$TAG/bench_write16.err; echo bench_rc=$?
+  timeout 600 python bench.py --impl reference > gpurun_out/$TAG/bench_ref.json 2> gpurun_out/$TAG/bench_ref.err; echo ref_rc=$? ;;
+stencil)
+  timeout 900 python bench.py --workload stencil17 --steps 100 > gpurun_out/$TAG/bench_stencil17.json 2> gpurun_out/$TAG/bench_stencil17.err; echo stencil_rc=$? ;;
+ncu)
+  timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 60 --csv --log-file gpurun_out/$TAG/launches_write16.csv python bench.py --steps 20 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1; echo ncu_rc=$?
+  timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 40 --csv --log-file gpurun_out/$TAG/launches_stencil17.csv python bench.py --workload stencil17 --steps 10 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1; echo ncu2_rc=$? ;;
+ncufull)
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:lambda_stream -s 3 -c 1 -o gpurun_out/$TAG/prof_write16 python bench.py --steps 2 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1; echo ncuf_rc=$?
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:lambda_stream -s 3 -c 1 -o gpurun_out/$TAG/prof_stencil17 python bench.py --workload stencil17 --steps 2 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1; echo ncuf2_rc=$? ;;
+probe)
+  ./scripts/probe_stride > gpurun_out/$TAG/probe_stride.txt 2>&1; echo probe_rc=$? ;;
+variants)
+  timeout 600 python scripts/variants.py write16 stencil17 > gpurun_out/$TAG/variants.txt 2>&1; echo variants_rc=$? ;;
+ncustencil)
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:lambda_stream -s 2 -c 1 -o gpurun_out/$TAG/prof_stencil17 python bench.py --workload stencil17 --steps 2 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1; echo ncus_rc=$? ;;
+esac
+done

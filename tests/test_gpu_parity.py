@@ -290,7 +290,6 @@ def test_numpy_host_path(gpu, oracle, monkeypatch, transport):
         g = grid0.copy()
         gpu.backends.run_bounding_box(g, src, 16, kind, 9)
         assert np.array_equal(g, want)
-        gpu.device.unmap_host(g)
 
 
 def test_src_alias_is_snapshotted(gpu, oracle):
