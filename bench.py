@@ -47,7 +47,10 @@ WORKLOADS = {
     "write16-i32": (16, "int32", 0, 32, "n=2^16 gasket write pass (const 1), int32 cells, lambda map"),
     "stencil17": (17, "int8", 2, 64, "n=2^17 8-neighbour CA step, int8 states, lambda map"),
     "stencil17-nsum4": (17, "int8", 1, 64, "n=2^17 4-neighbour CA step, int8 states, lambda map"),
+    "part18": (18, "int8", 2, 0, "n=2^18 8-neighbour CA step, int8 states, level-5 sub-gasket partition over "
+                                 "the ranks, NCCL all_gather of the changing halo cells"),
 }
+PART_LEVEL = 5
 FALLBACK_HBM_GBS = 6650.0
 
 
@@ -296,10 +299,13 @@ def _e2e(workload: str, rho: int, steps: int) -> dict:
             call()
         dt = (time.perf_counter() - t0) / k
         if transport == "mapped":
-            # zero-copy: only what the kernel touches crosses PCIe -- the gasket cells it
-            # stores (byte-masked, no read-back) and, for stencils, the neighbour sectors
-            h2d = 0 if kind == 0 else R.stencil_read_bytes(r, c, kind == 2)
-            d2h = 3**r * c
+            # zero-copy: only the sectors the kernel touches cross PCIe -- partial gasket
+            # sectors are read, blended and written back whole; stencils also read the
+            # neighbour sectors of the snapshot
+            touched = R.write_bytes(r, c)
+            full = R.SECTOR * 3 ** (r - R._k(c)) if r >= R._k(c) else 0
+            h2d = touched - full if kind == 0 else R.stencil_read_bytes(r, c, kind == 2) + touched
+            d2h = touched
         else:
             h2d = n * n * c * (1 if kind == 0 else 2)
             d2h = n * n * c
@@ -361,14 +367,31 @@ def run_ours(args) -> None:
     native.lib()
     flusher = device.L2Flusher()
 
-    grid = torch.zeros((n, n), dtype=tdt, device="cuda")
-    src = None
-    flags = 0
-    if kind != 0:
-        src = device.fill_hash(n, tdt, 1 + rank, 0)
-        grid.copy_(src)
-        flags = native.FLAG_DST_FROM_SRC
-    step = _make_step(workload, grid, src, rho, flags)
+    part = None
+    if workload.startswith("part"):
+        import torch.distributed as dist
+
+        from paper_1706_04552_b200 import partition as P
+
+        plan = P.PartitionPlan(n, PART_LEVEL, world, eight=kind == 2)
+        init = device.fill_hash(n, tdt, 1, 0)  # every rank holds the same initial state
+        part = P.PartitionedCA(plan, rank, init, kind, 1, group=dist.group.WORLD if world > 1 else None)
+        del init
+        torch.cuda.empty_cache()
+        if world == 1:
+            step = lambda: (part.compute(), part.finish())  # noqa: E731  (no peers: nothing to exchange)
+        else:
+            step = part.step
+        grid = src = None
+    else:
+        grid = torch.zeros((n, n), dtype=tdt, device="cuda")
+        src = None
+        flags = 0
+        if kind != 0:
+            src = device.fill_hash(n, tdt, 1 + rank, 0)
+            grid.copy_(src)
+            flags = native.FLAG_DST_FROM_SRC
+        step = _make_step(workload, grid, src, rho, flags)
     for _ in range(args.warmup):
         flusher()
         step()
@@ -387,7 +410,7 @@ def run_ours(args) -> None:
     total_ms = _max_over_ranks(sum(ms), world)
     ms_per_step = total_ms / args.steps
     cells = 3**r
-    value = world * cells / (ms_per_step * 1e-3)
+    value = (1 if part is not None else world) * cells / (ms_per_step * 1e-3)
 
     peak, peak_src = _peaks()
     alg_bytes = R.pass_bytes(r, c, kind)
@@ -402,13 +425,14 @@ def run_ours(args) -> None:
         "warmup": args.warmup,
         "ms_per_step": ms_per_step,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if part is not None else "weak",
         "vs_baseline": None,
         "dtype": {"int8": "i8", "int32": "i32"}[dname],
         "data": "synthetic (zero grid, param=1)" if kind == 0 else "synthetic (splitmix64 hash states, all cells)",
         "config": {"workload": workload, "description": desc, "n": n, "rho": rho, "mapping": "lambda",
                    "strategy": "tuned", "kind": ["const", "nsum4", "nsum8"][kind], "cells_per_step": cells,
-                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "parallelism": (f"subgasket-partition{world} (level {PART_LEVEL})" if part is not None
+                                   else f"replicas{world}" if world > 1 else "single"),
                    "l2": "flushed before every timed step (4x L2 read, outside the events)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src, "algorithmic_bytes_per_launch": alg_bytes,
@@ -418,9 +442,13 @@ def run_ours(args) -> None:
         "gpu_launches": int(launches),
         "timed_region_wall_s": t_wall,
     }
+    if part is not None:
+        line["config"]["halo_bytes_per_step"] = part.halo.bytes_per_step if world > 1 else 0
+        line["config"]["subgasket_ranges"] = part.plan.ranges
+        del part
     del grid, src
     torch.cuda.empty_cache()
-    if rank == 0 and world == 1:
+    if rank == 0 and world == 1 and not workload.startswith("part"):
         if not args.no_sweep and kind == 0:
             line["sweep"] = _sweep(r, tdt, flusher)
         if not args.no_e2e:

@@ -85,6 +85,17 @@ int gm_run_block_space(void* grid, const void* src, int64_t n, int32_t cell_byte
 int gm_launch(const gm_cfg_t* cfg, void* grid, const void* src, const int32_t* tab_x,
               const int32_t* tab_y, int32_t ntab, void* stream);
 
+/* Multi-GPU partition (no reference counterpart): the tuned kernel
+ * restricted to the level-`level` sub-gaskets [sg_begin, sg_end) in base-3 digit
+ * order (a contiguous tile range of the lambda digit order). */
+int gm_run_part(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
+                int32_t flags, int32_t level, uint32_t sg_begin, uint32_t sg_end, void* stream);
+/* Halo plumbing: out[i] = grid[idx[i]] / grid[idx[i]] = in[i] (linear cell indices). */
+int gm_gather_cells(const void* grid, int32_t cell_bytes, const int64_t* idx, int64_t count, void* out,
+                    void* stream);
+int gm_scatter_cells(void* grid, int32_t cell_bytes, const int64_t* idx, int64_t count, const void* in,
+                     void* stream);
+
 /* blockmap.py:91-108: (lx, ly) = lambda(wx, wy) element-wise, int64, floor semantics. */
 int gm_map_blocks(const int64_t* wx, const int64_t* wy, int64_t count, int32_t r_b, int64_t* lx,
                   int64_t* ly, void* stream);
@@ -125,6 +136,9 @@ int gm_l2_flush(const void* buf, int64_t bytes, uint64_t* sink_dev, void* stream
 int gm_host_map(void* host, int64_t bytes, int32_t register_if_needed, void** dev_ptr,
                 int32_t* registered);
 int gm_host_unmap(void* host);
+
+/* Device-wide L2 fetch granularity hint (cudaLimitMaxL2FetchGranularity, 0..128 bytes). */
+int gm_set_l2_fetch_granularity(int32_t bytes);
 
 /* Number of kernels this library has launched (all entry points). */
 uint64_t gm_launch_count(void);

@@ -126,7 +126,10 @@ def _shares_memory(a: Any, b: Any) -> bool:
 def _run(grid: Any, src: Any, kind: int, launch, *, mapped_ok: bool) -> None:
     """Route one launch: device tensors directly, numpy through a host transport.
 
-    ``launch(grid_ptr, src_ptr, n, cell_bytes, stream)`` issues the C-ABI call."""
+    ``launch(grid_ptr, src_ptr, n, cell_bytes, stream, extra_flags)`` issues the C-ABI call.
+    In the mapped (zero-copy) transport the kernel is asked for whole-sector
+    writes (``FLAG_EXPLICIT_RMW``): PCIe cannot carry byte-masked partial lines
+    efficiently, so partial sectors are read, blended and written back whole."""
     device.require_cuda()
     n = device.check_square(grid)
     c = device.cell_bytes_of(grid)
@@ -149,7 +152,7 @@ def _run(grid: Any, src: Any, kind: int, launch, *, mapped_ok: bool) -> None:
                 src_dev = snap
             else:
                 device.check_square(src, "src")
-        launch(device.data_ptr(grid), device.data_ptr(src_dev) if reads_src else 0, n, c, stream)
+        launch(device.data_ptr(grid), device.data_ptr(src_dev) if reads_src else 0, n, c, stream, 0)
         return
 
     if not isinstance(grid, np.ndarray):
@@ -161,10 +164,10 @@ def _run(grid: Any, src: Any, kind: int, launch, *, mapped_ok: bool) -> None:
         src_host = np.ascontiguousarray(src) if reads_src else None
         with device.MappedHost(grid) as gptr:
             if src_host is None:
-                launch(gptr, 0, n, c, stream)
+                launch(gptr, 0, n, c, stream, native.FLAG_EXPLICIT_RMW)
             else:
                 with device.MappedHost(src_host) as sptr:
-                    launch(gptr, sptr, n, c, stream)
+                    launch(gptr, sptr, n, c, stream, native.FLAG_EXPLICIT_RMW)
             torch.cuda.current_stream().synchronize()
         return
 
@@ -180,7 +183,7 @@ def _run(grid: Any, src: Any, kind: int, launch, *, mapped_ok: bool) -> None:
         else:
             dev_src.copy_(torch.from_numpy(np.ascontiguousarray(src)), non_blocking=True)
         src_ptr = dev_src.data_ptr()
-    launch(dev_grid.data_ptr(), src_ptr, n, c, stream)
+    launch(dev_grid.data_ptr(), src_ptr, n, c, stream, 0)
     host_grid.copy_(dev_grid, non_blocking=True)
     torch.cuda.current_stream().synchronize()
 
@@ -197,7 +200,7 @@ def run_bounding_box(grid, src, rho: int, kind: int, param: int, backend: str = 
     p = _param32(param)
     kind = int(kind)
 
-    def launch(gp, sp, n, c, stream):
+    def launch(gp, sp, n, c, stream, extra_flags):
         native.call("gm_run_bounding_box", gp, sp, n, c, int(rho), kind, p, 1 if early_exit else 0, stream)
 
     _run(grid, src, kind, launch, mapped_ok=False)
@@ -222,9 +225,9 @@ def run_block_space(grid, src, rho: int, r_b: int, strategy, local_x: Optional[n
         device.require_cuda()
         tx, ty, ntab = _device_table(local_x, local_y, int(rho))
 
-    def launch(gp, sp, n, c, stream):
+    def launch(gp, sp, n, c, stream, extra_flags):
         native.call("gm_run_block_space", gp, sp, n, c, int(rho), int(r_b), tag, tx, ty, ntab, kind, p,
-                    int(flags), stream)
+                    int(flags) | extra_flags, stream)
 
     _run(grid, src, kind, launch, mapped_ok=(tag == STRAT_TUNED))
 

@@ -23,6 +23,8 @@ cudaError_t launch_fill_hash(void*, int64_t, int, uint64_t, int, cudaStream_t);
 cudaError_t launch_checksum(const void*, int64_t, int, uint64_t*, cudaStream_t);
 cudaError_t launch_count_equal(const void*, const void*, int64_t, unsigned long long*, cudaStream_t);
 cudaError_t launch_l2_flush(const void*, int64_t, uint64_t*, cudaStream_t);
+cudaError_t launch_gather(const void*, int, const int64_t*, int64_t, void*, cudaStream_t);
+cudaError_t launch_scatter(void*, int, const int64_t*, int64_t, const void*, cudaStream_t);
 
 static std::atomic<uint64_t> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
@@ -163,6 +165,48 @@ int gm_run_block_space(void* grid, const void* src, int64_t n, int32_t cell_byte
     return launch_cfg(&c, grid, src, tab_x, tab_y, ntab, stream);
 }
 
+int gm_run_part(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
+                int32_t flags, int32_t level, uint32_t sg_begin, uint32_t sg_end, void* stream) {
+    gm_cfg_t c{};
+    c.n = n;
+    c.rho = 1;
+    c.mapping = GM_MAP_LAMBDA;
+    c.strategy = GM_STRAT_TUNED;
+    c.kind = kind;
+    c.cell_bytes = cell_bytes;
+    c.param = param;
+    c.flags = flags & ~GM_FLAG_OMEGA_ORDER;  // partitions are digit-order ranges
+    if (int rc = check_common(n, cell_bytes, 1, kind)) return rc;
+    if (!grid) return fail(GM_EINVAL, "null grid");
+    if (kind != GM_KIND_CONST && (!src || src == grid))
+        return fail(GM_EINVAL, "neighbour kernels need a separate src snapshot");
+    const int r = log2i(n);
+    // the tuned kernels tile at 128-byte rows: a sub-gasket must hold whole tiles
+    const int64_t tile = cell_bytes <= 4 ? 128 / cell_bytes : 32;
+    if (level < 0 || (n >> level) < tile)
+        return fail(GM_EINVAL, "partition level %d too deep for n=2^%d (sub-gaskets narrower than a tile)", level, r);
+    uint64_t nsg = 1;
+    for (int i = 0; i < level; ++i) nsg *= 3;
+    if (sg_begin > sg_end || sg_end > nsg) return fail(GM_EINVAL, "sub-gasket range [%u, %u) outside [0, %llu)",
+                                                       sg_begin, sg_end, (unsigned long long)nsg);
+    gm::LaunchArgs a = make_args(&c, grid, src, nullptr, nullptr, 0, stream);
+    a.part_level = level;
+    a.sg_begin = sg_begin;
+    a.sg_end = sg_end;
+    return cuda_rc(gm::launch_tuned(a), "partition launch");
+}
+
+int gm_gather_cells(const void* grid, int32_t cell_bytes, const int64_t* idx, int64_t count, void* out, void* stream) {
+    return cuda_rc(gm::launch_gather(grid, cell_bytes, idx, count, out, reinterpret_cast<cudaStream_t>(stream)),
+                   "gather_cells");
+}
+
+int gm_scatter_cells(void* grid, int32_t cell_bytes, const int64_t* idx, int64_t count, const void* in,
+                     void* stream) {
+    return cuda_rc(gm::launch_scatter(grid, cell_bytes, idx, count, in, reinterpret_cast<cudaStream_t>(stream)),
+                   "scatter_cells");
+}
+
 int gm_map_blocks(const int64_t* wx, const int64_t* wy, int64_t count, int32_t r_b, int64_t* lx, int64_t* ly,
                   void* stream) {
     if (count < 0) return fail(GM_EINVAL, "negative count");
@@ -255,6 +299,10 @@ int gm_host_unmap(void* host) {
         return GM_OK;
     }
     return cuda_rc(e, "cudaHostUnregister");
+}
+
+int gm_set_l2_fetch_granularity(int32_t bytes) {
+    return cuda_rc(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)bytes), "cudaDeviceSetLimit");
 }
 
 uint64_t gm_launch_count(void) { return gm::g_launches.load(); }

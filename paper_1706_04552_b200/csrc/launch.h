@@ -22,7 +22,24 @@ struct LaunchArgs {
     int ntab;
     int flags;             // GM_FLAG_* (see include/gasket_b200.h)
     cudaStream_t stream;
+    // partitioned launches (tuned kernels only): restrict to level-part_level
+    // sub-gaskets [sg_begin, sg_end) in digit order; part_level < 0 = whole gasket
+    int part_level = -1;
+    uint32_t sg_begin = 0, sg_end = 0;
 };
+
+// Tile-index range [lo, hi) of a launch whose kernel tiles the gasket at level r_t.
+inline void tile_range(const LaunchArgs& a, int r_t, uint32_t& lo, uint32_t& hi) {
+    uint32_t all = 1;
+    for (int i = 0; i < r_t; ++i) all *= 3u;
+    if (a.part_level < 0 || a.part_level > r_t) { lo = 0; hi = all; return; }
+    uint32_t per = 1;
+    for (int i = 0; i < r_t - a.part_level; ++i) per *= 3u;
+    lo = a.sg_begin * per;
+    hi = a.sg_end * per;
+    if (hi > all) hi = all;
+    if (lo > hi) lo = hi;
+}
 
 void note_launch();
 

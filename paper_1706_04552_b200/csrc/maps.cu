@@ -181,6 +181,20 @@ __global__ void l2_flush_kernel(const uint4* __restrict__ buf, int64_t nvec, uns
     if (acc == 0x9E3779B9u) atomicAdd(sink, 1ull);  // practically never; keeps the loads live
 }
 
+// --- halo cells of partitioned stencils: gather / scatter by linear cell index
+template <int C>
+__global__ void gather_kernel(const uint8_t* __restrict__ grid, const int64_t* __restrict__ idx, int64_t count,
+                              uint8_t* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+        st_cell<C>(out, i, ld_cell<C>(grid, idx[i]));
+}
+template <int C>
+__global__ void scatter_kernel(uint8_t* __restrict__ grid, const int64_t* __restrict__ idx, int64_t count,
+                               const uint8_t* __restrict__ in) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+        st_cell<C>(grid, idx[i], ld_cell<C>(in, i));
+}
+
 // --- launchers (called from capi.cu) ------------------------------------------
 
 cudaError_t launch_map_blocks(const int64_t* wx, const int64_t* wy, int64_t count, int r_b, int64_t* lx, int64_t* ly,
@@ -275,6 +289,36 @@ cudaError_t launch_count_equal(const void* a, const void* b, int64_t bytes, unsi
     if (bytes == 0) return cudaSuccess;
     count_equal_kernel<<<grid_for(bytes / 16), 256, 0, s>>>(reinterpret_cast<const uint4*>(a),
                                                               reinterpret_cast<const uint4*>(b), bytes / 16, out);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather(const void* grid, int c, const int64_t* idx, int64_t count, void* out, cudaStream_t s) {
+    if (count == 0) return cudaSuccess;
+    const uint8_t* g = reinterpret_cast<const uint8_t*>(grid);
+    uint8_t* o = reinterpret_cast<uint8_t*>(out);
+    switch (c) {
+    case 1: gather_kernel<1><<<grid_for(count), 256, 0, s>>>(g, idx, count, o); break;
+    case 2: gather_kernel<2><<<grid_for(count), 256, 0, s>>>(g, idx, count, o); break;
+    case 4: gather_kernel<4><<<grid_for(count), 256, 0, s>>>(g, idx, count, o); break;
+    case 8: gather_kernel<8><<<grid_for(count), 256, 0, s>>>(g, idx, count, o); break;
+    default: return cudaErrorInvalidValue;
+    }
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scatter(void* grid, int c, const int64_t* idx, int64_t count, const void* in, cudaStream_t s) {
+    if (count == 0) return cudaSuccess;
+    uint8_t* g = reinterpret_cast<uint8_t*>(grid);
+    const uint8_t* i8 = reinterpret_cast<const uint8_t*>(in);
+    switch (c) {
+    case 1: scatter_kernel<1><<<grid_for(count), 256, 0, s>>>(g, idx, count, i8); break;
+    case 2: scatter_kernel<2><<<grid_for(count), 256, 0, s>>>(g, idx, count, i8); break;
+    case 4: scatter_kernel<4><<<grid_for(count), 256, 0, s>>>(g, idx, count, i8); break;
+    case 8: scatter_kernel<8><<<grid_for(count), 256, 0, s>>>(g, idx, count, i8); break;
+    default: return cudaErrorInvalidValue;
+    }
     note_launch();
     return cudaGetLastError();
 }

@@ -31,8 +31,8 @@ namespace gm {
 namespace {
 
 constexpr int ROWB = 128;              // tile row bytes
-constexpr int PITCH = ROWB + 32;       // smem row: 16 B left halo + row + 16 B right halo
-constexpr int THREADS = 256;
+constexpr int PITCH = ROWB + 48;       // smem row: 16 B halo + row + 16 B halo + 16 B pad (bank spread)
+constexpr int CHUNKS = (ROWB + 32) / 16;  // staged 16-byte chunks per row (halo, 8 row chunks, halo)
 
 template <int C>
 struct SG {
@@ -42,6 +42,10 @@ struct SG {
     static constexpr int NSEC = ROWB / 32;   // sectors per tile row (4)
     static constexpr int ROWS = TT + 2;      // staged rows
     static constexpr int BUF = ROWS * PITCH; // bytes per staged tile
+    // touched sectors per tile: rows come in 4 groups of SC rows whose row pattern
+    // t >> log2(SC) is 0,1,2,3 -> 1,2,2,4 touched sectors per row = 9 * SC in all
+    static constexpr int NTOUCH = 9 * SC;
+    static constexpr int THREADS = (NTOUCH + 31) / 32 * 32;  // one thread per touched sector
 };
 
 template <int C>
@@ -115,113 +119,135 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_prev() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-// Issue the staging copies of one tile (rows -1..TT, chunks 0..9 of 16 bytes).
+// Chunk (j, q) of a staged tile holds a cell some gasket cell's neighbourhood reads
+// (tile-local test; grid-boundary rows/columns are zero-filled at staging time).
 template <int C, bool EIGHT>
-__device__ __forceinline__ void stage_tile(uint8_t* buf, const uint8_t* __restrict__ src, int64_t n, int64_t x0,
-                                           int64_t y0) {
+__device__ __forceinline__ bool chunk_needed(int j, int q) {
+    using S = SG<C>;
+    const int t = j - 1;
+    if (q == 0) return EIGHT ? (row_in<C>(t - 1) || row_in<C>(t) || row_in<C>(t + 1)) : row_in<C>(t);
+    if (q == CHUNKS - 1)
+        return EIGHT ? (cell_member<C>(t - 1, S::TT - 1) || cell_member<C>(t, S::TT - 1) ||
+                        cell_member<C>(t + 1, S::TT - 1))
+                     : cell_member<C>(t, S::TT - 1);
+    return sec_needed<C, EIGHT>(t, (q - 1) >> 1);
+}
+
+// Issue the staging copies of one tile from the precomputed chunk list.
+template <int C>
+__device__ __forceinline__ void stage_tile(uint8_t* buf, const uint16_t* chunks, int nchunks,
+                                           const uint8_t* __restrict__ src, int64_t n, int64_t x0, int64_t y0) {
     using S = SG<C>;
     const int64_t rowstride = n * C;
-    constexpr int CHUNKS = PITCH / 16;  // 10
-    for (int i = threadIdx.x; i < S::ROWS * CHUNKS; i += THREADS) {
-        const int j = i / CHUNKS, q = i - j * CHUNKS;
-        const int t = j - 1;
-        const int64_t y = y0 + t;
-        const bool yin = y >= 0 && y < n;
-        bool need;
-        const uint8_t* gp;
-        if (q == 0) {  // left halo: only its last cell (x0-1) is read
-            need = EIGHT ? (row_in<C>(t - 1) || row_in<C>(t) || row_in<C>(t + 1)) : row_in<C>(t);
-            gp = src + y * rowstride + x0 * C - 16;
-            if (need && (!yin || x0 == 0)) { cp_async16(buf + j * PITCH, src, true); continue; }
-        } else if (q == CHUNKS - 1) {  // right halo: only its first cell (x0+TT) is read
-            need = EIGHT ? (cell_member<C>(t - 1, S::TT - 1) || cell_member<C>(t, S::TT - 1) ||
-                            cell_member<C>(t + 1, S::TT - 1))
-                         : cell_member<C>(t, S::TT - 1);
-            gp = src + y * rowstride + (x0 + S::TT) * C;
-            if (need && (!yin || x0 + S::TT >= n)) { cp_async16(buf + j * PITCH + q * 16, src, true); continue; }
-        } else {
-            need = sec_needed<C, EIGHT>(t, (q - 1) >> 1);
-            gp = src + y * rowstride + x0 * C + (q - 1) * 16;
-            if (need && !yin) { cp_async16(buf + j * PITCH + q * 16, src, true); continue; }
-        }
-        if (need) cp_async16(buf + j * PITCH + q * 16, gp, false);
+    for (int i = threadIdx.x; i < nchunks; i += S::THREADS) {
+        const int j = chunks[i] >> 4, q = chunks[i] & 15;
+        const int64_t y = y0 + j - 1;
+        const int64_t xb = x0 * C + (q - 1) * 16;  // byte column of the chunk
+        const bool in = y >= 0 && y < n && xb >= 0 && xb < rowstride;
+        cp_async16(buf + j * PITCH + q * 16, in ? src + y * rowstride + xb : src, !in);
     }
 }
 
 template <int C, int KIND>
-__global__ void __launch_bounds__(THREADS) stencil_tile(uint8_t* __restrict__ grid, const uint8_t* __restrict__ src,
-                                                        int64_t n, uint32_t ntiles, uint64_t param, int flags) {
+__global__ void __launch_bounds__(SG<C>::THREADS) stencil_tile(uint8_t* __restrict__ grid,
+                                                               const uint8_t* __restrict__ src, int64_t n,
+                                                               uint32_t tile_lo, uint32_t tile_hi, uint64_t param, int flags) {
     using S = SG<C>;
     constexpr bool EIGHT = KIND == KIND_NSUM8;
     extern __shared__ __align__(16) uint8_t smem[];
     uint8_t* bufs[2] = {smem, smem + S::BUF};
-    uint16_t* secs = reinterpret_cast<uint16_t*>(smem + 2 * S::BUF);  // touched (t, g) list
+    uint16_t* chunks = reinterpret_cast<uint16_t*>(smem + 2 * S::BUF);  // needed (row, chunk) list
     __shared__ uint16_t tab[243];
-    __shared__ int nsecs;
+    __shared__ int nchunks;
     digit_table_init(tab);
-    if (threadIdx.x == 0) {
-        int k = 0;
-        for (int t = 0; t < S::TT; ++t)
-            for (int g = 0; g < S::NSEC; ++g)
-                if (((g * S::SC) & ~t) == 0) secs[k++] = (uint16_t)((t << 2) | g);
-        nsecs = k;
+    if (threadIdx.x == 0) nchunks = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < S::ROWS * CHUNKS; i += S::THREADS) {
+        const int j = i / CHUNKS, q = i - j * CHUNKS;
+        if (chunk_needed<C, EIGHT>(j, q)) chunks[atomicAdd(&nchunks, 1)] = (uint16_t)((j << 4) | q);
     }
     __syncthreads();
+    const int nch = nchunks;
     const int64_t rowstride = n * C;
     const bool dst_from_src = (flags & GM_FLAG_DST_FROM_SRC) != 0;
     const uint32_t pw = C == 1 ? 0x01010101u * (uint32_t)(param & 0xffu)
                                : C == 2 ? 0x00010001u * (uint32_t)(param & 0xffffu) : (uint32_t)param;
 
-    uint32_t tile = blockIdx.x;
-    if (tile >= ntiles) return;
+    // this thread's touched sector (t, g): rows in groups of SC with 1,2,2,4 sectors each
+    const int e = threadIdx.x;
+    int h, off;
+    if (e < S::SC) { h = 0; off = 0; }
+    else if (e < 3 * S::SC) { h = 1; off = S::SC; }
+    else if (e < 5 * S::SC) { h = 2; off = 3 * S::SC; }
+    else { h = 3; off = 5 * S::SC; }
+    const int per_row = h == 0 ? 1 : h == 3 ? 4 : 2;
+    const int t = h * S::SC + (e - off) / per_row;
+    const int ii = (e - off) % per_row;
+    const int g = h == 2 ? 2 * ii : ii;
+    const bool active = e < S::NTOUCH;
+    const uint32_t tmask = member_mask<C>((uint32_t)t);
+
+    uint32_t tile = tile_lo + blockIdx.x;
+    if (tile >= tile_hi) return;
     uint32_t bx, by;
     lambda_digit_order(tile, tab, bx, by);
-    stage_tile<C, EIGHT>(bufs[0], src, n, (int64_t)bx * S::TT, (int64_t)by * S::TT);
+    stage_tile<C>(bufs[0], chunks, nch, src, n, (int64_t)bx * S::TT, (int64_t)by * S::TT);
     cp_async_commit();
     int cur = 0;
-    for (; tile < ntiles; tile += gridDim.x) {
+    for (; tile < tile_hi; tile += gridDim.x) {
         const int64_t x0 = (int64_t)bx * S::TT, y0 = (int64_t)by * S::TT;
-        // prefetch the next tile into the other buffer
         const uint32_t next = tile + gridDim.x;
         uint32_t nbx = 0, nby = 0;
-        if (next < ntiles) {
+        if (next < tile_hi) {  // prefetch the next tile into the other buffer
             lambda_digit_order(next, tab, nbx, nby);
-            stage_tile<C, EIGHT>(bufs[cur ^ 1], src, n, (int64_t)nbx * S::TT, (int64_t)nby * S::TT);
+            stage_tile<C>(bufs[cur ^ 1], chunks, nch, src, n, (int64_t)nbx * S::TT, (int64_t)nby * S::TT);
         }
         cp_async_commit();
         cp_async_wait_prev();
         __syncthreads();
 
-        const uint8_t* b = bufs[cur];
-        for (int e = threadIdx.x; e < nsecs; e += THREADS) {
-            const int t = secs[e] >> 2, g = secs[e] & 3;
+        if (active) {
+            const uint8_t* b = bufs[cur];
             const uint32_t* up = reinterpret_cast<const uint32_t*>(b + t * PITCH);  // smem row t-1
             const uint32_t* md = up + PITCH / 4;
             const uint32_t* dn = md + PITCH / 4;
             const int k0 = 4 + 8 * g;  // first word of the sector (4 halo words on the left)
+            uint32_t r[3][10];         // words k0-1 .. k0+8 of rows t-1, t, t+1
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const uint32_t* row = k == 0 ? up : k == 1 ? md : dn;
+                if (!EIGHT && k != 1) {
+                    const uint4 a = *reinterpret_cast<const uint4*>(row + k0);
+                    const uint4 c = *reinterpret_cast<const uint4*>(row + k0 + 4);
+                    r[k][1] = a.x; r[k][2] = a.y; r[k][3] = a.z; r[k][4] = a.w;
+                    r[k][5] = c.x; r[k][6] = c.y; r[k][7] = c.z; r[k][8] = c.w;
+                    r[k][0] = r[k][9] = 0;
+                    continue;
+                }
+                const uint4 a = *reinterpret_cast<const uint4*>(row + k0);
+                const uint4 c = *reinterpret_cast<const uint4*>(row + k0 + 4);
+                r[k][0] = row[k0 - 1];
+                r[k][1] = a.x; r[k][2] = a.y; r[k][3] = a.z; r[k][4] = a.w;
+                r[k][5] = c.x; r[k][6] = c.y; r[k][7] = c.z; r[k][8] = c.w;
+                r[k][9] = row[k0 + 8];
+            }
             uint32_t out[8];
-            // words k0-1 .. k0+8 of each row
-            uint32_t pu = up[k0 - 1], pm = md[k0 - 1], pd = dn[k0 - 1];
-            uint32_t cu = up[k0], cm = md[k0], cd = dn[k0];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                const uint32_t nu = up[k0 + i + 1], nm = md[k0 + i + 1], nd = dn[k0 + i + 1];
-                const int w = 8 * g + i;  // word index in the tile row
                 uint32_t s;
                 if (EIGHT) {
-                    const uint32_t A = vadd<C>(vadd<C>(pu, pm), pd);
-                    const uint32_t B = vadd<C>(vadd<C>(cu, cm), cd);
-                    const uint32_t Cc = vadd<C>(vadd<C>(nu, nm), nd);
-                    s = vadd<C>(vadd<C>(lft<C>(A, B), B), rgt<C>(B, Cc));
-                    s = vadd<C>(vsub<C>(s, cm), pw);
+                    const uint32_t A = vadd<C>(vadd<C>(r[0][i], r[1][i]), r[2][i]);
+                    const uint32_t B = vadd<C>(vadd<C>(r[0][i + 1], r[1][i + 1]), r[2][i + 1]);
+                    const uint32_t D = vadd<C>(vadd<C>(r[0][i + 2], r[1][i + 2]), r[2][i + 2]);
+                    s = vadd<C>(vadd<C>(lft<C>(A, B), B), rgt<C>(B, D));
+                    s = vadd<C>(vsub<C>(s, r[1][i + 1]), pw);
                 } else {
-                    s = vadd<C>(vadd<C>(lft<C>(pm, cm), rgt<C>(cm, nm)), vadd<C>(vadd<C>(cu, cd), pw));
+                    s = vadd<C>(vadd<C>(lft<C>(r[1][i], r[1][i + 1]), rgt<C>(r[1][i + 1], r[1][i + 2])),
+                                vadd<C>(vadd<C>(r[0][i + 1], r[2][i + 1]), pw));
                 }
-                const bool touched = ((w * S::V) & ~t) == 0;
-                const uint32_t m = touched ? member_mask<C>((uint32_t)t) : 0u;
-                out[i] = (s & m) | (cm & ~m);
-                pu = cu; pm = cm; pd = cd;
-                cu = nu; cm = nm; cd = nd;
+                const bool touched = (((8 * g + i) * S::V) & ~t) == 0;
+                const uint32_t m = touched ? tmask : 0u;
+                out[i] = (s & m) | (r[1][i + 1] & ~m);
             }
             uint8_t* gp = grid + (y0 + t) * rowstride + x0 * C + g * 32;
             if (!dst_from_src) {  // off-gasket cells from the grid itself (whole-sector write)
@@ -231,14 +257,14 @@ __global__ void __launch_bounds__(THREADS) stencil_tile(uint8_t* __restrict__ gr
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
                     const bool touched = (((8 * g + i) * S::V) & ~t) == 0;
-                    const uint32_t m = touched ? member_mask<C>((uint32_t)t) : 0u;
+                    const uint32_t m = touched ? tmask : 0u;
                     out[i] = (out[i] & m) | (old[i] & ~m);
                 }
             }
             reinterpret_cast<uint4*>(gp)[0] = make_uint4(out[0], out[1], out[2], out[3]);
             reinterpret_cast<uint4*>(gp)[1] = make_uint4(out[4], out[5], out[6], out[7]);
         }
-        __syncthreads();  // buffer `cur` is refilled two tiles from now
+        __syncthreads();  // buffer `cur` is refilled by the next iteration's prefetch
         cur ^= 1;
         bx = nbx;
         by = nby;
@@ -249,9 +275,11 @@ __global__ void __launch_bounds__(THREADS) stencil_tile(uint8_t* __restrict__ gr
 template <int C, int KIND>
 cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
     using S = SG<C>;
-    uint32_t ntiles = 1;
-    for (int i = 0; i < r_t; ++i) ntiles *= 3u;
-    const size_t smem = 2 * S::BUF + 2 * S::TT * S::NSEC + 16;
+    uint32_t lo, hi;
+    tile_range(a, r_t, lo, hi);
+    if (hi == lo) return cudaSuccess;
+    const uint32_t ntiles = hi - lo;
+    const size_t smem = 2 * S::BUF + 2 * S::ROWS * CHUNKS + 16;
     auto* kern = stencil_tile<C, KIND>;
     static bool configured = false;
     if (!configured) {
@@ -261,11 +289,11 @@ cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, S::THREADS, smem);
     uint64_t blocks = (uint64_t)sms * (per_sm > 0 ? per_sm : 1);
     if (blocks > ntiles) blocks = ntiles;
-    kern<<<(unsigned)blocks, THREADS, smem, a.stream>>>(reinterpret_cast<uint8_t*>(a.grid),
-                                                        reinterpret_cast<const uint8_t*>(a.src), a.n, ntiles, a.param,
+    kern<<<(unsigned)blocks, S::THREADS, smem, a.stream>>>(reinterpret_cast<uint8_t*>(a.grid),
+                                                        reinterpret_cast<const uint8_t*>(a.src), a.n, lo, hi, a.param,
                                                         a.flags);
     note_launch();
     return cudaGetLastError();

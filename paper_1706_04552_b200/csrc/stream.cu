@@ -135,8 +135,8 @@ __device__ __forceinline__ bool sec_needed(int t, int g) {
 
 template <int C, int KIND, int BAND, bool DIGIT_ORDER>
 __global__ void __launch_bounds__(256) lambda_stream(uint8_t* __restrict__ grid, const uint8_t* __restrict__ src,
-                                                     int64_t n, uint32_t ntiles, int band_shift, uint32_t W,
-                                                     uint64_t param, int flags) {
+                                                     int64_t n, uint32_t tile_lo, uint32_t tile_hi, int band_shift,
+                                                     uint32_t W, uint64_t param, int flags) {
     using WT = typename WordT<C>::T;
     using G = Geo<C>;
     constexpr bool EIGHT = KIND == KIND_NSUM8;
@@ -147,11 +147,12 @@ __global__ void __launch_bounds__(256) lambda_stream(uint8_t* __restrict__ grid,
     const int lane = threadIdx.x & 31;
     const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const uint64_t units = (uint64_t)ntiles << band_shift;
+    const uint64_t u_lo = (uint64_t)tile_lo << band_shift;
+    const uint64_t units = ((uint64_t)tile_hi << band_shift) - u_lo;
     // contiguous chunk of units per warp: lambda once per tile, bands of a tile in order
     const uint64_t chunk = (units + nwarps - 1) / nwarps;
-    const uint64_t u_begin = warp0 * chunk;
-    const uint64_t u_end = u_begin + chunk < units ? u_begin + chunk : units;
+    const uint64_t u_begin = u_lo + warp0 * chunk;
+    const uint64_t u_end = u_begin + chunk < u_lo + units ? u_begin + chunk : u_lo + units;
     const int64_t rowstride = n * C;  // bytes
     const int g = lane / G::LPS;      // this lane's sector in the tile row
     const int c0 = lane * G::V;       // first cell of this lane's word
@@ -314,8 +315,10 @@ __global__ void __launch_bounds__(256) lambda_stream(uint8_t* __restrict__ grid,
 template <int C, int KIND, int BAND>
 cudaError_t launch_band(const LaunchArgs& a, int r_t) {
     using G = Geo<C>;
-    uint32_t ntiles = 1;
-    for (int i = 0; i < r_t; ++i) ntiles *= 3u;
+    uint32_t lo, hi;
+    tile_range(a, r_t, lo, hi);
+    if (hi == lo) return cudaSuccess;
+    const uint32_t ntiles = hi - lo;
     int band_shift = 0;
     while ((BAND << band_shift) < G::TT) ++band_shift;
     uint32_t W = 1;
@@ -331,7 +334,7 @@ cudaError_t launch_band(const LaunchArgs& a, int r_t) {
     const uint64_t cap = (uint64_t)sms * (per_sm > 0 ? per_sm : 1);
     if (blocks > cap) blocks = cap;
     kern<<<(unsigned)blocks, 256, 0, a.stream>>>(reinterpret_cast<uint8_t*>(a.grid),
-                                                 reinterpret_cast<const uint8_t*>(a.src), a.n, ntiles, band_shift, W,
+                                                 reinterpret_cast<const uint8_t*>(a.src), a.n, lo, hi, band_shift, W,
                                                  a.param, a.flags);
     note_launch();
     return cudaGetLastError();

@@ -58,11 +58,14 @@ _SIGS = {
     "gm_l2_flush": [_vp, _i64, _vp, _vp],
     "gm_host_map": [_vp, _i64, _i32, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_int32)],
     "gm_host_unmap": [_vp],
+    "gm_set_l2_fetch_granularity": [_i32],
+    "gm_run_part": [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, ctypes.c_uint32, ctypes.c_uint32, _vp],
+    "gm_gather_cells": [_vp, _i32, _vp, _i64, _vp, _vp],
+    "gm_scatter_cells": [_vp, _i32, _vp, _i64, _vp, _vp],
 }
 
 # Every symbol include/gasket_b200.h declares (checked by tests/test_native_abi.py).
 EXPORTED = tuple(_SIGS) + ("gm_launch_count", "gm_last_error", "gm_version")
-OPTIONAL = ("gm_part_halo_plan",)
 
 
 class GasketError(RuntimeError):

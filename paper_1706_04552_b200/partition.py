@@ -1,0 +1,299 @@
+"""Multi-GPU partition of the gasket by self-similar sub-gaskets.
+
+No reference counterpart: the reference is single-process (numba ``prange``,
+backends.py:147, 162).  The level-L sub-gaskets of an edge-n gasket are the
+3**L member blocks of edge m = n >> L; in the base-3 digit order of the
+lambda map (digit i <-> level i+1) sub-gasket s is exactly the contiguous tile
+range [s * 3**(r_t-L), (s+1) * 3**(r_t-L)) of the tuned kernels, so a rank
+owning the sub-gaskets [s0, s1) launches one kernel over one tile range
+(``gm_run_part``).
+
+Write passes need no communication (lambda is a bijection: ranks write
+disjoint cells).  A neighbour-sum CA step reads a one-cell halo; because the
+reference never writes off-gasket cells (backends.py:155-156), the only halo
+cells that change are gasket cells next to another sub-gasket -- a handful of
+cells at the sub-gasket corners (at most 5 per sub-gasket for 8 neighbours,
+3 for 4).  ``PartitionPlan`` finds them exhaustively; ``HaloExchange`` moves
+them after every step with one fixed-size ``all_gather`` (NCCL on the GPU,
+gloo on CPU, or an in-process loopback for several virtual ranks on one GPU).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+import torch
+
+from .geometry import scale_level
+
+
+def subgasket_block(s: int, level: int) -> tuple[int, int]:
+    """Block coordinates of level-`level` sub-gasket s (digit i -> bit i: 0 top, 1 below, 2 below-right)."""
+    bx = by = 0
+    for i in range(level):
+        s, d = divmod(s, 3)
+        if d:
+            by |= 1 << i
+            if d == 2:
+                bx |= 1 << i
+    return bx, by
+
+
+def subgasket_index(bx: int, by: int, level: int) -> Optional[int]:
+    """Inverse of subgasket_block; None for blocks off the gasket."""
+    if bx & ~by:
+        return None
+    s = 0
+    for i in reversed(range(level)):
+        yb, xb = (by >> i) & 1, (bx >> i) & 1
+        s = s * 3 + (0 if not yb else (2 if xb else 1))
+    return s
+
+
+def rank_ranges(nsg: int, world: int) -> list[tuple[int, int]]:
+    """Contiguous, balanced sub-gasket ranges per rank."""
+    return [(r * nsg // world, (r + 1) * nsg // world) for r in range(world)]
+
+
+def _is_member(x: np.ndarray, y: np.ndarray, n: int) -> np.ndarray:
+    return (x & (n - 1 - y)) == 0
+
+
+@dataclass
+class PartitionPlan:
+    n: int
+    level: int
+    world: int
+    eight: bool = True
+    ranges: list[tuple[int, int]] = field(init=False)
+    halo: dict[int, np.ndarray] = field(init=False)  # sub-gasket -> linear indices of changing halo cells
+
+    def __post_init__(self) -> None:
+        r = scale_level(self.n)
+        if not 0 <= self.level <= r:
+            raise ValueError(f"partition level {self.level} outside [0, {r}]")
+        self.nsg = 3 ** self.level
+        self.m = self.n >> self.level
+        self.ranges = rank_ranges(self.nsg, self.world)
+        self.halo = {s: self._halo_cells(s) for s in range(self.nsg)}
+
+    # -- ownership --------------------------------------------------------
+    def owner_of_subgasket(self, s: int) -> int:
+        for rank, (lo, hi) in enumerate(self.ranges):
+            if lo <= s < hi:
+                return rank
+        raise ValueError(s)
+
+    def owner_of_cells(self, lin: np.ndarray) -> np.ndarray:
+        y, x = np.divmod(lin, self.n)
+        bx, by = x // self.m, y // self.m
+        owners = np.empty(lin.shape, dtype=np.int64)
+        for i, (a, b) in enumerate(zip(bx.tolist(), by.tolist())):
+            s = subgasket_index(a, b, self.level)
+            owners[i] = -1 if s is None else self.owner_of_subgasket(s)
+        return owners
+
+    # -- halo -------------------------------------------------------------
+    def _halo_cells(self, s: int) -> np.ndarray:
+        """Gasket cells outside sub-gasket s that a gasket cell inside s reads."""
+        n, m = self.n, self.m
+        bx, by = subgasket_block(s, self.level)
+        ox, oy = bx * m, by * m
+        ring = np.arange(-1, m + 1, dtype=np.int64)
+        xs = np.concatenate([ring, ring, np.full(m, -1), np.full(m, m)])
+        ys = np.concatenate([np.full(m + 2, -1), np.full(m + 2, m), np.arange(m), np.arange(m)])
+        gx, gy = ox + xs, oy + ys
+        ok = (gx >= 0) & (gx < n) & (gy >= 0) & (gy < n)
+        xs, ys, gx, gy = xs[ok], ys[ok], gx[ok], gy[ok]
+        ok = _is_member(gx, gy, n)
+        xs, ys, gx, gy = xs[ok], ys[ok], gx[ok], gy[ok]
+        offs = [(1, 0), (-1, 0), (0, 1), (0, -1)]
+        if self.eight:
+            offs += [(1, 1), (1, -1), (-1, 1), (-1, -1)]
+        read = np.zeros(xs.shape, dtype=bool)
+        for dx, dy in offs:
+            ix, iy = xs + dx, ys + dy
+            inside = (ix >= 0) & (ix < m) & (iy >= 0) & (iy < m)
+            read |= inside & _is_member(ox + np.clip(ix, 0, m - 1), oy + np.clip(iy, 0, m - 1), n)
+        return np.unique(gy[read] * n + gx[read])
+
+    def exchange_slots(self) -> tuple[list[np.ndarray], int]:
+        """Per owner rank, the sorted linear indices of its cells some other rank reads."""
+        need: list[set[int]] = [set() for _ in range(self.world)]
+        for s in range(self.nsg):
+            reader = self.owner_of_subgasket(s)
+            cells = self.halo[s]
+            if cells.size == 0:
+                continue
+            for c, o in zip(cells.tolist(), self.owner_of_cells(cells).tolist()):
+                if o >= 0 and o != reader:
+                    need[o].add(c)
+        slots = [np.array(sorted(v), dtype=np.int64) for v in need]
+        width = max([1] + [len(v) for v in slots])
+        return slots, width
+
+
+class LoopbackGroup:
+    """In-process stand-in for a process group: `world` virtual ranks on one device.
+
+    all_gather is called once per virtual rank; the last call completes the
+    gather for everyone (ranks are stepped in order by the driver)."""
+
+    def __init__(self, world: int) -> None:
+        self.world = world
+        self._parts: dict[int, torch.Tensor] = {}
+
+    def contribute(self, rank: int, t: torch.Tensor) -> None:
+        self._parts[rank] = t.clone()
+
+    def gathered(self) -> torch.Tensor:
+        return torch.cat([self._parts[r] for r in range(self.world)])
+
+
+class HaloExchange:
+    """Moves the changing halo cells after each step: gather own slots, one
+    fixed-size all_gather, scatter the other ranks' slots."""
+
+    def __init__(self, plan: PartitionPlan, rank: int, device: torch.device, dtype: torch.dtype,
+                 group=None, loopback: Optional[LoopbackGroup] = None) -> None:
+        self.plan, self.rank, self.device, self.dtype = plan, rank, device, dtype
+        self.group, self.loopback = group, loopback
+        slots, self.width = plan.exchange_slots()
+        self.send_idx = torch.from_numpy(slots[rank]).to(device)
+        recv = [slots[r] for r in range(plan.world)]
+        # positions in the gathered buffer and the cells they belong to (other ranks only)
+        pos, cells = [], []
+        for r, v in enumerate(recv):
+            if r == rank or v.size == 0:
+                continue
+            pos.append(r * self.width + np.arange(v.size))
+            cells.append(v)
+        self.recv_pos = torch.from_numpy(np.concatenate(pos) if pos else np.zeros(0, np.int64)).to(device)
+        self.recv_idx = torch.from_numpy(np.concatenate(cells) if cells else np.zeros(0, np.int64)).to(device)
+        self.sendbuf = torch.zeros(self.width, dtype=dtype, device=device)
+        self.gathered = torch.zeros(self.width * plan.world, dtype=dtype, device=device)
+        self.bytes_per_step = int(self.width * plan.world * self.sendbuf.element_size())
+
+    # device-side gather/scatter through the C ABI; torch indexing on CPU (gloo tests)
+    def _gather(self, grid: torch.Tensor) -> None:
+        k = self.send_idx.numel()
+        if k == 0:
+            return
+        if grid.is_cuda:
+            from . import device as dev
+            from . import native
+
+            native.call("gm_gather_cells", grid.data_ptr(), grid.element_size(), self.send_idx.data_ptr(), k,
+                        self.sendbuf.data_ptr(), dev.stream_handle())
+        else:
+            self.sendbuf[:k] = grid.view(-1)[self.send_idx]
+
+    def _scatter(self, grid: torch.Tensor) -> None:
+        k = self.recv_idx.numel()
+        if k == 0:
+            return
+        vals = self.gathered[self.recv_pos]
+        if grid.is_cuda:
+            from . import device as dev
+            from . import native
+
+            vals = vals.contiguous()
+            native.call("gm_scatter_cells", grid.data_ptr(), grid.element_size(), self.recv_idx.data_ptr(), k,
+                        vals.data_ptr(), dev.stream_handle())
+        else:
+            grid.view(-1)[self.recv_idx] = vals
+
+    def post(self, grid: torch.Tensor) -> None:
+        """Contribute this rank's halo values (loopback: before anyone completes)."""
+        self._gather(grid)
+        if self.loopback is not None:
+            self.loopback.contribute(self.rank, self.sendbuf)
+        else:
+            import torch.distributed as dist
+
+            if self.sendbuf.is_cuda:
+                dist.all_gather_into_tensor(self.gathered, self.sendbuf, group=self.group)
+            else:  # gloo: list form
+                dist.all_gather(list(self.gathered.chunk(self.plan.world)), self.sendbuf, group=self.group)
+
+    def complete(self, grid: torch.Tensor) -> None:
+        if self.loopback is not None:
+            self.gathered.copy_(self.loopback.gathered())
+        self._scatter(grid)
+
+    def exchange(self, grid: torch.Tensor) -> None:
+        self.post(grid)
+        self.complete(grid)
+
+
+StepFn = Callable[[torch.Tensor, torch.Tensor, int, int], None]
+
+
+class PartitionedCA:
+    """One rank of the partitioned CA: full-size ping-pong buffers, own sub-gaskets
+    computed by `step_fn(dst, src, sg_lo, sg_hi)` (the GPU kernel by default)."""
+
+    def __init__(self, plan: PartitionPlan, rank: int, init: torch.Tensor, kind: int, param: int = 1,
+                 group=None, loopback: Optional[LoopbackGroup] = None, step_fn: Optional[StepFn] = None) -> None:
+        self.plan, self.rank, self.kind, self.param = plan, rank, kind, param
+        self.a = init.clone()
+        self.b = init.clone()  # both buffers agree off the gasket -> whole-sector writes from src
+        self.halo = HaloExchange(plan, rank, init.device, init.dtype, group=group, loopback=loopback)
+        self.step_fn = step_fn or self._gpu_step
+        self.lo, self.hi = plan.ranges[rank]
+
+    def _gpu_step(self, dst: torch.Tensor, src: torch.Tensor, lo: int, hi: int) -> None:
+        from . import device as dev
+        from . import native
+
+        native.call("gm_run_part", dst.data_ptr(), src.data_ptr(), self.plan.n, dst.element_size(), self.kind,
+                    int(np.int32(self.param)), native.FLAG_DST_FROM_SRC, self.plan.level, lo, hi,
+                    dev.stream_handle())
+
+    def compute(self) -> None:
+        self.step_fn(self.b, self.a, self.lo, self.hi)
+
+    def finish(self) -> None:
+        self.a, self.b = self.b, self.a
+
+    def step(self) -> None:
+        """compute -> exchange halo of the new state -> swap (real process group)."""
+        self.compute()
+        self.halo.exchange(self.b)
+        self.finish()
+
+    def owned_mask(self) -> torch.Tensor:
+        """Cells of this rank's sub-gaskets (for assembling results in tests)."""
+        n, m = self.plan.n, self.plan.m
+        mask = torch.zeros((n, n), dtype=torch.bool, device=self.a.device)
+        for s in range(self.lo, self.hi):
+            bx, by = subgasket_block(s, self.plan.level)
+            mask[by * m:(by + 1) * m, bx * m:(bx + 1) * m] = True
+        return mask
+
+
+def run_loopback(plan: PartitionPlan, init: torch.Tensor, kind: int, steps: int, param: int = 1,
+                 step_fn: Optional[StepFn] = None) -> torch.Tensor:
+    """All virtual ranks on one device; returns the assembled grid after `steps`."""
+    lb = LoopbackGroup(plan.world)
+    ranks = [PartitionedCA(plan, r, init, kind, param, loopback=lb, step_fn=step_fn) for r in range(plan.world)]
+    for _ in range(steps):
+        for ca in ranks:
+            ca.compute()
+        for ca in ranks:
+            ca.halo.post(ca.b)
+        for ca in ranks:
+            ca.halo.complete(ca.b)
+        for ca in ranks:
+            ca.finish()
+    out = init.clone()
+    for ca in ranks:
+        mask = ca.owned_mask()
+        out[mask] = ca.a[mask]
+    return out
+
+
+__all__: Sequence[str] = ("subgasket_block", "subgasket_index", "rank_ranges", "PartitionPlan", "LoopbackGroup",
+                          "HaloExchange", "PartitionedCA", "run_loopback")

@@ -21,8 +21,12 @@ ncufull)
 probe)
   ./scripts/probe_stride > gpurun_out/$TAG/probe_stride.txt 2>&1; echo probe_rc=$? ;;
 variants)
-  timeout 600 python scripts/variants.py write16 stencil17 > gpurun_out/$TAG/variants.txt 2>&1; echo variants_rc=$? ;;
+  timeout 600 python scripts/variants.py ${VARIANTS:-write16 stencil17} > gpurun_out/$TAG/variants.txt 2>&1; echo variants_rc=$? ;;
 ncustencil)
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:lambda_stream -s 2 -c 1 -o gpurun_out/$TAG/prof_stencil17 python bench.py --workload stencil17 --steps 2 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1; echo ncus_rc=$? ;;
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:stencil_tile -s 2 -c 1 -o gpurun_out/$TAG/prof_stencil17 python bench.py --workload stencil17 --steps 2 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1; echo ncus_rc=$? ;;
+part)
+  timeout 900 python bench.py --workload part18 --steps 20 --warmup 3 > gpurun_out/$TAG/bench_part18.json 2> gpurun_out/$TAG/bench_part18.err; echo part_rc=$? ;;
+e2e)
+  timeout 900 python bench.py --no-sweep --no-cpu --steps 50 > gpurun_out/$TAG/bench_e2e.json 2> gpurun_out/$TAG/bench_e2e.err; echo e2e_rc=$? ;;
 esac
 done

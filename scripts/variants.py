@@ -57,6 +57,13 @@ def main():
         n = 1 << r
         src = device.fill_hash(n, torch.int8, 1, 0)
         dst = src.clone()
+        for gran in (None, 32, 64, 128):
+            if gran is not None:
+                native.call("gm_set_l2_fetch_granularity", gran)
+            fl = native.FLAG_DST_FROM_SRC
+            m, mn = timeit(lambda: backends.run_block_space(dst, src, 64, r - 6, T, kind=2, param=1, flags=fl), flush, k=10)
+            print(f"stencil r={r} nsum8 l2fetch={gran} mean {m * 1e3:8.1f} us  min {mn * 1e3:8.1f} us", flush=True)
+        native.call("gm_set_l2_fetch_granularity", 64)
         for kind in (2, 1):
             alg = R.pass_bytes(r, 1, kind)
             for name, fl in (("dst_from_src", native.FLAG_DST_FROM_SRC), ("masked", 0)):

@@ -1,0 +1,153 @@
+"""Sub-gasket partition (multi-GPU path): planner, halo sets, and the
+exchange protocol over a real process group (gloo, world_size 2, CPU) with the
+CPU oracle as the per-rank step; the CUDA kernels through the same protocol on
+one GPU with an in-process loopback group."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+from paper_1706_04552_b200 import partition as P
+
+
+def test_subgasket_block_index_roundtrip():
+    for level in range(0, 6):
+        blocks = {P.subgasket_block(s, level) for s in range(3**level)}
+        assert len(blocks) == 3**level
+        for s in range(3**level):
+            bx, by = P.subgasket_block(s, level)
+            assert bx & ~by == 0
+            assert P.subgasket_index(bx, by, level) == s
+    assert P.subgasket_index(1, 0, 3) is None
+
+
+def test_rank_ranges_balanced():
+    for nsg in (27, 243):
+        for world in (1, 2, 4, 8):
+            rr = P.rank_ranges(nsg, world)
+            assert rr[0][0] == 0 and rr[-1][1] == nsg
+            sizes = [b - a for a, b in rr]
+            assert max(sizes) - min(sizes) <= 1
+
+
+@pytest.mark.parametrize("eight", [False, True])
+def test_halo_cells_are_corner_cells(eight):
+    """At most 5 (8-nbr) / 3 (4-nbr) changing halo cells per sub-gasket, all among the
+    tile-relative candidates of SURVEY §8e."""
+    for n, level in ((1 << 8, 3), (1 << 10, 5), (1 << 9, 2)):
+        plan = P.PartitionPlan(n, level, world=4, eight=eight)
+        m = plan.m
+        cand8 = {(-1, -1), (0, -1), (1, -1), (-1, m - 1), (0, m), (m, m - 2), (m, m - 1), (m, m)}
+        cand4 = {(0, -1), (-1, m - 1), (m, m - 1), (0, m)}
+        for s in range(plan.nsg):
+            bx, by = P.subgasket_block(s, level)
+            rel = {(int(c % n) - bx * m, int(c // n) - by * m) for c in plan.halo[s]}
+            assert rel <= (cand8 if eight else cand4), (n, level, s, rel)
+            assert len(rel) <= (5 if eight else 3)
+
+
+def _oracle_step_fn(plan, kind, param):
+    import oracle
+
+    def step(dst, src, lo, hi):
+        tmp = dst.numpy().copy()
+        oracle.run_bounding_box(tmp, src.numpy(), 1, kind, param)
+        mask = np.zeros(tmp.shape, dtype=bool)
+        m = plan.m
+        for s in range(lo, hi):
+            bx, by = P.subgasket_block(s, plan.level)
+            mask[by * m:(by + 1) * m, bx * m:(bx + 1) * m] = True
+        d = dst.numpy()
+        d[mask] = tmp[mask]
+
+    return step
+
+
+def _reference_steps(init, kind, param, steps):
+    import oracle
+
+    a = init.copy()
+    for _ in range(steps):
+        b = a.copy()
+        oracle.run_bounding_box(b, a, 1, kind, param)
+        a = b
+    return a
+
+
+def test_loopback_protocol_cpu_oracle():
+    import oracle
+
+    n, level, steps = 1 << 7, 3, 5
+    init = oracle.fill_hash(n, np.int8, 3, 0)
+    want = _reference_steps(init, 2, 1, steps)
+    for world in (1, 2, 5):
+        plan = P.PartitionPlan(n, level, world, eight=True)
+        got = P.run_loopback(plan, torch.from_numpy(init), 2, steps, step_fn=_oracle_step_fn(plan, 2, 1))
+        assert np.array_equal(got.numpy(), want), world
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _gloo_worker(rank, world, port, n, level, kind, steps, out):
+    import torch.distributed as dist
+
+    import oracle
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        plan = P.PartitionPlan(n, level, world, eight=kind == 2)
+        init = oracle.fill_hash(n, np.int8, 9, 0)
+        ca = P.PartitionedCA(plan, rank, torch.from_numpy(init), kind, 1, step_fn=_oracle_step_fn(plan, kind, 1))
+        for _ in range(steps):
+            ca.step()
+        want = _reference_steps(init, kind, 1, steps)
+        mask = ca.owned_mask().numpy()
+        out[rank] = bool(np.array_equal(ca.a.numpy()[mask], want[mask]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind", [1, 2])
+def test_gloo_world2_matches_single_process(kind):
+    import torch.multiprocessing as mp
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, world, port, 1 << 7, 3, kind, 4, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+        assert p.exitcode == 0
+    assert dict(out) == {0: True, 1: True}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", [1, 2])
+def test_partition_loopback_gpu_matches_full_grid(gpu, kind):
+    """The gm_run_part kernels + halo exchange (loopback, several virtual ranks on
+    one GPU) == the unpartitioned tuned stencil, bit for bit."""
+    be = gpu.backends
+    S = gpu.geometry.IntraStrategy
+    for n, level, worlds in ((1 << 12, 3, (2, 3, 8)), (1 << 14, 5, (8,)), (1 << 10, 2, (4,))):
+        init = gpu.device.fill_hash(n, torch.int8, 5, 0)
+        a = init.clone()
+        for _ in range(4):
+            b = a.clone()
+            be.run_block_space(b, a, 64, (n // 64).bit_length() - 1, S.TUNED, kind=kind, param=1)
+            a = b
+        for world in worlds:
+            plan = P.PartitionPlan(n, level, world, eight=kind == 2)
+            got = P.run_loopback(plan, init, kind, 4)
+            assert gpu.device.count_mismatch(got, a) == 0, (n, level, world)
