@@ -375,7 +375,8 @@ def run_ours(args) -> None:
 
         plan = P.PartitionPlan(n, PART_LEVEL, world, eight=kind == 2)
         init = device.fill_hash(n, tdt, 1, 0)  # every rank holds the same initial state
-        part = P.PartitionedCA(plan, rank, init, kind, 1, group=dist.group.WORLD if world > 1 else None)
+        part = P.PartitionedCA(plan, rank, init, kind, 1, group=dist.group.WORLD if world > 1 else None,
+                               adopt_init=True)
         del init
         torch.cuda.empty_cache()
         if world == 1:

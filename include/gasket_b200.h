@@ -53,6 +53,8 @@ extern "C" {
 #define GM_FLAG_OMEGA_ORDER 1  /* tuned: visit tiles in b = wy*W + wx order */
 #define GM_FLAG_DST_FROM_SRC 2 /* stencil: grid == copy of src off-gasket (engine.py:201) */
 #define GM_FLAG_EXPLICIT_RMW 4 /* tuned write: load partial sectors, store whole sectors */
+#define GM_FLAG_WHOLE_LINES 8  /* with EXPLICIT_RMW: read-modify-write whole 128-byte tile rows */
+#define GM_FLAG_HOST_ROWS 16   /* write pass on a host-mapped grid: row-ordered whole-line schedule */
 
 #define GM_OK 0
 #define GM_EINVAL 1  /* bad shape / size / tag (the reference's ValueError) */

@@ -164,10 +164,10 @@ def _run(grid: Any, src: Any, kind: int, launch, *, mapped_ok: bool) -> None:
         src_host = np.ascontiguousarray(src) if reads_src else None
         with device.MappedHost(grid) as gptr:
             if src_host is None:
-                launch(gptr, 0, n, c, stream, native.FLAG_EXPLICIT_RMW)
+                launch(gptr, 0, n, c, stream, device.host_flags())
             else:
                 with device.MappedHost(src_host) as sptr:
-                    launch(gptr, sptr, n, c, stream, native.FLAG_EXPLICIT_RMW)
+                    launch(gptr, sptr, n, c, stream, device.host_flags())
             torch.cuda.current_stream().synchronize()
         return
 

@@ -1,0 +1,156 @@
+// hostrows.cu -- write pass over a host-mapped grid (zero-copy transport).
+//
+// Same cells and values as every other write-pass kernel (backends.py:158-222
+// with the CONST _cell_value): the gasket cells of the grid, each written once.
+// Only the schedule differs, because over PCIe the cost model changes
+// (scripts/probe_sysmem.cu): reads travel in 64-byte units, small writes are
+// TLP-rate bound, and accesses that hop to a new 4 KB host page every time run
+// at a fraction of the link rate.  So the grid is walked row by row: in row
+// y = 128*Y + y_lo the gasket's 128-byte tile lines are the lines l that are
+// bit-subsets of Y (the lambda tiles of block row Y), and every one of them has
+// the same in-line cell pattern (cells c subset of y_lo).  A work unit is one
+// row and a chunk of K consecutive member lines; consecutive units cover
+// consecutive lines of the same row, so host pages are hit K-at-a-time, and
+// every line is read once, blended and written back whole.
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "gasket.cuh"
+#include "launch.h"
+
+namespace gm {
+namespace {
+
+constexpr int K = 8;  // member lines per work unit
+
+__device__ __forceinline__ uint32_t pdep(uint32_t i, uint32_t mask) {
+    uint32_t out = 0;
+    while (mask) {
+        const uint32_t low = mask & (0u - mask);
+        if (i & 1u) out |= low;
+        i >>= 1;
+        mask ^= low;
+    }
+    return out;
+}
+
+template <int C>
+__device__ __forceinline__ uint32_t splat4(uint64_t p) {
+    if constexpr (C == 1) return 0x01010101u * (uint32_t)(p & 0xffu);
+    else if constexpr (C == 2) return 0x00010001u * (uint32_t)(p & 0xffffu);
+    else return (uint32_t)p;
+}
+
+// cells of lane word w (4 bytes) that are gasket cells in a row with in-line pattern yl
+template <int C>
+__device__ __forceinline__ uint32_t word_mask(int w, uint32_t yl) {
+    constexpr int V = 4 / C;
+    if (((uint32_t)(w * V) & ~yl) != 0) return 0u;
+    if constexpr (C == 1) {
+        const uint32_t p = yl & 3u;
+        return p == 0 ? 0x000000ffu : p == 1 ? 0x0000ffffu : p == 2 ? 0x00ff00ffu : 0xffffffffu;
+    } else if constexpr (C == 2) {
+        return (yl & 1u) ? 0xffffffffu : 0x0000ffffu;
+    } else {
+        return 0xffffffffu;
+    }
+}
+
+template <int C>
+__global__ void __launch_bounds__(256) host_rows_write(uint8_t* __restrict__ grid, int64_t n, int rbits,
+                                                       const uint64_t* __restrict__ prefix, uint32_t nY,
+                                                       uint64_t param) {
+    constexpr int TT = 128 / C;  // cells per line
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t total = prefix[nY];
+    const uint32_t pv = splat4<C>(param);
+    const int64_t rowstride = n * C;
+    for (uint64_t u = warp0; u < total; u += nwarps) {
+        // block row Y: largest Y with prefix[Y] <= u
+        uint32_t lo = 0, hi = nY;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (__ldg(prefix + mid) <= u) lo = mid; else hi = mid;
+        }
+        const uint32_t Y = lo;
+        const uint32_t lines = 1u << __popc(Y);
+        const uint32_t chunks = (lines + K - 1) / K;
+        const uint64_t rem = u - __ldg(prefix + Y);
+        const uint32_t y_lo = (uint32_t)(rem / chunks);
+        const uint32_t j = (uint32_t)(rem - (uint64_t)y_lo * chunks);
+        const int64_t y = (int64_t)Y * TT + y_lo;
+        const uint32_t m = word_mask<C>(lane, y_lo);
+        uint8_t* row = grid + y * rowstride + lane * 4;
+        const uint32_t i0 = j * K;
+        const int cnt = (int)min((uint32_t)K, lines - i0);
+        uint32_t old[K];
+        uint32_t* p[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            p[k] = reinterpret_cast<uint32_t*>(row + (int64_t)pdep(i0 + k, Y) * 128);
+            if (k < cnt && m != 0xffffffffu) old[k] = *reinterpret_cast<volatile uint32_t*>(p[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+            if (k < cnt) *p[k] = (m == 0xffffffffu) ? pv : ((pv & m) | (old[k] & ~m));
+    }
+}
+
+std::mutex g_mu;
+std::map<std::pair<int, int>, uint64_t*> g_prefix;  // (device, nYbits*1024 + rows per block row) -> table
+
+uint64_t* prefix_table(int nYbits, int rows, uint32_t& nY) {
+    nY = 1u << nYbits;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_mu);
+    const int key = nYbits * 1024 + rows;
+    auto it = g_prefix.find({dev, key});
+    if (it != g_prefix.end()) return it->second;
+    std::vector<uint64_t> pre(nY + 1, 0);
+    for (uint32_t Y = 0; Y < nY; ++Y) {
+        const uint64_t lines = 1ull << __builtin_popcount(Y);
+        pre[Y + 1] = pre[Y] + (uint64_t)((lines + K - 1) / K) * rows;  // rows per block row = tile edge
+    }
+    uint64_t* d = nullptr;
+    if (cudaMalloc(&d, pre.size() * sizeof(uint64_t)) != cudaSuccess) return nullptr;
+    cudaMemcpy(d, pre.data(), pre.size() * sizeof(uint64_t), cudaMemcpyHostToDevice);
+    g_prefix[{dev, key}] = d;
+    return d;
+}
+
+template <int C>
+cudaError_t launch_c(const LaunchArgs& a, int r) {
+    constexpr int TT = 128 / C;
+    int k = 0;
+    while ((1 << k) < TT) ++k;
+    uint32_t nY;
+    uint64_t* pre = prefix_table(r - k, TT, nY);
+    if (!pre) return cudaErrorMemoryAllocation;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    host_rows_write<C><<<sms * 8, 256, 0, a.stream>>>(reinterpret_cast<uint8_t*>(a.grid), a.n, r, pre, nY, a.param);
+    note_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+// CONST write pass on a grid at least one 128-byte line wide with 1/2/4-byte cells.
+cudaError_t launch_host_rows(const LaunchArgs& a) {
+    if (a.kind != KIND_CONST || a.part_level >= 0) return cudaErrorNotSupported;
+    int r = 0;
+    while ((int64_t(1) << r) < a.n) ++r;
+    switch (a.cell_bytes) {
+    case 1: if (a.n >= 128) return launch_c<1>(a, r); break;
+    case 2: if (a.n >= 64) return launch_c<2>(a, r); break;
+    case 4: if (a.n >= 32) return launch_c<4>(a, r); break;
+    }
+    return cudaErrorNotSupported;
+}
+
+}  // namespace gm

@@ -193,19 +193,22 @@ __global__ void __launch_bounds__(256) lambda_stream(uint8_t* __restrict__ grid,
             if (flags & GM_FLAG_EXPLICIT_RMW) {
                 // whole-sector writes: load the partial touched sectors first (all rows of
                 // the band in flight), blend the gasket cells in, store every touched sector
+                // GM_FLAG_WHOLE_LINES (host-mapped grids): move whole 128-byte rows -- PCIe
+                // reads come in 64-byte units and small writes are TLP-rate bound
+                const bool lines = (flags & GM_FLAG_WHOLE_LINES) != 0;
                 WT old[BAND];
 #pragma unroll
                 for (int i = 0; i < BAND; ++i) {
                     const int t = t0 + i;
                     const bool full = ((g * G::SC + G::SC - 1) & ~t) == 0;
-                    old[i] = (sec_touched<C>(t, g) && !full)
+                    old[i] = ((sec_touched<C>(t, g) || lines) && !full)
                                  ? *reinterpret_cast<const volatile WT*>(drow + (int64_t)i * rowstride)
                                  : WT(0);
                 }
 #pragma unroll
                 for (int i = 0; i < BAND; ++i) {
                     const int t = t0 + i;
-                    if (sec_touched<C>(t, g)) {
+                    if (sec_touched<C>(t, g) || lines) {
                         const WT m = (c0 & ~t) == 0 ? cell_mask<C>((uint32_t)t) : WT(0);
                         *reinterpret_cast<WT*>(drow + (int64_t)i * rowstride) = (pv & m) | (old[i] & ~m);
                     }

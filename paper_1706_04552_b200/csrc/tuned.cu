@@ -260,6 +260,12 @@ static cudaError_t launch_c(const LaunchArgs& a) {
 }
 
 cudaError_t launch_tuned(const LaunchArgs& a) {
+    // host-mapped grids: row-ordered whole-line schedule for the write pass (hostrows.cu)
+    if (a.flags & GM_FLAG_HOST_ROWS) {
+        const cudaError_t eh = launch_host_rows(a);
+        if (eh != cudaErrorNotSupported) return eh;
+        cudaGetLastError();
+    }
     // neighbour sums on grids at least one 128-byte tile wide: shared-memory tiles (stencil.cu)
     if (a.kind == KIND_NSUM4 || a.kind == KIND_NSUM8) {
         const cudaError_t es = launch_stencil_tile(a);

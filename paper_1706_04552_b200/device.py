@@ -35,6 +35,16 @@ _NUMPY_CELL = {
 }
 
 HOST_TRANSPORT_ENV = "GASKET_HOST_TRANSPORT"
+HOST_FLAGS_ENV = "GASKET_HOST_FLAGS"  # kernel flags for the mapped transport (tuning knob)
+
+
+def host_flags() -> int:
+    from . import native
+
+    v = os.environ.get(HOST_FLAGS_ENV)
+    if v:
+        return int(v, 0)
+    return native.FLAG_HOST_ROWS | native.FLAG_EXPLICIT_RMW | native.FLAG_WHOLE_LINES
 
 
 def require_cuda() -> None:

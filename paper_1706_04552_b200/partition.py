@@ -236,9 +236,10 @@ class PartitionedCA:
     computed by `step_fn(dst, src, sg_lo, sg_hi)` (the GPU kernel by default)."""
 
     def __init__(self, plan: PartitionPlan, rank: int, init: torch.Tensor, kind: int, param: int = 1,
-                 group=None, loopback: Optional[LoopbackGroup] = None, step_fn: Optional[StepFn] = None) -> None:
+                 group=None, loopback: Optional[LoopbackGroup] = None, step_fn: Optional[StepFn] = None,
+                 adopt_init: bool = False) -> None:
         self.plan, self.rank, self.kind, self.param = plan, rank, kind, param
-        self.a = init.clone()
+        self.a = init if adopt_init else init.clone()  # adopt: no third full-size buffer (n=2^18 int8 is 64 GiB)
         self.b = init.clone()  # both buffers agree off the gasket -> whole-sector writes from src
         self.halo = HaloExchange(plan, rank, init.device, init.dtype, group=group, loopback=loopback)
         self.step_fn = step_fn or self._gpu_step

@@ -28,5 +28,9 @@ part)
   timeout 900 python bench.py --workload part18 --steps 20 --warmup 3 > gpurun_out/$TAG/bench_part18.json 2> gpurun_out/$TAG/bench_part18.err; echo part_rc=$? ;;
 e2e)
   timeout 900 python bench.py --no-sweep --no-cpu --steps 50 > gpurun_out/$TAG/bench_e2e.json 2> gpurun_out/$TAG/bench_e2e.err; echo e2e_rc=$? ;;
+sysprobe)
+  cat /sys/kernel/mm/transparent_hugepage/enabled > gpurun_out/$TAG/probe_sysmem.txt; ./scripts/probe_sysmem >> gpurun_out/$TAG/probe_sysmem.txt 2>&1; ./scripts/probe_sysmem thp >> gpurun_out/$TAG/probe_sysmem.txt 2>&1; echo sys_rc=$? ;;
+e2evar)
+  timeout 900 python scripts/e2e_variants.py 16 > gpurun_out/$TAG/e2e_variants.txt 2>&1; echo e2evar_rc=$? ;;
 esac
 done
