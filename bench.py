@@ -299,13 +299,18 @@ def _e2e(workload: str, rho: int, steps: int) -> dict:
             call()
         dt = (time.perf_counter() - t0) / k
         if transport == "mapped":
-            # zero-copy: only the sectors the kernel touches cross PCIe -- partial gasket
-            # sectors are read, blended and written back whole; stencils also read the
-            # neighbour sectors of the snapshot
-            touched = R.write_bytes(r, c)
-            full = R.SECTOR * 3 ** (r - R._k(c)) if r >= R._k(c) else 0
-            h2d = touched - full if kind == 0 else R.stencil_read_bytes(r, c, kind == 2) + touched
-            d2h = touched
+            # zero-copy: only what the kernel touches crosses PCIe.  Write pass (row-ordered
+            # schedule): every 128-byte line holding gasket cells is read (unless all its
+            # cells are gasket cells) and written back whole.  Stencils: the neighbour
+            # sectors of the snapshot are read, touched sectors read-modified-written.
+            if kind == 0:
+                kl = (128 // c).bit_length() - 1
+                lines = (1 << kl) * 3 ** (r - kl)
+                full = 3 ** (r - kl)
+                h2d, d2h = (lines - full) * 128, lines * 128
+            else:
+                touched = R.write_bytes(r, c)
+                h2d, d2h = R.stencil_read_bytes(r, c, kind == 2) + touched, touched
         else:
             h2d = n * n * c * (1 if kind == 0 else 2)
             d2h = n * n * c
@@ -517,6 +522,60 @@ def run_reference(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+def run_nsweep(args) -> None:
+    """BASELINE config 4: n = 2^8..2^18 write pass (int8) on one B200, lambda vs BB for every
+    rho, rows in the reference CSV schema (bench.py:25-29), crossover n0 per rho."""
+    import torch
+
+    from paper_1706_04552_b200 import bench as B
+    from paper_1706_04552_b200.engine import Mapping
+    from paper_1706_04552_b200.geometry import IntraStrategy
+
+    torch.cuda.set_device(0)
+    strategies = (IntraStrategy.SUBBOX, IntraStrategy.TABLE, IntraStrategy.UNROLL, IntraStrategy.TUNED)
+    cfg = B.SweepConfig(r_min=args.r_min, r_max=args.r_max, strategies=strategies, reps=(10, 10),
+                        mappings=(Mapping.BOUNDING_BOX, Mapping.BLOCK_SPACE), dtype=torch.int8,
+                        mem_limit_bytes=100 * 2**30, time_budget_s=2.0, max_launch_s=3.0)
+    recs = B.run_sweep(cfg)
+    out = Path(args.nsweep_out)
+    out.parent.mkdir(parents=True, exist_ok=True)
+    B.write_csv(recs, out)
+    # speedup of the best lambda row over BB per (r, rho); n0 = smallest n from which it stays > 1
+    table: dict = {}
+    for rec in recs:
+        if not rec.status.startswith("ok"):
+            continue
+        row = table.setdefault(rec.rho, {}).setdefault(rec.r, {})
+        if rec.mapping == "bb":
+            row["bb"] = rec.wall_ns_mean
+        else:
+            row[rec.strategy] = rec.wall_ns_mean
+    summary = {}
+    for rho, rows in sorted(table.items()):
+        curve = {}
+        for r, row in sorted(rows.items()):
+            if "bb" not in row:
+                continue
+            lit = min(v for k, v in row.items() if k in ("subbox", "table", "unroll"))
+            curve[r] = {"paper_literal": row["bb"] / lit, "best": row["bb"] / min(v for k, v in row.items() if k != "bb")}
+        n0 = None
+        for r in sorted(curve):
+            if all(curve[q]["paper_literal"] > 1 for q in curve if q >= r):
+                n0 = 1 << r
+                break
+        summary[str(rho)] = {"n0_paper_literal": n0, "speedup_by_r": curve}
+    # best-vs-best per n
+    best = {}
+    for r in sorted({r for rows in table.values() for r in rows}):
+        bb = [rows[r]["bb"] for rows in table.values() if r in rows and "bb" in rows[r]]
+        lam = [v for rows in table.values() if r in rows for k, v in rows[r].items() if k in ("subbox", "table", "unroll")]
+        if bb and lam:
+            best[r] = min(bb) / min(lam)
+    n0_best = next((1 << r for r in sorted(best) if all(best[q] > 1 for q in best if q >= r)), None)
+    print(json.dumps({"nsweep_csv": str(out), "rows": len(recs), "per_rho": summary,
+                      "best_vs_best_paper_literal_by_r": best, "n0_best_vs_best": n0_best}), flush=True)
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -528,7 +587,14 @@ def main() -> None:
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--nsweep", action="store_true", help="BASELINE config 4: n sweep + crossover n0, CSV")
+    ap.add_argument("--r-min", type=int, default=8)
+    ap.add_argument("--r-max", type=int, default=18)
+    ap.add_argument("--nsweep-out", default="profiles/r1_nsweep.csv")
     args = ap.parse_args()
+    if args.nsweep:
+        run_nsweep(args)
+        return
     if args.impl == "reference":
         args.steps = args.steps or 10
         args.warmup = args.warmup if args.warmup is not None else 3

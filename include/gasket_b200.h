@@ -55,6 +55,8 @@ extern "C" {
 #define GM_FLAG_EXPLICIT_RMW 4 /* tuned write: load partial sectors, store whole sectors */
 #define GM_FLAG_WHOLE_LINES 8  /* with EXPLICIT_RMW: read-modify-write whole 128-byte tile rows */
 #define GM_FLAG_HOST_ROWS 16   /* write pass on a host-mapped grid: row-ordered whole-line schedule */
+#define GM_FLAG_ROWMAJOR 32    /* tuned stencil: visit tiles row-major (shared halo lines adjacent) */
+#define GM_FLAG_CHUNKED 64     /* tuned stencil: contiguous tile run per CTA instead of interleaved */
 
 #define GM_OK 0
 #define GM_EINVAL 1  /* bad shape / size / tag (the reference's ValueError) */

@@ -53,6 +53,7 @@ class SweepConfig:
     dtype: torch.dtype = torch.int32
     flush_l2: bool = True
     time_budget_s: Optional[float] = None
+    max_launch_s: Optional[float] = None  # skip rows predicted slower than this ("skipped-time")
 
 
 @dataclass
@@ -172,6 +173,8 @@ def run_sweep(cfg: SweepConfig) -> list[BenchRecord]:
     cell = torch.empty(0, dtype=cfg.dtype).element_size()
     records: list[BenchRecord] = []
     combos = _combos(cfg)
+    last_ns: dict = {}
+    last_threads: dict = {}
     for r in range(cfg.r_min, cfg.r_max + 1):
         n = 1 << r
         for rho in cfg.rho_set:
@@ -190,8 +193,19 @@ def run_sweep(cfg: SweepConfig) -> list[BenchRecord]:
             bb_mean: Optional[float] = None
             for mapping, strat in combos:
                 counts = work_counts(spec, mapping, strat)
+                key = (mapping, strat, rho)
+                if cfg.max_launch_s is not None and key in last_ns:
+                    # launch time grows with the launched threads: predict from the previous level
+                    grow = counts.threads_launched / max(1, last_threads[key])
+                    if last_ns[key] * grow > cfg.max_launch_s * 1e9:
+                        records.append(BenchRecord(mapping.value, strat.value if strat else "none", r, n, rho,
+                                                   status="skipped-time"))
+                        last_ns[key] *= grow
+                        last_threads[key] = counts.threads_launched
+                        continue
                 plan = prepare(LaunchConfig(spec=spec, mapping=mapping, strategy=strat), cfg.backend)
                 mean, stderr, used = _time_plan(plan, grid, cfg.reps, cfg.flush_l2, cfg.time_budget_s)
+                last_ns[key], last_threads[key] = mean, counts.threads_launched
                 is_bb = mapping is Mapping.BOUNDING_BOX
                 if is_bb:
                     bb_mean = mean

@@ -176,6 +176,41 @@ __device__ __forceinline__ void lambda_digit_order(uint32_t c, const uint16_t* t
     lx = two;
 }
 
+// Row-major order of the member tiles of a level-q gasket: tile k-th in the
+// row-major enumeration (block row Y ascending, then column l ascending over the
+// l that are bit-subsets of Y).  F(Y) = #member tiles in block rows < Y
+//      = sum over set bits b of Y of 3^b * 2^popcount(Y >> (b+1)).
+__device__ __forceinline__ uint32_t rows_before(uint32_t Y) {
+    uint32_t f = 0, p3 = 1, above = __popc(Y);
+    for (int b = 0; b < 20 && (Y >> b); ++b) {
+        if ((Y >> b) & 1u) {
+            --above;
+            f += p3 << above;
+        }
+        p3 *= 3u;
+    }
+    return f;
+}
+__device__ __forceinline__ uint32_t pdep32(uint32_t i, uint32_t mask) {
+    uint32_t out = 0;
+    while (mask) {
+        const uint32_t low = mask & (0u - mask);
+        if (i & 1u) out |= low;
+        i >>= 1;
+        mask ^= low;
+    }
+    return out;
+}
+__device__ __forceinline__ void tile_rowmajor(uint32_t k, int q, uint32_t& l, uint32_t& Y) {
+    uint32_t lo = 0, hi = 1u << q;  // largest Y with rows_before(Y) <= k
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (rows_before(mid) <= k) lo = mid; else hi = mid;
+    }
+    Y = lo;
+    l = pdep32(k - rows_before(lo), lo);
+}
+
 // ---------------------------------------------------------------------------
 // synthetic inputs (shared definition with oracle/gasket_oracle.c)
 // ---------------------------------------------------------------------------

@@ -18,6 +18,7 @@
 
 #include "gasket.cuh"
 #include "launch.h"
+#include "../../include/gasket_b200.h"
 
 namespace gm {
 namespace {
@@ -57,7 +58,10 @@ __device__ __forceinline__ uint32_t word_mask(int w, uint32_t yl) {
     }
 }
 
-template <int C>
+// MODE 0: whole-line read-modify-write (host-mapped grids: PCIe moves 64-byte units)
+// MODE 1: whole-sector read-modify-write of the touched sectors only (DRAM: no partial-sector fills)
+// MODE 2: byte-masked stores of the gasket cells only (the L2 merges / read-modify-writes)
+template <int C, int MODE>
 __global__ void __launch_bounds__(256) host_rows_write(uint8_t* __restrict__ grid, int64_t n, int rbits,
                                                        const uint64_t* __restrict__ prefix, uint32_t nY,
                                                        uint64_t param) {
@@ -86,16 +90,39 @@ __global__ void __launch_bounds__(256) host_rows_write(uint8_t* __restrict__ gri
         uint8_t* row = grid + y * rowstride + lane * 4;
         const uint32_t i0 = j * K;
         const int cnt = (int)min((uint32_t)K, lines - i0);
+        // sector of this lane's word holds gasket cells / is entirely gasket cells
+        constexpr int SC = 32 / C;  // cells per sector
+        const uint32_t g = (uint32_t)(lane * 4 / 32);
+        const bool sec_touched = ((g * SC) & ~y_lo) == 0;
+        const bool sec_full = ((g * SC + SC - 1) & ~y_lo) == 0;
+        bool do_load, do_store;
+        if constexpr (MODE == 0) { do_load = m != 0xffffffffu; do_store = true; }
+        else if constexpr (MODE == 1) { do_load = sec_touched && !sec_full; do_store = sec_touched; }
+        else { do_load = false; do_store = m != 0u; }
         uint32_t old[K];
         uint32_t* p[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             p[k] = reinterpret_cast<uint32_t*>(row + (int64_t)pdep(i0 + k, Y) * 128);
-            if (k < cnt && m != 0xffffffffu) old[k] = *reinterpret_cast<volatile uint32_t*>(p[k]);
+            old[k] = 0u;
+            if (k < cnt && do_load) old[k] = *reinterpret_cast<volatile uint32_t*>(p[k]);
         }
+        if constexpr (MODE == 2) {
+            // masked stores: the row's in-word pattern is uniform across the warp
 #pragma unroll
-        for (int k = 0; k < K; ++k)
-            if (k < cnt) *p[k] = (m == 0xffffffffu) ? pv : ((pv & m) | (old[k] & ~m));
+            for (int k = 0; k < K; ++k) {
+                if (k >= cnt || !do_store) continue;
+                uint8_t* b = reinterpret_cast<uint8_t*>(p[k]);
+                if (m == 0xffffffffu) *p[k] = pv;
+                else if (m == 0x0000ffffu) *reinterpret_cast<uint16_t*>(b) = (uint16_t)pv;
+                else if (m == 0x00ff00ffu) { b[0] = (uint8_t)pv; b[2] = (uint8_t)pv; }
+                else b[0] = (uint8_t)pv;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+                if (k < cnt && do_store) *p[k] = (m == 0xffffffffu) ? pv : ((pv & m) | (old[k] & ~m));
+        }
     }
 }
 
@@ -124,6 +151,7 @@ uint64_t* prefix_table(int nYbits, int rows, uint32_t& nY) {
 
 template <int C>
 cudaError_t launch_c(const LaunchArgs& a, int r) {
+    const int mode = !(a.flags & GM_FLAG_EXPLICIT_RMW) ? 2 : (a.flags & GM_FLAG_WHOLE_LINES) ? 0 : 1;
     constexpr int TT = 128 / C;
     int k = 0;
     while ((1 << k) < TT) ++k;
@@ -133,7 +161,10 @@ cudaError_t launch_c(const LaunchArgs& a, int r) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    host_rows_write<C><<<sms * 8, 256, 0, a.stream>>>(reinterpret_cast<uint8_t*>(a.grid), a.n, r, pre, nY, a.param);
+    uint8_t* g = reinterpret_cast<uint8_t*>(a.grid);
+    if (mode == 0) host_rows_write<C, 0><<<sms * 8, 256, 0, a.stream>>>(g, a.n, r, pre, nY, a.param);
+    else if (mode == 1) host_rows_write<C, 1><<<sms * 8, 256, 0, a.stream>>>(g, a.n, r, pre, nY, a.param);
+    else host_rows_write<C, 2><<<sms * 8, 256, 0, a.stream>>>(g, a.n, r, pre, nY, a.param);
     note_launch();
     return cudaGetLastError();
 }

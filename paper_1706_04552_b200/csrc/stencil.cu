@@ -151,7 +151,8 @@ __device__ __forceinline__ void stage_tile(uint8_t* buf, const uint16_t* chunks,
 template <int C, int KIND>
 __global__ void __launch_bounds__(SG<C>::THREADS) stencil_tile(uint8_t* __restrict__ grid,
                                                                const uint8_t* __restrict__ src, int64_t n,
-                                                               uint32_t tile_lo, uint32_t tile_hi, uint64_t param, int flags) {
+                                                               uint32_t tile_lo, uint32_t tile_hi, int r_t, int part_level,
+                                                               uint64_t param, int flags) {
     using S = SG<C>;
     constexpr bool EIGHT = KIND == KIND_NSUM8;
     extern __shared__ __align__(16) uint8_t smem[];
@@ -187,19 +188,46 @@ __global__ void __launch_bounds__(SG<C>::THREADS) stencil_tile(uint8_t* __restri
     const bool active = e < S::NTOUCH;
     const uint32_t tmask = member_mask<C>((uint32_t)t);
 
-    uint32_t tile = tile_lo + blockIdx.x;
-    if (tile >= tile_hi) return;
+    // Tiles in [tile_lo, tile_hi) (digit order of lambda: a range of level-L
+    // sub-gaskets).  Visiting order (flags): GM_FLAG_ROWMAJOR visits each
+    // sub-gasket's member tiles in row-major order so consecutive tiles are
+    // horizontal neighbours sharing the 128-byte halo line; GM_FLAG_CHUNKED gives
+    // every CTA a contiguous run of tiles instead of interleaving CTAs.
+    const bool rowmajor = (flags & GM_FLAG_ROWMAJOR) != 0;
+    const bool chunked = (flags & GM_FLAG_CHUNKED) != 0;
+    const int L = part_level < 0 ? 0 : part_level;
+    const int q = r_t - L;
+    uint32_t per_sg = 1;
+    for (int i = 0; i < q; ++i) per_sg *= 3u;
+    auto tile_xy = [&](uint32_t tile, uint32_t& bx, uint32_t& by) {
+        if (!rowmajor) {
+            lambda_digit_order(tile, tab, bx, by);
+            return;
+        }
+        const uint32_t sg = tile / per_sg, k = tile - sg * per_sg;
+        uint32_t sx = 0, sy = 0, l, Y;
+        if (L > 0) lambda_digit_order(sg, tab, sx, sy);
+        tile_rowmajor(k, q, l, Y);
+        bx = (sx << q) + l;
+        by = (sy << q) + Y;
+    };
+    const uint32_t span = tile_hi - tile_lo;
+    const uint32_t chunk = chunked ? (span + gridDim.x - 1) / gridDim.x : 1u;
+    const uint32_t step = chunked ? 1u : gridDim.x;
+    uint32_t tile = tile_lo + blockIdx.x * chunk;
+    const uint32_t tile_end = chunked ? min(tile_hi, tile + chunk) : tile_hi;
+    if (tile >= tile_end) return;
     uint32_t bx, by;
-    lambda_digit_order(tile, tab, bx, by);
+    tile_xy(tile, bx, by);
     stage_tile<C>(bufs[0], chunks, nch, src, n, (int64_t)bx * S::TT, (int64_t)by * S::TT);
     cp_async_commit();
     int cur = 0;
-    for (; tile < tile_hi; tile += gridDim.x) {
+    for (; tile < tile_end; tile += step) {
         const int64_t x0 = (int64_t)bx * S::TT, y0 = (int64_t)by * S::TT;
-        const uint32_t next = tile + gridDim.x;
+        const uint32_t next = tile + step;
         uint32_t nbx = 0, nby = 0;
-        if (next < tile_hi) {  // prefetch the next tile into the other buffer
-            lambda_digit_order(next, tab, nbx, nby);
+        if (next < tile_end) {  // prefetch the next tile into the other buffer
+            tile_xy(next, nbx, nby);
             stage_tile<C>(bufs[cur ^ 1], chunks, nch, src, n, (int64_t)nbx * S::TT, (int64_t)nby * S::TT);
         }
         cp_async_commit();
@@ -293,7 +321,7 @@ cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
     uint64_t blocks = (uint64_t)sms * (per_sm > 0 ? per_sm : 1);
     if (blocks > ntiles) blocks = ntiles;
     kern<<<(unsigned)blocks, S::THREADS, smem, a.stream>>>(reinterpret_cast<uint8_t*>(a.grid),
-                                                        reinterpret_cast<const uint8_t*>(a.src), a.n, lo, hi, a.param,
+                                                        reinterpret_cast<const uint8_t*>(a.src), a.n, lo, hi, r_t, a.part_level, a.param,
                                                         a.flags);
     note_launch();
     return cudaGetLastError();

@@ -20,6 +20,7 @@ KIND_CONST, KIND_NSUM4, KIND_NSUM8, KIND_COUNT = 0, 1, 2, 3
 STRAT_UNROLL, STRAT_TABLE, STRAT_SUBBOX, STRAT_TUNED = 0, 1, 2, 3
 MAP_BB, MAP_LAMBDA, MAP_BB_EXIT = 0, 1, 2
 FLAG_OMEGA_ORDER, FLAG_DST_FROM_SRC, FLAG_EXPLICIT_RMW, FLAG_WHOLE_LINES, FLAG_HOST_ROWS = 1, 2, 4, 8, 16
+FLAG_ROWMAJOR, FLAG_CHUNKED = 32, 64
 
 
 class GmCfg(ctypes.Structure):

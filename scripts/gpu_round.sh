@@ -32,5 +32,15 @@ sysprobe)
   cat /sys/kernel/mm/transparent_hugepage/enabled > gpurun_out/$TAG/probe_sysmem.txt; ./scripts/probe_sysmem >> gpurun_out/$TAG/probe_sysmem.txt 2>&1; ./scripts/probe_sysmem thp >> gpurun_out/$TAG/probe_sysmem.txt 2>&1; echo sys_rc=$? ;;
 e2evar)
   timeout 900 python scripts/e2e_variants.py 16 > gpurun_out/$TAG/e2e_variants.txt 2>&1; echo e2evar_rc=$? ;;
+profile)
+  ./scripts/probe_partial > gpurun_out/$TAG/probe_partial.txt 2>&1
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --csv --log-file gpurun_out/$TAG/probe_partial_ncu.csv ./scripts/probe_partial > /dev/null 2>&1
+  timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"lambda|stencil|l2_flush|fill_hash" -c 60 --csv --log-file gpurun_out/$TAG/launches_write16.csv python bench.py --steps 20 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1
+  timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"lambda|stencil|l2_flush|fill_hash" -c 40 --csv --log-file gpurun_out/$TAG/launches_stencil17.csv python bench.py --workload stencil17 --steps 10 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:lambda_stream -s 3 -c 1 -o gpurun_out/$TAG/prof_write16 python bench.py --steps 2 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:stencil_tile -s 2 -c 1 -o gpurun_out/$TAG/prof_stencil17 python bench.py --workload stencil17 --steps 2 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1
+  echo profile_done ;;
+nsweep)
+  timeout 1500 python bench.py --nsweep --nsweep-out gpurun_out/$TAG/nsweep.csv > gpurun_out/$TAG/nsweep.json 2> gpurun_out/$TAG/nsweep.err; echo nsweep_rc=$? ;;
 esac
 done

@@ -83,6 +83,17 @@ __global__ void k_byte_sparse(uint8_t* p, int64_t nsec) {
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nsec / 4; s += (int64_t)gridDim.x * blockDim.x)
         p[s * 128 + 5] = 7;
 }
+// 32-byte sector reads (lane pairs) at a stride of `step` sectors: DRAM fetch granularity probe
+__global__ void k_read_sparse(const uint8_t* p, int64_t nsec, int step, unsigned* sink) {
+    unsigned acc = 0;
+    const int64_t nh = (nsec / step) * 2;
+    for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < nh; h += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = (h >> 1) * step;
+        uint4 v = reinterpret_cast<const uint4*>(p + s * 32)[h & 1];
+        acc ^= v.x ^ v.w;
+    }
+    if (acc == 0x12345678u) atomicAdd(sink, 1u);
+}
 __global__ void k_flush(const uint4* p, int64_t n, unsigned* sink) {
     unsigned acc = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -110,7 +121,8 @@ int main() {
     struct T { const char* name; int id; double useful; };
     T tests[] = {{"full32", 0, 1.0}, {"full32_pair", 1, 1.0}, {"half16", 2, 0.5}, {"byte1", 3, 1.0 / 32},
                  {"u64", 4, 0.25}, {"warp_bytes8", 5, 0.25}, {"rmw16", 6, 0.5}, {"rmw32_pair", 7, 1.0},
-                 {"rmw32_pair_ilp4", 8, 1.0}, {"read", 9, 1.0}, {"byte_sparse4", 10, 1.0 / 128}};
+                 {"rmw32_pair_ilp4", 8, 1.0}, {"read", 9, 1.0}, {"byte_sparse4", 10, 1.0 / 128},
+                 {"read_every2nd_sector", 11, 0.5}, {"read_every4th_sector", 12, 0.25}};
     for (auto& t : tests) {
         for (int rep = 0; rep < 3; ++rep) {
             flush();
@@ -127,6 +139,8 @@ int main() {
             case 8: k_rmw32_pair_ilp4<<<grid, block>>>(buf, nsec * 2); break;
             case 9: k_read<<<grid, block>>>(buf, nsec * 2, sink); break;
             case 10: k_byte_sparse<<<grid, block>>>(buf, nsec); break;
+            case 11: k_read_sparse<<<grid, block>>>(buf, nsec, 2, sink); break;
+            case 12: k_read_sparse<<<grid, block>>>(buf, nsec, 4, sink); break;
             }
             cudaEventRecord(b);
             CK(cudaEventSynchronize(b));

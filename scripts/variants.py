@@ -45,8 +45,9 @@ def main():
                 continue
             g = torch.zeros((n, n), dtype=dt, device="cuda")
             alg = R.write_bytes(r, c)
+            H, E, L = native.FLAG_HOST_ROWS, native.FLAG_EXPLICIT_RMW, native.FLAG_WHOLE_LINES
             for name, fl in (("masked", 0), ("omega", native.FLAG_OMEGA_ORDER), ("rmw", native.FLAG_EXPLICIT_RMW),
-                             ("rmw+omega", native.FLAG_EXPLICIT_RMW | native.FLAG_OMEGA_ORDER)):
+                             ("rows-lines", H | E | L), ("rows-sectors", H | E), ("rows-masked", H)):
                 m, mn = timeit(lambda: backends.run_block_space(g, g, 32, r - 5, T, kind=0, param=1, flags=fl), flush)
                 print(f"write r={r} c={c} {name:10s} mean {m * 1e3:8.1f} us  min {mn * 1e3:8.1f} us  "
                       f"{3**r / (m * 1e-3) / 1e9:7.1f} Gcells/s  alg {alg / (m * 1e-3) / 1e9:6.0f} GB/s", flush=True)
@@ -57,13 +58,11 @@ def main():
         n = 1 << r
         src = device.fill_hash(n, torch.int8, 1, 0)
         dst = src.clone()
-        for gran in (None, 32, 64, 128):
-            if gran is not None:
-                native.call("gm_set_l2_fetch_granularity", gran)
-            fl = native.FLAG_DST_FROM_SRC
+        D, RM, CH = native.FLAG_DST_FROM_SRC, native.FLAG_ROWMAJOR, native.FLAG_CHUNKED
+        for name, fl in (("digit-interleaved", D), ("rowmajor-interleaved", D | RM), ("rowmajor-chunked", D | RM | CH),
+                         ("digit-chunked", D | CH)):
             m, mn = timeit(lambda: backends.run_block_space(dst, src, 64, r - 6, T, kind=2, param=1, flags=fl), flush, k=10)
-            print(f"stencil r={r} nsum8 l2fetch={gran} mean {m * 1e3:8.1f} us  min {mn * 1e3:8.1f} us", flush=True)
-        native.call("gm_set_l2_fetch_granularity", 64)
+            print(f"stencil r={r} nsum8 {name:22s} mean {m * 1e3:8.1f} us  min {mn * 1e3:8.1f} us", flush=True)
         for kind in (2, 1):
             alg = R.pass_bytes(r, 1, kind)
             for name, fl in (("dst_from_src", native.FLAG_DST_FROM_SRC), ("masked", 0)):
