@@ -57,6 +57,8 @@ extern "C" {
 #define GM_FLAG_HOST_ROWS 16   /* write pass on a host-mapped grid: row-ordered whole-line schedule */
 #define GM_FLAG_ROWMAJOR 32    /* tuned stencil: visit tiles row-major (shared halo lines adjacent) */
 #define GM_FLAG_CHUNKED 64     /* tuned stencil: contiguous tile run per CTA instead of interleaved */
+#define GM_FLAG_NO_TMA 128     /* tuned stencil: always stage tiles with cp.async */
+#define GM_FLAG_FORCE_TMA 256  /* tuned stencil: always stage tiles with TMA */
 
 #define GM_OK 0
 #define GM_EINVAL 1  /* bad shape / size / tag (the reference's ValueError) */

@@ -48,5 +48,6 @@ cudaError_t launch_tuned(const LaunchArgs& a);
 cudaError_t launch_stream(const LaunchArgs& a);
 cudaError_t launch_stencil_tile(const LaunchArgs& a);
 cudaError_t launch_host_rows(const LaunchArgs& a);
+cudaError_t launch_stencil_tma(const LaunchArgs& a);
 
 }  // namespace gm

@@ -268,6 +268,9 @@ cudaError_t launch_tuned(const LaunchArgs& a) {
     }
     // neighbour sums on grids at least one 128-byte tile wide: shared-memory tiles (stencil.cu)
     if (a.kind == KIND_NSUM4 || a.kind == KIND_NSUM8) {
+        const cudaError_t et = launch_stencil_tma(a);  // TMA-staged tiles (stencil_tma.cu)
+        if (et != cudaErrorNotSupported) return et;
+        cudaGetLastError();
         const cudaError_t es = launch_stencil_tile(a);
         if (es != cudaErrorNotSupported) return es;
         cudaGetLastError();

@@ -12,7 +12,10 @@ from pathlib import Path
 
 from . import _build
 
-LIB_PATH: Path = _build.LIB
+import os
+
+# GASKET_B200_LIB: load another build of the same ABI (A/B kernel experiments)
+LIB_PATH: Path = Path(os.environ["GASKET_B200_LIB"]) if os.environ.get("GASKET_B200_LIB") else _build.LIB
 
 GM_OK, GM_EINVAL, GM_ECUDA, GM_ENOMEM = 0, 1, 2, 3
 
@@ -20,7 +23,7 @@ KIND_CONST, KIND_NSUM4, KIND_NSUM8, KIND_COUNT = 0, 1, 2, 3
 STRAT_UNROLL, STRAT_TABLE, STRAT_SUBBOX, STRAT_TUNED = 0, 1, 2, 3
 MAP_BB, MAP_LAMBDA, MAP_BB_EXIT = 0, 1, 2
 FLAG_OMEGA_ORDER, FLAG_DST_FROM_SRC, FLAG_EXPLICIT_RMW, FLAG_WHOLE_LINES, FLAG_HOST_ROWS = 1, 2, 4, 8, 16
-FLAG_ROWMAJOR, FLAG_CHUNKED = 32, 64
+FLAG_ROWMAJOR, FLAG_CHUNKED, FLAG_NO_TMA, FLAG_FORCE_TMA = 32, 64, 128, 256
 
 
 class GmCfg(ctypes.Structure):

@@ -42,5 +42,7 @@ profile)
   echo profile_done ;;
 nsweep)
   timeout 1500 python bench.py --nsweep --nsweep-out gpurun_out/$TAG/nsweep.csv > gpurun_out/$TAG/nsweep.json 2> gpurun_out/$TAG/nsweep.err; echo nsweep_rc=$? ;;
+ab)
+  for L in ${ABLIBS:-A B A B}; do echo "== lib$L" >> gpurun_out/$TAG/ab.txt; GASKET_B200_LIB=ab/lib$L.so timeout 600 python scripts/variants.py ${VARIANTS:-stencil17} >> gpurun_out/$TAG/ab.txt 2>&1; done; echo ab_done ;;
 esac
 done

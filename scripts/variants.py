@@ -59,8 +59,9 @@ def main():
         src = device.fill_hash(n, torch.int8, 1, 0)
         dst = src.clone()
         D, RM, CH = native.FLAG_DST_FROM_SRC, native.FLAG_ROWMAJOR, native.FLAG_CHUNKED
-        for name, fl in (("digit-interleaved", D), ("rowmajor-interleaved", D | RM), ("rowmajor-chunked", D | RM | CH),
-                         ("digit-chunked", D | CH)):
+        NT = native.FLAG_NO_TMA
+        for name, fl in (("tma", D | native.FLAG_FORCE_TMA), ("cp.async", D | NT), ("masked-tma", 0),
+                         ("masked-cp.async", NT)):
             m, mn = timeit(lambda: backends.run_block_space(dst, src, 64, r - 6, T, kind=2, param=1, flags=fl), flush, k=10)
             print(f"stencil r={r} nsum8 {name:22s} mean {m * 1e3:8.1f} us  min {mn * 1e3:8.1f} us", flush=True)
         for kind in (2, 1):

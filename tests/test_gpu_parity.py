@@ -109,7 +109,7 @@ def _gpu_all(gpu, grid0, src, rho, kind, param):
         be.run_bounding_box(g, sdev, rho, kind, param, early_exit=early)
         yield ("bb-exit" if early else "bb"), g
     for strat in _strategies(gpu):
-        for flags in ((0, 1, 4, 12, 16, 32, 96) if strat.value == "tuned" else (0,)):
+        for flags in ((0, 1, 4, 12, 16, 32, 96, 128, 256) if strat.value == "tuned" else (0,)):
             g = _to_dev(grid0)
             lx, ly = be.local_cell_arrays(strat, rho)
             be.run_block_space(g, sdev, rho, r_b, strat, lx, ly, kind, param, flags=flags)
