@@ -15,6 +15,6 @@ __version__ = "0.1.0"
 def __getattr__(name):  # lazy: torch-dependent modules load on first use
     import importlib
 
-    if name in ("backends", "blockmap", "bench", "core", "device", "engine", "intra", "partition"):
+    if name in ("backends", "blockmap", "bench", "ca", "core", "device", "engine", "intra", "partition", "roofline"):
         return importlib.import_module(f".{name}", __name__)
     raise AttributeError(name)

@@ -46,8 +46,7 @@ def main():
             g = torch.zeros((n, n), dtype=dt, device="cuda")
             alg = R.write_bytes(r, c)
             H, E, L = native.FLAG_HOST_ROWS, native.FLAG_EXPLICIT_RMW, native.FLAG_WHOLE_LINES
-            for name, fl in (("masked", 0), ("omega", native.FLAG_OMEGA_ORDER), ("rmw", native.FLAG_EXPLICIT_RMW),
-                             ("rows-lines", H | E | L), ("rows-sectors", H | E), ("rows-masked", H)):
+            for name, fl in (("masked", 0), ("rmw-sectors", E), ("rmw-lines", E | L)):
                 m, mn = timeit(lambda: backends.run_block_space(g, g, 32, r - 5, T, kind=0, param=1, flags=fl), flush)
                 print(f"write r={r} c={c} {name:10s} mean {m * 1e3:8.1f} us  min {mn * 1e3:8.1f} us  "
                       f"{3**r / (m * 1e-3) / 1e9:7.1f} Gcells/s  alg {alg / (m * 1e-3) / 1e9:6.0f} GB/s", flush=True)

@@ -325,3 +325,52 @@ def test_launch_counter_moves(gpu):
     gpu.backends.run_block_space(g, g, 8, 3, gpu.geometry.IntraStrategy.TUNED)
     torch.cuda.synchronize()
     assert gpu.native.launch_count() == before + 1
+
+
+# ---------------------------------------------------------------------------
+# multi-step CA driver (ping-pong + CUDA graph) and wide cells
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("kind", [1, 2])
+def test_ca_runner_matches_oracle_steps(gpu, oracle, kind):
+    from paper_1706_04552_b200 import ca
+
+    n, steps = 512, 7
+    init = oracle.fill_hash(n, np.int8, 13, 0)
+    want = init.copy()
+    for _ in range(steps):
+        nxt = want.copy()
+        oracle.run_bounding_box(nxt, want, 1, kind, 3)
+        want = nxt
+    for use_graph in (False, True):
+        g = torch.from_numpy(init.copy()).cuda()
+        runner = ca.CARunner(g, kind=kind, param=3, use_graph=use_graph)
+        out = runner.run(3)
+        out = runner.run(4)
+        assert runner.steps_done == steps
+        assert np.array_equal(out.cpu().numpy(), want), use_graph
+    g = torch.from_numpy(init.copy()).cuda()
+    ca.run_ca(g, steps, kind=kind, param=3)
+    assert np.array_equal(g.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2])
+def test_int64_and_uint16_cells(gpu, oracle, kind):
+    for dtype in (np.int64, np.uint16):
+        for n in (64, 256):
+            grid0 = oracle.fill_hash(n, dtype, 3, 0)
+            src = oracle.fill_hash(n, dtype, 4, 0)
+            want = _oracle_result(oracle, grid0, src, 8, kind, -9)
+            for label, got in _gpu_all(gpu, grid0, src, 8, kind, -9):
+                assert np.array_equal(got.cpu().numpy(), want), (np.dtype(dtype).name, n, label)
+
+
+def test_whole_grid_tile_and_unit_grid(gpu, oracle):
+    """rho == n (one block) and n == 1 (a single cell) for every mapping."""
+    for n in (1, 2, 128):
+        for kind in KINDS:
+            grid0 = oracle.fill_hash(n, np.int8, 8, 0)
+            src = oracle.fill_hash(n, np.int8, 9, 0)
+            want = _oracle_result(oracle, grid0, src, n, kind, 5)
+            for label, got in _gpu_all(gpu, grid0, src, n, kind, 5):
+                assert np.array_equal(got.cpu().numpy(), want), (n, kind, label)
