@@ -304,10 +304,11 @@ def _e2e(workload: str, rho: int, steps: int) -> dict:
             # cells are gasket cells) and written back whole.  Stencils: the neighbour
             # sectors of the snapshot are read, touched sectors read-modified-written.
             if kind == 0:
-                kl = (128 // c).bit_length() - 1
-                lines = (1 << kl) * 3 ** (r - kl)
-                full = 3 ** (r - kl)
-                h2d, d2h = (lines - full) * 128, lines * 128
+                # 64-byte halves of 128-byte lines that hold gasket cells (halves: k = log2(64/c))
+                kh = (64 // c).bit_length() - 1
+                halves = (1 << kh) * 3 ** (r - kh)
+                full = 3 ** (r - kh)  # halves made only of gasket cells need no read
+                h2d, d2h = (halves - full) * 64, halves * 64
             else:
                 touched = R.write_bytes(r, c)
                 h2d, d2h = R.stencil_read_bytes(r, c, kind == 2) + touched, touched

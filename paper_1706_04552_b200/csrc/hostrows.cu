@@ -96,7 +96,13 @@ __global__ void __launch_bounds__(256) host_rows_write(uint8_t* __restrict__ gri
         const bool sec_touched = ((g * SC) & ~y_lo) == 0;
         const bool sec_full = ((g * SC + SC - 1) & ~y_lo) == 0;
         bool do_load, do_store;
-        if constexpr (MODE == 0) { do_load = m != 0xffffffffu; do_store = true; }
+        if constexpr (MODE == 0) {
+            // whole 64-byte halves (the PCIe read unit) of the line that hold gasket cells
+            const uint32_t half0 = (uint32_t)((lane * 4 / 64) * (64 / C));  // first cell of this lane's half
+            const bool half_touched = (half0 & ~y_lo) == 0;
+            do_load = half_touched && m != 0xffffffffu;
+            do_store = half_touched;
+        }
         else if constexpr (MODE == 1) { do_load = sec_touched && !sec_full; do_store = sec_touched; }
         else { do_load = false; do_store = m != 0u; }
         uint32_t old[K];

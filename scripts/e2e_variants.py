@@ -16,8 +16,8 @@ n = 1 << r
 host = torch.zeros((n, n), dtype=torch.int8, pin_memory=True)
 g = host.numpy()
 os.environ[device.HOST_TRANSPORT_ENV] = "mapped"
-for name, fl in (("rows", native.FLAG_HOST_ROWS), ("sectors", native.FLAG_EXPLICIT_RMW), ("lines", native.FLAG_EXPLICIT_RMW | native.FLAG_WHOLE_LINES),
-                 ("masked", 0), ("lines+omega", native.FLAG_EXPLICIT_RMW | native.FLAG_WHOLE_LINES | 1)):
+H, E, L = native.FLAG_HOST_ROWS, native.FLAG_EXPLICIT_RMW, native.FLAG_WHOLE_LINES
+for name, fl in (("rows-halves", H | E | L), ("rows-sectors", H | E), ("rows-masked", H), ("tiles-lines", E | L)):
     os.environ[device.HOST_FLAGS_ENV] = str(fl)
     backends.run_block_space(g, g, 32, r - 5, IntraStrategy.TUNED, kind=0, param=1)
     t0 = time.perf_counter()
