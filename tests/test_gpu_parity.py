@@ -133,15 +133,20 @@ def test_grids_small_exhaustive(gpu, oracle, dtype):
 
 
 @pytest.mark.parametrize("dtype", [np.int8, np.int32])
-@pytest.mark.parametrize("n", [1 << 10, 1 << 12])
+@pytest.mark.parametrize("n", [1 << 10, 1 << 12, 1 << 13])
 def test_grids_medium(gpu, oracle, dtype, n):
+    """SURVEY §4 plan: n up to 2^13 x rho in {1..32} x every mapping/strategy x kernel."""
     for kind in KINDS:
         grid0 = oracle.fill_hash(n, dtype, 5, 1)
         src = oracle.fill_hash(n, dtype, 6, 0)
         want = _oracle_result(oracle, grid0, src, 8, kind, 7)
-        for rho in (1, 8, 32, 128):
+        ck = oracle.checksum(want)
+        for rho in (1, 2, 4, 8, 16, 32, 128):
             for label, got in _gpu_all(gpu, grid0, src, rho, kind, 7):
-                assert np.array_equal(got.cpu().numpy(), want), (n, rho, kind, label)
+                if n <= 1 << 10:
+                    assert np.array_equal(got.cpu().numpy(), want), (n, rho, kind, label)
+                else:
+                    assert gpu.device.checksum(got) == ck, (n, rho, kind, label)
 
 
 def test_golden_kernel_checksums_on_device(gpu, oracle, golden):
@@ -183,6 +188,23 @@ def test_n16_int8_vs_oracle_checksum(gpu, oracle, kind):
         assert gpu.device.checksum(g) == ck, (rho, strat, kind)
     g.copy_(src)
     gpu.backends.run_bounding_box(g, src, 32, kind, 1, early_exit=True)
+    assert gpu.device.checksum(g) == ck
+
+
+def test_n16_int32_nsum4_vs_oracle(gpu, oracle):
+    """full grid at n=2^16 int32 (16 GiB per host grid) -- checksum vs the oracle."""
+    n = 1 << 16
+    src_np = oracle.fill_hash(n, np.int32, 21, 0)
+    want = src_np.copy()
+    oracle.run_block_space(want, src_np, 16, 12, oracle.STRAT_SUBBOX, None, None, 1, 1)
+    ck = oracle.checksum(want)
+    del want, src_np
+    src = gpu.device.fill_hash(n, torch.int32, 21, 0)
+    g = src.clone()
+    gpu.backends.run_block_space(g, src, 16, 12, gpu.geometry.IntraStrategy.TUNED, kind=1, param=1)
+    assert gpu.device.checksum(g) == ck
+    g.copy_(src)
+    gpu.backends.run_block_space(g, src, 16, 12, gpu.geometry.IntraStrategy.TUNED, kind=1, param=1, flags=2)
     assert gpu.device.checksum(g) == ck
 
 

@@ -129,3 +129,17 @@ def test_coverage_counts_golden(oracle, golden):
         lx, ly = oracle.local_cells(STRATS[row["strategy"]], rho)
         counts = oracle.coverage_counts(bx, by, lx, ly, rho, n)
         assert oracle.checksum(counts) == row["counts"]
+
+
+def test_mutations_break_elementwise_lambda(oracle):
+    """SURVEY §4 blind spot: 'parity' survives verify_bijection at even r_b, but
+    every corrupted map differs from lambda element-wise at every r_b >= 1."""
+    from paper_1706_04552_b200.geometry import corrupted_map_fn, packing_dims
+
+    for defect in ("parity", "divisor", "offset"):
+        fn = corrupted_map_fn(defect)
+        for r_b in range(1, 8):
+            w, h = packing_dims(r_b)
+            lx, ly = oracle.map_rectangle(r_b)
+            got = [fn((b % w, b // w), r_b).coord for b in range(w * h)]
+            assert any((gx, gy) != (int(x), int(y)) for (gx, gy), x, y in zip(got, lx, ly)), (defect, r_b)
