@@ -55,10 +55,18 @@ extern "C" {
 #define GM_FLAG_EXPLICIT_RMW 4 /* tuned write: load partial sectors, store whole sectors */
 #define GM_FLAG_WHOLE_LINES 8  /* with EXPLICIT_RMW: read-modify-write whole 128-byte tile rows */
 #define GM_FLAG_HOST_ROWS 16   /* write pass on a host-mapped grid: row-ordered whole-line schedule */
-#define GM_FLAG_ROWMAJOR 32    /* tuned stencil: visit tiles row-major (shared halo lines adjacent) */
+#define GM_FLAG_ROWMAJOR 32    /* tuned: visit tiles row-major per sub-gasket (the default since v2; kept for ABI) */
 #define GM_FLAG_CHUNKED 64     /* tuned stencil: contiguous tile run per CTA instead of interleaved */
 #define GM_FLAG_NO_TMA 128     /* tuned stencil: always stage tiles with cp.async */
 #define GM_FLAG_FORCE_TMA 256  /* tuned stencil: always stage tiles with TMA */
+#define GM_FLAG_FETCH_LINE 512 /* tuned kernels: loads without the .L2::64B fetch-size hint (whole 128-byte lines) */
+#define GM_FLAG_FETCH64 1024   /* tuned write: touch each written 64-byte half with an .L2::64B load first */
+#define GM_FLAG_STENCIL_V1 2048 /* tuned stencil: the v1 kernel (stencil.cu) instead of v2 (stencil2.cu) */
+#define GM_FLAG_STAGES2 4096   /* tuned stencil v2: 2-deep staging ring instead of 3/4 */
+#define GM_FLAG_PROBE_NOSTORE 8192  /* design probe, stencil v2: stage tiles but store nothing (result undefined) */
+#define GM_FLAG_PROBE_NOLOAD 16384  /* design probe, stencil v2: store sectors without staging (result undefined) */
+#define GM_FLAG_PROBE_NOCOMPUTE 32768 /* design probe, stencil v2: stage + store, no arithmetic (result undefined) */
+#define GM_FLAG_DIGIT_ORDER 65536 /* tuned: visit tiles in lambda digit order instead of row-major per sub-gasket */
 
 #define GM_OK 0
 #define GM_EINVAL 1  /* bad shape / size / tag (the reference's ValueError) */

@@ -104,16 +104,27 @@ __device__ __forceinline__ bool sec_needed(int t, int g) {
     return need;
 }
 
-__device__ __forceinline__ uint4 ld_cg16(const void* p) {
+__device__ __forceinline__ uint4 ld_cg16(const void* p, bool line) {
     uint4 v;
-    asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    if (line)
+        asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    else
+        asm volatile("ld.global.cg.L2::64B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
     return v;
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool zero_fill) {
+// An L2 miss of a plain load or cp.async fetches the whole 128-byte line from DRAM;
+// with the .L2::64B fetch-size hint only the 64-byte half holding the chunk comes in
+// (scripts/probe_fetch.cu: half the DRAM bytes, same per-line rate).
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool zero_fill, bool line) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     const int src_bytes = zero_fill ? 0 : 16;
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
+    if (line)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
+    else
+        asm volatile("cp.async.cg.shared.global.L2::64B [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(src_bytes)
+                     : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_prev() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
@@ -136,7 +147,8 @@ __device__ __forceinline__ bool chunk_needed(int j, int q) {
 // Issue the staging copies of one tile from the precomputed chunk list.
 template <int C>
 __device__ __forceinline__ void stage_tile(uint8_t* buf, const uint16_t* chunks, int nchunks,
-                                           const uint8_t* __restrict__ src, int64_t n, int64_t x0, int64_t y0) {
+                                           const uint8_t* __restrict__ src, int64_t n, int64_t x0, int64_t y0,
+                                           bool line) {
     using S = SG<C>;
     const int64_t rowstride = n * C;
     for (int i = threadIdx.x; i < nchunks; i += S::THREADS) {
@@ -144,7 +156,7 @@ __device__ __forceinline__ void stage_tile(uint8_t* buf, const uint16_t* chunks,
         const int64_t y = y0 + j - 1;
         const int64_t xb = x0 * C + (q - 1) * 16;  // byte column of the chunk
         const bool in = y >= 0 && y < n && xb >= 0 && xb < rowstride;
-        cp_async16(buf + j * PITCH + q * 16, in ? src + y * rowstride + xb : src, !in);
+        cp_async16(buf + j * PITCH + q * 16, in ? src + y * rowstride + xb : src, !in, line);
     }
 }
 
@@ -171,6 +183,7 @@ __global__ void __launch_bounds__(SG<C>::THREADS) stencil_tile(uint8_t* __restri
     const int nch = nchunks;
     const int64_t rowstride = n * C;
     const bool dst_from_src = (flags & GM_FLAG_DST_FROM_SRC) != 0;
+    const bool fetch_line = (flags & GM_FLAG_FETCH_LINE) != 0;
     const uint32_t pw = C == 1 ? 0x01010101u * (uint32_t)(param & 0xffu)
                                : C == 2 ? 0x00010001u * (uint32_t)(param & 0xffffu) : (uint32_t)param;
 
@@ -219,7 +232,7 @@ __global__ void __launch_bounds__(SG<C>::THREADS) stencil_tile(uint8_t* __restri
     if (tile >= tile_end) return;
     uint32_t bx, by;
     tile_xy(tile, bx, by);
-    stage_tile<C>(bufs[0], chunks, nch, src, n, (int64_t)bx * S::TT, (int64_t)by * S::TT);
+    stage_tile<C>(bufs[0], chunks, nch, src, n, (int64_t)bx * S::TT, (int64_t)by * S::TT, fetch_line);
     cp_async_commit();
     int cur = 0;
     for (; tile < tile_end; tile += step) {
@@ -228,7 +241,7 @@ __global__ void __launch_bounds__(SG<C>::THREADS) stencil_tile(uint8_t* __restri
         uint32_t nbx = 0, nby = 0;
         if (next < tile_end) {  // prefetch the next tile into the other buffer
             tile_xy(next, nbx, nby);
-            stage_tile<C>(bufs[cur ^ 1], chunks, nch, src, n, (int64_t)nbx * S::TT, (int64_t)nby * S::TT);
+            stage_tile<C>(bufs[cur ^ 1], chunks, nch, src, n, (int64_t)nbx * S::TT, (int64_t)nby * S::TT, fetch_line);
         }
         cp_async_commit();
         cp_async_wait_prev();
@@ -279,8 +292,8 @@ __global__ void __launch_bounds__(SG<C>::THREADS) stencil_tile(uint8_t* __restri
             }
             uint8_t* gp = grid + (y0 + t) * rowstride + x0 * C + g * 32;
             if (!dst_from_src) {  // off-gasket cells from the grid itself (whole-sector write)
-                const uint4 o0 = ld_cg16(gp);
-                const uint4 o1 = ld_cg16(gp + 16);
+                const uint4 o0 = ld_cg16(gp, fetch_line);
+                const uint4 o1 = ld_cg16(gp + 16, fetch_line);
                 const uint32_t old[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {

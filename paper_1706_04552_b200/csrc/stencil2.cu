@@ -1,0 +1,491 @@
+// stencil2.cu -- tuned lambda neighbour-sum kernel, v2 (strategy STRAT_TUNED,
+// KIND_NSUM4 / KIND_NSUM8, cells of 1, 2 or 4 bytes).  Default stencil path;
+// GM_FLAG_STENCIL_V1 selects the v1 kernel in stencil.cu for A/B runs.
+//
+// Same decomposition and DRAM rules as v1 (stencil.cu): one CTA per lambda
+// tile of TT x TT cells whose rows are one 128-byte line, only the 16-byte
+// chunks some gasket cell's neighbourhood reads are staged (cp.async with the
+// .L2::64B fetch-size hint), one thread per touched 32-byte sector, every
+// touched sector stored whole.  What changed, from the ncu profile of v1
+// (issue-bound at 54% issue slots, barrier + scoreboard stalls, DRAM 53%):
+//
+//  * arithmetic in split lanes.  Byte cells are spread into two 16-bit-lane
+//    words with one PRMT each (even cells, odd cells); a 9-cell sum of bytes
+//    never carries out of its 16-bit lane, so plain IADD3s replace the
+//    emulated __vadd4 (5+ instructions each).  Neighbours one cell left/right
+//    are one funnel shift of the other parity's word.  2-byte cells use 32-bit
+//    lanes the same way; 4-byte cells are plain 32-bit words.  One PRMT packs
+//    the result back.  About 16 instructions per 4-byte word instead of ~40.
+//  * an NST-stage cp.async ring with a single barrier per tile: tile i+NST-1
+//    is issued right after the barrier that ends tile i-1's compute, so
+//    NST-1 tiles per CTA are in flight (v1: one, plus a second barrier).
+//  * the chunk list holds the shared-memory offset of every needed chunk;
+//    interior tiles skip all bounds tests (edge tiles zero-fill as before).
+//  * each touched sector leaves as one 256-bit store (st.global.v8.b32).
+//
+// Semantics: backends.py:127-141 (_cell_value NEIGHBOR_SUM: param + in-grid
+// 4-neighbours, out-of-grid = 0, result wraps to the cell width) and our
+// labelled 8-neighbour extension; only gasket cells change.
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <vector>
+
+#include "gasket.cuh"
+#include "launch.h"
+#include "../../include/gasket_b200.h"
+
+namespace gm {
+namespace {
+
+constexpr int ROWB = 128;                 // tile row bytes (one line)
+constexpr int PITCH = ROWB + 48;          // smem row: 16 B halo | 128 B row | 16 B halo | 16 B pad
+constexpr int CHUNKS = (ROWB + 32) / 16;  // 10 staged 16-byte chunks per row
+
+template <int C>
+struct T2 {
+    static constexpr int V = 4 / C;           // cells per 4-byte word
+    static constexpr int TT = ROWB / C;       // tile edge (cells)
+    static constexpr int SC = 32 / C;         // cells per sector
+    static constexpr int NSEC = ROWB / 32;    // sectors per tile row
+    static constexpr int ROWS = TT + 2;       // staged rows (-1 .. TT)
+    static constexpr int BUF = ROWS * PITCH;  // bytes per staged tile
+    static constexpr int NTOUCH = 9 * SC;     // touched sectors per tile (1,2,2,4 per row group)
+    static constexpr int THREADS = (NTOUCH + 31) / 32 * 32;
+};
+
+__device__ __forceinline__ bool row_in(int t, int tt) { return t >= 0 && t < tt; }
+
+template <int C>
+__device__ __forceinline__ bool sec_touched(int t, int g) {
+    return row_in(t, T2<C>::TT) && g >= 0 && g < T2<C>::NSEC && ((g * T2<C>::SC) & ~t) == 0;
+}
+template <int C>
+__device__ __forceinline__ bool cell_member(int t, int c) {
+    return row_in(t, T2<C>::TT) && c >= 0 && c < T2<C>::TT && (c & ~t) == 0;
+}
+// sector g of staged tile row t is read by some gasket cell's neighbourhood
+template <int C, bool EIGHT>
+__device__ __forceinline__ bool sec_needed(int t, int g) {
+    constexpr int SC = T2<C>::SC;
+    bool need = sec_touched<C>(t - 1, g) || sec_touched<C>(t, g) || sec_touched<C>(t + 1, g);
+    need = need || sec_touched<C>(t, g + 1) || cell_member<C>(t, g * SC - 1);
+    if (EIGHT) {
+        need = need || sec_touched<C>(t - 1, g + 1) || sec_touched<C>(t + 1, g + 1);
+        need = need || cell_member<C>(t - 1, g * SC - 1) || cell_member<C>(t + 1, g * SC - 1);
+    }
+    return need;
+}
+// chunk q of staged row j (j = tile row + 1; q = 0 left halo, 1..8 row, 9 right halo)
+template <int C, bool EIGHT>
+__device__ __forceinline__ bool chunk_needed(int j, int q) {
+    constexpr int TT = T2<C>::TT;
+    const int t = j - 1;
+    if (q == 0) return EIGHT ? (row_in(t - 1, TT) || row_in(t, TT) || row_in(t + 1, TT)) : row_in(t, TT);
+    if (q == CHUNKS - 1)
+        return EIGHT ? (cell_member<C>(t - 1, TT - 1) || cell_member<C>(t, TT - 1) || cell_member<C>(t + 1, TT - 1))
+                     : cell_member<C>(t, TT - 1);
+    return sec_needed<C, EIGHT>(t, (q - 1) >> 1);
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t smem, const void* gmem, int src_bytes, bool line) {
+    if (line)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem), "l"(gmem), "r"(src_bytes) : "memory");
+    else
+        asm volatile("cp.async.cg.shared.global.L2::64B [%0], [%1], 16, %2;" ::"r"(smem), "l"(gmem), "r"(src_bytes)
+                     : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ void ld_sector(const uint8_t* p, bool line, bool v8, uint32_t (&v)[8]) {
+    if (!v8) {
+        const uint4 a = __ldcg(reinterpret_cast<const uint4*>(p));
+        const uint4 b = __ldcg(reinterpret_cast<const uint4*>(p) + 1);
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else if (line)
+        asm volatile("ld.global.cg.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                     : "l"(p));
+    else
+        asm volatile("ld.global.cg.L2::64B.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                     : "l"(p));
+}
+// one 256-bit store when the grid is 32-byte aligned (device allocations),
+// else two 16-byte stores (e.g. a page-locked numpy array mapped over PCIe)
+__device__ __forceinline__ void st_sector(uint8_t* p, const uint32_t (&v)[8], bool v8) {
+    if (v8) {
+        asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),
+                     "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                     : "memory");
+    } else {
+        reinterpret_cast<uint4*>(p)[0] = make_uint4(v[0], v[1], v[2], v[3]);
+        reinterpret_cast<uint4*>(p)[1] = make_uint4(v[4], v[5], v[6], v[7]);
+    }
+}
+
+// ---- split-lane arithmetic --------------------------------------------------
+// even(w)/odd(w): the word's even/odd cells, each in its own lane wide enough
+// that sums of up to 9 cells never carry into the next lane.
+template <int C>
+__device__ __forceinline__ uint32_t even_cells(uint32_t w) {
+    if constexpr (C == 1) return __byte_perm(w, 0u, 0x4240);  // bytes 0,2 -> 16-bit lanes
+    else return w & 0xffffu;                                  // C == 2: cell 0 -> 32-bit lane
+}
+template <int C>
+__device__ __forceinline__ uint32_t odd_cells(uint32_t w) {
+    if constexpr (C == 1) return __byte_perm(w, 0u, 0x4341);  // bytes 1,3 -> 16-bit lanes
+    else return w >> 16;
+}
+// lanes shifted one cell pair: lane i <- lane i-1 (lane 0 from the previous word)
+template <int C>
+__device__ __forceinline__ uint32_t lane_up(uint32_t prev, uint32_t cur) {
+    if constexpr (C == 1) return __funnelshift_l(prev, cur, 16);
+    else return prev;
+}
+// lane i <- lane i+1 (last lane from the next word)
+template <int C>
+__device__ __forceinline__ uint32_t lane_dn(uint32_t cur, uint32_t next) {
+    if constexpr (C == 1) return __funnelshift_r(cur, next, 16);
+    else return next;
+}
+template <int C>
+__device__ __forceinline__ uint32_t pack_cells(uint32_t e, uint32_t o) {
+    if constexpr (C == 1) return __byte_perm(e, o, 0x6240);
+    else return __byte_perm(e, o, 0x5410);
+}
+// gasket cells of a word of tile row t (cell j member iff j subset of t & (V-1))
+template <int C>
+__device__ __forceinline__ uint32_t member_mask(uint32_t t) {
+    if constexpr (C == 1) {
+        const uint32_t p = t & 3u;
+        return p == 0 ? 0x000000ffu : p == 1 ? 0x0000ffffu : p == 2 ? 0x00ff00ffu : 0xffffffffu;
+    } else if constexpr (C == 2) {
+        return (t & 1u) ? 0xffffffffu : 0x0000ffffu;
+    } else {
+        return 0xffffffffu;
+    }
+}
+
+// The 8 result words of sector (t, g) from the staged rows (w[r][p] = word k0-1+p
+// of rows t-1, t, t+1).
+template <int C, bool EIGHT>
+__device__ __forceinline__ void sector_sums(const uint32_t (&w)[3][10], uint32_t pv, uint32_t (&out)[8]) {
+    if constexpr (C == 4) {
+        if constexpr (EIGHT) {
+            uint32_t s[10];
+#pragma unroll
+            for (int p = 0; p < 10; ++p) s[p] = w[0][p] + w[1][p] + w[2][p];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) out[i] = s[i] + s[i + 1] + s[i + 2] - w[1][i + 1] + pv;
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) out[i] = w[1][i] + w[1][i + 2] + w[0][i + 1] + w[2][i + 1] + pv;
+        }
+    } else {
+        if constexpr (EIGHT) {
+            uint32_t ce[10], co[10];
+#pragma unroll
+            for (int p = 0; p < 10; ++p) {
+                ce[p] = even_cells<C>(w[0][p]) + even_cells<C>(w[1][p]) + even_cells<C>(w[2][p]);
+                co[p] = odd_cells<C>(w[0][p]) + odd_cells<C>(w[1][p]) + odd_cells<C>(w[2][p]);
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int p = i + 1;
+                const uint32_t both = ce[p] + co[p];
+                // box sum minus the centre plus param; the centre is part of the box, so no borrow
+                const uint32_t re = both + lane_up<C>(co[p - 1], co[p]) - even_cells<C>(w[1][p]) + pv;
+                const uint32_t ro = both + lane_dn<C>(ce[p], ce[p + 1]) - odd_cells<C>(w[1][p]) + pv;
+                out[i] = pack_cells<C>(re, ro);
+            }
+        } else {
+            uint32_t em[10], om[10];
+#pragma unroll
+            for (int p = 0; p < 10; ++p) {
+                em[p] = even_cells<C>(w[1][p]);
+                om[p] = odd_cells<C>(w[1][p]);
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int p = i + 1;
+                const uint32_t re = even_cells<C>(w[0][p]) + even_cells<C>(w[2][p]) + om[p] + lane_up<C>(om[p - 1], om[p]) + pv;
+                const uint32_t ro = odd_cells<C>(w[0][p]) + odd_cells<C>(w[2][p]) + em[p] + lane_dn<C>(em[p], em[p + 1]) + pv;
+                out[i] = pack_cells<C>(re, ro);
+            }
+        }
+    }
+}
+
+template <int C, int KIND, int NST>
+__global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict__ grid, const uint8_t* __restrict__ src,
+                                                             int64_t n, uint32_t tile_lo, uint32_t tile_hi, int r_t,
+                                                             int part_level, uint64_t param, int flags,
+                                                             const uint32_t* __restrict__ order) {
+    using S = T2<C>;
+    constexpr bool EIGHT = KIND == KIND_NSUM8;
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint32_t* chunks = reinterpret_cast<uint32_t*>(smem + NST * S::BUF);  // needed chunks: smem off | j << 16 | q << 24
+    __shared__ uint16_t tab[243];
+    __shared__ int nchunks;
+    digit_table_init(tab);
+    // row-major list (consecutive threads stage consecutive chunks of one row)
+    if (threadIdx.x < 32) {
+        int cnt = 0;
+        for (int base = 0; base < S::ROWS * CHUNKS; base += 32) {
+            const int i = base + threadIdx.x;
+            const int j = i / CHUNKS, q = i - j * CHUNKS;
+            const bool need = i < S::ROWS * CHUNKS && chunk_needed<C, EIGHT>(j, q);
+            const unsigned m = __ballot_sync(0xffffffffu, need);
+            if (need)
+                chunks[cnt + __popc(m & ((1u << threadIdx.x) - 1u))] =
+                    (uint32_t)(j * PITCH + q * 16) | ((uint32_t)j << 16) | ((uint32_t)q << 24);
+            cnt += __popc(m);
+        }
+        if (threadIdx.x == 0) nchunks = cnt;
+    }
+    __syncthreads();
+    const int nch = nchunks;
+    const int64_t rowstride = n * C;
+    const bool dst_from_src = (flags & GM_FLAG_DST_FROM_SRC) != 0;
+    const bool fetch_line = (flags & GM_FLAG_FETCH_LINE) != 0;
+    const bool v8 = (reinterpret_cast<uintptr_t>(grid) & 31u) == 0;
+    const bool probe_nostore = (flags & GM_FLAG_PROBE_NOSTORE) != 0;
+    const bool probe_noload = (flags & GM_FLAG_PROBE_NOLOAD) != 0;
+    const bool probe_nocompute = (flags & GM_FLAG_PROBE_NOCOMPUTE) != 0;
+    const uint32_t smem0 = (uint32_t)__cvta_generic_to_shared(smem);
+    uint32_t pv;
+    if constexpr (C == 1) pv = 0x00010001u * (uint32_t)(param & 0xffu);
+    else if constexpr (C == 2) pv = (uint32_t)(param & 0xffffu);
+    else pv = (uint32_t)param;
+
+    // this thread's touched sector (t, g): row groups of SC rows with 1,2,2,4 sectors
+    const int e = threadIdx.x;
+    int h, off;
+    if (e < S::SC) { h = 0; off = 0; }
+    else if (e < 3 * S::SC) { h = 1; off = S::SC; }
+    else if (e < 5 * S::SC) { h = 2; off = 3 * S::SC; }
+    else { h = 3; off = 5 * S::SC; }
+    const int per_row = h == 0 ? 1 : h == 3 ? 4 : 2;
+    const int t = h * S::SC + (e - off) / per_row;
+    const int ii = (e - off) % per_row;
+    const int g = h == 2 ? 2 * ii : ii;
+    const bool active = e < S::NTOUCH;
+    const uint32_t tmask = member_mask<C>((uint32_t)t);
+    uint32_t wmask[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) wmask[i] = (((8 * g + i) * S::V) & ~t) == 0 ? tmask : 0u;
+
+    // tile visiting order: lambda digit order, or (GM_FLAG_ROWMAJOR) the precomputed
+    // table `order` = member tiles row-major within each level-L sub-gasket, so that
+    // concurrently running CTAs stage horizontally adjacent tiles (same DRAM pages)
+    const bool chunked = (flags & GM_FLAG_CHUNKED) != 0;
+    auto tile_xy = [&](uint32_t tile, uint32_t& bx, uint32_t& by) {
+        if (order == nullptr) {
+            lambda_digit_order(tile, tab, bx, by);
+        } else {
+            const uint32_t v = __ldg(order + tile);
+            bx = v & 0xffffu;
+            by = v >> 16;
+        }
+    };
+    const uint32_t span = tile_hi - tile_lo;
+    const uint32_t chunk = chunked ? (span + gridDim.x - 1) / gridDim.x : 1u;
+    const uint32_t step = chunked ? 1u : gridDim.x;
+    const uint32_t first = tile_lo + blockIdx.x * chunk;
+    const uint32_t last = chunked ? min(tile_hi, first + chunk) : tile_hi;  // exclusive
+    if (first >= last) return;
+    const uint32_t count = (last - first + step - 1) / step;
+
+    auto stage = [&](uint32_t idx) {  // stage this CTA's tile #idx into ring slot idx % NST
+        if (idx >= count || probe_noload) return;
+        uint32_t bx, by;
+        tile_xy(first + idx * step, bx, by);
+        const int64_t x0 = (int64_t)bx * S::TT, y0 = (int64_t)by * S::TT;
+        const uint32_t sb = smem0 + (idx % NST) * S::BUF;
+        const uint8_t* base = src + (y0 - 1) * rowstride + x0 * C - 16;  // staged (row 0, chunk 0)
+        const bool interior = y0 > 0 && y0 + S::TT < n && x0 > 0 && x0 + S::TT < n;
+        if (interior) {
+            for (int i = threadIdx.x; i < nch; i += S::THREADS) {
+                const uint32_t c = chunks[i];
+                const uint32_t j = (c >> 16) & 0xffu, qq = c >> 24;
+                cp_async16(sb + (c & 0xffffu), base + (int64_t)j * rowstride + qq * 16, 16, fetch_line);
+            }
+        } else {
+            for (int i = threadIdx.x; i < nch; i += S::THREADS) {
+                const uint32_t c = chunks[i];
+                const int j = (int)((c >> 16) & 0xffu), qq = (int)(c >> 24);
+                const int64_t y = y0 + j - 1;
+                const int64_t xb = x0 * C + (qq - 1) * 16;
+                const bool in = y >= 0 && y < n && xb >= 0 && xb < rowstride;
+                cp_async16(sb + (c & 0xffffu), in ? src + y * rowstride + xb : src, in ? 16 : 0, fetch_line);
+            }
+        }
+    };
+
+#pragma unroll
+    for (int s = 0; s < NST - 1; ++s) {
+        stage((uint32_t)s);
+        cp_async_commit();
+    }
+    for (uint32_t idx = 0; idx < count; ++idx) {
+        cp_async_wait<NST - 2>();  // this thread's copies of tile idx have landed
+        __syncthreads();           // everyone's have; everyone is done with tile idx-1's slot
+        stage(idx + NST - 1);      // refill the slot tile idx-1 used
+        cp_async_commit();
+        if (active) {
+            uint32_t bx, by;
+            tile_xy(first + idx * step, bx, by);
+            const int64_t x0 = (int64_t)bx * S::TT, y0 = (int64_t)by * S::TT;
+            const uint8_t* b = smem + (idx % NST) * S::BUF;
+            const uint32_t* up = reinterpret_cast<const uint32_t*>(b + t * PITCH);  // staged row t = tile row t-1
+            const int k0 = 4 + 8 * g;  // first word of the sector (4 halo words on the left)
+            uint32_t w[3][10];
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+                const uint32_t* row = up + r * (PITCH / 4);
+                const uint4 a = *reinterpret_cast<const uint4*>(row + k0);
+                const uint4 c = *reinterpret_cast<const uint4*>(row + k0 + 4);
+                w[r][1] = a.x; w[r][2] = a.y; w[r][3] = a.z; w[r][4] = a.w;
+                w[r][5] = c.x; w[r][6] = c.y; w[r][7] = c.z; w[r][8] = c.w;
+                if (EIGHT || r == 1) {
+                    w[r][0] = row[k0 - 1];
+                    w[r][9] = row[k0 + 8];
+                } else {
+                    w[r][0] = w[r][9] = 0u;
+                }
+            }
+            uint32_t out[8];
+            if (probe_nocompute) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) out[i] = w[0][i + 1] ^ w[2][i + 1];
+            } else {
+                sector_sums<C, EIGHT>(w, pv, out);
+            }
+            uint8_t* gp = grid + (y0 + t) * rowstride + x0 * C + g * 32;
+            if (dst_from_src) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) out[i] = (out[i] & wmask[i]) | (w[1][i + 1] & ~wmask[i]);
+            } else {  // off-gasket cells from the grid itself (still a whole-sector write)
+                uint32_t old[8];
+                ld_sector(gp, fetch_line, v8, old);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) out[i] = (out[i] & wmask[i]) | (old[i] & ~wmask[i]);
+            }
+            if (!probe_nostore) st_sector(gp, out, v8);
+        }
+    }
+    cp_async_wait<0>();
+}
+
+template <int C, int KIND, int NST>
+cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
+    using S = T2<C>;
+    uint32_t lo, hi;
+    tile_range(a, r_t, lo, hi);
+    if (hi == lo) return cudaSuccess;
+    const uint32_t ntiles = hi - lo;
+    const size_t smem = (size_t)NST * S::BUF + 4 * S::ROWS * CHUNKS;
+    auto* kern = stencil_v2<C, KIND, NST>;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, S::THREADS, smem);
+    uint64_t blocks = (uint64_t)sms * (per_sm > 0 ? per_sm : 1);
+    if (blocks > ntiles) blocks = ntiles;
+    const uint32_t* order = nullptr;
+    if (!(a.flags & GM_FLAG_DIGIT_ORDER)) order = rowmajor_table(r_t, a.part_level < 0 ? 0 : a.part_level);
+    kern<<<(unsigned)blocks, S::THREADS, smem, a.stream>>>(reinterpret_cast<uint8_t*>(a.grid),
+                                                          reinterpret_cast<const uint8_t*>(a.src), a.n, lo, hi, r_t,
+                                                          a.part_level, a.param, a.flags, order);
+    note_launch();
+    return cudaGetLastError();
+}
+
+template <int C, int KIND>
+cudaError_t launch_kind(const LaunchArgs& a, int r_t) {
+    // ring depth: GM_FLAG_STAGES2 / default 3 (byte cells; 2-byte and 4-byte tiles are smaller: 4)
+    if (a.flags & GM_FLAG_STAGES2) return launch_ck<C, KIND, 2>(a, r_t);
+    if constexpr (C == 1) return launch_ck<C, KIND, 3>(a, r_t);
+    else return launch_ck<C, KIND, 4>(a, r_t);
+}
+
+template <int C>
+cudaError_t launch_c(const LaunchArgs& a, int r) {
+    int k = 0;
+    while ((1 << k) < T2<C>::TT) ++k;
+    if (a.kind == KIND_NSUM4) return launch_kind<C, KIND_NSUM4>(a, r - k);
+    if (a.kind == KIND_NSUM8) return launch_kind<C, KIND_NSUM8>(a, r - k);
+    return cudaErrorNotSupported;
+}
+
+}  // namespace
+
+// Device table of the member tiles of a level-q gasket (tile edge 1), packed
+// bx | by << 16, ordered sub-gasket by sub-gasket (level-L digit order, the
+// order tile ranges of partitioned launches refer to) and row-major inside each
+// sub-gasket (block row Y ascending, then the columns l subset of Y).  Built on
+// the host once per (device, q, L) and kept for the life of the process.
+// Why: concurrently running CTAs then stage/store horizontally adjacent tiles,
+// i.e. the same rows and DRAM pages at the same time (scripts/probe_gasket.cu:
+// tile reads 43.7 -> 48.6 G lines/s, partial-line writes 39.7 -> 44.5 G lines/s;
+// stencil n=2^17 518 -> 436 us, write pass n=2^16 118 -> 104 us).
+const uint32_t* rowmajor_table(int q, int L) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, int>, uint32_t*> cache;
+    if (q > 15 || L > q) return nullptr;  // caller falls back to digit order
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    const auto key = std::make_tuple(dev, q, L);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    uint64_t nsg = 1;
+    for (int i = 0; i < L; ++i) nsg *= 3u;
+    const int m = q - L;
+    std::vector<uint32_t> v;
+    for (uint64_t sg = 0; sg < nsg; ++sg) {
+        uint32_t sx = 0, sy = 0, d = (uint32_t)sg;
+        for (int i = 0; i < L; ++i, d /= 3u) {  // digit i -> level i+1: 1 = (0,1), 2 = (1,1)
+            sx |= (uint32_t)(d % 3u == 2u) << i;
+            sy |= (uint32_t)(d % 3u != 0u) << i;
+        }
+        for (uint32_t Y = 0; Y < (1u << m); ++Y) {
+            for (uint32_t l = Y;; l = (l - 1) & Y) {  // subsets of Y, descending; reversed below
+                v.push_back(((sx << m) + l) | (((sy << m) + Y) << 16));
+                if (l == 0) break;
+            }
+            std::reverse(v.end() - (1u << __builtin_popcount(Y)), v.end());
+        }
+    }
+    uint32_t* d_tab = nullptr;
+    if (cudaMalloc(&d_tab, v.size() * sizeof(uint32_t)) != cudaSuccess) return nullptr;
+    if (cudaMemcpy(d_tab, v.data(), v.size() * sizeof(uint32_t), cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaFree(d_tab);
+        return nullptr;
+    }
+    cache[key] = d_tab;
+    return d_tab;
+}
+
+cudaError_t launch_stencil_v2(const LaunchArgs& a) {
+    if (a.flags & (GM_FLAG_OMEGA_ORDER | GM_FLAG_STENCIL_V1)) return cudaErrorNotSupported;
+    int r = 0;
+    while ((int64_t(1) << r) < a.n) ++r;
+    switch (a.cell_bytes) {
+    case 1: if (a.n >= T2<1>::TT) return launch_c<1>(a, r); break;
+    case 2: if (a.n >= T2<2>::TT) return launch_c<2>(a, r); break;
+    case 4: if (a.n >= T2<4>::TT) return launch_c<4>(a, r); break;
+    }
+    return cudaErrorNotSupported;
+}
+
+}  // namespace gm

@@ -93,6 +93,25 @@ __device__ __forceinline__ W shfl_dn1(W v) {
     }
 }
 
+// Loads with the .L2::64B fetch-size hint: an L2 miss brings in the 64-byte half
+// holding the word instead of the whole 128-byte line (scripts/probe_fetch.cu).
+template <class W>
+__device__ __forceinline__ W ld_half(const void* p) {
+    if constexpr (sizeof(W) == 8) {
+        uint64_t v;
+        asm volatile("ld.global.cg.L2::64B.u64 %0, [%1];" : "=l"(v) : "l"(p));
+        return v;
+    } else {
+        uint32_t v;
+        asm volatile("ld.global.cg.L2::64B.u32 %0, [%1];" : "=r"(v) : "l"(p));
+        return v;
+    }
+}
+template <class W>
+__device__ __forceinline__ W ld_line(const void* p) {
+    return *reinterpret_cast<const volatile W*>(p);
+}
+
 // Left / right neighbour cells of every cell of the word.
 template <int C>
 __device__ __forceinline__ typename WordT<C>::T left_of(typename WordT<C>::T prev, typename WordT<C>::T cur) {
@@ -136,7 +155,8 @@ __device__ __forceinline__ bool sec_needed(int t, int g) {
 template <int C, int KIND, int BAND, bool DIGIT_ORDER>
 __global__ void __launch_bounds__(256) lambda_stream(uint8_t* __restrict__ grid, const uint8_t* __restrict__ src,
                                                      int64_t n, uint32_t tile_lo, uint32_t tile_hi, int band_shift,
-                                                     uint32_t W, uint64_t param, int flags) {
+                                                     uint32_t W, uint64_t param, int flags,
+                                                     const uint32_t* __restrict__ order) {
     using WT = typename WordT<C>::T;
     using G = Geo<C>;
     constexpr bool EIGHT = KIND == KIND_NSUM8;
@@ -149,10 +169,14 @@ __global__ void __launch_bounds__(256) lambda_stream(uint8_t* __restrict__ grid,
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint64_t u_lo = (uint64_t)tile_lo << band_shift;
     const uint64_t units = ((uint64_t)tile_hi << band_shift) - u_lo;
-    // contiguous chunk of units per warp: lambda once per tile, bands of a tile in order
-    const uint64_t chunk = (units + nwarps - 1) / nwarps;
+    // contiguous chunk of units per warp: lambda once per tile, bands of a tile in order;
+    // with a precomputed tile order (GM_FLAG_ROWMAJOR) units are interleaved over the
+    // warps instead, so concurrently running warps work on neighbouring tiles
+    const bool interleave = order != nullptr;
+    const uint64_t chunk = interleave ? 1 : (units + nwarps - 1) / nwarps;
     const uint64_t u_begin = u_lo + warp0 * chunk;
-    const uint64_t u_end = u_begin + chunk < u_lo + units ? u_begin + chunk : u_lo + units;
+    const uint64_t u_end = interleave ? u_lo + units : (u_begin + chunk < u_lo + units ? u_begin + chunk : u_lo + units);
+    const uint64_t u_step = interleave ? nwarps : 1;
     const int64_t rowstride = n * C;  // bytes
     const int g = lane / G::LPS;      // this lane's sector in the tile row
     const int c0 = lane * G::V;       // first cell of this lane's word
@@ -165,13 +189,17 @@ __global__ void __launch_bounds__(256) lambda_stream(uint8_t* __restrict__ grid,
     uint32_t cur_tile = 0xffffffffu;
     int64_t x0 = 0, y0 = 0;
     int prev_t0 = -BAND;
-    for (uint64_t u = u_begin; u < u_end; ++u) {
+    for (uint64_t u = u_begin; u < u_end; u += u_step) {
         const uint32_t tile = (uint32_t)(u >> band_shift);
         const int t0 = (int)(u & ((1u << band_shift) - 1u)) * BAND;
         const bool same_tile = tile == cur_tile;
         if (!same_tile) {
             uint32_t bx, by;
-            if (DIGIT_ORDER) {
+            if (order != nullptr) {
+                const uint32_t v = __ldg(order + tile);
+                bx = v & 0xffffu;
+                by = v >> 16;
+            } else if (DIGIT_ORDER) {
                 lambda_digit_order(tile, tab, bx, by);
             } else {
                 const uint32_t wy = tile / W;
@@ -201,8 +229,9 @@ __global__ void __launch_bounds__(256) lambda_stream(uint8_t* __restrict__ grid,
                 for (int i = 0; i < BAND; ++i) {
                     const int t = t0 + i;
                     const bool full = ((g * G::SC + G::SC - 1) & ~t) == 0;
+                    const uint8_t* p = drow + (int64_t)i * rowstride;
                     old[i] = ((sec_touched<C>(t, g) || lines) && !full)
-                                 ? *reinterpret_cast<const volatile WT*>(drow + (int64_t)i * rowstride)
+                                 ? ((flags & GM_FLAG_FETCH_LINE) ? ld_line<WT>(p) : ld_half<WT>(p))
                                  : WT(0);
                 }
 #pragma unroll
@@ -214,6 +243,14 @@ __global__ void __launch_bounds__(256) lambda_stream(uint8_t* __restrict__ grid,
                     }
                 }
             } else {
+            if (flags & GM_FLAG_FETCH64) {
+                // bring the touched 64-byte halves into L2 with plain reads first, so the
+                // partial stores below merge into valid sectors instead of each forcing
+                // its own DRAM read-modify-write fill
+#pragma unroll
+                for (int i = 0; i < BAND; ++i)
+                    if ((c0 & ~(t0 + i)) == 0) (void)ld_half<WT>(drow + (int64_t)i * rowstride);  // asm volatile: kept
+            }
             // rows come in groups of V (t0 is a multiple of V): within a group the word's
             // touched flag is constant and slot j's cell pattern is j (cells k subset of j)
 #pragma unroll
@@ -336,9 +373,12 @@ cudaError_t launch_band(const LaunchArgs& a, int r_t) {
     uint64_t blocks = (units * 32 + 255) / 256;
     const uint64_t cap = (uint64_t)sms * (per_sm > 0 ? per_sm : 1);
     if (blocks > cap) blocks = cap;
+    const uint32_t* order = nullptr;
+    if (digit && !(a.flags & GM_FLAG_DIGIT_ORDER) && KIND != KIND_COUNT)
+        order = rowmajor_table(r_t, a.part_level < 0 ? 0 : a.part_level);
     kern<<<(unsigned)blocks, 256, 0, a.stream>>>(reinterpret_cast<uint8_t*>(a.grid),
                                                  reinterpret_cast<const uint8_t*>(a.src), a.n, lo, hi, band_shift, W,
-                                                 a.param, a.flags);
+                                                 a.param, a.flags, order);
     note_launch();
     return cudaGetLastError();
 }

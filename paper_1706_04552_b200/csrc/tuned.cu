@@ -268,6 +268,11 @@ cudaError_t launch_tuned(const LaunchArgs& a) {
     }
     // neighbour sums on grids at least one 128-byte tile wide: shared-memory tiles (stencil.cu)
     if (a.kind == KIND_NSUM4 || a.kind == KIND_NSUM8) {
+        if (!(a.flags & GM_FLAG_FORCE_TMA)) {  // v2 tiles (stencil2.cu) unless a variant is asked for
+            const cudaError_t e2 = launch_stencil_v2(a);
+            if (e2 != cudaErrorNotSupported) return e2;
+            cudaGetLastError();
+        }
         const cudaError_t et = launch_stencil_tma(a);  // TMA-staged tiles (stencil_tma.cu)
         if (et != cudaErrorNotSupported) return et;
         cudaGetLastError();

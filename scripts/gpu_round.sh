@@ -44,5 +44,11 @@ nsweep)
   timeout 1500 python bench.py --nsweep --nsweep-out gpurun_out/$TAG/nsweep.csv > gpurun_out/$TAG/nsweep.json 2> gpurun_out/$TAG/nsweep.err; echo nsweep_rc=$? ;;
 ab)
   for L in ${ABLIBS:-A B A B}; do echo "== lib$L" >> gpurun_out/$TAG/ab.txt; GASKET_B200_LIB=ab/lib$L.so timeout 600 python scripts/variants.py ${VARIANTS:-stencil17} >> gpurun_out/$TAG/ab.txt 2>&1; done; echo ab_done ;;
+fetch)
+  for G in def; do A=$G; [ $G = def ] && A=; echo "== granularity $G" >> gpurun_out/$TAG/probe_fetch.txt; ./scripts/probe_fetch $A >> gpurun_out/$TAG/probe_fetch.txt 2>&1
+    ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,lts__t_sectors_srcunit_tex_op_read.sum,lts__t_requests_srcunit_tex_op_read.sum,lts__t_sectors_srcunit_tex_op_read_lookup_miss.sum,dram__bytes_write.sum --csv --log-file gpurun_out/$TAG/probe_fetch_ncu_$G.csv ./scripts/probe_fetch $A > /dev/null 2>&1; done; echo fetch_done ;;
+gasket)
+  ./scripts/probe_gasket > gpurun_out/$TAG/probe_gasket.txt 2>&1; echo gasket_rc=$?
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --csv --log-file gpurun_out/$TAG/probe_gasket_ncu.csv ./scripts/probe_gasket > /dev/null 2>&1 ;;
 esac
 done

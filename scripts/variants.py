@@ -46,7 +46,10 @@ def main():
             g = torch.zeros((n, n), dtype=dt, device="cuda")
             alg = R.write_bytes(r, c)
             H, E, L = native.FLAG_HOST_ROWS, native.FLAG_EXPLICIT_RMW, native.FLAG_WHOLE_LINES
-            for name, fl in (("masked", 0), ("rmw-sectors", E), ("rmw-lines", E | L)):
+            F64, FL = native.FLAG_FETCH64, native.FLAG_FETCH_LINE
+            RMJ = native.FLAG_ROWMAJOR
+            for name, fl in (("masked", 0), ("masked-rowmajor", RMJ), ("masked+touch64-rowmajor", F64 | RMJ),
+                             ("rmw-sectors", E), ("rmw-sectors-rowmajor", E | RMJ), ("rmw-lines-rowmajor", E | L | RMJ)):
                 m, mn = timeit(lambda: backends.run_block_space(g, g, 32, r - 5, T, kind=0, param=1, flags=fl), flush)
                 print(f"write r={r} c={c} {name:10s} mean {m * 1e3:8.1f} us  min {mn * 1e3:8.1f} us  "
                       f"{3**r / (m * 1e-3) / 1e9:7.1f} Gcells/s  alg {alg / (m * 1e-3) / 1e9:6.0f} GB/s", flush=True)
@@ -59,18 +62,54 @@ def main():
         dst = src.clone()
         D, RM, CH = native.FLAG_DST_FROM_SRC, native.FLAG_ROWMAJOR, native.FLAG_CHUNKED
         NT = native.FLAG_NO_TMA
-        for name, fl in (("tma", D | native.FLAG_FORCE_TMA), ("cp.async", D | NT), ("masked-tma", 0),
-                         ("masked-cp.async", NT)):
+        FL = native.FLAG_FETCH_LINE
+        V1, S2 = native.FLAG_STENCIL_V1, native.FLAG_STAGES2
+        PN, PL = native.FLAG_PROBE_NOSTORE, native.FLAG_PROBE_NOLOAD
+        for name, fl in (("v2", D), ("v2-rowmajor", D | RM), ("v2-rowmajor-stages2", D | RM | S2),
+                         ("v2-rowmajor-chunked", D | RM | CH),
+                         ("probe v2-rowmajor no compute", D | RM | native.FLAG_PROBE_NOCOMPUTE),
+                         ("v2-line", D | FL), ("v2-stages2", D | S2), ("v2-chunked", D | CH),
+                         ("probe v2 reads only", D | PN), ("probe v2 reads only, line", D | PN | FL),
+                         ("probe v2 stores only", D | PL), ("probe v2 no memory", D | PN | PL),
+                         ("probe v2 no compute", D | native.FLAG_PROBE_NOCOMPUTE),
+                         ("probe v2 no compute, reads only", D | native.FLAG_PROBE_NOCOMPUTE | PN),
+                         ("v2-masked", 0), ("v2-masked-line", FL),
+                         ("v1-tma", D | native.FLAG_FORCE_TMA), ("v1-cp.async", D | NT | V1),
+                         ("v1-masked-tma", V1), ("v1-masked-cp.async", NT | V1)):
             m, mn = timeit(lambda: backends.run_block_space(dst, src, 64, r - 6, T, kind=2, param=1, flags=fl), flush, k=10)
             print(f"stencil r={r} nsum8 {name:22s} mean {m * 1e3:8.1f} us  min {mn * 1e3:8.1f} us", flush=True)
         for kind in (2, 1):
             alg = R.pass_bytes(r, 1, kind)
-            for name, fl in (("dst_from_src", native.FLAG_DST_FROM_SRC), ("masked", 0)):
+            for name, fl in (("dst_from_src", native.FLAG_DST_FROM_SRC), ("masked", 0),
+                             ("v1-dst_from_src", native.FLAG_DST_FROM_SRC | native.FLAG_STENCIL_V1)):
                 m, mn = timeit(lambda: backends.run_block_space(dst, src, 64, r - 6, T, kind=kind, param=1, flags=fl),
                                flush, k=10)
                 print(f"stencil r={r} nsum{4 * kind} {name:12s} mean {m * 1e3:8.1f} us  min {mn * 1e3:8.1f} us  "
                       f"{3**r / (m * 1e-3) / 1e9:7.1f} Gcells/s  alg {alg / (m * 1e-3) / 1e9:6.0f} GB/s", flush=True)
 
 
+
+
+def offsets(r=17):
+    """Stencil v2 time vs the byte offset between the src and dst allocations (DRAM bank mapping)."""
+    n = 1 << r
+    flush = device.L2Flusher()
+    T = IntraStrategy.TUNED
+    src = device.fill_hash(n, torch.int8, 1, 0)
+    D = native.FLAG_DST_FROM_SRC
+    for off in (0, 128, 2048, 4096, 65536 + 2048, (1 << 20) + 4096, (1 << 21) + 8192 + 128):
+        big = torch.empty(n * n + off, dtype=torch.int8, device="cuda")
+        dst = big[off:off + n * n].view(n, n)
+        dst.copy_(src)
+        m, mn = timeit(lambda: backends.run_block_space(dst, src, 64, r - 6, T, kind=2, param=1, flags=D), flush, k=10)
+        print(f"stencil r={r} nsum8 v2 dst offset {off:8d} (src-dst delta {dst.data_ptr() - src.data_ptr():+d}) "
+              f"mean {m * 1e3:8.1f} us  min {mn * 1e3:8.1f} us", flush=True)
+        del big, dst
+        torch.cuda.empty_cache()
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["offsets"]:
+        offsets()
+    else:
+        main()

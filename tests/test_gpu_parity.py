@@ -18,6 +18,11 @@ pytestmark = pytest.mark.gpu
 DTYPES = {np.int8: torch.int8, np.int16: torch.int16, np.int32: torch.int32, np.int64: torch.int64,
           np.uint8: torch.uint8}
 KINDS = (0, 1, 2)  # CONST, NSUM4, NSUM8 (ours)
+# every result-preserving kernel variant of the tuned strategy (include/gasket_b200.h):
+# omega order, explicit RMW (+ whole lines), host-row schedule, row-major/chunked,
+# cp.async/TMA staging, whole-line fetch, L2 touch, stencil v1, 2-deep ring, digit order
+TUNED_FLAGS = (0, 1, 4, 12, 16, 32, 96, 128, 256, 512, 1024, 2048, 2048 | 65536, 2048 | 128, 4096, 65536,
+               4 | 512, 65536 | 4096)
 
 
 def _to_dev(a: np.ndarray) -> torch.Tensor:
@@ -109,7 +114,7 @@ def _gpu_all(gpu, grid0, src, rho, kind, param):
         be.run_bounding_box(g, sdev, rho, kind, param, early_exit=early)
         yield ("bb-exit" if early else "bb"), g
     for strat in _strategies(gpu):
-        for flags in ((0, 1, 4, 12, 16, 32, 96, 128, 256) if strat.value == "tuned" else (0,)):
+        for flags in (TUNED_FLAGS if strat.value == "tuned" else (0,)):
             g = _to_dev(grid0)
             lx, ly = be.local_cell_arrays(strat, rho)
             be.run_block_space(g, sdev, rho, r_b, strat, lx, ly, kind, param, flags=flags)
@@ -374,6 +379,23 @@ def test_ca_runner_matches_oracle_steps(gpu, oracle, kind):
     g = torch.from_numpy(init.copy()).cuda()
     ca.run_ca(g, steps, kind=kind, param=3)
     assert np.array_equal(g.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("dtype", [np.int8, np.int16, np.int32])
+def test_dst_from_src_variants(gpu, oracle, dtype):
+    """GM_FLAG_DST_FROM_SRC (grid == snapshot off the gasket: engine.launch / CA
+    ping-pong) through every stencil kernel variant, including edge tiles."""
+    be, S = gpu.backends, gpu.geometry.IntraStrategy
+    n0 = 128 // np.dtype(dtype).itemsize  # one tile
+    for n in (n0, 2 * n0, 8 * n0, 1 << 12):
+        src = oracle.fill_hash(n, dtype, 31, 0)
+        for kind in (1, 2):
+            want = _oracle_result(oracle, src.copy(), src, 8, kind, -5)
+            for flags in (2, 2 | 65536, 2 | 2048, 2 | 2048 | 128, 2 | 4096, 2 | 512, 2 | 64, 2 | 256):
+                g = _to_dev(src)
+                r_b = (n // 8).bit_length() - 1
+                be.run_block_space(g, _to_dev(src), 8, r_b, S.TUNED, kind=kind, param=-5, flags=flags)
+                assert np.array_equal(g.cpu().numpy(), want), (np.dtype(dtype).name, n, kind, flags)
 
 
 @pytest.mark.parametrize("kind", [0, 1, 2])
