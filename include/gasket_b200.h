@@ -67,6 +67,8 @@ extern "C" {
 #define GM_FLAG_PROBE_NOLOAD 16384  /* design probe, stencil v2: store sectors without staging (result undefined) */
 #define GM_FLAG_PROBE_NOCOMPUTE 32768 /* design probe, stencil v2: stage + store, no arithmetic (result undefined) */
 #define GM_FLAG_DIGIT_ORDER 65536 /* tuned: visit tiles in lambda digit order instead of row-major per sub-gasket */
+#define GM_FLAG_STORE_CS 131072   /* tuned write pass / stencil v2: streaming (evict-first) stores */
+#define GM_FLAG_BAND_MAJOR 262144 /* tuned write pass: hand out (band, tile) units band-major */
 
 #define GM_OK 0
 #define GM_EINVAL 1  /* bad shape / size / tag (the reference's ValueError) */

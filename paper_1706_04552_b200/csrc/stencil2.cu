@@ -116,8 +116,12 @@ __device__ __forceinline__ void ld_sector(const uint8_t* p, bool line, bool v8, 
 }
 // one 256-bit store when the grid is 32-byte aligned (device allocations),
 // else two 16-byte stores (e.g. a page-locked numpy array mapped over PCIe)
-__device__ __forceinline__ void st_sector(uint8_t* p, const uint32_t (&v)[8], bool v8) {
-    if (v8) {
+__device__ __forceinline__ void st_sector(uint8_t* p, const uint32_t (&v)[8], bool v8, bool cs) {
+    if (v8 && cs) {
+        asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),
+                     "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                     : "memory");
+    } else if (v8) {
         asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),
                      "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
                      : "memory");
@@ -256,6 +260,7 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
     const bool probe_nostore = (flags & GM_FLAG_PROBE_NOSTORE) != 0;
     const bool probe_noload = (flags & GM_FLAG_PROBE_NOLOAD) != 0;
     const bool probe_nocompute = (flags & GM_FLAG_PROBE_NOCOMPUTE) != 0;
+    const bool store_cs = (flags & GM_FLAG_STORE_CS) != 0;
     const uint32_t smem0 = (uint32_t)__cvta_generic_to_shared(smem);
     uint32_t pv;
     if constexpr (C == 1) pv = 0x00010001u * (uint32_t)(param & 0xffu);
@@ -375,7 +380,7 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
 #pragma unroll
                 for (int i = 0; i < 8; ++i) out[i] = (out[i] & wmask[i]) | (old[i] & ~wmask[i]);
             }
-            if (!probe_nostore) st_sector(gp, out, v8);
+            if (!probe_nostore) st_sector(gp, out, v8, store_cs);
         }
     }
     cp_async_wait<0>();

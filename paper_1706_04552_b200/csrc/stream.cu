@@ -112,6 +112,13 @@ __device__ __forceinline__ W ld_line(const void* p) {
     return *reinterpret_cast<const volatile W*>(p);
 }
 
+// Plain store, or (GM_FLAG_STORE_CS) a streaming / evict-first store.
+template <class T>
+__device__ __forceinline__ void st_cell(void* p, T v, bool cs) {
+    if (cs) __stcs(reinterpret_cast<T*>(p), v);
+    else *reinterpret_cast<T*>(p) = v;
+}
+
 // Left / right neighbour cells of every cell of the word.
 template <int C>
 __device__ __forceinline__ typename WordT<C>::T left_of(typename WordT<C>::T prev, typename WordT<C>::T cur) {
@@ -189,9 +196,22 @@ __global__ void __launch_bounds__(256) lambda_stream(uint8_t* __restrict__ grid,
     uint32_t cur_tile = 0xffffffffu;
     int64_t x0 = 0, y0 = 0;
     int prev_t0 = -BAND;
+    // GM_FLAG_BAND_MAJOR (with a tile order table): unit = band * ntiles + tile, so the
+    // warps running together store the same rows of neighbouring tiles (DRAM pages)
+    const bool band_major = interleave && (flags & GM_FLAG_BAND_MAJOR) != 0;
+    const uint64_t ntl = (uint64_t)(tile_hi - tile_lo);
     for (uint64_t u = u_begin; u < u_end; u += u_step) {
-        const uint32_t tile = (uint32_t)(u >> band_shift);
-        const int t0 = (int)(u & ((1u << band_shift) - 1u)) * BAND;
+        uint32_t tile;
+        int t0;
+        if (band_major) {
+            const uint64_t v = u - u_lo;
+            const uint64_t b = v / ntl;
+            tile = tile_lo + (uint32_t)(v - b * ntl);
+            t0 = (int)b * BAND;
+        } else {
+            tile = (uint32_t)(u >> band_shift);
+            t0 = (int)(u & ((1u << band_shift) - 1u)) * BAND;
+        }
         const bool same_tile = tile == cur_tile;
         if (!same_tile) {
             uint32_t bx, by;
@@ -258,17 +278,18 @@ __global__ void __launch_bounds__(256) lambda_stream(uint8_t* __restrict__ grid,
                 const int tq = t0 + q * G::V;
                 if ((c0 & ~tq) == 0) {
                     uint8_t* p = drow + (int64_t)(q * G::V) * rowstride;
+                    const bool cs = (flags & GM_FLAG_STORE_CS) != 0;
                     if constexpr (G::V == 1) {
-                        *reinterpret_cast<WT*>(p) = pv;
+                        st_cell<WT>(p, pv, cs);
                     } else if constexpr (G::V == 2) {
-                        *reinterpret_cast<uint16_t*>(p) = (uint16_t)pv;
-                        *reinterpret_cast<uint32_t*>(p + rowstride) = pv;
+                        st_cell<uint16_t>(p, (uint16_t)pv, cs);
+                        st_cell<uint32_t>(p + rowstride, pv, cs);
                     } else {
-                        p[0] = (uint8_t)pv;
-                        *reinterpret_cast<uint16_t*>(p + rowstride) = (uint16_t)pv;
-                        p[2 * rowstride] = (uint8_t)pv;
-                        p[2 * rowstride + 2] = (uint8_t)pv;
-                        *reinterpret_cast<uint32_t*>(p + 3 * rowstride) = pv;
+                        st_cell<uint8_t>(p, (uint8_t)pv, cs);
+                        st_cell<uint16_t>(p + rowstride, (uint16_t)pv, cs);
+                        st_cell<uint8_t>(p + 2 * rowstride, (uint8_t)pv, cs);
+                        st_cell<uint8_t>(p + 2 * rowstride + 2, (uint8_t)pv, cs);
+                        st_cell<uint32_t>(p + 3 * rowstride, pv, cs);
                     }
                 }
             }

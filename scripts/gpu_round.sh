@@ -17,13 +17,13 @@ ncu)
   timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 40 --csv --log-file gpurun_out/$TAG/launches_stencil17.csv python bench.py --workload stencil17 --steps 10 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1; echo ncu2_rc=$? ;;
 ncufull)
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:lambda_stream -s 3 -c 1 -o gpurun_out/$TAG/prof_write16 python bench.py --steps 2 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1; echo ncuf_rc=$?
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:lambda_stream -s 3 -c 1 -o gpurun_out/$TAG/prof_stencil17 python bench.py --workload stencil17 --steps 2 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1; echo ncuf2_rc=$? ;;
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:stencil_v2 -s 3 -c 1 -o gpurun_out/$TAG/prof_stencil17 python bench.py --workload stencil17 --steps 2 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1; echo ncuf2_rc=$? ;;
 probe)
   ./scripts/probe_stride > gpurun_out/$TAG/probe_stride.txt 2>&1; echo probe_rc=$? ;;
 variants)
   timeout 600 python scripts/variants.py ${VARIANTS:-write16 stencil17} > gpurun_out/$TAG/variants.txt 2>&1; echo variants_rc=$? ;;
 ncustencil)
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:stencil_tile -s 2 -c 1 -o gpurun_out/$TAG/prof_stencil17 python bench.py --workload stencil17 --steps 2 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1; echo ncus_rc=$? ;;
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:stencil_v2 -s 2 -c 1 -o gpurun_out/$TAG/prof_stencil17 python bench.py --workload stencil17 --steps 2 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1; echo ncus_rc=$? ;;
 part)
   timeout 900 python bench.py --workload part18 --steps 20 --warmup 3 > gpurun_out/$TAG/bench_part18.json 2> gpurun_out/$TAG/bench_part18.err; echo part_rc=$? ;;
 e2e)
@@ -38,7 +38,7 @@ profile)
   timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"lambda|stencil|l2_flush|fill_hash" -c 60 --csv --log-file gpurun_out/$TAG/launches_write16.csv python bench.py --steps 20 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1
   timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"lambda|stencil|l2_flush|fill_hash" -c 40 --csv --log-file gpurun_out/$TAG/launches_stencil17.csv python bench.py --workload stencil17 --steps 10 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:lambda_stream -s 3 -c 1 -o gpurun_out/$TAG/prof_write16 python bench.py --steps 2 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:stencil_tile -s 2 -c 1 -o gpurun_out/$TAG/prof_stencil17 python bench.py --workload stencil17 --steps 2 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:stencil_v2 -s 2 -c 1 -o gpurun_out/$TAG/prof_stencil17 python bench.py --workload stencil17 --steps 2 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1
   echo profile_done ;;
 nsweep)
   timeout 1500 python bench.py --nsweep --nsweep-out gpurun_out/$TAG/nsweep.csv > gpurun_out/$TAG/nsweep.json 2> gpurun_out/$TAG/nsweep.err; echo nsweep_rc=$? ;;

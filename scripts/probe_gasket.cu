@@ -86,6 +86,35 @@ __global__ void k_tiles(const uint8_t* a, uint8_t* b, const uint32_t* tiles, int
     if (acc == 0x12345u) atomicAdd(sink, 1u);
 }
 
+// strips order: warp handles the member tiles of one 8-line-aligned strip of a tile
+// row in lockstep: for each row, the member lines side by side (4 per instruction)
+template <int MODE>
+__global__ void k_strips(const uint8_t* a, uint8_t* b, const uint32_t* strips, int64_t nstrips, unsigned* sink) {
+    const int lane = threadIdx.x & 31, grp = lane >> 3, sub = lane & 7;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned acc = 0;
+    for (int64_t t = warp; t < nstrips; t += nw) {
+        const uint32_t v = strips[t];
+        const uint32_t X8 = v & 0xffff, Yb = v >> 16;
+        const uint32_t low = Yb & 7u;
+        const int cnt = 1 << __popc(low);
+        for (int r = 0; r < 128; ++r) {
+            for (int k = grp; k < cnt; k += 4) {
+                uint32_t j = 0, m = low, kk = (uint32_t)k;
+                while (m) {
+                    const uint32_t lo = m & (0u - m);
+                    if (kk & 1u) j |= lo;
+                    kk >>= 1;
+                    m ^= lo;
+                }
+                acc ^= do_line<MODE>(a, b, (int64_t)Yb * 128 + r, (int64_t)X8 * 8 + j, sub);
+            }
+        }
+    }
+    if (acc == 0x12345u) atomicAdd(sink, 1u);
+}
+
 __global__ void k_flush(const uint4* p, int64_t n, unsigned* sink) {
     unsigned acc = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) acc ^= p[i].x;
@@ -115,6 +144,15 @@ int main() {
     std::sort(rm.begin(), rm.end(), [](uint32_t p, uint32_t q) {
         return (p >> 16) != (q >> 16) ? (p >> 16) < (q >> 16) : (p & 0xffff) < (q & 0xffff);
     });
+    // strips: (X8, Y) with X8 subset of Y >> 3, row-major
+    std::vector<uint32_t> st;
+    for (uint32_t Y = 0; Y < (1u << Q); ++Y)
+        for (uint32_t X8 = 0; X8 < (1u << (Q - 3)); ++X8)
+            if ((X8 & ~(Y >> 3)) == 0) st.push_back(X8 | (Y << 16));
+    const int64_t ns = (int64_t)st.size();
+    uint32_t* d_st;
+    CK(cudaMalloc(&d_st, ns * 4));
+    CK(cudaMemcpy(d_st, st.data(), ns * 4, cudaMemcpyHostToDevice));
     uint32_t *d_dig, *d_rm;
     CK(cudaMalloc(&d_dig, nt * 4));
     CK(cudaMalloc(&d_rm, nt * 4));
@@ -125,14 +163,18 @@ int main() {
     cudaEventCreate(&e1);
     const double lines = 128.0 * nt;
     const char* modes[] = {"read", "write", "copy"};
-    for (int order = 0; order < 3; ++order) {
+    for (int order = 0; order < 4; ++order) {
         for (int mode = 0; mode < 3; ++mode) {
             float best = 1e9;
             for (int rep = 0; rep < 3; ++rep) {
                 k_flush<<<148 * 8, 256>>>(reinterpret_cast<const uint4*>(fl), (1ll << 30) / 16, sink);
                 cudaEventRecord(e0);
                 const int grid = 148 * 8, block = 256;
-                if (order == 0) {
+                if (order == 3) {
+                    if (mode == 0) k_strips<0><<<grid, block>>>(a, b, d_st, ns, sink);
+                    if (mode == 1) k_strips<1><<<grid, block>>>(a, b, d_st, ns, sink);
+                    if (mode == 2) k_strips<2><<<grid, block>>>(a, b, d_st, ns, sink);
+                } else if (order == 0) {
                     if (mode == 0) k_rows<0><<<grid, block>>>(a, b, sink);
                     if (mode == 1) k_rows<1><<<grid, block>>>(a, b, sink);
                     if (mode == 2) k_rows<2><<<grid, block>>>(a, b, sink);
@@ -149,7 +191,7 @@ int main() {
                 cudaEventElapsedTime(&ms, e0, e1);
                 best = std::min(best, ms);
             }
-            printf("%-8s %-6s %8.1f us  %6.1f G lines/s\n", order == 0 ? "rows" : order == 1 ? "tiles" : "tilesrm",
+            printf("%-8s %-6s %8.1f us  %6.1f G lines/s\n", order == 0 ? "rows" : order == 1 ? "tiles" : order == 2 ? "tilesrm" : "strips",
                    modes[mode], best * 1e3, lines / (best * 1e-3) / 1e9);
         }
     }

@@ -48,8 +48,11 @@ def main():
             H, E, L = native.FLAG_HOST_ROWS, native.FLAG_EXPLICIT_RMW, native.FLAG_WHOLE_LINES
             F64, FL = native.FLAG_FETCH64, native.FLAG_FETCH_LINE
             RMJ = native.FLAG_ROWMAJOR
-            for name, fl in (("masked", 0), ("masked-rowmajor", RMJ), ("masked+touch64-rowmajor", F64 | RMJ),
-                             ("rmw-sectors", E), ("rmw-sectors-rowmajor", E | RMJ), ("rmw-lines-rowmajor", E | L | RMJ)):
+            DO, CS = native.FLAG_DIGIT_ORDER, native.FLAG_STORE_CS
+            BM = native.FLAG_BAND_MAJOR
+            for name, fl in (("masked", 0), ("masked-bandmajor", BM), ("masked-bandmajor-cs", BM | CS),
+                             ("masked-digit", DO), ("masked-cs", CS), ("masked+touch64", F64),
+                             ("rmw-sectors", E), ("rmw-lines", E | L)):
                 m, mn = timeit(lambda: backends.run_block_space(g, g, 32, r - 5, T, kind=0, param=1, flags=fl), flush)
                 print(f"write r={r} c={c} {name:10s} mean {m * 1e3:8.1f} us  min {mn * 1e3:8.1f} us  "
                       f"{3**r / (m * 1e-3) / 1e9:7.1f} Gcells/s  alg {alg / (m * 1e-3) / 1e9:6.0f} GB/s", flush=True)
@@ -65,10 +68,10 @@ def main():
         FL = native.FLAG_FETCH_LINE
         V1, S2 = native.FLAG_STENCIL_V1, native.FLAG_STAGES2
         PN, PL = native.FLAG_PROBE_NOSTORE, native.FLAG_PROBE_NOLOAD
-        for name, fl in (("v2", D), ("v2-rowmajor", D | RM), ("v2-rowmajor-stages2", D | RM | S2),
-                         ("v2-rowmajor-chunked", D | RM | CH),
-                         ("probe v2-rowmajor no compute", D | RM | native.FLAG_PROBE_NOCOMPUTE),
-                         ("v2-line", D | FL), ("v2-stages2", D | S2), ("v2-chunked", D | CH),
+        DO, CS = native.FLAG_DIGIT_ORDER, native.FLAG_STORE_CS
+        for name, fl in (("v2", D), ("v2-cs", D | CS), ("v2-digit", D | DO), ("v2-stages2", D | S2),
+                         ("v2-chunked", D | CH), ("probe v2 no compute", D | native.FLAG_PROBE_NOCOMPUTE),
+                         ("v2-line", D | FL),
                          ("probe v2 reads only", D | PN), ("probe v2 reads only, line", D | PN | FL),
                          ("probe v2 stores only", D | PL), ("probe v2 no memory", D | PN | PL),
                          ("probe v2 no compute", D | native.FLAG_PROBE_NOCOMPUTE),
