@@ -157,6 +157,10 @@ int gm_host_unmap(void* host);
 int gm_set_l2_fetch_granularity(int32_t bytes);
 
 /* Number of kernels this library has launched (all entry points). */
+/* The tuned kernels' tile visiting order (host-side, no GPU needed): the 3^q
+ * member tiles of a level-q gasket as bx | by << 16, level-`level` sub-gaskets in
+ * lambda digit order, row-major inside each.  out must hold 3^q entries. */
+int gm_tile_order(int32_t q, int32_t level, uint32_t* out, int64_t capacity);
 uint64_t gm_launch_count(void);
 const char* gm_last_error(void);
 const char* gm_version(void);

@@ -1,3 +1,4 @@
+#include <algorithm>
 // capi.cu -- extern "C" drop-in boundary (include/gasket_b200.h).
 //
 // Validation mirrors the reference's ValueError conditions (core.py:40-41,
@@ -303,6 +304,15 @@ int gm_host_unmap(void* host) {
 
 int gm_set_l2_fetch_granularity(int32_t bytes) {
     return cuda_rc(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)bytes), "cudaDeviceSetLimit");
+}
+
+int gm_tile_order(int32_t q, int32_t level, uint32_t* out, int64_t capacity) {
+    if (q < 0 || q > 15 || level < 0 || level > q || out == nullptr) return fail(GM_EINVAL, "gm_tile_order: bad q/level");
+    std::vector<uint32_t> v;
+    gm::rowmajor_order_host(q, level, v);
+    if ((int64_t)v.size() > capacity) return fail(GM_EINVAL, "gm_tile_order: capacity < 3^q");
+    std::copy(v.begin(), v.end(), out);
+    return GM_OK;
 }
 
 uint64_t gm_launch_count(void) { return gm::g_launches.load(); }

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 namespace gm {
 
 struct LaunchArgs {
@@ -52,5 +54,6 @@ cudaError_t launch_stencil_tma(const LaunchArgs& a);
 cudaError_t launch_stencil_v2(const LaunchArgs& a);
 // member tiles of a level-q gasket, row-major inside each level-L sub-gasket (stencil2.cu)
 const uint32_t* rowmajor_table(int q, int L);
+void rowmajor_order_host(int q, int L, std::vector<uint32_t>& v);
 
 }  // namespace gm

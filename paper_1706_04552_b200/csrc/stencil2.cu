@@ -443,20 +443,11 @@ cudaError_t launch_c(const LaunchArgs& a, int r) {
 // i.e. the same rows and DRAM pages at the same time (scripts/probe_gasket.cu:
 // tile reads 43.7 -> 48.6 G lines/s, partial-line writes 39.7 -> 44.5 G lines/s;
 // stencil n=2^17 518 -> 436 us, write pass n=2^16 118 -> 104 us).
-const uint32_t* rowmajor_table(int q, int L) {
-    static std::mutex mu;
-    static std::map<std::tuple<int, int, int>, uint32_t*> cache;
-    if (q > 15 || L > q) return nullptr;  // caller falls back to digit order
-    int dev = 0;
-    cudaGetDevice(&dev);
-    std::lock_guard<std::mutex> lock(mu);
-    const auto key = std::make_tuple(dev, q, L);
-    auto it = cache.find(key);
-    if (it != cache.end()) return it->second;
+void rowmajor_order_host(int q, int L, std::vector<uint32_t>& v) {
     uint64_t nsg = 1;
     for (int i = 0; i < L; ++i) nsg *= 3u;
     const int m = q - L;
-    std::vector<uint32_t> v;
+    v.clear();
     for (uint64_t sg = 0; sg < nsg; ++sg) {
         uint32_t sx = 0, sy = 0, d = (uint32_t)sg;
         for (int i = 0; i < L; ++i, d /= 3u) {  // digit i -> level i+1: 1 = (0,1), 2 = (1,1)
@@ -471,9 +462,27 @@ const uint32_t* rowmajor_table(int q, int L) {
             std::reverse(v.end() - (1u << __builtin_popcount(Y)), v.end());
         }
     }
+}
+
+const uint32_t* rowmajor_table(int q, int L) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, int>, uint32_t*> cache;
+    if (q > 15 || L > q || L < 0) return nullptr;  // caller falls back to digit order
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    const auto key = std::make_tuple(dev, q, L);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    std::vector<uint32_t> v;
+    rowmajor_order_host(q, L, v);
     uint32_t* d_tab = nullptr;
-    if (cudaMalloc(&d_tab, v.size() * sizeof(uint32_t)) != cudaSuccess) return nullptr;
+    if (cudaMalloc(&d_tab, v.size() * sizeof(uint32_t)) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
     if (cudaMemcpy(d_tab, v.data(), v.size() * sizeof(uint32_t), cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaGetLastError();
         cudaFree(d_tab);
         return nullptr;
     }

@@ -69,6 +69,7 @@ _SIGS = {
     "gm_run_part": [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, ctypes.c_uint32, ctypes.c_uint32, _vp],
     "gm_gather_cells": [_vp, _i32, _vp, _i64, _vp, _vp],
     "gm_scatter_cells": [_vp, _i32, _vp, _i64, _vp, _vp],
+    "gm_tile_order": [_i32, _i32, _vp, _i64],
 }
 
 # Every symbol include/gasket_b200.h declares (checked by tests/test_native_abi.py).
@@ -122,3 +123,12 @@ def launch_count() -> int:
 
 def version() -> str:
     return lib().gm_version().decode()
+
+
+def tile_order(q: int, level: int = 0):
+    """The tuned kernels' tile visiting order (gm_tile_order): (bx, by) int64 arrays."""
+    import numpy as np
+
+    out = np.zeros(3**q, dtype=np.uint32)
+    check(lib().gm_tile_order(q, level, out.ctypes.data, out.size))
+    return (out & 0xFFFF).astype(np.int64), (out >> 16).astype(np.int64)
