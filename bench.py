@@ -265,6 +265,36 @@ def _sweep(r: int, dtype, flusher, budget_s: float = 3.0) -> dict:
             "summary": summary}
 
 
+def _multi_step(r: int, tdt, kind: int, flusher, steps: int = 40) -> dict:
+    """The multi-step CA driver (ca.CARunner): single-step launches vs two fused steps
+    per launch (temporal blocking, stencil_tb.cu), CUDA graphs, L2 flushed once before
+    the run.  Not the headline: `value` above is one step = one pass."""
+    import torch
+
+    from paper_1706_04552_b200 import ca, device
+
+    n = 1 << r
+    out = {"steps": steps, "l2": "flushed once before the run (the state never fits L2)"}
+    for temporal in (1, 2):
+        g = device.fill_hash(n, tdt, 1, 0)
+        run = ca.CARunner(g, kind=kind, param=1, use_graph=True, temporal=temporal)
+        run.run(8)  # warm-up + graph capture
+        torch.cuda.synchronize()
+        flusher()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        run.run(steps)
+        b.record()
+        b.synchronize()
+        ms = a.elapsed_time(b) / steps
+        out[f"temporal{temporal}"] = {"ms_per_step": ms, "cells_per_s": 3**r / (ms * 1e-3),
+                                      "steps_per_launch": temporal}
+        del run, g
+        torch.cuda.empty_cache()
+    out["speedup_fused"] = out["temporal1"]["ms_per_step"] / out["temporal2"]["ms_per_step"]
+    return out
+
+
 def _e2e(workload: str, rho: int, steps: int) -> dict:
     """The reference-facing call (backends.run_block_space on host numpy grids)."""
     import numpy as np
@@ -464,6 +494,8 @@ def run_ours(args) -> None:
     if rank == 0 and world == 1 and not workload.startswith("part"):
         if not args.no_sweep and kind == 0:
             line["sweep"] = _sweep(r, tdt, flusher)
+        if kind != 0 and c in (1, 2, 4):
+            line["multi_step"] = _multi_step(r, tdt, kind, flusher)
         if not args.no_e2e:
             line["e2e"] = _e2e(workload, rho, steps=max(3, min(args.steps, 10)))
         if not args.no_cpu:

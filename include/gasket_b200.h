@@ -157,6 +157,12 @@ int gm_host_unmap(void* host);
 int gm_set_l2_fetch_granularity(int32_t bytes);
 
 /* Number of kernels this library has launched (all entry points). */
+/* Two CA steps in one pass (temporal blocking, stencil_tb.cu): grid <- kind(kind(src)),
+ * each step the neighbour-sum launch with engine.launch's snapshot semantics.
+ * Precondition (the CA ping-pong invariant): grid == src on every off-gasket cell.
+ * kind = GM_KIND_NSUM4 or GM_KIND_NSUM8; 1-, 2- or 4-byte cells; async on `stream`. */
+int gm_ca_step2(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
+                int32_t flags, void* stream);
 /* The tuned kernels' tile visiting order (host-side, no GPU needed): the 3^q
  * member tiles of a level-q gasket as bx | by << 16, level-`level` sub-gaskets in
  * lambda digit order, row-major inside each.  out must hold 3^q entries. */

@@ -306,6 +306,29 @@ int gm_set_l2_fetch_granularity(int32_t bytes) {
     return cuda_rc(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)bytes), "cudaDeviceSetLimit");
 }
 
+int gm_ca_step2(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
+                int32_t flags, void* stream) {
+    gm_cfg_t c{};
+    c.n = n;
+    c.rho = 1;
+    c.mapping = GM_MAP_LAMBDA;
+    c.strategy = GM_STRAT_TUNED;
+    c.kind = kind;
+    c.cell_bytes = cell_bytes;
+    c.param = param;
+    c.flags = flags;
+    if (int rc = check_common(n, cell_bytes, 1, kind)) return rc;
+    if (kind != GM_KIND_NSUM4 && kind != GM_KIND_NSUM8) return fail(GM_EINVAL, "gm_ca_step2: kind must be NSUM4 or NSUM8");
+    if (!grid || !src || src == grid) return fail(GM_EINVAL, "gm_ca_step2 needs distinct grid and src buffers");
+    gm::LaunchArgs a = make_args(&c, grid, src, nullptr, nullptr, 0, stream);
+    const cudaError_t e = gm::launch_stencil_tb2(a);
+    if (e == cudaErrorNotSupported) {
+        cudaGetLastError();
+        return fail(GM_EINVAL, "gm_ca_step2: needs 1-, 2- or 4-byte cells and n >= one 128-byte tile (<= 2^15 tiles per edge)");
+    }
+    return cuda_rc(e, "two-step CA launch");
+}
+
 int gm_tile_order(int32_t q, int32_t level, uint32_t* out, int64_t capacity) {
     if (q < 0 || q > 15 || level < 0 || level > q || out == nullptr) return fail(GM_EINVAL, "gm_tile_order: bad q/level");
     std::vector<uint32_t> v;

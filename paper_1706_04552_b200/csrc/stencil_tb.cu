@@ -1,0 +1,376 @@
+// stencil_tb.cu -- two CA steps fused in one pass over memory (temporal
+// blocking), for the multi-step CA driver (ca.py).
+//
+// A CA step is the reference's neighbour-sum launch with engine.launch's
+// snapshot semantics (engine.py:201; backends.py:127-141 for 4 neighbours, our
+// labelled 8-neighbour extension): state t+1 = param + sum of the in-grid
+// neighbours of state t on gasket cells, state t elsewhere (off-gasket cells
+// never change).  The single-step kernel (stencil2.cu) is bound by the DRAM
+// access pattern of one read of the dilated gasket + one partial-line write
+// per step; this kernel does that traffic once per TWO steps:
+//
+//   per lambda tile (TT x TT cells, rows one 128-byte line; CTAs in the row-major
+//   tile order of stencil2.cu):
+//   1. stage state t on rows -2..TT+1 (16-byte halo chunk each side) -- only the
+//      chunks phase 1 or the off-gasket blend read (host-precomputed list);
+//   2. phase 1: state t+1 on every 4-byte word of rows -1..TT holding a cell
+//      that a gasket cell of the tile reads (its 4/8-neighbourhood and itself):
+//      words that can hold gasket cells are computed (exact global membership
+//      (x & ~y) == 0 and in-grid, so ring words of non-gasket neighbour tiles
+//      stay state t), the others copied -- the ring belongs to neighbouring
+//      tiles and is computed redundantly (overlapped tiling);
+//   3. phase 2: state t+2 on the tile's words that hold gasket cells, into a
+//      shared-memory output tile;
+//   4. every touched sector stored whole, off-gasket cells from state t (the
+//      CA invariant that both ping-pong buffers agree off the gasket).
+// Work is per word, not per sector: only ~42% of a touched sector's words hold
+// gasket cells, and the fused pass is arithmetic-heavy (two steps per tile).
+// Work lists are host-precomputed (tile-independent supersets).  Arithmetic:
+// the split-lane SIMD of stencil_common.cuh.  Results are bit-identical to two
+// single steps (tests/test_gpu_parity.py).
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <vector>
+
+#include "gasket.cuh"
+#include "launch.h"
+#include "stencil_common.cuh"
+#include "../../include/gasket_b200.h"
+
+namespace gm {
+namespace {
+
+using namespace sc;
+
+constexpr int ROWB = 128;
+constexpr int PITCH = ROWB + 48;  // 16 B halo | 128 B row | 16 B halo | 16 B pad
+constexpr int CHUNKS = 10;
+
+template <int C>
+struct TB {
+    static constexpr int V = 4 / C;
+    static constexpr int TT = ROWB / C;
+    static constexpr int SC = 32 / C;
+    static constexpr int CC = 16 / C;          // cells per chunk
+    static constexpr int SROWS = TT + 4;       // state-t rows -2 .. TT+1
+    static constexpr int IROWS = TT + 2;       // state-t+1 rows -1 .. TT
+    static constexpr int SBUF = SROWS * PITCH;
+    static constexpr int IBUF = IROWS * PITCH;
+    static constexpr int NTOUCH = 9 * SC;
+    static constexpr int THREADS = (NTOUCH + 31) / 32 * 32;
+};
+
+// gasket cells of a word whose first cell is (x, y) (x a multiple of the word's
+// cell count, so x + j = x | j): all-or-nothing on x, then the pattern of y's low bits
+template <int C>
+__device__ __forceinline__ uint32_t word_mask(int64_t x, int64_t y, int64_t n) {
+    const bool in = y >= 0 && y < n && x >= 0 && x < n && (x & ~y) == 0;
+    return in ? member_mask<C>((uint32_t)y) : 0u;
+}
+
+// word k (0..39, 4 halo words each side) of staged rows ji-1+0..2 -> one result word
+template <int C, bool EIGHT>
+__device__ __forceinline__ uint32_t word_sum(const uint8_t* rows, int k, uint32_t pv, uint32_t& centre) {
+    uint32_t w[3][3];
+#pragma unroll
+    for (int rr = 0; rr < 3; ++rr) {
+        const uint32_t* row = reinterpret_cast<const uint32_t*>(rows + rr * PITCH);
+        w[rr][0] = row[k - 1];
+        w[rr][1] = row[k];
+        w[rr][2] = row[k + 1];
+    }
+    uint32_t o[1];
+    sector_sums<C, EIGHT, 1>(w, pv, o);
+    centre = w[1][1];
+    return o[0];
+}
+
+template <int C, int KIND, int NST>
+__global__ void __launch_bounds__(TB<C>::THREADS)
+    stencil_tb2(uint8_t* __restrict__ grid, const uint8_t* __restrict__ src, int64_t n, uint32_t ntiles,
+                uint64_t param, const uint32_t* __restrict__ order, const uint32_t* __restrict__ lists_g, int ns,
+                int np1, int ng1, int np2) {
+    using S = TB<C>;
+    constexpr bool EIGHT = KIND == KIND_NSUM8;
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint8_t* ibuf = smem + NST * S::SBUF;          // state t+1, rows -1..TT
+    uint8_t* obuf = ibuf + S::IBUF;                // state t+2 words, rows 0..TT-1
+    uint32_t* slist = reinterpret_cast<uint32_t*>(obuf + S::TT * PITCH);
+    uint32_t* p1list = slist + ns;                 // (I row << 8 | word), gasket-capable words first
+    uint32_t* p2list = p1list + np1;               // (tile row << 8 | word) holding gasket cells
+    for (int i = threadIdx.x; i < ns + np1 + np2; i += S::THREADS) slist[i] = lists_g[i];
+    __syncthreads();
+
+    const int64_t rowstride = n * C;
+    const bool v8 = (reinterpret_cast<uintptr_t>(grid) & 31u) == 0;
+    const uint32_t smem0 = (uint32_t)__cvta_generic_to_shared(smem);
+    uint32_t pv;
+    if constexpr (C == 1) pv = 0x00010001u * (uint32_t)(param & 0xffu);
+    else if constexpr (C == 2) pv = (uint32_t)(param & 0xffffu);
+    else pv = (uint32_t)param;
+
+    // store-pass thread -> touched sector (t, g), as stencil2.cu
+    const int e = threadIdx.x;
+    int h, off;
+    if (e < S::SC) { h = 0; off = 0; }
+    else if (e < 3 * S::SC) { h = 1; off = S::SC; }
+    else if (e < 5 * S::SC) { h = 2; off = 3 * S::SC; }
+    else { h = 3; off = 5 * S::SC; }
+    const int per_row = h == 0 ? 1 : h == 3 ? 4 : 2;
+    const int t = h * S::SC + (e - off) / per_row;
+    const int ii = (e - off) % per_row;
+    const int g = h == 2 ? 2 * ii : ii;
+    const bool active = e < S::NTOUCH;
+    const uint32_t tmask = member_mask<C>((uint32_t)t);
+    uint32_t wmask[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) wmask[i] = (((8 * g + i) * S::V) & ~t) == 0 ? tmask : 0u;
+
+    const uint32_t count = blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
+    auto tile_xy = [&](uint32_t idx, int64_t& x0, int64_t& y0) {
+        const uint32_t v = __ldg(order + blockIdx.x + idx * gridDim.x);
+        x0 = (int64_t)(v & 0xffffu) * S::TT;
+        y0 = (int64_t)(v >> 16) * S::TT;
+    };
+    auto stage = [&](uint32_t idx) {
+        if (idx >= count) return;
+        int64_t x0, y0;
+        tile_xy(idx, x0, y0);
+        const uint32_t sb = smem0 + (idx % NST) * S::SBUF;
+        const uint8_t* base = src + (y0 - 2) * rowstride + x0 * C - 16;  // staged (row -2, chunk 0)
+        const bool interior = y0 >= 2 && y0 + S::TT + 2 <= n && x0 > 0 && x0 + S::TT < n;
+        for (int i = threadIdx.x; i < ns; i += S::THREADS) {
+            const uint32_t c = slist[i];
+            const int j = (int)((c >> 16) & 0xffu), q = (int)(c >> 24);
+            if (interior) {
+                cp_async16(sb + (c & 0xffffu), base + (int64_t)j * rowstride + q * 16, 16, false);
+            } else {
+                const int64_t y = y0 + j - 2;
+                const int64_t xb = x0 * C + (q - 1) * 16;
+                const bool in = y >= 0 && y < n && xb >= 0 && xb < rowstride;
+                cp_async16(sb + (c & 0xffffu), in ? src + y * rowstride + xb : src, in ? 16 : 0, false);
+            }
+        }
+    };
+
+#pragma unroll
+    for (int s = 0; s < NST - 1; ++s) {
+        stage((uint32_t)s);
+        cp_async_commit();
+    }
+    for (uint32_t idx = 0; idx < count; ++idx) {
+        cp_async_wait<NST - 2>();
+        __syncthreads();  // state t of tile idx staged; tile idx-1 fully stored (I, O and its S slot free)
+        stage(idx + NST - 1);
+        cp_async_commit();
+        int64_t x0, y0;
+        tile_xy(idx, x0, y0);
+        const uint8_t* sbuf = smem + (idx % NST) * S::SBUF;
+
+        // ---- phase 1: state t+1 on the listed words of rows -1..TT (I row ji = r + 1 = S row ji + 1)
+        for (int i = threadIdx.x; i < np1; i += S::THREADS) {
+            const uint32_t c = p1list[i];
+            const int ji = (int)(c >> 8), k = (int)(c & 0xffu);
+            uint32_t v;
+            if (i < ng1) {  // may hold gasket cells: compute, keep state t on the others
+                uint32_t centre;
+                const uint32_t sum = word_sum<C, EIGHT>(sbuf + ji * PITCH, k, pv, centre);
+                const uint32_t m = word_mask<C>(x0 + (int64_t)(k - 4) * S::V, y0 + ji - 1, n);
+                v = (sum & m) | (centre & ~m);
+            } else {        // off the gasket: state t
+                v = reinterpret_cast<const uint32_t*>(sbuf + (ji + 1) * PITCH)[k];
+            }
+            reinterpret_cast<uint32_t*>(ibuf + ji * PITCH)[k] = v;
+        }
+        __syncthreads();
+
+        // ---- phase 2: state t+2 on the tile's words holding gasket cells (I rows t-1..t+1)
+        for (int i = threadIdx.x; i < np2; i += S::THREADS) {
+            const uint32_t c = p2list[i];
+            const int tt = (int)(c >> 8), k = (int)(c & 0xffu);
+            uint32_t centre;
+            reinterpret_cast<uint32_t*>(obuf + tt * PITCH)[k] = word_sum<C, EIGHT>(ibuf + tt * PITCH, k, pv, centre);
+        }
+        __syncthreads();
+
+        // ---- store: every touched sector whole, off-gasket cells = state t
+        if (active) {
+            const int k0 = 4 + 8 * g;
+            const uint32_t* orow = reinterpret_cast<const uint32_t*>(obuf + t * PITCH);
+            const uint32_t* srow = reinterpret_cast<const uint32_t*>(sbuf + (t + 2) * PITCH);
+            const uint4 a = *reinterpret_cast<const uint4*>(srow + k0);
+            const uint4 b = *reinterpret_cast<const uint4*>(srow + k0 + 4);
+            const uint4 oa = *reinterpret_cast<const uint4*>(orow + k0);
+            const uint4 ob = *reinterpret_cast<const uint4*>(orow + k0 + 4);
+            const uint32_t old[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+            const uint32_t nw[8] = {oa.x, oa.y, oa.z, oa.w, ob.x, ob.y, ob.z, ob.w};
+            uint32_t out[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) out[i] = (nw[i] & wmask[i]) | (old[i] & ~wmask[i]);
+            st_sector(grid + (y0 + t) * rowstride + x0 * C + g * 32, out, v8, false);
+        }
+    }
+    cp_async_wait<0>();
+}
+
+// ---- host: the work lists (tile-independent supersets) ----------------------
+struct TbLists {
+    uint32_t* lists = nullptr;  // [staged chunks | phase-1 words | phase-2 words]
+    int ns = 0, np1 = 0, ng1 = 0, np2 = 0;
+};
+
+// Cells of the staged window: c in [-CC, TT+CC), r in [-2, TT+1]; staged word k
+// (0..39) holds cells (k-4)*V .. (k-4)*V+V-1.
+template <int C>
+void build_lists(bool eight, std::vector<uint32_t>& out, int& ns, int& np1, int& ng1, int& np2) {
+    using S = TB<C>;
+    const int TT = S::TT, CC = S::CC, V = S::V;
+    const int W = TT + 2 * CC, H = TT + 4;  // window: column c -> c + CC, row r -> r + 2
+    auto mod = [&](int v) { return ((v % TT) + TT) % TT; };
+    // superset membership: every neighbouring tile assumed to be a gasket tile
+    auto member_sup = [&](int c, int r) { return (mod(c) & ~mod(r)) == 0; };
+    auto own = [&](int c, int r) { return c >= 0 && c < TT && r >= 0 && r < TT && (c & ~r) == 0; };
+    std::vector<char> D1(W * H, 0), need(W * H, 0);
+    auto at = [&](std::vector<char>& v, int c, int r) -> char& { return v[(r + 2) * W + (c + CC)]; };
+    auto inwin = [&](int c, int r) { return c >= -CC && c < TT + CC && r >= -2 && r < TT + 2; };
+    std::vector<std::pair<int, int>> offs = {{1, 0}, {-1, 0}, {0, 1}, {0, -1}};
+    if (eight) offs.insert(offs.end(), {{1, 1}, {1, -1}, {-1, 1}, {-1, -1}});
+    // D1: cells phase 2 reads (the tile's gasket cells and their neighbours)
+    for (int r = 0; r < TT; ++r)
+        for (int c = 0; c < TT; ++c)
+            if (own(c, r)) {
+                at(D1, c, r) = 1;
+                for (auto [dx, dy] : offs) at(D1, c + dx, r + dy) = 1;
+            }
+    // state t needed: D1 itself, the neighbours of D1's (superset) gasket cells,
+    // and the tile's touched sectors whole (the off-gasket blend of the store)
+    for (int r = -1; r <= TT; ++r)
+        for (int c = -CC; c < TT + CC; ++c)
+            if (at(D1, c, r)) {
+                at(need, c, r) = 1;
+                if (member_sup(c, r))
+                    for (auto [dx, dy] : offs)
+                        if (inwin(c + dx, r + dy)) at(need, c + dx, r + dy) = 1;
+            }
+    for (int r = 0; r < TT; ++r)
+        for (int g = 0; g < ROWB / 32; ++g)
+            if (((g * S::SC) & ~r) == 0)
+                for (int c = g * S::SC; c < (g + 1) * S::SC; ++c) at(need, c, r) = 1;
+    out.clear();
+    for (int r = -2; r < TT + 2; ++r)
+        for (int q = 0; q < CHUNKS; ++q) {
+            bool any = false;
+            for (int c = (q - 1) * CC; c < q * CC; ++c) any = any || at(need, c, r);
+            const int j = r + 2;
+            if (any) out.push_back((uint32_t)(j * PITCH + q * 16) | ((uint32_t)j << 16) | ((uint32_t)q << 24));
+        }
+    ns = (int)out.size();
+    // phase 1: words of rows -1..TT holding a D1 cell; those that may hold gasket cells first
+    std::vector<uint32_t> comp, copy;
+    for (int r = -1; r <= TT; ++r)
+        for (int k = 0; k < 4 * CHUNKS; ++k) {
+            bool d = false, gsk = false;
+            for (int c = (k - 4) * V; c < (k - 3) * V; ++c) {
+                d = d || at(D1, c, r);
+                gsk = gsk || member_sup(c, r);
+            }
+            if (!d) continue;
+            (gsk ? comp : copy).push_back(((uint32_t)(r + 1) << 8) | (uint32_t)k);
+        }
+    ng1 = (int)comp.size();
+    np1 = ng1 + (int)copy.size();
+    out.insert(out.end(), comp.begin(), comp.end());
+    out.insert(out.end(), copy.begin(), copy.end());
+    // phase 2: the tile's words holding gasket cells
+    np2 = 0;
+    for (int t = 0; t < TT; ++t)
+        for (int w = 0; w < TT / V; ++w)
+            if (((w * V) & ~t) == 0) {
+                out.push_back(((uint32_t)t << 8) | (uint32_t)(w + 4));
+                ++np2;
+            }
+}
+
+template <int C>
+const TbLists* tb_lists(bool eight) {
+    static std::mutex mu;
+    static std::map<std::pair<int, bool>, TbLists> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    auto key = std::make_pair(dev, eight);
+    auto it = cache.find(key);
+    if (it != cache.end()) return &it->second;
+    std::vector<uint32_t> v;
+    TbLists L;
+    build_lists<C>(eight, v, L.ns, L.np1, L.ng1, L.np2);
+    if (cudaMalloc(&L.lists, v.size() * 4) != cudaSuccess ||
+        cudaMemcpy(L.lists, v.data(), v.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return &(cache[key] = L);
+}
+
+template <int C, int KIND, int NST>
+cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
+    using S = TB<C>;
+    uint32_t ntiles = 1;
+    for (int i = 0; i < r_t; ++i) ntiles *= 3u;
+    const TbLists* L = tb_lists<C>(KIND == KIND_NSUM8);
+    const uint32_t* order = rowmajor_table(r_t, 0);
+    if (L == nullptr || order == nullptr) return cudaErrorMemoryAllocation;
+    const size_t smem = (size_t)NST * S::SBUF + S::IBUF + (size_t)S::TT * PITCH + 4 * (size_t)(L->ns + L->np1 + L->np2);
+    auto* kern = stencil_tb2<C, KIND, NST>;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, S::THREADS, smem);
+    uint64_t blocks = (uint64_t)sms * (per_sm > 0 ? per_sm : 1);
+    if (blocks > ntiles) blocks = ntiles;
+    kern<<<(unsigned)blocks, S::THREADS, smem, a.stream>>>(reinterpret_cast<uint8_t*>(a.grid),
+                                                          reinterpret_cast<const uint8_t*>(a.src), a.n, ntiles,
+                                                          a.param, order, L->lists, L->ns, L->np1, L->ng1, L->np2);
+    note_launch();
+    return cudaGetLastError();
+}
+
+template <int C, int KIND>
+cudaError_t launch_kind(const LaunchArgs& a, int r_t) {
+    // a 2-deep ring keeps two CTAs per SM (byte cells: 110 KB of shared memory each),
+    // measured faster than a 3-deep ring at one CTA per SM (759 vs 1104 us, n=2^17)
+    return launch_ck<C, KIND, 2>(a, r_t);
+}
+
+template <int C>
+cudaError_t launch_c(const LaunchArgs& a, int r) {
+    int k = 0;
+    while ((1 << k) < TB<C>::TT) ++k;
+    if (r - k > 15) return cudaErrorNotSupported;  // tile-order table limit
+    if (a.kind == KIND_NSUM4) return launch_kind<C, KIND_NSUM4>(a, r - k);
+    if (a.kind == KIND_NSUM8) return launch_kind<C, KIND_NSUM8>(a, r - k);
+    return cudaErrorNotSupported;
+}
+
+}  // namespace
+
+// Two fused CA steps: grid <- step(step(src)); grid must equal src off the gasket.
+// cudaErrorNotSupported for grids narrower than one tile or cell widths other than 1, 2, 4.
+cudaError_t launch_stencil_tb2(const LaunchArgs& a) {
+    int r = 0;
+    while ((int64_t(1) << r) < a.n) ++r;
+    switch (a.cell_bytes) {
+    case 1: if (a.n >= TB<1>::TT) return launch_c<1>(a, r); break;
+    case 2: if (a.n >= TB<2>::TT) return launch_c<2>(a, r); break;
+    case 4: if (a.n >= TB<4>::TT) return launch_c<4>(a, r); break;
+    }
+    return cudaErrorNotSupported;
+}
+
+}  // namespace gm

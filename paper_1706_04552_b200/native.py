@@ -70,6 +70,7 @@ _SIGS = {
     "gm_gather_cells": [_vp, _i32, _vp, _i64, _vp, _vp],
     "gm_scatter_cells": [_vp, _i32, _vp, _i64, _vp, _vp],
     "gm_tile_order": [_i32, _i32, _vp, _i64],
+    "gm_ca_step2": [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _vp],
 }
 
 # Every symbol include/gasket_b200.h declares (checked by tests/test_native_abi.py).

@@ -23,7 +23,14 @@ def main():
     n = 1 << r
     flush = device.L2Flusher()
     T = IntraStrategy.TUNED
-    if wl.startswith("stencil"):
+    if wl.startswith("ca"):
+        from paper_1706_04552_b200 import native
+        kind = 1 if "nsum4" in wl else 2
+        src = device.fill_hash(n, torch.int8, 1, 0)
+        dst = src.clone()
+        fn = lambda: native.call("gm_ca_step2", dst.data_ptr(), src.data_ptr(), n, 1, kind, 1, flags,  # noqa: E731
+                                 device.stream_handle())
+    elif wl.startswith("stencil"):
         kind = 1 if "nsum4" in wl else 2
         src = device.fill_hash(n, torch.int8, 1, 0)
         dst = src.clone()

@@ -111,8 +111,29 @@ def offsets(r=17):
         torch.cuda.empty_cache()
 
 
+def ca_pairs(r=17):
+    """Two fused CA steps (gm_ca_step2) vs one single step, NSUM8/NSUM4 int8."""
+    n = 1 << r
+    flush = device.L2Flusher()
+    src = device.fill_hash(n, torch.int8, 1, 0)
+    dst = src.clone()
+    for kind in (2, 1):
+        for name, fl in (("fused pair", 0), ("fused pair stages2", native.FLAG_STAGES2)):
+            fn = lambda: native.call("gm_ca_step2", dst.data_ptr(), src.data_ptr(), n, 1, kind, 1, fl,  # noqa: E731
+                                     device.stream_handle())
+            m, mn = timeit(fn, flush, k=10)
+            print(f"ca r={r} nsum{4 * kind} {name:20s} mean {m * 1e3:8.1f} us  min {mn * 1e3:8.1f} us  "
+                  f"per step {m * 1e3 / 2:8.1f} us", flush=True)
+        T = IntraStrategy.TUNED
+        m, mn = timeit(lambda: backends.run_block_space(dst, src, 64, r - 6, T, kind=kind, param=1,
+                                                        flags=native.FLAG_DST_FROM_SRC), flush, k=10)
+        print(f"ca r={r} nsum{4 * kind} {'single step':20s} mean {m * 1e3:8.1f} us  min {mn * 1e3:8.1f} us", flush=True)
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["offsets"]:
         offsets()
+    elif sys.argv[1:] == ["ca"]:
+        ca_pairs()
     else:
         main()

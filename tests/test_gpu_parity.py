@@ -358,27 +358,55 @@ def test_launch_counter_moves(gpu):
 # multi-step CA driver (ping-pong + CUDA graph) and wide cells
 # ---------------------------------------------------------------------------
 
-@pytest.mark.parametrize("kind", [1, 2])
-def test_ca_runner_matches_oracle_steps(gpu, oracle, kind):
-    from paper_1706_04552_b200 import ca
-
-    n, steps = 512, 7
-    init = oracle.fill_hash(n, np.int8, 13, 0)
+def _oracle_steps(oracle, init, kind, param, steps):
     want = init.copy()
     for _ in range(steps):
         nxt = want.copy()
-        oracle.run_bounding_box(nxt, want, 1, kind, 3)
+        oracle.run_bounding_box(nxt, want, 1, kind, param)
         want = nxt
-    for use_graph in (False, True):
+    return want
+
+
+@pytest.mark.parametrize("kind", [1, 2])
+@pytest.mark.parametrize("temporal", [1, 2])
+def test_ca_runner_matches_oracle_steps(gpu, oracle, kind, temporal):
+    from paper_1706_04552_b200 import ca
+
+    for dtype, n in ((np.int8, 512), (np.int8, 128), (np.int16, 256), (np.int32, 64), (np.int32, 32)):
+        steps = 7
+        init = oracle.fill_hash(n, dtype, 13, 0)
+        want = _oracle_steps(oracle, init, kind, 3, steps)
+        for use_graph in (False, True):
+            g = torch.from_numpy(init.copy()).cuda()
+            runner = ca.CARunner(g, kind=kind, param=3, use_graph=use_graph, temporal=temporal)
+            out = runner.run(3)
+            out = runner.run(4)
+            assert runner.steps_done == steps
+            assert np.array_equal(out.cpu().numpy(), want), (np.dtype(dtype).name, n, use_graph)
         g = torch.from_numpy(init.copy()).cuda()
-        runner = ca.CARunner(g, kind=kind, param=3, use_graph=use_graph)
-        out = runner.run(3)
-        out = runner.run(4)
-        assert runner.steps_done == steps
-        assert np.array_equal(out.cpu().numpy(), want), use_graph
-    g = torch.from_numpy(init.copy()).cuda()
-    ca.run_ca(g, steps, kind=kind, param=3)
-    assert np.array_equal(g.cpu().numpy(), want)
+        ca.run_ca(g, 10, kind=kind, param=3, temporal=temporal)
+        assert np.array_equal(g.cpu().numpy(), _oracle_steps(oracle, init, kind, 3, 10)), (np.dtype(dtype).name, n)
+
+
+@pytest.mark.parametrize("dtype", [np.int8, np.int16, np.int32])
+def test_fused_two_steps_vs_oracle(gpu, oracle, dtype):
+    """gm_ca_step2 (two CA steps per pass) == two oracle steps, cell by cell, incl.
+    grid-edge tiles and a 2^12 grid; also on a CA state that is 0 off the gasket."""
+    from paper_1706_04552_b200 import device, native
+
+    n0 = 128 // np.dtype(dtype).itemsize
+    for n in (n0, 2 * n0, 4 * n0, 1 << 12):
+        for mode in (0, 1):
+            init = oracle.fill_hash(n, dtype, 41 + mode, mode)
+            for kind in (1, 2):
+                for param in (1, -7):
+                    want = _oracle_steps(oracle, init, kind, param, 2)
+                    src = torch.from_numpy(init.copy()).cuda()
+                    dst = src.clone()
+                    native.call("gm_ca_step2", dst.data_ptr(), src.data_ptr(), n, src.element_size(), kind, param, 0,
+                                device.stream_handle())
+                    assert np.array_equal(dst.cpu().numpy(), want), (np.dtype(dtype).name, n, mode, kind, param)
+                    assert np.array_equal(src.cpu().numpy(), init)
 
 
 @pytest.mark.parametrize("dtype", [np.int8, np.int16, np.int32])
