@@ -58,20 +58,23 @@ struct TB {
     static constexpr int SBUF = SROWS * PITCH;
     static constexpr int IBUF = IROWS * PITCH;
     static constexpr int NTOUCH = 9 * SC;
-    static constexpr int THREADS = (NTOUCH + 31) / 32 * 32;
+    // two threads per touched sector: the store pass uses the first half, the
+    // word lists of phases 1-2 all of them (latency hiding: 2 CTAs x 18 warps per SM)
+    static constexpr int THREADS = 2 * ((NTOUCH + 31) / 32 * 32);
 };
 
 // gasket cells of a word whose first cell is (x, y) (x a multiple of the word's
 // cell count, so x + j = x | j): all-or-nothing on x, then the pattern of y's low bits
 template <int C>
-__device__ __forceinline__ uint32_t word_mask(int64_t x, int64_t y, int64_t n) {
-    const bool in = y >= 0 && y < n && x >= 0 && x < n && (x & ~y) == 0;
+__device__ __forceinline__ uint32_t word_mask(int x, int y, int n) {
+    const bool in = (unsigned)y < (unsigned)n && (unsigned)x < (unsigned)n && (x & ~y) == 0;
     return in ? member_mask<C>((uint32_t)y) : 0u;
 }
 
 // word k (0..39, 4 halo words each side) of staged rows ji-1+0..2 -> one result word
 template <int C, bool EIGHT>
 __device__ __forceinline__ uint32_t word_sum(const uint8_t* rows, int k, uint32_t pv, uint32_t& centre) {
+    // rows points at row 0 of the three (k = word index relative to `rows`)
     uint32_t w[3][3];
 #pragma unroll
     for (int rr = 0; rr < 3; ++rr) {
@@ -90,15 +93,15 @@ template <int C, int KIND, int NST>
 __global__ void __launch_bounds__(TB<C>::THREADS)
     stencil_tb2(uint8_t* __restrict__ grid, const uint8_t* __restrict__ src, int64_t n, uint32_t ntiles,
                 uint64_t param, const uint32_t* __restrict__ order, const uint32_t* __restrict__ lists_g, int ns,
-                int np1, int ng1, int np2) {
+                int np1, int ng1, int ni1, int np2) {
     using S = TB<C>;
     constexpr bool EIGHT = KIND == KIND_NSUM8;
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* ibuf = smem + NST * S::SBUF;          // state t+1, rows -1..TT
     uint8_t* obuf = ibuf + S::IBUF;                // state t+2 words, rows 0..TT-1
     uint32_t* slist = reinterpret_cast<uint32_t*>(obuf + S::TT * PITCH);
-    uint32_t* p1list = slist + ns;                 // (I row << 8 | word), gasket-capable words first
-    uint32_t* p2list = p1list + np1;               // (tile row << 8 | word) holding gasket cells
+    uint32_t* p1list = slist + ns;                 // words: inner gasket, ring gasket, then copies
+    uint32_t* p2list = p1list + np1;               // the tile's words holding gasket cells
     for (int i = threadIdx.x; i < ns + np1 + np2; i += S::THREADS) slist[i] = lists_g[i];
     __syncthreads();
 
@@ -168,29 +171,36 @@ __global__ void __launch_bounds__(TB<C>::THREADS)
         tile_xy(idx, x0, y0);
         const uint8_t* sbuf = smem + (idx % NST) * S::SBUF;
 
-        // ---- phase 1: state t+1 on the listed words of rows -1..TT (I row ji = r + 1 = S row ji + 1)
+        // ---- phase 1: state t+1 on the listed words of rows -1..TT.  Entry = byte offset
+        //      of (I row ji, word k) | ji << 16 | k << 24; I row ji = S row ji + 1 = row ji - 1.
         for (int i = threadIdx.x; i < np1; i += S::THREADS) {
             const uint32_t c = p1list[i];
-            const int ji = (int)(c >> 8), k = (int)(c & 0xffu);
+            const int o = (int)(c & 0xffffu);
             uint32_t v;
             if (i < ng1) {  // may hold gasket cells: compute, keep state t on the others
                 uint32_t centre;
-                const uint32_t sum = word_sum<C, EIGHT>(sbuf + ji * PITCH, k, pv, centre);
-                const uint32_t m = word_mask<C>(x0 + (int64_t)(k - 4) * S::V, y0 + ji - 1, n);
+                const uint32_t sum = word_sum<C, EIGHT>(sbuf + o, 0, pv, centre);
+                const int ji = (int)((c >> 16) & 0xffu);
+                uint32_t m;
+                if (i < ni1) {  // inside the tile (a gasket tile): the local pattern is exact
+                    m = member_mask<C>((uint32_t)(ji - 1));
+                } else {        // ring word of a neighbouring tile: exact global test
+                    const int k = (int)(c >> 24);
+                    m = word_mask<C>((int)x0 + (k - 4) * S::V, (int)y0 + ji - 1, (int)n);
+                }
                 v = (sum & m) | (centre & ~m);
             } else {        // off the gasket: state t
-                v = reinterpret_cast<const uint32_t*>(sbuf + (ji + 1) * PITCH)[k];
+                v = *reinterpret_cast<const uint32_t*>(sbuf + o + PITCH);
             }
-            reinterpret_cast<uint32_t*>(ibuf + ji * PITCH)[k] = v;
+            *reinterpret_cast<uint32_t*>(ibuf + o) = v;
         }
         __syncthreads();
 
         // ---- phase 2: state t+2 on the tile's words holding gasket cells (I rows t-1..t+1)
         for (int i = threadIdx.x; i < np2; i += S::THREADS) {
-            const uint32_t c = p2list[i];
-            const int tt = (int)(c >> 8), k = (int)(c & 0xffu);
+            const int o = (int)p2list[i];  // byte offset of (tile row t, word k) = I row t-1 .. t+1 base
             uint32_t centre;
-            reinterpret_cast<uint32_t*>(obuf + tt * PITCH)[k] = word_sum<C, EIGHT>(ibuf + tt * PITCH, k, pv, centre);
+            *reinterpret_cast<uint32_t*>(obuf + o) = word_sum<C, EIGHT>(ibuf + o, 0, pv, centre);
         }
         __syncthreads();
 
@@ -217,13 +227,13 @@ __global__ void __launch_bounds__(TB<C>::THREADS)
 // ---- host: the work lists (tile-independent supersets) ----------------------
 struct TbLists {
     uint32_t* lists = nullptr;  // [staged chunks | phase-1 words | phase-2 words]
-    int ns = 0, np1 = 0, ng1 = 0, np2 = 0;
+    int ns = 0, np1 = 0, ng1 = 0, ni1 = 0, np2 = 0;
 };
 
 // Cells of the staged window: c in [-CC, TT+CC), r in [-2, TT+1]; staged word k
 // (0..39) holds cells (k-4)*V .. (k-4)*V+V-1.
 template <int C>
-void build_lists(bool eight, std::vector<uint32_t>& out, int& ns, int& np1, int& ng1, int& np2) {
+void build_lists(bool eight, std::vector<uint32_t>& out, int& ns, int& np1, int& ng1, int& ni1, int& np2) {
     using S = TB<C>;
     const int TT = S::TT, CC = S::CC, V = S::V;
     const int W = TT + 2 * CC, H = TT + 4;  // window: column c -> c + CC, row r -> r + 2
@@ -266,8 +276,10 @@ void build_lists(bool eight, std::vector<uint32_t>& out, int& ns, int& np1, int&
             if (any) out.push_back((uint32_t)(j * PITCH + q * 16) | ((uint32_t)j << 16) | ((uint32_t)q << 24));
         }
     ns = (int)out.size();
-    // phase 1: words of rows -1..TT holding a D1 cell; those that may hold gasket cells first
-    std::vector<uint32_t> comp, copy;
+    // phase 1: words of rows -1..TT holding a D1 cell: inner words that hold gasket
+    // cells, ring words that may (neighbouring tile assumed a gasket tile), then the
+    // rest (copied).  Entry: byte offset (I row ji, word k) | ji << 16 | k << 24.
+    std::vector<uint32_t> inner, ring, copy;
     for (int r = -1; r <= TT; ++r)
         for (int k = 0; k < 4 * CHUNKS; ++k) {
             bool d = false, gsk = false;
@@ -276,18 +288,24 @@ void build_lists(bool eight, std::vector<uint32_t>& out, int& ns, int& np1, int&
                 gsk = gsk || member_sup(c, r);
             }
             if (!d) continue;
-            (gsk ? comp : copy).push_back(((uint32_t)(r + 1) << 8) | (uint32_t)k);
+            const int ji = r + 1;
+            const uint32_t e = (uint32_t)(ji * PITCH + k * 4) | ((uint32_t)ji << 16) | ((uint32_t)k << 24);
+            const bool in_tile = r >= 0 && r < TT && k >= 4 && k < 4 + TT / V;
+            (gsk ? (in_tile ? inner : ring) : copy).push_back(e);
         }
-    ng1 = (int)comp.size();
+    ni1 = (int)inner.size();
+    ng1 = ni1 + (int)ring.size();
     np1 = ng1 + (int)copy.size();
-    out.insert(out.end(), comp.begin(), comp.end());
+    out.insert(out.end(), inner.begin(), inner.end());
+    out.insert(out.end(), ring.begin(), ring.end());
     out.insert(out.end(), copy.begin(), copy.end());
-    // phase 2: the tile's words holding gasket cells
+    // phase 2: the tile's words holding gasket cells, as the byte offset of
+    // (I row t, word k) = (O row t, word k): I rows t..t+2 are tile rows t-1..t+1
     np2 = 0;
     for (int t = 0; t < TT; ++t)
         for (int w = 0; w < TT / V; ++w)
             if (((w * V) & ~t) == 0) {
-                out.push_back(((uint32_t)t << 8) | (uint32_t)(w + 4));
+                out.push_back((uint32_t)(t * PITCH + (w + 4) * 4));
                 ++np2;
             }
 }
@@ -304,7 +322,7 @@ const TbLists* tb_lists(bool eight) {
     if (it != cache.end()) return &it->second;
     std::vector<uint32_t> v;
     TbLists L;
-    build_lists<C>(eight, v, L.ns, L.np1, L.ng1, L.np2);
+    build_lists<C>(eight, v, L.ns, L.np1, L.ng1, L.ni1, L.np2);
     if (cudaMalloc(&L.lists, v.size() * 4) != cudaSuccess ||
         cudaMemcpy(L.lists, v.data(), v.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
         cudaGetLastError();
@@ -336,7 +354,7 @@ cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
     if (blocks > ntiles) blocks = ntiles;
     kern<<<(unsigned)blocks, S::THREADS, smem, a.stream>>>(reinterpret_cast<uint8_t*>(a.grid),
                                                           reinterpret_cast<const uint8_t*>(a.src), a.n, ntiles,
-                                                          a.param, order, L->lists, L->ns, L->np1, L->ng1, L->np2);
+                                                          a.param, order, L->lists, L->ns, L->np1, L->ng1, L->ni1, L->np2);
     note_launch();
     return cudaGetLastError();
 }
