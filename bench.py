@@ -54,6 +54,23 @@ PART_LEVEL = 5
 FALLBACK_HBM_GBS = 6650.0
 
 
+def _metric(workload: str) -> str:
+    """The metric string both arms print (BASELINE.json metric, this workload)."""
+    r, _, _, _, desc = WORKLOADS[workload]
+    what = desc.split(',')[1].strip() if ',' in desc else ''
+    return "gasket cells/s (lambda map), n=2^%d %s; lambda-vs-BB speedup and %% HBM roofline alongside" % (r, what)
+
+
+def _config(workload: str, rho: int, world: int, partitioned: bool) -> dict:
+    """The workload description both arms print."""
+    r, _, kind, _, desc = WORKLOADS[workload]
+    return {"workload": workload, "description": desc, "n": 1 << r, "rho": rho, "mapping": "lambda",
+            "strategy": "tuned", "kind": ["const", "nsum4", "nsum8"][kind], "cells_per_step": 3**r,
+            "parallelism": (f"subgasket-partition{world} (level {PART_LEVEL})" if partitioned
+                            else f"replicas{world}" if world > 1 else "single"),
+            "l2": "flushed before every timed step (4x L2 read, outside the events)"}
+
+
 def _peaks() -> tuple[float, str]:
     p = ROOT / "MEASURED_PEAKS.json"
     try:
@@ -454,7 +471,7 @@ def run_ours(args) -> None:
     achieved = alg_bytes / (statistics.fmean(ms) * 1e-3) / 1e9
     traffic = _traffic_from_profiles(workload)
     line = {
-        "metric": "gasket cells/s (lambda map), n=2^%d %s; lambda-vs-BB speedup and %% HBM roofline alongside" % (r, desc.split(',')[1].strip() if ',' in desc else ''),
+        "metric": _metric(workload),
         "value": value,
         "unit": "cells/s",
         "n_gpus": world,
@@ -466,11 +483,7 @@ def run_ours(args) -> None:
         "vs_baseline": None,
         "dtype": {"int8": "i8", "int32": "i32"}[dname],
         "data": "synthetic (zero grid, param=1)" if kind == 0 else "synthetic (splitmix64 hash states, all cells)",
-        "config": {"workload": workload, "description": desc, "n": n, "rho": rho, "mapping": "lambda",
-                   "strategy": "tuned", "kind": ["const", "nsum4", "nsum8"][kind], "cells_per_step": cells,
-                   "parallelism": (f"subgasket-partition{world} (level {PART_LEVEL})" if part is not None
-                                   else f"replicas{world}" if world > 1 else "single"),
-                   "l2": "flushed before every timed step (4x L2 read, outside the events)"},
+        "config": _config(workload, rho, world, part is not None),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src, "algorithmic_bytes_per_launch": alg_bytes,
                      "bytes_model": "exact 32-byte-sector minimum on the dense row-major grid (SURVEY §8d)",
@@ -541,7 +554,7 @@ def run_reference(args) -> None:
     value = 3**r_s / sec
     line = {
         "impl": "reference",
-        "metric": "gasket cells/s (lambda map)",
+        "metric": _metric(workload),
         "value": value,
         "unit": "cells/s",
         "n_gpus": world,
@@ -553,9 +566,11 @@ def run_reference(args) -> None:
         "vs_baseline": None,
         "dtype": {"int8": "i8", "int32": "i32"}[dname],
         "data": "synthetic",
-        "config": {"workload": workload, "description": desc, "sample_n": n, "rho": rho, "strategy": "table"},
+        "config": _config(workload, WORKLOADS[workload][3], world, workload.startswith("part")),
         "cpu_baseline": {"value": value, "unit": "cells/s", "cores": oracle.max_threads(), "kind": "port",
-                         "sample": f"lambda TABLE rho=16 pass over n=2^{r_s} {dname} per step"},
+                         "sample": f"one lambda TABLE rho=16 pass over n=2^{r_s} {dname} per step "
+                                   f"(oracle/gasket_oracle.c, the reference's numba kernel restated; cells/s is "
+                                   f"size-independent for this pass)"},
         "e2e": {"value": value, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

@@ -231,6 +231,27 @@ __global__ void __launch_bounds__(256) lambda_stream(uint8_t* __restrict__ grid,
         }
         uint8_t* drow = grid + (y0 + t0) * rowstride + x0 * C + lane * G::WB;
 
+        if constexpr (KIND == KIND_CONST) {
+            // GM_FLAG_PREFETCH_AHEAD (interleaved order): pull the lines this warp stores
+            // PF units from now into L2, so the partial-sector stores merge into resident
+            // sectors instead of each waiting for its own read-modify-write fill
+            if (interleave && (flags & GM_FLAG_PREFETCH_AHEAD)) {
+                constexpr int PF = 2;
+                const uint64_t uf = u + PF * u_step;
+                if (uf < u_end) {
+                    const uint32_t ftile = (uint32_t)(uf >> band_shift);
+                    const int ft0 = (int)(uf & ((1u << band_shift) - 1u)) * BAND;
+                    const uint32_t v = __ldg(order + ftile);
+                    const uint8_t* frow = grid + ((int64_t)(v >> 16) * G::TT + ft0) * rowstride +
+                                          (int64_t)(v & 0xffffu) * G::TT * C + lane * G::WB;
+#pragma unroll
+                    for (int i = 0; i < BAND; ++i)
+                        if ((c0 & ~(ft0 + i)) == 0)
+                            asm volatile("prefetch.global.L2 [%0];" ::"l"(frow + (int64_t)i * rowstride));
+                }
+            }
+        }
+
         if constexpr (KIND == KIND_COUNT) {
 #pragma unroll
             for (int i = 0; i < BAND; ++i) {
