@@ -70,6 +70,7 @@ extern "C" {
 #define GM_FLAG_STORE_CS 131072   /* tuned write pass / stencil v2: streaming (evict-first) stores */
 #define GM_FLAG_BAND_MAJOR 262144 /* tuned write pass: hand out (band, tile) units band-major */
 #define GM_FLAG_PREFETCH_AHEAD 524288 /* tuned write pass: L2-prefetch the lines of the unit two ahead */
+#define GM_FLAG_FETCH_MIXED 1048576   /* stencil v2: whole-line fetch for lines needed in both halves */
 
 #define GM_OK 0
 #define GM_EINVAL 1  /* bad shape / size / tag (the reference's ValueError) */

@@ -112,9 +112,18 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
             const int j = i / CHUNKS, q = i - j * CHUNKS;
             const bool need = i < S::ROWS * CHUNKS && chunk_needed<C, EIGHT>(j, q);
             const unsigned m = __ballot_sync(0xffffffffu, need);
+            // bit 28: the tile's own line needs chunks in both 64-byte halves -> fetch it
+            // whole (one DRAM access instead of two; GM_FLAG_FETCH_MIXED)
+            bool both = false;
+            if (need && q >= 1 && q <= 8) {
+                bool lo = false, hi = false;
+                for (int qq = 1; qq <= 4; ++qq) lo = lo || chunk_needed<C, EIGHT>(j, qq);
+                for (int qq = 5; qq <= 8; ++qq) hi = hi || chunk_needed<C, EIGHT>(j, qq);
+                both = lo && hi;
+            }
             if (need)
                 chunks[cnt + __popc(m & ((1u << threadIdx.x) - 1u))] =
-                    (uint32_t)(j * PITCH + q * 16) | ((uint32_t)j << 16) | ((uint32_t)q << 24);
+                    (uint32_t)(j * PITCH + q * 16) | ((uint32_t)j << 16) | ((uint32_t)q << 24) | ((uint32_t)both << 28);
             cnt += __popc(m);
         }
         if (threadIdx.x == 0) nchunks = cnt;
@@ -124,6 +133,7 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
     const int64_t rowstride = n * C;
     const bool dst_from_src = (flags & GM_FLAG_DST_FROM_SRC) != 0;
     const bool fetch_line = (flags & GM_FLAG_FETCH_LINE) != 0;
+    const bool fetch_mixed = (flags & GM_FLAG_FETCH_MIXED) != 0;
     const bool v8 = (reinterpret_cast<uintptr_t>(grid) & 31u) == 0;
     const bool probe_nostore = (flags & GM_FLAG_PROBE_NOSTORE) != 0;
     const bool probe_noload = (flags & GM_FLAG_PROBE_NOLOAD) != 0;
@@ -184,17 +194,19 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
         if (interior) {
             for (int i = threadIdx.x; i < nch; i += S::THREADS) {
                 const uint32_t c = chunks[i];
-                const uint32_t j = (c >> 16) & 0xffu, qq = c >> 24;
-                cp_async16(sb + (c & 0xffffu), base + (int64_t)j * rowstride + qq * 16, 16, fetch_line);
+                const uint32_t j = (c >> 16) & 0xffu, qq = (c >> 24) & 15u;
+                cp_async16(sb + (c & 0xffffu), base + (int64_t)j * rowstride + qq * 16, 16,
+                           fetch_line || (fetch_mixed && (c >> 28)));
             }
         } else {
             for (int i = threadIdx.x; i < nch; i += S::THREADS) {
                 const uint32_t c = chunks[i];
-                const int j = (int)((c >> 16) & 0xffu), qq = (int)(c >> 24);
+                const int j = (int)((c >> 16) & 0xffu), qq = (int)((c >> 24) & 15u);
                 const int64_t y = y0 + j - 1;
                 const int64_t xb = x0 * C + (qq - 1) * 16;
                 const bool in = y >= 0 && y < n && xb >= 0 && xb < rowstride;
-                cp_async16(sb + (c & 0xffffu), in ? src + y * rowstride + xb : src, in ? 16 : 0, fetch_line);
+                cp_async16(sb + (c & 0xffffu), in ? src + y * rowstride + xb : src, in ? 16 : 0,
+                           fetch_line || (fetch_mixed && (c >> 28)));
             }
         }
     };

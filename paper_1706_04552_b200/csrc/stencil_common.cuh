@@ -10,7 +10,8 @@ namespace sc {
 
 __device__ __forceinline__ void cp_async16(uint32_t smem, const void* gmem, int src_bytes, bool line) {
     if (line)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem), "l"(gmem), "r"(src_bytes) : "memory");
+        asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16, %2;" ::"r"(smem), "l"(gmem), "r"(src_bytes)
+                     : "memory");
     else
         asm volatile("cp.async.cg.shared.global.L2::64B [%0], [%1], 16, %2;" ::"r"(smem), "l"(gmem), "r"(src_bytes)
                      : "memory");

@@ -19,8 +19,8 @@
 //      (x & ~y) == 0 and in-grid, so ring words of non-gasket neighbour tiles
 //      stay state t), the others copied -- the ring belongs to neighbouring
 //      tiles and is computed redundantly (overlapped tiling);
-//   3. phase 2: state t+2 on the tile's words that hold gasket cells, into a
-//      shared-memory output tile;
+//   3. phase 2: state t+2 on the tile's words that hold gasket cells, written
+//      over state t in the staging slot;
 //   4. every touched sector stored whole, off-gasket cells from state t (the
 //      CA invariant that both ping-pong buffers agree off the gasket).
 // Work is per word, not per sector: only ~42% of a touched sector's words hold
@@ -98,8 +98,7 @@ __global__ void __launch_bounds__(TB<C>::THREADS)
     constexpr bool EIGHT = KIND == KIND_NSUM8;
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* ibuf = smem + NST * S::SBUF;          // state t+1, rows -1..TT
-    uint8_t* obuf = ibuf + S::IBUF;                // state t+2 words, rows 0..TT-1
-    uint32_t* slist = reinterpret_cast<uint32_t*>(obuf + S::TT * PITCH);
+    uint32_t* slist = reinterpret_cast<uint32_t*>(ibuf + S::IBUF);
     uint32_t* p1list = slist + ns;                 // words: inner gasket, ring gasket, then copies
     uint32_t* p2list = p1list + np1;               // the tile's words holding gasket cells
     for (int i = threadIdx.x; i < ns + np1 + np2; i += S::THREADS) slist[i] = lists_g[i];
@@ -125,10 +124,6 @@ __global__ void __launch_bounds__(TB<C>::THREADS)
     const int ii = (e - off) % per_row;
     const int g = h == 2 ? 2 * ii : ii;
     const bool active = e < S::NTOUCH;
-    const uint32_t tmask = member_mask<C>((uint32_t)t);
-    uint32_t wmask[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) wmask[i] = (((8 * g + i) * S::V) & ~t) == 0 ? tmask : 0u;
 
     const uint32_t count = blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
     auto tile_xy = [&](uint32_t idx, int64_t& x0, int64_t& y0) {
@@ -196,28 +191,27 @@ __global__ void __launch_bounds__(TB<C>::THREADS)
         }
         __syncthreads();
 
-        // ---- phase 2: state t+2 on the tile's words holding gasket cells (I rows t-1..t+1)
+        // ---- phase 2: state t+2 on the tile's words holding gasket cells (I rows t-1..t+1),
+        //      blended with state t and written over state t in the staging slot (phase 1
+        //      is done with it; the store pass below reads the slot)
         for (int i = threadIdx.x; i < np2; i += S::THREADS) {
-            const int o = (int)p2list[i];  // byte offset of (tile row t, word k) = I row t-1 .. t+1 base
+            const uint32_t c = p2list[i];  // byte offset of (I row t, word k) | t << 16
+            const int o = (int)(c & 0xffffu);
             uint32_t centre;
-            *reinterpret_cast<uint32_t*>(obuf + o) = word_sum<C, EIGHT>(ibuf + o, 0, pv, centre);
+            const uint32_t sum = word_sum<C, EIGHT>(ibuf + o, 0, pv, centre);
+            uint32_t* sp = reinterpret_cast<uint32_t*>(const_cast<uint8_t*>(sbuf) + o + 2 * PITCH);
+            const uint32_t m = member_mask<C>(c >> 16);
+            *sp = (sum & m) | (*sp & ~m);
         }
         __syncthreads();
 
-        // ---- store: every touched sector whole, off-gasket cells = state t
+        // ---- store: every touched sector whole (its slot row now holds state t+2)
         if (active) {
             const int k0 = 4 + 8 * g;
-            const uint32_t* orow = reinterpret_cast<const uint32_t*>(obuf + t * PITCH);
             const uint32_t* srow = reinterpret_cast<const uint32_t*>(sbuf + (t + 2) * PITCH);
             const uint4 a = *reinterpret_cast<const uint4*>(srow + k0);
             const uint4 b = *reinterpret_cast<const uint4*>(srow + k0 + 4);
-            const uint4 oa = *reinterpret_cast<const uint4*>(orow + k0);
-            const uint4 ob = *reinterpret_cast<const uint4*>(orow + k0 + 4);
-            const uint32_t old[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-            const uint32_t nw[8] = {oa.x, oa.y, oa.z, oa.w, ob.x, ob.y, ob.z, ob.w};
-            uint32_t out[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) out[i] = (nw[i] & wmask[i]) | (old[i] & ~wmask[i]);
+            const uint32_t out[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
             st_sector(grid + (y0 + t) * rowstride + x0 * C + g * 32, out, v8, false);
         }
     }
@@ -305,7 +299,7 @@ void build_lists(bool eight, std::vector<uint32_t>& out, int& ns, int& np1, int&
     for (int t = 0; t < TT; ++t)
         for (int w = 0; w < TT / V; ++w)
             if (((w * V) & ~t) == 0) {
-                out.push_back((uint32_t)(t * PITCH + (w + 4) * 4));
+                out.push_back((uint32_t)(t * PITCH + (w + 4) * 4) | ((uint32_t)t << 16));
                 ++np2;
             }
 }
@@ -339,7 +333,7 @@ cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
     const TbLists* L = tb_lists<C>(KIND == KIND_NSUM8);
     const uint32_t* order = rowmajor_table(r_t, 0);
     if (L == nullptr || order == nullptr) return cudaErrorMemoryAllocation;
-    const size_t smem = (size_t)NST * S::SBUF + S::IBUF + (size_t)S::TT * PITCH + 4 * (size_t)(L->ns + L->np1 + L->np2);
+    const size_t smem = (size_t)NST * S::SBUF + S::IBUF + 4 * (size_t)(L->ns + L->np1 + L->np2);
     auto* kern = stencil_tb2<C, KIND, NST>;
     static bool configured = false;
     if (!configured) {

@@ -70,7 +70,7 @@ def main():
         V1, S2 = native.FLAG_STENCIL_V1, native.FLAG_STAGES2
         PN, PL = native.FLAG_PROBE_NOSTORE, native.FLAG_PROBE_NOLOAD
         DO, CS = native.FLAG_DIGIT_ORDER, native.FLAG_STORE_CS
-        for name, fl in (("v2", D), ("v2-cs", D | CS), ("v2-digit", D | DO), ("v2-stages2", D | S2),
+        for name, fl in (("v2", D), ("v2-mixed", D | native.FLAG_FETCH_MIXED), ("v2-cs", D | CS), ("v2-digit", D | DO), ("v2-stages2", D | S2),
                          ("v2-chunked", D | CH), ("probe v2 no compute", D | native.FLAG_PROBE_NOCOMPUTE),
                          ("v2-line", D | FL),
                          ("probe v2 reads only", D | PN), ("probe v2 reads only, line", D | PN | FL),
