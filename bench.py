@@ -47,6 +47,8 @@ WORKLOADS = {
     "write16-i32": (16, "int32", 0, 32, "n=2^16 gasket write pass (const 1), int32 cells, lambda map"),
     "stencil17": (17, "int8", 2, 64, "n=2^17 8-neighbour CA step, int8 states, lambda map"),
     "stencil17-nsum4": (17, "int8", 1, 64, "n=2^17 4-neighbour CA step, int8 states, lambda map"),
+    "part15": (15, "int8", 2, 0, "n=2^15 8-neighbour CA step, int8 states, level-5 sub-gasket partition (functional "
+                                 "check of the multi-rank path)"),
     "part18": (18, "int8", 2, 0, "n=2^18 8-neighbour CA step, int8 states, level-5 sub-gasket partition over "
                                  "the ranks, NCCL all_gather of the changing halo cells"),
 }
@@ -152,8 +154,14 @@ def _dist_init(ngpus: int):
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if os.environ.get("GASKET_BENCH_SHARED_GPU") == "1":
+            # functional test of the multi-rank path on a one-GPU box: every rank on
+            # cuda:0, gloo for the host plumbing (numbers are time-sliced, not a bench)
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+            return world, rank, 0
+        torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         if torch.cuda.is_available():
@@ -174,7 +182,8 @@ def _max_over_ranks(v: float, world: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dev = "cpu" if dist.get_backend() == "gloo" else "cuda"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -427,10 +436,18 @@ def run_ours(args) -> None:
         from paper_1706_04552_b200 import partition as P
 
         plan = P.PartitionPlan(n, PART_LEVEL, world, eight=kind == 2)
-        init = device.fill_hash(n, tdt, 1, 0)  # every rank holds the same initial state
-        part = P.PartitionedCA(plan, rank, init, kind, 1, group=dist.group.WORLD if world > 1 else None,
-                               adopt_init=True)
-        del init
+        group = dist.group.WORLD if world > 1 else None
+        if world > 1 and args.halo == "peer":
+            # halo over peer memory (CUDA IPC + release/acquire flags): no collective per step
+            def fill(t):
+                native.call("gm_fill_hash", t.data_ptr(), n, c, 1, 0, device.stream_handle())
+
+            part = P.PartitionedCA(plan, rank, torch.empty((n, n), dtype=tdt, device="meta"), kind, 1,
+                                   group=group, halo="peer", init_fill=fill)
+        else:
+            init = device.fill_hash(n, tdt, 1, 0)  # every rank holds the same initial state
+            part = P.PartitionedCA(plan, rank, init, kind, 1, group=group, adopt_init=True)
+            del init
         torch.cuda.empty_cache()
         if world == 1:
             step = lambda: (part.compute(), part.finish())  # noqa: E731  (no peers: nothing to exchange)
@@ -499,7 +516,10 @@ def run_ours(args) -> None:
         "timed_region_wall_s": t_wall,
     }
     if part is not None:
-        line["config"]["halo_bytes_per_step"] = part.halo.bytes_per_step if world > 1 else 0
+        line["config"]["halo_bytes_per_step"] = part.halo_bytes_per_step if world > 1 else 0
+        line["config"]["halo"] = (args.halo if world > 1 else "none (one rank)")
+        if hasattr(part, "close"):
+            part.close()
         line["config"]["subgasket_ranges"] = part.plan.ranges
         del part
     del grid, src
@@ -642,6 +662,8 @@ def main() -> None:
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--nsweep", action="store_true", help="BASELINE config 4: n sweep + crossover n0, CSV")
+    ap.add_argument("--halo", choices=("collective", "peer"), default="collective",
+                    help="part* workloads, N>1: NCCL all_gather of the halo cells, or peer-memory puts (CUDA IPC)")
     ap.add_argument("--r-min", type=int, default=8)
     ap.add_argument("--r-max", type=int, default=18)
     ap.add_argument("--nsweep-out", default="profiles/r1_nsweep.csv")

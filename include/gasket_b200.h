@@ -165,6 +165,24 @@ int gm_set_l2_fetch_granularity(int32_t bytes);
  * kind = GM_KIND_NSUM4 or GM_KIND_NSUM8; 1-, 2- or 4-byte cells; async on `stream`. */
 int gm_ca_step2(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
                 int32_t flags, void* stream);
+/* Peer-memory halo exchange of the partitioned CA (peer.cu).
+ * gm_dev_alloc/free: plain cudaMalloc'd buffers (allocation bases, so they can be
+ * exported); gm_ipc_get_handle writes a 64-byte cudaIpcMemHandle_t; gm_ipc_open_handle
+ * maps a peer's buffer.  gm_peer_halo_put copies the `count` cells at linear indices
+ * `idx` from `mine` into each peer grid (peers = device array of `world` grid
+ * pointers, own entry unused), then release-stores `epoch` into slot `rank` of each
+ * peer's flag array (peer_flags = device array of `world` flag-array pointers).
+ * gm_peer_halo_wait acquires slots != rank of the own flag array until they reach
+ * `epoch`; after timeout_ns it sets bit p of *status instead of hanging. */
+int gm_dev_alloc(int64_t bytes, void** out);
+int gm_dev_free(void* p);
+int gm_ipc_get_handle(void* base, void* handle_out);
+int gm_ipc_open_handle(const void* handle, void** out);
+int gm_ipc_close(void* p);
+int gm_peer_halo_put(const void* mine, const uint64_t* peers, const int64_t* idx, int64_t count, int32_t cell_bytes,
+                     const uint64_t* peer_flags, int32_t rank, int32_t world, uint64_t epoch, void* stream);
+int gm_peer_halo_wait(const uint64_t* flags, int32_t rank, int32_t world, uint64_t epoch, uint64_t timeout_ns,
+                      uint32_t* status, void* stream);
 /* The tuned kernels' tile visiting order (host-side, no GPU needed): the 3^q
  * member tiles of a level-q gasket as bx | by << 16, level-`level` sub-gaskets in
  * lambda digit order, row-major inside each.  out must hold 3^q entries. */

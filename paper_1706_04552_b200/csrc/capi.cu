@@ -329,6 +329,48 @@ int gm_ca_step2(void* grid, const void* src, int64_t n, int32_t cell_bytes, int3
     return cuda_rc(e, "two-step CA launch");
 }
 
+int gm_dev_alloc(int64_t bytes, void** out) {
+    if (bytes <= 0 || !out) return fail(GM_EINVAL, "gm_dev_alloc: bad size/out");
+    return cuda_rc(cudaMalloc(out, (size_t)bytes), "cudaMalloc");
+}
+
+int gm_dev_free(void* p) { return cuda_rc(cudaFree(p), "cudaFree"); }
+
+int gm_ipc_get_handle(void* base, void* handle_out) {
+    if (!base || !handle_out) return fail(GM_EINVAL, "gm_ipc_get_handle: null argument");
+    cudaIpcMemHandle_t h;
+    if (int rc = cuda_rc(cudaIpcGetMemHandle(&h, base), "cudaIpcGetMemHandle")) return rc;
+    memcpy(handle_out, &h, sizeof(h));
+    return GM_OK;
+}
+
+int gm_ipc_open_handle(const void* handle, void** out) {
+    if (!handle || !out) return fail(GM_EINVAL, "gm_ipc_open_handle: null argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    return cuda_rc(cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+}
+
+int gm_ipc_close(void* p) { return cuda_rc(cudaIpcCloseMemHandle(p), "cudaIpcCloseMemHandle"); }
+
+int gm_peer_halo_put(const void* mine, const uint64_t* peers, const int64_t* idx, int64_t count, int32_t cell_bytes,
+                     const uint64_t* peer_flags, int32_t rank, int32_t world, uint64_t epoch, void* stream) {
+    if (!mine || !peers || !peer_flags || (count && !idx) || count < 0) return fail(GM_EINVAL, "gm_peer_halo_put: bad arguments");
+    if (world < 1 || rank < 0 || rank >= world) return fail(GM_EINVAL, "gm_peer_halo_put: rank %d outside world %d", rank, world);
+    if (cell_bytes != 1 && cell_bytes != 2 && cell_bytes != 4 && cell_bytes != 8)
+        return fail(GM_EINVAL, "gm_peer_halo_put: cell_bytes must be 1, 2, 4 or 8");
+    return cuda_rc(gm::launch_peer_put(mine, peers, idx, count, cell_bytes, peer_flags, rank, world, epoch,
+                                       reinterpret_cast<cudaStream_t>(stream)), "peer_halo_put");
+}
+
+int gm_peer_halo_wait(const uint64_t* flags, int32_t rank, int32_t world, uint64_t epoch, uint64_t timeout_ns,
+                      uint32_t* status, void* stream) {
+    if (!flags || !status) return fail(GM_EINVAL, "gm_peer_halo_wait: null argument");
+    if (world < 1 || rank < 0 || rank >= world) return fail(GM_EINVAL, "gm_peer_halo_wait: rank %d outside world %d", rank, world);
+    return cuda_rc(gm::launch_peer_wait(flags, rank, world, epoch, timeout_ns, status,
+                                        reinterpret_cast<cudaStream_t>(stream)), "peer_halo_wait");
+}
+
 int gm_tile_order(int32_t q, int32_t level, uint32_t* out, int64_t capacity) {
     if (q < 0 || q > 15 || level < 0 || level > q || out == nullptr) return fail(GM_EINVAL, "gm_tile_order: bad q/level");
     std::vector<uint32_t> v;

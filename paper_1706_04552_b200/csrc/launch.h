@@ -56,5 +56,9 @@ cudaError_t launch_stencil_tb2(const LaunchArgs& a);
 // member tiles of a level-q gasket, row-major inside each level-L sub-gasket (stencil2.cu)
 const uint32_t* rowmajor_table(int q, int L);
 void rowmajor_order_host(int q, int L, std::vector<uint32_t>& v);
+cudaError_t launch_peer_put(const void* mine, const uint64_t* peers, const int64_t* idx, int64_t k, int cell_bytes,
+                            const uint64_t* peer_flags, int rank, int world, uint64_t epoch, cudaStream_t s);
+cudaError_t launch_peer_wait(const uint64_t* flags, int rank, int world, uint64_t epoch, uint64_t timeout_ns,
+                             uint32_t* status, cudaStream_t s);
 
 }  // namespace gm

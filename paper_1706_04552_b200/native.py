@@ -72,6 +72,13 @@ _SIGS = {
     "gm_scatter_cells": [_vp, _i32, _vp, _i64, _vp, _vp],
     "gm_tile_order": [_i32, _i32, _vp, _i64],
     "gm_ca_step2": [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _vp],
+    "gm_dev_alloc": [_i64, ctypes.POINTER(ctypes.c_void_p)],
+    "gm_dev_free": [_vp],
+    "gm_ipc_get_handle": [_vp, _vp],
+    "gm_ipc_open_handle": [_vp, ctypes.POINTER(ctypes.c_void_p)],
+    "gm_ipc_close": [_vp],
+    "gm_peer_halo_put": [_vp, _vp, _vp, _i64, _i32, _vp, _i32, _i32, _u64, _vp],
+    "gm_peer_halo_wait": [_vp, _i32, _i32, _u64, _u64, _vp, _vp],
 }
 
 # Every symbol include/gasket_b200.h declares (checked by tests/test_native_abi.py).

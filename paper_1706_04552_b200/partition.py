@@ -228,6 +228,119 @@ class HaloExchange:
         self.complete(grid)
 
 
+class DeviceBuffer:
+    """A plain cudaMalloc'd buffer (an allocation base, so CUDA IPC can export it),
+    viewed as a torch tensor through __cuda_array_interface__."""
+
+    _TYPESTR = {torch.int8: "|i1", torch.uint8: "|u1", torch.int16: "<i2", torch.uint16: "<u2",
+                torch.int32: "<i4", torch.int64: "<i8", torch.uint64: "<u8"}
+
+    def __init__(self, shape: tuple[int, ...], dtype: torch.dtype) -> None:
+        import ctypes
+
+        from . import native
+
+        self.shape, self.dtype = tuple(shape), dtype
+        self.nbytes = int(np.prod(shape)) * torch.empty((), dtype=dtype).element_size()
+        p = ctypes.c_void_p()
+        native.call("gm_dev_alloc", self.nbytes, ctypes.byref(p))
+        self.ptr = int(p.value)
+        self.__cuda_array_interface__ = {"shape": self.shape, "typestr": self._TYPESTR[dtype],
+                                         "data": (self.ptr, False), "version": 3, "strides": None}
+        self.tensor = torch.as_tensor(self, device="cuda")
+
+    def ipc_handle(self) -> bytes:
+        from . import native
+
+        h = (np.zeros(64, dtype=np.uint8))
+        native.call("gm_ipc_get_handle", self.ptr, h.ctypes.data)
+        return h.tobytes()
+
+    def free(self) -> None:
+        from . import native
+
+        if self.ptr:
+            self.tensor = None
+            native.call("gm_dev_free", self.ptr)
+            self.ptr = 0
+
+
+class PeerHaloExchange:
+    """Halo exchange over peer memory (peer.cu): each rank maps its peers' ping-pong
+    buffers and flag words once (CUDA IPC, bootstrapped with all_gather_object on the
+    process group), then per step writes its changing halo cells straight into every
+    peer's new state and release-stores a step counter into each peer's flags; the
+    next step waits (acquire) for every peer's counter.  No collective per step."""
+
+    TIMEOUT_NS = 10_000_000_000
+
+    def __init__(self, plan: PartitionPlan, rank: int, bufs: Sequence[DeviceBuffer], group=None) -> None:
+        import torch.distributed as dist
+
+        from . import native
+
+        self.plan, self.rank, self.world = plan, rank, plan.world
+        self.cell_bytes = bufs[0].tensor.element_size()
+        slots, _ = plan.exchange_slots()
+        self.send_idx = torch.from_numpy(slots[rank]).cuda()
+        self.bytes_per_step = int(self.send_idx.numel() * self.cell_bytes * (self.world - 1))
+        self.flags = DeviceBuffer((self.world,), torch.uint64)
+        self.flags.tensor.zero_()
+        self.status = torch.zeros(1, dtype=torch.int32, device="cuda")
+        torch.cuda.synchronize()
+        mine = [b.ipc_handle() for b in bufs] + [self.flags.ipc_handle()]
+        everyone: list = [None] * self.world
+        dist.all_gather_object(everyone, mine, group=group)
+        import ctypes
+
+        self._opened: list[int] = []
+        ptrs = [[0] * self.world for _ in range(3)]  # buffer 0, buffer 1, flags
+        for q in range(self.world):
+            for j in range(3):
+                if q == rank:
+                    ptrs[j][q] = bufs[j].ptr if j < 2 else self.flags.ptr
+                    continue
+                p = ctypes.c_void_p()
+                h = np.frombuffer(everyone[q][j], dtype=np.uint8).copy()
+                native.call("gm_ipc_open_handle", h.ctypes.data, ctypes.byref(p))
+                ptrs[j][q] = int(p.value)
+                self._opened.append(int(p.value))
+        self.peer_bufs = [torch.tensor(ptrs[j], dtype=torch.int64).cuda() for j in range(2)]
+        self.peer_flags = torch.tensor(ptrs[2], dtype=torch.int64).cuda()
+        self.bufs = bufs
+        self.epoch = 0
+        dist.barrier(group=group)
+
+    def exchange(self, which: int) -> None:
+        """After this rank wrote its new state into buffer `which`: put + wait (stream-ordered)."""
+        from . import device as dev
+        from . import native
+
+        self.epoch += 1
+        s = dev.stream_handle()
+        native.call("gm_peer_halo_put", self.bufs[which].ptr, self.peer_bufs[which].data_ptr(),
+                    self.send_idx.data_ptr(), self.send_idx.numel(), self.cell_bytes, self.peer_flags.data_ptr(),
+                    self.rank, self.world, self.epoch, s)
+        native.call("gm_peer_halo_wait", self.flags.ptr, self.rank, self.world, self.epoch, self.TIMEOUT_NS,
+                    self.status.data_ptr(), s)
+
+    def check(self) -> None:
+        bad = int(self.status.item())
+        if bad:
+            from .native import GasketError
+
+            raise GasketError(f"peer halo wait timed out (peer bitmask {bad:#x})")
+
+    def close(self) -> None:
+        from . import native
+
+        torch.cuda.synchronize()
+        for p in self._opened:
+            native.call("gm_ipc_close", p)
+        self._opened = []
+        self.flags.free()
+
+
 StepFn = Callable[[torch.Tensor, torch.Tensor, int, int], None]
 
 
@@ -237,11 +350,31 @@ class PartitionedCA:
 
     def __init__(self, plan: PartitionPlan, rank: int, init: torch.Tensor, kind: int, param: int = 1,
                  group=None, loopback: Optional[LoopbackGroup] = None, step_fn: Optional[StepFn] = None,
-                 adopt_init: bool = False) -> None:
+                 adopt_init: bool = False, halo: str = "collective",
+                 init_fill: Optional[Callable[[torch.Tensor], None]] = None) -> None:
+        """`init_fill(t)` (peer halo only) writes the initial state into the first buffer in
+        place; `init` then only gives shape and dtype (a meta tensor is enough), so a
+        2^18 grid needs two full-size buffers, not three."""
         self.plan, self.rank, self.kind, self.param = plan, rank, kind, param
-        self.a = init if adopt_init else init.clone()  # adopt: no third full-size buffer (n=2^18 int8 is 64 GiB)
-        self.b = init.clone()  # both buffers agree off the gasket -> whole-sector writes from src
-        self.halo = HaloExchange(plan, rank, init.device, init.dtype, group=group, loopback=loopback)
+        self.peer = None
+        if halo == "peer":
+            # buffers the peers can map (CUDA IPC needs allocation bases)
+            self._dbufs = [DeviceBuffer(tuple(init.shape), init.dtype) for _ in range(2)]
+            if init_fill is not None:
+                init_fill(self._dbufs[0].tensor)
+            else:
+                self._dbufs[0].tensor.copy_(init)
+            self._dbufs[1].tensor.copy_(self._dbufs[0].tensor)
+            self.a, self.b = self._dbufs[0].tensor, self._dbufs[1].tensor
+            self.peer = PeerHaloExchange(plan, rank, self._dbufs, group=group)
+            self._dst = 1  # index of the buffer the next step writes
+            self.halo = None
+        elif halo == "collective":
+            self.a = init if adopt_init else init.clone()  # adopt: no third full-size buffer (n=2^18 int8 is 64 GiB)
+            self.b = init.clone()  # both buffers agree off the gasket -> whole-sector writes from src
+            self.halo = HaloExchange(plan, rank, init.device, init.dtype, group=group, loopback=loopback)
+        else:
+            raise ValueError("halo must be 'collective' (all_gather) or 'peer' (peer memory)")
         self.step_fn = step_fn or self._gpu_step
         self.lo, self.hi = plan.ranges[rank]
 
@@ -258,12 +391,30 @@ class PartitionedCA:
 
     def finish(self) -> None:
         self.a, self.b = self.b, self.a
+        if self.peer is not None:
+            self._dst ^= 1
 
     def step(self) -> None:
         """compute -> exchange halo of the new state -> swap (real process group)."""
         self.compute()
-        self.halo.exchange(self.b)
+        if self.peer is not None:
+            self.peer.exchange(self._dst)
+        else:
+            self.halo.exchange(self.b)
         self.finish()
+
+    @property
+    def halo_bytes_per_step(self) -> int:
+        return self.peer.bytes_per_step if self.peer is not None else self.halo.bytes_per_step
+
+    def close(self) -> None:
+        if self.peer is not None:
+            self.peer.check()
+            self.peer.close()
+            self.a = self.b = None
+            for d in self._dbufs:
+                d.free()
+            self.peer = None
 
     def owned_mask(self) -> torch.Tensor:
         """Cells of this rank's sub-gaskets (for assembling results in tests)."""
@@ -297,4 +448,4 @@ def run_loopback(plan: PartitionPlan, init: torch.Tensor, kind: int, steps: int,
 
 
 __all__: Sequence[str] = ("subgasket_block", "subgasket_index", "rank_ranges", "PartitionPlan", "LoopbackGroup",
-                          "HaloExchange", "PartitionedCA", "run_loopback")
+                          "HaloExchange", "DeviceBuffer", "PeerHaloExchange", "PartitionedCA", "run_loopback")

@@ -151,3 +151,53 @@ def test_partition_loopback_gpu_matches_full_grid(gpu, kind):
             plan = P.PartitionPlan(n, level, world, eight=kind == 2)
             got = P.run_loopback(plan, init, kind, 4)
             assert gpu.device.count_mismatch(got, a) == 0, (n, level, world)
+
+
+def _peer_worker(rank, world, port, n, level, kind, steps, out):
+    """One rank of the partitioned CA with the peer-memory halo (peer.cu): both ranks
+    share the one GPU of the test box and map each other's buffers with CUDA IPC."""
+    import torch.distributed as dist
+
+    import oracle
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        plan = P.PartitionPlan(n, level, world, eight=kind == 2)
+        init = oracle.fill_hash(n, np.int8, 9, 0)
+        ca = P.PartitionedCA(plan, rank, torch.from_numpy(init).cuda(), kind, 1, group=dist.group.WORLD, halo="peer")
+        for _ in range(steps):
+            ca.step()
+        torch.cuda.synchronize()
+        ca.peer.check()
+        mask = ca.owned_mask().cpu().numpy()
+        got = ca.a.cpu().numpy()[mask]
+        want = _reference_steps(init, kind, 1, steps)[mask]
+        out[rank] = bool(np.array_equal(got, want))
+        out[f"bytes{rank}"] = ca.halo_bytes_per_step
+        ca.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", [1, 2])
+def test_peer_memory_halo_two_processes(gpu, kind):
+    """PartitionedCA(halo="peer"): no collective per step, halo cells written into the
+    peer's buffer over CUDA IPC + release/acquire step flags == the oracle's steps."""
+    import torch.multiprocessing as mp
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, 1 << 10, 3, kind, 5, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    assert out[0] is True and out[1] is True
+    assert out["bytes0"] > 0 and out["bytes1"] > 0
