@@ -505,12 +505,14 @@ def run_ours(args) -> None:
                      "traffic": traffic, "peak_source": peak_src, "algorithmic_bytes_per_launch": alg_bytes,
                      "bytes_model": "exact 32-byte-sector minimum on the dense row-major grid (SURVEY §8d)",
                      "element_bytes_frac": R.element_bytes(r, c, kind) / (statistics.fmean(ms) * 1e-3) / 1e9 / peak,
-                     # what DRAM must move on this layout: a write pass stores partial 32-byte
-                     # sectors, and every partial-sector store costs a DRAM read of the sector
-                     # (ECC read-modify-write, scripts/probe_partial.cu) -> 2x the sector bytes
-                     "hw_model": ({"bytes": 2 * alg_bytes, "note": "sector write + forced RMW re-read",
-                                   "frac": 2 * alg_bytes / (statistics.fmean(ms) * 1e-3) / 1e9 / peak}
-                                  if kind == 0 else None)},
+                     # what DRAM must move on this layout (roofline.hw_bytes): a write pass's
+                     # partial-sector stores cost a DRAM read of the sector (ECC RMW,
+                     # scripts/probe_partial.cu); a stencil's reads come in 64-byte halves at
+                     # best (scripts/probe_fetch.cu).  Explains the gap, not the headline frac.
+                     "hw_model": {"bytes": R.hw_bytes(r, c, kind),
+                                  "note": ("sector writes + forced RMW re-read" if kind == 0 else
+                                           "64-byte-half reads of the dilated gasket + sector writes"),
+                                  "frac": R.hw_bytes(r, c, kind) / (statistics.fmean(ms) * 1e-3) / 1e9 / peak}},
         "clocks": clk.summary(),
         "gpu_launches": int(launches),
         "timed_region_wall_s": t_wall,

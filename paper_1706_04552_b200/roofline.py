@@ -32,8 +32,8 @@ except (OSError, ValueError):  # pragma: no cover
     _TABLE = {}
 
 
-def _k(c: int) -> int:
-    return (SECTOR // c).bit_length() - 1
+def _k(c: int, unit: int = SECTOR) -> int:
+    return (unit // c).bit_length() - 1
 
 
 def write_sectors(r: int, c: int) -> int:
@@ -53,10 +53,11 @@ def _subset_rows(Y: np.ndarray, nsec: int) -> np.ndarray:
 
 
 @functools.lru_cache(maxsize=None)
-def stencil_read_sectors(r: int, c: int, eight: bool, chunk: int = 2048) -> int:
-    """Exact number of 32-byte sectors holding a neighbour of some gasket cell."""
+def stencil_read_sectors(r: int, c: int, eight: bool, chunk: int = 2048, unit: int = SECTOR) -> int:
+    """Exact number of `unit`-byte blocks (default: 32-byte sectors) holding a
+    neighbour of some gasket cell."""
     n = 1 << r
-    k = _k(c)
+    k = _k(c, unit)
     if r <= k:
         # a row is a single (partial) sector: count rows holding any needed cell
         mask = (np.arange(n)[None, :] & (n - 1 - np.arange(n))[:, None]) == 0
@@ -103,6 +104,28 @@ def stencil_read_sectors(r: int, c: int, eight: bool, chunk: int = 2048) -> int:
 def stencil_read_bytes(r: int, c: int, eight: bool) -> int:
     hit = _TABLE.get(f"{r},{c},{int(eight)}")
     return SECTOR * (int(hit) if hit is not None else stencil_read_sectors(r, c, eight))
+
+
+# The smallest unit an L2 read miss fetches on B200 is a 64-byte half line (the
+# .L2::64B fetch-size hint; scripts/probe_fetch.cu), so the stencil's read set at
+# that granularity is what DRAM must deliver at best.  Precomputed like _TABLE
+# (keys "r,c,eight,64"); tests/test_roofline.py re-derives small entries.
+FETCH = 64
+
+
+def stencil_read_bytes_fetch(r: int, c: int, eight: bool) -> int:
+    hit = _TABLE.get(f"{r},{c},{int(eight)},{FETCH}")
+    return FETCH * (int(hit) if hit is not None else stencil_read_sectors(r, c, eight, unit=FETCH))
+
+
+def hw_bytes(r: int, c: int, kind: int) -> int:
+    """DRAM bytes the B200 memory system must move for a pass on this layout: a write
+    pass's partial-sector stores are read-modify-written (2x the sector bytes); a
+    stencil reads 64-byte halves and writes whole sectors."""
+    w = write_bytes(r, c)
+    if kind == 0:
+        return 2 * w
+    return w + stencil_read_bytes_fetch(r, c, kind == 2)
 
 
 def pass_bytes(r: int, c: int, kind: int) -> int:

@@ -7,11 +7,11 @@ import pytest
 from paper_1706_04552_b200 import roofline as R
 
 
-def _brute(r, c, kind):
+def _brute(r, c, kind, unit=32):
     n = 1 << r
     ys, xs = np.mgrid[0:n, 0:n]
     member = (xs & (n - 1 - ys)) == 0
-    per = 32 // c  # cells per sector
+    per = unit // c  # cells per sector (or fetch unit)
     sec = lambda m: {(int(y), int(x) // per) for y, x in zip(*np.nonzero(m))}  # noqa: E731
     write = sec(member)
     if kind == 0:
@@ -36,11 +36,29 @@ def test_sector_counts_match_brute_force(c):
             assert R.stencil_read_sectors(r, c, kind == 2) == rd, (r, c, kind)
 
 
+@pytest.mark.parametrize("c", [1, 2, 4])
+def test_fetch_unit_counts_match_brute_force(c):
+    """The 64-byte-fetch read set (hw_bytes) against a brute-force neighbour scan."""
+    for r in range(0, 10):
+        for kind in (1, 2):
+            _, rd = _brute(r, c, kind, unit=64)
+            assert R.stencil_read_sectors(r, c, kind == 2, unit=64) == rd, (r, c, kind)
+
+
 def test_table_entries_match_counter():
     for key, v in list(R._TABLE.items())[::7]:
-        r, c, e = (int(t) for t in key.split(","))
+        parts = [int(t) for t in key.split(",")]
+        r, c, e = parts[:3]
+        unit = parts[3] if len(parts) > 3 else 32
         if r <= 12:
-            assert R.stencil_read_sectors(r, c, bool(e)) == v
+            assert R.stencil_read_sectors(r, c, bool(e), unit=unit) == v
+
+
+def test_hw_model_figures():
+    """bench.py's hw_model: write = sector RMW (2x), stencil = 64-byte reads + sector writes."""
+    assert R.hw_bytes(16, 1, 0) == 2 * 181_398_528
+    assert R.hw_bytes(17, 1, 2) == R.stencil_read_bytes_fetch(17, 1, True) + 544_195_584
+    assert R.stencil_read_bytes_fetch(17, 1, True) == 1_091_211_008  # ncu: 1101 MB read per launch
 
 
 def test_survey_figures():
