@@ -85,8 +85,10 @@ __device__ __forceinline__ uint32_t pack_cells(uint32_t e, uint32_t o) {
 template <int C>
 __device__ __forceinline__ uint32_t member_mask(uint32_t t) {
     if constexpr (C == 1) {
-        const uint32_t p = t & 3u;
-        return p == 0 ? 0x000000ffu : p == 1 ? 0x0000ffffu : p == 2 ? 0x00ff00ffu : 0xffffffffu;
+        // byte j of the word is a gasket cell iff j subset of (t & 3): a byte-permute of
+        // all-ones / zero with the selector for that pattern (0x4440, 0x4400, 0x4040, 0x0000)
+        const uint32_t sel = (uint32_t)(0x0000404044004440ull >> ((t & 3u) << 4));
+        return __byte_perm(0xffffffffu, 0u, sel);
     } else if constexpr (C == 2) {
         return (t & 1u) ? 0xffffffffu : 0x0000ffffu;
     } else {

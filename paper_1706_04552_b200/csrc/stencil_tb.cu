@@ -93,18 +93,23 @@ template <int C, int KIND, int NST>
 __global__ void __launch_bounds__(TB<C>::THREADS)
     stencil_tb2(uint8_t* __restrict__ grid, const uint8_t* __restrict__ src, int64_t n, uint32_t ntiles,
                 uint64_t param, const uint32_t* __restrict__ order, const uint32_t* __restrict__ lists_g, int ns,
-                int np1, int ng1, int ni1, int np2) {
+                int np1, int ng1, int ni1, int np2, int flags) {
     using S = TB<C>;
     constexpr bool EIGHT = KIND == KIND_NSUM8;
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* ibuf = smem + NST * S::SBUF;          // state t+1, rows -1..TT
-    uint32_t* slist = reinterpret_cast<uint32_t*>(ibuf + S::IBUF);
+    int64_t* goff = reinterpret_cast<int64_t*>(ibuf + S::IBUF);  // staged chunk -> byte offset in the grid
+    uint32_t* slist = reinterpret_cast<uint32_t*>(goff + ns);
     uint32_t* p1list = slist + ns;                 // words: inner gasket, ring gasket, then copies
     uint32_t* p2list = p1list + np1;               // the tile's words holding gasket cells
-    for (int i = threadIdx.x; i < ns + np1 + np2; i += S::THREADS) slist[i] = lists_g[i];
+    const int64_t rowstride = n * C;
+    for (int i = threadIdx.x; i < ns + np1 + np2; i += S::THREADS) {
+        const uint32_t c = lists_g[i];
+        slist[i] = c;
+        if (i < ns) goff[i] = (int64_t)((c >> 16) & 0xffu) * rowstride + (int64_t)(c >> 24) * 16;
+    }
     __syncthreads();
 
-    const int64_t rowstride = n * C;
     const bool v8 = (reinterpret_cast<uintptr_t>(grid) & 31u) == 0;
     const uint32_t smem0 = (uint32_t)__cvta_generic_to_shared(smem);
     uint32_t pv;
@@ -126,24 +131,28 @@ __global__ void __launch_bounds__(TB<C>::THREADS)
     const bool active = e < S::NTOUCH;
 
     const uint32_t count = blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
-    auto tile_xy = [&](uint32_t idx, int64_t& x0, int64_t& y0) {
-        const uint32_t v = __ldg(order + blockIdx.x + idx * gridDim.x);
+    auto tile_v = [&](uint32_t idx) { return idx < count ? __ldg(order + blockIdx.x + idx * gridDim.x) : 0u; };
+    auto tile_xy = [&](uint32_t v, int64_t& x0, int64_t& y0) {
         x0 = (int64_t)(v & 0xffffu) * S::TT;
         y0 = (int64_t)(v >> 16) * S::TT;
     };
-    auto stage = [&](uint32_t idx) {
-        if (idx >= count) return;
+    // design probes (scripts/variants.py): drop staging / arithmetic / stores
+    const bool probe_noload = (flags & GM_FLAG_PROBE_NOLOAD) != 0;
+    const bool probe_nocompute = (flags & GM_FLAG_PROBE_NOCOMPUTE) != 0;
+    const bool probe_nostore = (flags & GM_FLAG_PROBE_NOSTORE) != 0;
+    auto stage = [&](uint32_t idx, uint32_t v) {
+        if (idx >= count || probe_noload) return;
         int64_t x0, y0;
-        tile_xy(idx, x0, y0);
+        tile_xy(v, x0, y0);
         const uint32_t sb = smem0 + (idx % NST) * S::SBUF;
         const uint8_t* base = src + (y0 - 2) * rowstride + x0 * C - 16;  // staged (row -2, chunk 0)
         const bool interior = y0 >= 2 && y0 + S::TT + 2 <= n && x0 > 0 && x0 + S::TT < n;
         for (int i = threadIdx.x; i < ns; i += S::THREADS) {
             const uint32_t c = slist[i];
-            const int j = (int)((c >> 16) & 0xffu), q = (int)(c >> 24);
             if (interior) {
-                cp_async16(sb + (c & 0xffffu), base + (int64_t)j * rowstride + q * 16, 16, false);
+                cp_async16(sb + (c & 0xffffu), base + goff[i], 16, false);
             } else {
+                const int j = (int)((c >> 16) & 0xffu), q = (int)(c >> 24);
                 const int64_t y = y0 + j - 2;
                 const int64_t xb = x0 * C + (q - 1) * 16;
                 const bool in = y >= 0 && y < n && xb >= 0 && xb < rowstride;
@@ -152,23 +161,24 @@ __global__ void __launch_bounds__(TB<C>::THREADS)
         }
     };
 
-#pragma unroll
-    for (int s = 0; s < NST - 1; ++s) {
-        stage((uint32_t)s);
-        cp_async_commit();
-    }
+    static_assert(NST == 2, "the tile-order registers below assume a 2-deep ring");
+    uint32_t v_cur = tile_v(0);
+    stage(0, v_cur);
+    cp_async_commit();
     for (uint32_t idx = 0; idx < count; ++idx) {
         cp_async_wait<NST - 2>();
-        __syncthreads();  // state t of tile idx staged; tile idx-1 fully stored (I, O and its S slot free)
-        stage(idx + NST - 1);
+        __syncthreads();  // state t of tile idx staged; tile idx-1 fully stored (I and its S slot free)
+        const uint32_t v_next = tile_v(idx + 1);
+        stage(idx + 1, v_next);
         cp_async_commit();
         int64_t x0, y0;
-        tile_xy(idx, x0, y0);
+        tile_xy(v_cur, x0, y0);
+        v_cur = v_next;
         const uint8_t* sbuf = smem + (idx % NST) * S::SBUF;
 
         // ---- phase 1: state t+1 on the listed words of rows -1..TT.  Entry = byte offset
         //      of (I row ji, word k) | ji << 16 | k << 24; I row ji = S row ji + 1 = row ji - 1.
-        for (int i = threadIdx.x; i < np1; i += S::THREADS) {
+        for (int i = probe_nocompute ? np1 : threadIdx.x; i < np1; i += S::THREADS) {
             const uint32_t c = p1list[i];
             const int o = (int)(c & 0xffffu);
             uint32_t v;
@@ -194,7 +204,7 @@ __global__ void __launch_bounds__(TB<C>::THREADS)
         // ---- phase 2: state t+2 on the tile's words holding gasket cells (I rows t-1..t+1),
         //      blended with state t and written over state t in the staging slot (phase 1
         //      is done with it; the store pass below reads the slot)
-        for (int i = threadIdx.x; i < np2; i += S::THREADS) {
+        for (int i = probe_nocompute ? np2 : threadIdx.x; i < np2; i += S::THREADS) {
             const uint32_t c = p2list[i];  // byte offset of (I row t, word k) | t << 16
             const int o = (int)(c & 0xffffu);
             uint32_t centre;
@@ -206,7 +216,7 @@ __global__ void __launch_bounds__(TB<C>::THREADS)
         __syncthreads();
 
         // ---- store: every touched sector whole (its slot row now holds state t+2)
-        if (active) {
+        if (active && !probe_nostore) {
             const int k0 = 4 + 8 * g;
             const uint32_t* srow = reinterpret_cast<const uint32_t*>(sbuf + (t + 2) * PITCH);
             const uint4 a = *reinterpret_cast<const uint4*>(srow + k0);
@@ -333,7 +343,7 @@ cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
     const TbLists* L = tb_lists<C>(KIND == KIND_NSUM8);
     const uint32_t* order = rowmajor_table(r_t, 0);
     if (L == nullptr || order == nullptr) return cudaErrorMemoryAllocation;
-    const size_t smem = (size_t)NST * S::SBUF + S::IBUF + 4 * (size_t)(L->ns + L->np1 + L->np2);
+    const size_t smem = (size_t)NST * S::SBUF + S::IBUF + 8 * (size_t)L->ns + 4 * (size_t)(L->ns + L->np1 + L->np2);
     auto* kern = stencil_tb2<C, KIND, NST>;
     static bool configured = false;
     if (!configured) {
@@ -348,7 +358,7 @@ cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
     if (blocks > ntiles) blocks = ntiles;
     kern<<<(unsigned)blocks, S::THREADS, smem, a.stream>>>(reinterpret_cast<uint8_t*>(a.grid),
                                                           reinterpret_cast<const uint8_t*>(a.src), a.n, ntiles,
-                                                          a.param, order, L->lists, L->ns, L->np1, L->ng1, L->ni1, L->np2);
+                                                          a.param, order, L->lists, L->ns, L->np1, L->ng1, L->ni1, L->np2, a.flags);
     note_launch();
     return cudaGetLastError();
 }

@@ -119,7 +119,9 @@ def ca_pairs(r=17):
     src = device.fill_hash(n, torch.int8, 1, 0)
     dst = src.clone()
     for kind in (2, 1):
-        for name, fl in (("fused pair", 0), ("fused pair stages2", native.FLAG_STAGES2)):
+        for name, fl in (("fused pair", 0), ("probe no compute", native.FLAG_PROBE_NOCOMPUTE),
+                         ("probe no memory", native.FLAG_PROBE_NOLOAD | native.FLAG_PROBE_NOSTORE),
+                         ("probe no store", native.FLAG_PROBE_NOSTORE), ("probe no load", native.FLAG_PROBE_NOLOAD)):
             fn = lambda: native.call("gm_ca_step2", dst.data_ptr(), src.data_ptr(), n, 1, kind, 1, fl,  # noqa: E731
                                      device.stream_handle())
             m, mn = timeit(fn, flush, k=10)
