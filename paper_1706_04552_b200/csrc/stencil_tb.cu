@@ -89,6 +89,34 @@ __device__ __forceinline__ uint32_t word_sum(const uint8_t* rows, int k, uint32_
     return o[0];
 }
 
+// A vertical run of RUN words (word k of RUN consecutive rows) from RUN+2 staged rows
+// starting at `rows` (the row above the first output): row loads and lane splits
+// are shared between the outputs.  Word k of a tile row holds gasket cells for a
+// whole aligned run of V rows (its first cell k*V only constrains bits >= log2 V of
+// the row), and the cell pattern of run row j is member_mask(j).
+template <int C, bool EIGHT, int RUN>
+__device__ __forceinline__ void vstrip(const uint8_t* rows, uint32_t pv, uint32_t (&out)[RUN],
+                                       uint32_t (&centre)[RUN]) {
+    uint32_t w[RUN + 2][3];
+#pragma unroll
+    for (int i = 0; i < RUN + 2; ++i) {
+        const uint32_t* row = reinterpret_cast<const uint32_t*>(rows + i * PITCH);
+        w[i][0] = row[-1];
+        w[i][1] = row[0];
+        w[i][2] = row[1];
+    }
+#pragma unroll
+    for (int j = 0; j < RUN; ++j) {
+        const uint32_t win[3][3] = {{w[j][0], w[j][1], w[j][2]},
+                                    {w[j + 1][0], w[j + 1][1], w[j + 1][2]},
+                                    {w[j + 2][0], w[j + 2][1], w[j + 2][2]}};
+        uint32_t o[1];
+        sector_sums<C, EIGHT, 1>(win, pv, o);
+        out[j] = o[0];
+        centre[j] = w[j + 1][1];
+    }
+}
+
 template <int C, int KIND, int NST>
 __global__ void __launch_bounds__(TB<C>::THREADS)
     stencil_tb2(uint8_t* __restrict__ grid, const uint8_t* __restrict__ src, int64_t n, uint32_t ntiles,
@@ -176,42 +204,48 @@ __global__ void __launch_bounds__(TB<C>::THREADS)
         v_cur = v_next;
         const uint8_t* sbuf = smem + (idx % NST) * S::SBUF;
 
-        // ---- phase 1: state t+1 on the listed words of rows -1..TT.  Entry = byte offset
-        //      of (I row ji, word k) | ji << 16 | k << 24; I row ji = S row ji + 1 = row ji - 1.
+        // ---- phase 1: state t+1 on rows -1..TT.  Entries: byte offset o of (I row ji, word k)
+        //      (| ji << 16 | k << 24 for single words); I row ji = S row ji + 1 = row ji - 1.
+        //      [0, ni1): runs of V tile rows of a word holding gasket cells, o = first row;
+        //      [ni1, ng1): ring words that may hold gasket cells (exact global test);
+        //      [ng1, np1): words without gasket cells (state t copied).
         for (int i = probe_nocompute ? np1 : threadIdx.x; i < np1; i += S::THREADS) {
             const uint32_t c = p1list[i];
             const int o = (int)(c & 0xffffu);
-            uint32_t v;
-            if (i < ng1) {  // may hold gasket cells: compute, keep state t on the others
+            if (i < ni1) {
+                uint32_t sum[S::V], centre[S::V];
+                vstrip<C, EIGHT, S::V>(sbuf + o, pv, sum, centre);
+#pragma unroll
+                for (int j = 0; j < S::V; ++j) {
+                    const uint32_t m = member_mask<C>((uint32_t)j);
+                    *reinterpret_cast<uint32_t*>(ibuf + o + j * PITCH) = (sum[j] & m) | (centre[j] & ~m);
+                }
+            } else if (i < ng1) {
                 uint32_t centre;
                 const uint32_t sum = word_sum<C, EIGHT>(sbuf + o, 0, pv, centre);
-                const int ji = (int)((c >> 16) & 0xffu);
-                uint32_t m;
-                if (i < ni1) {  // inside the tile (a gasket tile): the local pattern is exact
-                    m = member_mask<C>((uint32_t)(ji - 1));
-                } else {        // ring word of a neighbouring tile: exact global test
-                    const int k = (int)(c >> 24);
-                    m = word_mask<C>((int)x0 + (k - 4) * S::V, (int)y0 + ji - 1, (int)n);
-                }
-                v = (sum & m) | (centre & ~m);
-            } else {        // off the gasket: state t
-                v = *reinterpret_cast<const uint32_t*>(sbuf + o + PITCH);
+                const int ji = (int)((c >> 16) & 0xffu), k = (int)(c >> 24);
+                const uint32_t m = word_mask<C>((int)x0 + (k - 4) * S::V, (int)y0 + ji - 1, (int)n);
+                *reinterpret_cast<uint32_t*>(ibuf + o) = (sum & m) | (centre & ~m);
+            } else {
+                *reinterpret_cast<uint32_t*>(ibuf + o) = *reinterpret_cast<const uint32_t*>(sbuf + o + PITCH);
             }
-            *reinterpret_cast<uint32_t*>(ibuf + o) = v;
         }
         __syncthreads();
 
-        // ---- phase 2: state t+2 on the tile's words holding gasket cells (I rows t-1..t+1),
-        //      blended with state t and written over state t in the staging slot (phase 1
-        //      is done with it; the store pass below reads the slot)
+        // ---- phase 2: state t+2 on the tile's gasket words, in runs of V rows (I rows t-1..t+V),
+        //      blended with state t and written over state t in the staging slot (phase 1 is
+        //      done with it; the store pass below reads the slot).  Entry: byte offset of
+        //      (I row t, word k) for the run's first tile row t.
         for (int i = probe_nocompute ? np2 : threadIdx.x; i < np2; i += S::THREADS) {
-            const uint32_t c = p2list[i];  // byte offset of (I row t, word k) | t << 16
-            const int o = (int)(c & 0xffffu);
-            uint32_t centre;
-            const uint32_t sum = word_sum<C, EIGHT>(ibuf + o, 0, pv, centre);
-            uint32_t* sp = reinterpret_cast<uint32_t*>(const_cast<uint8_t*>(sbuf) + o + 2 * PITCH);
-            const uint32_t m = member_mask<C>(c >> 16);
-            *sp = (sum & m) | (*sp & ~m);
+            const int o = (int)p2list[i];
+            uint32_t sum[S::V], centre[S::V];
+            vstrip<C, EIGHT, S::V>(ibuf + o, pv, sum, centre);
+#pragma unroll
+            for (int j = 0; j < S::V; ++j) {
+                uint32_t* sp = reinterpret_cast<uint32_t*>(const_cast<uint8_t*>(sbuf) + o + (j + 2) * PITCH);
+                const uint32_t m = member_mask<C>((uint32_t)j);
+                *sp = (sum[j] & m) | (*sp & ~m);
+            }
         }
         __syncthreads();
 
@@ -280,9 +314,12 @@ void build_lists(bool eight, std::vector<uint32_t>& out, int& ns, int& np1, int&
             if (any) out.push_back((uint32_t)(j * PITCH + q * 16) | ((uint32_t)j << 16) | ((uint32_t)q << 24));
         }
     ns = (int)out.size();
-    // phase 1: words of rows -1..TT holding a D1 cell: inner words that hold gasket
-    // cells, ring words that may (neighbouring tile assumed a gasket tile), then the
-    // rest (copied).  Entry: byte offset (I row ji, word k) | ji << 16 | k << 24.
+    // phase 1: words of rows -1..TT holding a D1 cell.  The tile's own gasket words come
+    // in aligned runs of V rows (word w holds gasket cells of row t iff w*V subset of t,
+    // which leaves t's low log2(V) bits free): one entry per run, the byte offset of
+    // (I row r0 + 1, word k).  Then ring words that may hold gasket cells (neighbouring
+    // tile assumed a gasket tile), then the rest (copied); single-word entries are
+    // byte offset (I row ji, word k) | ji << 16 | k << 24.
     std::vector<uint32_t> inner, ring, copy;
     for (int r = -1; r <= TT; ++r)
         for (int k = 0; k < 4 * CHUNKS; ++k) {
@@ -291,11 +328,15 @@ void build_lists(bool eight, std::vector<uint32_t>& out, int& ns, int& np1, int&
                 d = d || at(D1, c, r);
                 gsk = gsk || member_sup(c, r);
             }
+            const bool in_tile = r >= 0 && r < TT && k >= 4 && k < 4 + TT / V;
+            if (in_tile && gsk) {  // exact inside the tile: part of a run
+                if (r % V == 0) inner.push_back((uint32_t)((r + 1) * PITCH + k * 4));
+                continue;
+            }
             if (!d) continue;
             const int ji = r + 1;
             const uint32_t e = (uint32_t)(ji * PITCH + k * 4) | ((uint32_t)ji << 16) | ((uint32_t)k << 24);
-            const bool in_tile = r >= 0 && r < TT && k >= 4 && k < 4 + TT / V;
-            (gsk ? (in_tile ? inner : ring) : copy).push_back(e);
+            (gsk ? ring : copy).push_back(e);
         }
     ni1 = (int)inner.size();
     ng1 = ni1 + (int)ring.size();
@@ -303,13 +344,13 @@ void build_lists(bool eight, std::vector<uint32_t>& out, int& ns, int& np1, int&
     out.insert(out.end(), inner.begin(), inner.end());
     out.insert(out.end(), ring.begin(), ring.end());
     out.insert(out.end(), copy.begin(), copy.end());
-    // phase 2: the tile's words holding gasket cells, as the byte offset of
-    // (I row t, word k) = (O row t, word k): I rows t..t+2 are tile rows t-1..t+1
+    // phase 2: the tile's gasket words, one entry per aligned run of V rows: the byte
+    // offset of (I row t, word k) (I rows t..t+V+1 are tile rows t-1..t+V)
     np2 = 0;
-    for (int t = 0; t < TT; ++t)
+    for (int t = 0; t < TT; t += V)
         for (int w = 0; w < TT / V; ++w)
             if (((w * V) & ~t) == 0) {
-                out.push_back((uint32_t)(t * PITCH + (w + 4) * 4) | ((uint32_t)t << 16));
+                out.push_back((uint32_t)(t * PITCH + (w + 4) * 4));
                 ++np2;
             }
 }
