@@ -318,6 +318,15 @@ def _multi_step(r: int, tdt, kind: int, flusher, steps: int = 40) -> dict:
         del run, g
         torch.cuda.empty_cache()
     out["speedup_fused"] = out["temporal1"]["ms_per_step"] / out["temporal2"]["ms_per_step"]
+    # work-equivalent roofline: the §8d bytes of one single step per fused step time (the
+    # fused pass moves about one step's bytes per two steps, so this can exceed what the
+    # memory system moves; labelled "effective", not the kernel's own roofline)
+    from paper_1706_04552_b200 import roofline as R
+
+    peak, _ = _peaks()
+    c = torch.empty((), dtype=tdt).element_size()
+    out["temporal2"]["effective_frac"] = (R.pass_bytes(r, c, kind) / (out["temporal2"]["ms_per_step"] * 1e-3)
+                                          / 1e9 / peak)
     return out
 
 
