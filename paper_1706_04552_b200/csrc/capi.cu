@@ -1,3 +1,4 @@
+#include <cstdlib>
 #include <algorithm>
 // capi.cu -- extern "C" drop-in boundary (include/gasket_b200.h).
 //
@@ -128,6 +129,17 @@ int launch_cfg(const gm_cfg_t* c, void* grid, const void* src, const int32_t* tx
 }
 
 }  // namespace
+
+namespace gm {
+int order_level(const LaunchArgs& a, int r_t) {
+    if (a.part_level >= 0) return a.part_level;
+    static const int env = [] {
+        const char* e = getenv("GASKET_TILE_ORDER_LEVEL");
+        return e ? atoi(e) : 0;
+    }();
+    return env < 0 ? 0 : (env > r_t ? r_t : env);
+}
+}  // namespace gm
 
 extern "C" {
 

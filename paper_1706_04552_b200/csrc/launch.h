@@ -45,6 +45,11 @@ inline void tile_range(const LaunchArgs& a, int r_t, uint32_t& lo, uint32_t& hi)
 
 void note_launch();
 
+// Sub-gasket level whose groups the row-major tile order keeps together: the partition
+// level for partitioned launches (their tile ranges are digit-order sub-gasket ranges),
+// else 0 (one row-major sweep) -- or GASKET_TILE_ORDER_LEVEL for experiments.
+int order_level(const LaunchArgs& a, int r_t);
+
 cudaError_t launch_literal(const LaunchArgs& a);
 cudaError_t launch_tuned(const LaunchArgs& a);
 cudaError_t launch_stream(const LaunchArgs& a);

@@ -287,7 +287,7 @@ cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
     uint64_t blocks = (uint64_t)sms * (per_sm > 0 ? per_sm : 1);
     if (blocks > ntiles) blocks = ntiles;
     const uint32_t* order = nullptr;
-    if (!(a.flags & GM_FLAG_DIGIT_ORDER)) order = rowmajor_table(r_t, a.part_level < 0 ? 0 : a.part_level);
+    if (!(a.flags & GM_FLAG_DIGIT_ORDER)) order = rowmajor_table(r_t, order_level(a, r_t));
     kern<<<(unsigned)blocks, S::THREADS, smem, a.stream>>>(reinterpret_cast<uint8_t*>(a.grid),
                                                           reinterpret_cast<const uint8_t*>(a.src), a.n, lo, hi, r_t,
                                                           a.part_level, a.param, a.flags, order);

@@ -417,7 +417,7 @@ cudaError_t launch_band(const LaunchArgs& a, int r_t) {
     if (blocks > cap) blocks = cap;
     const uint32_t* order = nullptr;
     if (digit && !(a.flags & GM_FLAG_DIGIT_ORDER) && KIND != KIND_COUNT)
-        order = rowmajor_table(r_t, a.part_level < 0 ? 0 : a.part_level);
+        order = rowmajor_table(r_t, order_level(a, r_t));
     kern<<<(unsigned)blocks, 256, 0, a.stream>>>(reinterpret_cast<uint8_t*>(a.grid),
                                                  reinterpret_cast<const uint8_t*>(a.src), a.n, lo, hi, band_shift, W,
                                                  a.param, a.flags, order);
