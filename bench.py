@@ -507,7 +507,7 @@ def run_ours(args) -> None:
         "higher_is_better": True,
         "scaling": "strong" if part is not None else "weak",
         "vs_baseline": None,
-        "dtype": {"int8": "i8", "int32": "i32"}[dname],
+        "dtype": dname,
         "data": "synthetic (zero grid, param=1)" if kind == 0 else "synthetic (splitmix64 hash states, all cells)",
         "config": _config(workload, rho, world, part is not None),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -595,7 +595,7 @@ def run_reference(args) -> None:
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": {"int8": "i8", "int32": "i32"}[dname],
+        "dtype": dname,
         "data": "synthetic",
         "config": _config(workload, WORKLOADS[workload][3], world, workload.startswith("part")),
         "cpu_baseline": {"value": value, "unit": "cells/s", "cores": oracle.max_threads(), "kind": "port",
