@@ -446,3 +446,24 @@ def test_whole_grid_tile_and_unit_grid(gpu, oracle):
             want = _oracle_result(oracle, grid0, src, n, kind, 5)
             for label, got in _gpu_all(gpu, grid0, src, n, kind, 5):
                 assert np.array_equal(got.cpu().numpy(), want), (n, kind, label)
+
+
+@pytest.mark.parametrize("dtype", [torch.int8, torch.int16, torch.int32])
+def test_fused_two_steps_equal_single_steps_large(gpu, dtype):
+    """At sizes past the oracle's reach: gm_ca_step2 == two single-step launches, bit for bit."""
+    from paper_1706_04552_b200 import device, native
+
+    be, S = gpu.backends, gpu.geometry.IntraStrategy
+    n = 1 << 15 if dtype == torch.int8 else 1 << 14
+    for kind in (1, 2):
+        src = device.fill_hash(n, dtype, 77, 0)
+        mid = src.clone()
+        be.run_block_space(mid, src, 64, (n // 64).bit_length() - 1, S.TUNED, kind=kind, param=5,
+                           flags=native.FLAG_DST_FROM_SRC)
+        two = src.clone()
+        be.run_block_space(two, mid, 64, (n // 64).bit_length() - 1, S.TUNED, kind=kind, param=5,
+                           flags=native.FLAG_DST_FROM_SRC)
+        fused = src.clone()
+        native.call("gm_ca_step2", fused.data_ptr(), src.data_ptr(), n, src.element_size(), kind, 5, 0,
+                    device.stream_handle())
+        assert torch.equal(fused, two), (dtype, kind)
