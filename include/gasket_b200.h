@@ -59,7 +59,7 @@ extern "C" {
 #define GM_FLAG_CHUNKED 64     /* tuned stencil: contiguous tile run per CTA instead of interleaved */
 #define GM_FLAG_NO_TMA 128     /* tuned stencil: always stage tiles with cp.async */
 #define GM_FLAG_FORCE_TMA 256  /* tuned stencil: always stage tiles with TMA */
-#define GM_FLAG_FETCH_LINE 512 /* tuned kernels: loads without the .L2::64B fetch-size hint (whole 128-byte lines) */
+#define GM_FLAG_FETCH_LINE 512 /* tuned kernels: whole-line (.L2::128B) loads (stencil v2: the default since round 1d) */
 #define GM_FLAG_FETCH64 1024   /* tuned write: touch each written 64-byte half with an .L2::64B load first */
 #define GM_FLAG_STENCIL_V1 2048 /* tuned stencil: the v1 kernel (stencil.cu) instead of v2 (stencil2.cu) */
 #define GM_FLAG_STAGES2 4096   /* tuned stencil v2: 2-deep staging ring instead of 3/4 */
@@ -70,7 +70,8 @@ extern "C" {
 #define GM_FLAG_STORE_CS 131072   /* tuned write pass / stencil v2: streaming (evict-first) stores */
 #define GM_FLAG_BAND_MAJOR 262144 /* tuned write pass: hand out (band, tile) units band-major */
 #define GM_FLAG_PREFETCH_AHEAD 524288 /* tuned write pass: L2-prefetch the lines of the unit two ahead */
-#define GM_FLAG_FETCH_MIXED 1048576   /* stencil v2: whole-line fetch for lines needed in both halves */
+#define GM_FLAG_FETCH_MIXED 1048576   /* stencil v2 with FETCH_HALF: whole-line fetch for lines needed in both halves */
+#define GM_FLAG_FETCH_HALF 2097152    /* stencil v2: stage with the .L2::64B hint (64-byte halves) instead of whole lines */
 
 #define GM_OK 0
 #define GM_EINVAL 1  /* bad shape / size / tag (the reference's ValueError) */

@@ -27,6 +27,8 @@
 // 4-neighbours, out-of-grid = 0, result wraps to the cell width) and our
 // labelled 8-neighbour extension; only gasket cells change.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -131,8 +133,21 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
     __syncthreads();
     const int nch = nchunks;
     const int64_t rowstride = n * C;
+    // with a 2-deep ring there is shared memory left for the chunks' grid offsets (one add
+    // per chunk when staging interior tiles); the 3-deep ring keeps 3 CTAs per SM without
+    [[maybe_unused]] int32_t* goff = reinterpret_cast<int32_t*>(chunks + S::ROWS * CHUNKS);
+    if constexpr (NST == 2) {
+        for (int i = threadIdx.x; i < nch; i += S::THREADS) {
+            const uint32_t c = chunks[i];
+            goff[i] = (int32_t)((int64_t)((c >> 16) & 0xffu) * rowstride + (int64_t)((c >> 24) & 15u) * 16);
+        }
+        __syncthreads();
+    }
     const bool dst_from_src = (flags & GM_FLAG_DST_FROM_SRC) != 0;
-    const bool fetch_line = (flags & GM_FLAG_FETCH_LINE) != 0;
+    // staging fetches whole 128-byte lines (.L2::128B) by default: the pass is bound by
+    // the number of DRAM accesses, not bytes (n=2^17 NSUM8: 428 us vs 441 us with the
+    // .L2::64B hint, which moves 1.10 instead of ~1.44 GB); GM_FLAG_FETCH_HALF = halves
+    const bool fetch_line = (flags & GM_FLAG_FETCH_HALF) == 0;
     const bool fetch_mixed = (flags & GM_FLAG_FETCH_MIXED) != 0;
     const bool v8 = (reinterpret_cast<uintptr_t>(grid) & 31u) == 0;
     const bool probe_nostore = (flags & GM_FLAG_PROBE_NOSTORE) != 0;
@@ -194,9 +209,13 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
         if (interior) {
             for (int i = threadIdx.x; i < nch; i += S::THREADS) {
                 const uint32_t c = chunks[i];
-                const uint32_t j = (c >> 16) & 0xffu, qq = (c >> 24) & 15u;
-                cp_async16(sb + (c & 0xffffu), base + (int64_t)j * rowstride + qq * 16, 16,
-                           fetch_line || (fetch_mixed && (c >> 28)));
+                int64_t go;
+                if constexpr (NST == 2) {
+                    go = goff[i];
+                } else {
+                    go = (int64_t)((c >> 16) & 0xffu) * rowstride + (int64_t)((c >> 24) & 15u) * 16;
+                }
+                cp_async16(sb + (c & 0xffffu), base + go, 16, fetch_line || (fetch_mixed && (c >> 28)));
             }
         } else {
             for (int i = threadIdx.x; i < nch; i += S::THREADS) {
@@ -273,7 +292,7 @@ cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
     tile_range(a, r_t, lo, hi);
     if (hi == lo) return cudaSuccess;
     const uint32_t ntiles = hi - lo;
-    const size_t smem = (size_t)NST * S::BUF + 4 * S::ROWS * CHUNKS;
+    const size_t smem = (size_t)NST * S::BUF + (NST == 2 ? 8 : 4) * S::ROWS * CHUNKS;
     auto* kern = stencil_v2<C, KIND, NST>;
     static bool configured = false;
     if (!configured) {
@@ -286,6 +305,7 @@ cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, S::THREADS, smem);
     uint64_t blocks = (uint64_t)sms * (per_sm > 0 ? per_sm : 1);
     if (blocks > ntiles) blocks = ntiles;
+    if (getenv("GASKET_DEBUG_OCC")) fprintf(stderr, "stencil_v2<C=%d,K=%d,NST=%d>: %d CTAs/SM, smem %zu\n", C, KIND, NST, per_sm, smem);
     const uint32_t* order = nullptr;
     if (!(a.flags & GM_FLAG_DIGIT_ORDER)) order = rowmajor_table(r_t, order_level(a, r_t));
     kern<<<(unsigned)blocks, S::THREADS, smem, a.stream>>>(reinterpret_cast<uint8_t*>(a.grid),

@@ -168,6 +168,7 @@ __global__ void __launch_bounds__(TB<C>::THREADS)
     const bool probe_noload = (flags & GM_FLAG_PROBE_NOLOAD) != 0;
     const bool probe_nocompute = (flags & GM_FLAG_PROBE_NOCOMPUTE) != 0;
     const bool probe_nostore = (flags & GM_FLAG_PROBE_NOSTORE) != 0;
+    const bool fetch_line = (flags & GM_FLAG_FETCH_LINE) != 0;
     auto stage = [&](uint32_t idx, uint32_t v) {
         if (idx >= count || probe_noload) return;
         int64_t x0, y0;
@@ -178,13 +179,13 @@ __global__ void __launch_bounds__(TB<C>::THREADS)
         for (int i = threadIdx.x; i < ns; i += S::THREADS) {
             const uint32_t c = slist[i];
             if (interior) {
-                cp_async16(sb + (c & 0xffffu), base + goff[i], 16, false);
+                cp_async16(sb + (c & 0xffffu), base + goff[i], 16, fetch_line);
             } else {
                 const int j = (int)((c >> 16) & 0xffu), q = (int)(c >> 24);
                 const int64_t y = y0 + j - 2;
                 const int64_t xb = x0 * C + (q - 1) * 16;
                 const bool in = y >= 0 && y < n && xb >= 0 && xb < rowstride;
-                cp_async16(sb + (c & 0xffffu), in ? src + y * rowstride + xb : src, in ? 16 : 0, false);
+                cp_async16(sb + (c & 0xffffu), in ? src + y * rowstride + xb : src, in ? 16 : 0, fetch_line);
             }
         }
     };

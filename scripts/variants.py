@@ -70,9 +70,10 @@ def main():
         V1, S2 = native.FLAG_STENCIL_V1, native.FLAG_STAGES2
         PN, PL = native.FLAG_PROBE_NOSTORE, native.FLAG_PROBE_NOLOAD
         DO, CS = native.FLAG_DIGIT_ORDER, native.FLAG_STORE_CS
-        for name, fl in (("v2", D), ("v2-mixed", D | native.FLAG_FETCH_MIXED), ("v2-cs", D | CS), ("v2-digit", D | DO), ("v2-stages2", D | S2),
+        FH = native.FLAG_FETCH_HALF
+        for name, fl in (("v2", D), ("v2-half", D | FH), ("v2 (again)", D), ("v2-half (again)", D | FH),
+                         ("v2-mixed", D | FH | native.FLAG_FETCH_MIXED), ("v2-cs", D | CS), ("v2-digit", D | DO), ("v2-stages2", D | S2),
                          ("v2-chunked", D | CH), ("probe v2 no compute", D | native.FLAG_PROBE_NOCOMPUTE),
-                         ("v2-line", D | FL),
                          ("probe v2 reads only", D | PN), ("probe v2 reads only, line", D | PN | FL),
                          ("probe v2 stores only", D | PL), ("probe v2 no memory", D | PN | PL),
                          ("probe v2 no compute", D | native.FLAG_PROBE_NOCOMPUTE),
@@ -119,7 +120,9 @@ def ca_pairs(r=17):
     src = device.fill_hash(n, torch.int8, 1, 0)
     dst = src.clone()
     for kind in (2, 1):
-        for name, fl in (("fused pair", 0), ("probe no compute", native.FLAG_PROBE_NOCOMPUTE),
+        for name, fl in (("fused pair", 0), ("fused pair line", native.FLAG_FETCH_LINE), ("fused pair (again)", 0),
+                         ("fused pair line (again)", native.FLAG_FETCH_LINE),
+                         ("probe no compute", native.FLAG_PROBE_NOCOMPUTE),
                          ("probe no memory", native.FLAG_PROBE_NOLOAD | native.FLAG_PROBE_NOSTORE),
                          ("probe no store", native.FLAG_PROBE_NOSTORE), ("probe no load", native.FLAG_PROBE_NOLOAD)):
             fn = lambda: native.call("gm_ca_step2", dst.data_ptr(), src.data_ptr(), n, 1, kind, 1, fl,  # noqa: E731

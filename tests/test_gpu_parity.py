@@ -22,7 +22,7 @@ KINDS = (0, 1, 2)  # CONST, NSUM4, NSUM8 (ours)
 # omega order, explicit RMW (+ whole lines), host-row schedule, row-major/chunked,
 # cp.async/TMA staging, whole-line fetch, L2 touch, stencil v1, 2-deep ring, digit order
 TUNED_FLAGS = (0, 1, 4, 12, 16, 32, 96, 128, 256, 512, 1024, 2048, 2048 | 65536, 2048 | 128, 4096, 65536,
-               4 | 512, 65536 | 4096)
+               4 | 512, 65536 | 4096, 2097152, 2097152 | 1048576)
 
 
 def _to_dev(a: np.ndarray) -> torch.Tensor:
@@ -419,7 +419,7 @@ def test_dst_from_src_variants(gpu, oracle, dtype):
         src = oracle.fill_hash(n, dtype, 31, 0)
         for kind in (1, 2):
             want = _oracle_result(oracle, src.copy(), src, 8, kind, -5)
-            for flags in (2, 2 | 65536, 2 | 2048, 2 | 2048 | 128, 2 | 4096, 2 | 512, 2 | 64, 2 | 256):
+            for flags in (2, 2 | 65536, 2 | 2048, 2 | 2048 | 128, 2 | 4096, 2 | 512, 2 | 64, 2 | 256, 2 | 2097152):
                 g = _to_dev(src)
                 r_b = (n // 8).bit_length() - 1
                 be.run_block_space(g, _to_dev(src), 8, r_b, S.TUNED, kind=kind, param=-5, flags=flags)
