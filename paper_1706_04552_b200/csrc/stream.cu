@@ -107,6 +107,10 @@ __device__ __forceinline__ W ld_half(const void* p) {
         return v;
     }
 }
+__device__ __forceinline__ void touch_line(const void* p) {
+    uint32_t v;
+    asm volatile("ld.global.cg.L2::128B.u32 %0, [%1];" : "=r"(v) : "l"(p));
+}
 template <class W>
 __device__ __forceinline__ W ld_line(const void* p) {
     return *reinterpret_cast<const volatile W*>(p);
@@ -290,7 +294,13 @@ __global__ void __launch_bounds__(256) lambda_stream(uint8_t* __restrict__ grid,
                 // its own DRAM read-modify-write fill
 #pragma unroll
                 for (int i = 0; i < BAND; ++i)
-                    if ((c0 & ~(t0 + i)) == 0) (void)ld_half<WT>(drow + (int64_t)i * rowstride);  // asm volatile: kept
+                    if ((c0 & ~(t0 + i)) == 0) {  // asm volatile: kept
+                        if (flags & GM_FLAG_FETCH_LINE) {
+                            if (lane == 0) touch_line(drow - lane * G::WB + (int64_t)i * rowstride);
+                        } else {
+                            (void)ld_half<WT>(drow + (int64_t)i * rowstride);
+                        }
+                    }
             }
             // rows come in groups of V (t0 is a multiple of V): within a group the word's
             // touched flag is constant and slot j's cell pattern is j (cells k subset of j)

@@ -51,7 +51,8 @@ def main():
             DO, CS = native.FLAG_DIGIT_ORDER, native.FLAG_STORE_CS
             BM = native.FLAG_BAND_MAJOR
             PA = native.FLAG_PREFETCH_AHEAD
-            for name, fl in (("masked", 0), ("masked-prefetch", PA), ("masked-bandmajor", BM),
+            for name, fl in (("masked", 0), ("masked+touchline", F64 | FL), ("masked (again)", 0),
+                             ("masked+touchline (again)", F64 | FL), ("masked-prefetch", PA), ("masked-bandmajor", BM),
                              ("masked-digit", DO), ("masked-cs", CS), ("masked+touch64", F64),
                              ("rmw-sectors", E), ("rmw-lines", E | L)):
                 m, mn = timeit(lambda: backends.run_block_space(g, g, 32, r - 5, T, kind=0, param=1, flags=fl), flush)
