@@ -72,6 +72,7 @@ extern "C" {
 #define GM_FLAG_PREFETCH_AHEAD 524288 /* tuned write pass: L2-prefetch the lines of the unit two ahead */
 #define GM_FLAG_FETCH_MIXED 1048576   /* stencil v2 with FETCH_HALF: whole-line fetch for lines needed in both halves */
 #define GM_FLAG_FETCH_HALF 2097152    /* stencil v2: stage with the .L2::64B hint (64-byte halves) instead of whole lines */
+#define GM_FLAG_FETCH256 4194304      /* stencil v2: stage interior tiles with the .L2::256B prefetch-size hint */
 
 #define GM_OK 0
 #define GM_EINVAL 1  /* bad shape / size / tag (the reference's ValueError) */

@@ -148,6 +148,7 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
     // the number of DRAM accesses, not bytes (n=2^17 NSUM8: 428 us vs 441 us with the
     // .L2::64B hint, which moves 1.10 instead of ~1.44 GB); GM_FLAG_FETCH_HALF = halves
     const bool fetch_line = (flags & GM_FLAG_FETCH_HALF) == 0;
+    const bool fetch256 = (flags & GM_FLAG_FETCH256) != 0;
     const bool fetch_mixed = (flags & GM_FLAG_FETCH_MIXED) != 0;
     const bool v8 = (reinterpret_cast<uintptr_t>(grid) & 31u) == 0;
     const bool probe_nostore = (flags & GM_FLAG_PROBE_NOSTORE) != 0;
@@ -215,7 +216,8 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
                 } else {
                     go = (int64_t)((c >> 16) & 0xffu) * rowstride + (int64_t)((c >> 24) & 15u) * 16;
                 }
-                cp_async16(sb + (c & 0xffffu), base + go, 16, fetch_line || (fetch_mixed && (c >> 28)));
+                if (fetch256) cp_async16_256(sb + (c & 0xffffu), base + go, 16);
+                else cp_async16(sb + (c & 0xffffu), base + go, 16, fetch_line || (fetch_mixed && (c >> 28)));
             }
         } else {
             for (int i = threadIdx.x; i < nch; i += S::THREADS) {

@@ -16,6 +16,11 @@ __device__ __forceinline__ void cp_async16(uint32_t smem, const void* gmem, int 
         asm volatile("cp.async.cg.shared.global.L2::64B [%0], [%1], 16, %2;" ::"r"(smem), "l"(gmem), "r"(src_bytes)
                      : "memory");
 }
+// 256-byte prefetch-size variant (the line and its neighbour), for A/B runs
+__device__ __forceinline__ void cp_async16_256(uint32_t smem, const void* gmem, int src_bytes) {
+    asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16, %2;" ::"r"(smem), "l"(gmem), "r"(src_bytes)
+                 : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }

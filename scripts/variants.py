@@ -72,7 +72,9 @@ def main():
         PN, PL = native.FLAG_PROBE_NOSTORE, native.FLAG_PROBE_NOLOAD
         DO, CS = native.FLAG_DIGIT_ORDER, native.FLAG_STORE_CS
         FH = native.FLAG_FETCH_HALF
-        for name, fl in (("v2", D), ("v2-half", D | FH), ("v2 (again)", D), ("v2-half (again)", D | FH),
+        F256 = native.FLAG_FETCH256
+        for name, fl in (("v2", D), ("v2-256", D | F256), ("v2 (again)", D), ("v2-256 (again)", D | F256),
+                         ("v2-half", D | FH), ("v2-half (again)", D | FH),
                          ("v2-mixed", D | FH | native.FLAG_FETCH_MIXED), ("v2-cs", D | CS), ("v2-digit", D | DO), ("v2-stages2", D | S2),
                          ("v2-chunked", D | CH), ("probe v2 no compute", D | native.FLAG_PROBE_NOCOMPUTE),
                          ("probe v2 reads only", D | PN), ("probe v2 reads only, line", D | PN | FL),
