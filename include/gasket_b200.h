@@ -50,6 +50,10 @@ extern "C" {
 #define GM_MAP_LAMBDA 1   /* engine.Mapping.BLOCK_SPACE */
 #define GM_MAP_BB_EXIT 2  /* bounding box with block-level early exit */
 
+/* Launch flags.  All but GM_FLAG_DST_FROM_SRC and GM_FLAG_HOST_ROWS select kernel
+ * variants kept for A/B measurement (scripts/variants.py; results in
+ * profiles/r1_probes.md); every variant computes the same cells except the
+ * GM_FLAG_PROBE_* design probes.  The defaults are the measured-best variants. */
 #define GM_FLAG_OMEGA_ORDER 1  /* tuned: visit tiles in b = wy*W + wx order */
 #define GM_FLAG_DST_FROM_SRC 2 /* stencil: grid == copy of src off-gasket (engine.py:201) */
 #define GM_FLAG_EXPLICIT_RMW 4 /* tuned write: load partial sectors, store whole sectors */
@@ -60,12 +64,13 @@ extern "C" {
 #define GM_FLAG_NO_TMA 128     /* tuned stencil: always stage tiles with cp.async */
 #define GM_FLAG_FORCE_TMA 256  /* tuned stencil: always stage tiles with TMA */
 #define GM_FLAG_FETCH_LINE 512 /* tuned kernels: whole-line (.L2::128B) loads (stencil v2: the default since round 1d) */
-#define GM_FLAG_FETCH64 1024   /* tuned write: touch each written 64-byte half with an .L2::64B load first */
+#define GM_FLAG_FETCH64 1024   /* tuned write: touch each written 64-byte half with an .L2::64B load first
+                                  (with GM_FLAG_FETCH_LINE: touch the whole line) */
 #define GM_FLAG_STENCIL_V1 2048 /* tuned stencil: the v1 kernel (stencil.cu) instead of v2 (stencil2.cu) */
 #define GM_FLAG_STAGES2 4096   /* tuned stencil v2: 2-deep staging ring instead of 3/4 */
-#define GM_FLAG_PROBE_NOSTORE 8192  /* design probe, stencil v2: stage tiles but store nothing (result undefined) */
-#define GM_FLAG_PROBE_NOLOAD 16384  /* design probe, stencil v2: store sectors without staging (result undefined) */
-#define GM_FLAG_PROBE_NOCOMPUTE 32768 /* design probe, stencil v2: stage + store, no arithmetic (result undefined) */
+#define GM_FLAG_PROBE_NOSTORE 8192  /* design probe, stencil v2 / gm_ca_step2: no stores (result undefined) */
+#define GM_FLAG_PROBE_NOLOAD 16384  /* design probe, stencil v2 / gm_ca_step2: no staging (result undefined) */
+#define GM_FLAG_PROBE_NOCOMPUTE 32768 /* design probe, stencil v2 / gm_ca_step2: no arithmetic (result undefined) */
 #define GM_FLAG_DIGIT_ORDER 65536 /* tuned: visit tiles in lambda digit order instead of row-major per sub-gasket */
 #define GM_FLAG_STORE_CS 131072   /* tuned write pass / stencil v2: streaming (evict-first) stores */
 #define GM_FLAG_BAND_MAJOR 262144 /* tuned write pass: hand out (band, tile) units band-major */
