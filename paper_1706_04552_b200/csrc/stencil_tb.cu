@@ -58,9 +58,12 @@ struct TB {
     static constexpr int SBUF = SROWS * PITCH;
     static constexpr int IBUF = IROWS * PITCH;
     static constexpr int NTOUCH = 9 * SC;
-    // two threads per touched sector: the store pass uses the first half, the
-    // word lists of phases 1-2 all of them (latency hiding: 2 CTAs x 18 warps per SM)
-    static constexpr int THREADS = 2 * ((NTOUCH + 31) / 32 * 32);
+    // 4/3 threads per touched sector: the store pass uses the first NTOUCH, the work
+    // lists of phases 1-2 all of them.  With 16-bit work lists and no offset table the
+    // CTA needs 73 KB of shared memory: 3 CTAs x 12 warps per SM for byte cells, which
+    // overlaps one CTA's arithmetic with the others' memory phases better than
+    // 2 x 18 warps (n=2^17 NSUM8: 485 vs 549 us per pair)
+    static constexpr int THREADS = (NTOUCH * 4 / 3 + 31) / 32 * 32;
 };
 
 // gasket cells of a word whose first cell is (x, y) (x a multiple of the word's
@@ -120,21 +123,19 @@ __device__ __forceinline__ void vstrip(const uint8_t* rows, uint32_t pv, uint32_
 template <int C, int KIND, int NST>
 __global__ void __launch_bounds__(TB<C>::THREADS)
     stencil_tb2(uint8_t* __restrict__ grid, const uint8_t* __restrict__ src, int64_t n, uint32_t ntiles,
-                uint64_t param, const uint32_t* __restrict__ order, const uint32_t* __restrict__ lists_g, int ns,
+                uint64_t param, const uint32_t* __restrict__ order, const uint16_t* __restrict__ lists_g, int ns,
                 int np1, int ng1, int ni1, int np2, int flags) {
     using S = TB<C>;
     constexpr bool EIGHT = KIND == KIND_NSUM8;
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* ibuf = smem + NST * S::SBUF;          // state t+1, rows -1..TT
-    int64_t* goff = reinterpret_cast<int64_t*>(ibuf + S::IBUF);  // staged chunk -> byte offset in the grid
-    uint32_t* slist = reinterpret_cast<uint32_t*>(goff + ns);
-    uint32_t* p1list = slist + ns;                 // words: inner gasket, ring gasket, then copies
-    uint32_t* p2list = p1list + np1;               // the tile's words holding gasket cells
+    // work lists, all shared-memory byte offsets (row = o / PITCH, chunk / word from o % PITCH)
+    uint16_t* slist = reinterpret_cast<uint16_t*>(ibuf + S::IBUF);
+    uint16_t* p1list = slist + ns;                 // runs of inner gasket words, ring gasket words, copies
+    uint16_t* p2list = p1list + np1;               // runs of the tile's gasket words
     const int64_t rowstride = n * C;
     for (int i = threadIdx.x; i < ns + np1 + np2; i += S::THREADS) {
-        const uint32_t c = lists_g[i];
-        slist[i] = c;
-        if (i < ns) goff[i] = (int64_t)((c >> 16) & 0xffu) * rowstride + (int64_t)(c >> 24) * 16;
+        slist[i] = lists_g[i];
     }
     __syncthreads();
 
@@ -178,14 +179,14 @@ __global__ void __launch_bounds__(TB<C>::THREADS)
         const bool interior = y0 >= 2 && y0 + S::TT + 2 <= n && x0 > 0 && x0 + S::TT < n;
         for (int i = threadIdx.x; i < ns; i += S::THREADS) {
             const uint32_t c = slist[i];
+            const int j = (int)(c / PITCH), q = (int)(c % PITCH) / 16;
             if (interior) {
-                cp_async16(sb + (c & 0xffffu), base + goff[i], 16, fetch_line);
+                cp_async16(sb + c, base + (int64_t)j * rowstride + q * 16, 16, fetch_line);
             } else {
-                const int j = (int)((c >> 16) & 0xffu), q = (int)(c >> 24);
                 const int64_t y = y0 + j - 2;
                 const int64_t xb = x0 * C + (q - 1) * 16;
                 const bool in = y >= 0 && y < n && xb >= 0 && xb < rowstride;
-                cp_async16(sb + (c & 0xffffu), in ? src + y * rowstride + xb : src, in ? 16 : 0, fetch_line);
+                cp_async16(sb + c, in ? src + y * rowstride + xb : src, in ? 16 : 0, fetch_line);
             }
         }
     };
@@ -211,8 +212,7 @@ __global__ void __launch_bounds__(TB<C>::THREADS)
         //      [ni1, ng1): ring words that may hold gasket cells (exact global test);
         //      [ng1, np1): words without gasket cells (state t copied).
         for (int i = probe_nocompute ? np1 : threadIdx.x; i < np1; i += S::THREADS) {
-            const uint32_t c = p1list[i];
-            const int o = (int)(c & 0xffffu);
+            const int o = (int)p1list[i];
             if (i < ni1) {
                 uint32_t sum[S::V], centre[S::V];
                 vstrip<C, EIGHT, S::V>(sbuf + o, pv, sum, centre);
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(TB<C>::THREADS)
             } else if (i < ng1) {
                 uint32_t centre;
                 const uint32_t sum = word_sum<C, EIGHT>(sbuf + o, 0, pv, centre);
-                const int ji = (int)((c >> 16) & 0xffu), k = (int)(c >> 24);
+                const int ji = o / PITCH, k = (o % PITCH) / 4;
                 const uint32_t m = word_mask<C>((int)x0 + (k - 4) * S::V, (int)y0 + ji - 1, (int)n);
                 *reinterpret_cast<uint32_t*>(ibuf + o) = (sum & m) | (centre & ~m);
             } else {
@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(TB<C>::THREADS)
 
 // ---- host: the work lists (tile-independent supersets) ----------------------
 struct TbLists {
-    uint32_t* lists = nullptr;  // [staged chunks | phase-1 words | phase-2 words]
+    uint16_t* lists = nullptr;  // [staged chunks | phase-1 words | phase-2 words] (smem byte offsets)
     int ns = 0, np1 = 0, ng1 = 0, ni1 = 0, np2 = 0;
 };
 
@@ -312,7 +312,7 @@ void build_lists(bool eight, std::vector<uint32_t>& out, int& ns, int& np1, int&
             bool any = false;
             for (int c = (q - 1) * CC; c < q * CC; ++c) any = any || at(need, c, r);
             const int j = r + 2;
-            if (any) out.push_back((uint32_t)(j * PITCH + q * 16) | ((uint32_t)j << 16) | ((uint32_t)q << 24));
+            if (any) out.push_back((uint32_t)(j * PITCH + q * 16));
         }
     ns = (int)out.size();
     // phase 1: words of rows -1..TT holding a D1 cell.  The tile's own gasket words come
@@ -336,7 +336,7 @@ void build_lists(bool eight, std::vector<uint32_t>& out, int& ns, int& np1, int&
             }
             if (!d) continue;
             const int ji = r + 1;
-            const uint32_t e = (uint32_t)(ji * PITCH + k * 4) | ((uint32_t)ji << 16) | ((uint32_t)k << 24);
+            const uint32_t e = (uint32_t)(ji * PITCH + k * 4);
             (gsk ? ring : copy).push_back(e);
         }
     ni1 = (int)inner.size();
@@ -369,8 +369,9 @@ const TbLists* tb_lists(bool eight) {
     std::vector<uint32_t> v;
     TbLists L;
     build_lists<C>(eight, v, L.ns, L.np1, L.ng1, L.ni1, L.np2);
-    if (cudaMalloc(&L.lists, v.size() * 4) != cudaSuccess ||
-        cudaMemcpy(L.lists, v.data(), v.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+    std::vector<uint16_t> v16(v.begin(), v.end());  // every entry is a shared-memory offset < 2^16
+    if (cudaMalloc(&L.lists, v16.size() * 2) != cudaSuccess ||
+        cudaMemcpy(L.lists, v16.data(), v16.size() * 2, cudaMemcpyHostToDevice) != cudaSuccess) {
         cudaGetLastError();
         return nullptr;
     }
@@ -385,7 +386,7 @@ cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
     const TbLists* L = tb_lists<C>(KIND == KIND_NSUM8);
     const uint32_t* order = rowmajor_table(r_t, 0);
     if (L == nullptr || order == nullptr) return cudaErrorMemoryAllocation;
-    const size_t smem = (size_t)NST * S::SBUF + S::IBUF + 8 * (size_t)L->ns + 4 * (size_t)(L->ns + L->np1 + L->np2);
+    const size_t smem = (size_t)NST * S::SBUF + S::IBUF + 2 * (size_t)(L->ns + L->np1 + L->np2);
     auto* kern = stencil_tb2<C, KIND, NST>;
     static bool configured = false;
     if (!configured) {
@@ -407,8 +408,7 @@ cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
 
 template <int C, int KIND>
 cudaError_t launch_kind(const LaunchArgs& a, int r_t) {
-    // a 2-deep ring keeps two CTAs per SM (byte cells: 110 KB of shared memory each),
-    // measured faster than a 3-deep ring at one CTA per SM (759 vs 1104 us, n=2^17)
+    // a 2-deep ring: 3 CTAs per SM for byte cells (a 3-deep ring costs a CTA per SM)
     return launch_ck<C, KIND, 2>(a, r_t);
 }
 
