@@ -73,6 +73,15 @@ def _config(workload: str, rho: int, world: int, partitioned: bool) -> dict:
             "l2": "flushed before every timed step (4x L2 read, outside the events)"}
 
 
+def _host_threads() -> int:
+    """All the host cores this process may use (torchrun sets OMP_NUM_THREADS=1 for its
+    workers; the CPU arms pass the count explicitly so they still use every core)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
 def _peaks() -> tuple[float, str]:
     p = ROOT / "MEASURED_PEAKS.json"
     try:
@@ -404,17 +413,18 @@ def _cpu_baseline(workload: str, budget_s: float = 12.0) -> dict:
     n = 1 << r_s
     rho = 16
     g = np.zeros((n, n), dtype=np.dtype(dname))
-    src = oracle.fill_hash(n, np.dtype(dname), 1, 0) if kind else g
+    T = _host_threads()
+    src = oracle.fill_hash(n, np.dtype(dname), 1, 0, threads=T) if kind else g
     lx, ly = oracle.local_cells(oracle.STRAT_TABLE, rho)
-    oracle.run_block_space(g, src, rho, r_s - 4, oracle.STRAT_TABLE, lx, ly, kind, 1)  # warm
+    oracle.run_block_space(g, src, rho, r_s - 4, oracle.STRAT_TABLE, lx, ly, kind, 1, threads=T)  # warm
     times = []
     t_end = time.perf_counter() + budget_s
     while time.perf_counter() < t_end or len(times) < 3:
         t0 = time.perf_counter()
-        oracle.run_block_space(g, src, rho, r_s - 4, oracle.STRAT_TABLE, lx, ly, kind, 1)
+        oracle.run_block_space(g, src, rho, r_s - 4, oracle.STRAT_TABLE, lx, ly, kind, 1, threads=T)
         times.append(time.perf_counter() - t0)
     mean = statistics.fmean(times)
-    return {"value": 3**r_s / mean, "unit": "cells/s", "cores": oracle.max_threads(), "kind": "port",
+    return {"value": 3**r_s / mean, "unit": "cells/s", "cores": T, "kind": "port",
             "sample": f"{len(times)} x lambda TABLE rho=16 pass over n=2^{r_s} {dname} "
                       f"({['write', 'nsum4', 'nsum8'][kind]}), oracle/gasket_oracle.c (OpenMP)",
             "s_per_pass": mean}
@@ -572,14 +582,15 @@ def run_reference(args) -> None:
     n = 1 << r_s
     rho = 16  # the reference's best lambda configuration on CPU
     g = np.zeros((n, n), dtype=np.dtype(dname))
-    src = oracle.fill_hash(n, np.dtype(dname), 1, 0) if kind else g
+    T = _host_threads()
+    src = oracle.fill_hash(n, np.dtype(dname), 1, 0, threads=T) if kind else g
     lx, ly = oracle.local_cells(oracle.STRAT_TABLE, rho)
     for _ in range(max(1, args.warmup)):
-        oracle.run_block_space(g, src, rho, r_s - 4, oracle.STRAT_TABLE, lx, ly, kind, 1)
+        oracle.run_block_space(g, src, rho, r_s - 4, oracle.STRAT_TABLE, lx, ly, kind, 1, threads=T)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        oracle.run_block_space(g, src, rho, r_s - 4, oracle.STRAT_TABLE, lx, ly, kind, 1)
+        oracle.run_block_space(g, src, rho, r_s - 4, oracle.STRAT_TABLE, lx, ly, kind, 1, threads=T)
         times.append(time.perf_counter() - t0)
     sec = statistics.fmean(times)
     value = 3**r_s / sec
@@ -598,7 +609,7 @@ def run_reference(args) -> None:
         "dtype": dname,
         "data": "synthetic",
         "config": _config(workload, WORKLOADS[workload][3], world, workload.startswith("part")),
-        "cpu_baseline": {"value": value, "unit": "cells/s", "cores": oracle.max_threads(), "kind": "port",
+        "cpu_baseline": {"value": value, "unit": "cells/s", "cores": T, "kind": "port",
                          "sample": f"one lambda TABLE rho=16 pass over n=2^{r_s} {dname} per step "
                                    f"(oracle/gasket_oracle.c, the reference's numba kernel restated; cells/s is "
                                    f"size-independent for this pass)"},
