@@ -27,7 +27,7 @@ from .geometry import FractalSpec, IntraStrategy
 
 class CARunner:
     def __init__(self, grid: torch.Tensor, kind: int = backends.KERNEL_NEIGHBOR_SUM8, param: int = 1,
-                 rho: int = 64, use_graph: bool = True, temporal: int = 1) -> None:
+                 rho: int = 64, use_graph: bool = True, temporal: int = 2) -> None:
         device.require_cuda()
         if not device.is_device(grid):
             raise TypeError("CARunner works on a CUDA grid tensor")
