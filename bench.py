@@ -454,7 +454,9 @@ def run_ours(args) -> None:
 
         from paper_1706_04552_b200 import partition as P
 
-        plan = P.PartitionPlan(n, PART_LEVEL, world, eight=kind == 2)
+        # --temporal 2: every timed step is one fused pair of CA steps (gm_run_part2) with
+        # one exchange of the depth-2 halo; the line then reports per-CA-step figures
+        plan = P.PartitionPlan(n, PART_LEVEL, world, eight=kind == 2, depth=args.temporal)
         group = dist.group.WORLD if world > 1 else None
         if world > 1 and args.halo == "peer":
             # halo over peer memory (CUDA IPC + release/acquire flags): no collective per step
@@ -499,6 +501,10 @@ def run_ours(args) -> None:
     launches = native.launch_count() - launches0
     total_ms = _max_over_ranks(sum(ms), world)
     ms_per_step = total_ms / args.steps
+    ca_steps = args.temporal if part is not None else 1  # CA steps per timed step
+    if ca_steps > 1:
+        ms = [t / ca_steps for t in ms]
+        ms_per_step /= ca_steps
     cells = 3**r
     value = (1 if part is not None else world) * cells / (ms_per_step * 1e-3)
 
@@ -539,6 +545,10 @@ def run_ours(args) -> None:
     if part is not None:
         line["config"]["halo_bytes_per_step"] = part.halo_bytes_per_step if world > 1 else 0
         line["config"]["halo"] = (args.halo if world > 1 else "none (one rank)")
+        if ca_steps > 1:
+            line["config"]["ca_steps_per_launch"] = ca_steps
+            line["config"]["timing"] = (f"{ca_steps} fused CA steps per timed launch; ms_per_step and value are per "
+                                        f"CA step; roofline fracs are work-equivalent (one step's bytes per step)")
         if hasattr(part, "close"):
             part.close()
         line["config"]["subgasket_ranges"] = part.plan.ranges
@@ -684,6 +694,8 @@ def main() -> None:
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--nsweep", action="store_true", help="BASELINE config 4: n sweep + crossover n0, CSV")
+    ap.add_argument("--temporal", type=int, choices=(1, 2), default=1,
+                    help="part* workloads: CA steps fused per launch and per halo exchange")
     ap.add_argument("--halo", choices=("collective", "peer"), default="collective",
                     help="part* workloads, N>1: NCCL all_gather of the halo cells, or peer-memory puts (CUDA IPC)")
     ap.add_argument("--r-min", type=int, default=8)

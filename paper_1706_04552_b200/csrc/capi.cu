@@ -383,6 +383,40 @@ int gm_peer_halo_wait(const uint64_t* flags, int32_t rank, int32_t world, uint64
                                         reinterpret_cast<cudaStream_t>(stream)), "peer_halo_wait");
 }
 
+int gm_run_part2(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
+                 int32_t flags, int32_t level, uint32_t sg_begin, uint32_t sg_end, void* stream) {
+    gm_cfg_t c{};
+    c.n = n;
+    c.rho = 1;
+    c.mapping = GM_MAP_LAMBDA;
+    c.strategy = GM_STRAT_TUNED;
+    c.kind = kind;
+    c.cell_bytes = cell_bytes;
+    c.param = param;
+    c.flags = flags;
+    if (int rc = check_common(n, cell_bytes, 1, kind)) return rc;
+    if (kind != GM_KIND_NSUM4 && kind != GM_KIND_NSUM8) return fail(GM_EINVAL, "gm_run_part2: kind must be NSUM4 or NSUM8");
+    if (!grid || !src || src == grid) return fail(GM_EINVAL, "gm_run_part2 needs distinct grid and src buffers");
+    const int r = log2i(n);
+    const int64_t tile = cell_bytes <= 4 ? 128 / cell_bytes : 32;
+    if (level < 0 || (n >> level) < tile)
+        return fail(GM_EINVAL, "partition level %d too deep for n=2^%d (sub-gaskets narrower than a tile)", level, r);
+    uint64_t nsg = 1;
+    for (int i = 0; i < level; ++i) nsg *= 3;
+    if (sg_begin > sg_end || sg_end > nsg) return fail(GM_EINVAL, "sub-gasket range [%u, %u) outside [0, %llu)",
+                                                       sg_begin, sg_end, (unsigned long long)nsg);
+    gm::LaunchArgs a = make_args(&c, grid, src, nullptr, nullptr, 0, stream);
+    a.part_level = level;
+    a.sg_begin = sg_begin;
+    a.sg_end = sg_end;
+    const cudaError_t e = gm::launch_stencil_tb2(a);
+    if (e == cudaErrorNotSupported) {
+        cudaGetLastError();
+        return fail(GM_EINVAL, "gm_run_part2: needs 1-, 2- or 4-byte cells");
+    }
+    return cuda_rc(e, "partitioned two-step CA launch");
+}
+
 int gm_tile_order(int32_t q, int32_t level, uint32_t* out, int64_t capacity) {
     if (q < 0 || q > 15 || level < 0 || level > q || out == nullptr) return fail(GM_EINVAL, "gm_tile_order: bad q/level");
     std::vector<uint32_t> v;

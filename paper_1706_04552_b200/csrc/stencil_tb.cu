@@ -381,10 +381,16 @@ const TbLists* tb_lists(bool eight) {
 template <int C, int KIND, int NST>
 cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
     using S = TB<C>;
-    uint32_t ntiles = 1;
-    for (int i = 0; i < r_t; ++i) ntiles *= 3u;
+    // tile range: the whole gasket, or (partitioned launches, gm_run_part2) the digit-order
+    // sub-gasket range [sg_begin, sg_end) of level part_level; the order table groups
+    // tiles by those sub-gaskets, so the range is a contiguous run of it
+    uint32_t lo, hi;
+    tile_range(a, r_t, lo, hi);
+    if (hi == lo) return cudaSuccess;
+    const uint32_t ntiles = hi - lo;
     const TbLists* L = tb_lists<C>(KIND == KIND_NSUM8);
-    const uint32_t* order = rowmajor_table(r_t, 0);
+    const uint32_t* order = rowmajor_table(r_t, order_level(a, r_t));
+    if (order != nullptr) order += lo;
     if (L == nullptr || order == nullptr) return cudaErrorMemoryAllocation;
     const size_t smem = (size_t)NST * S::SBUF + S::IBUF + 2 * (size_t)(L->ns + L->np1 + L->np2);
     auto* kern = stencil_tb2<C, KIND, NST>;

@@ -72,6 +72,7 @@ _SIGS = {
     "gm_scatter_cells": [_vp, _i32, _vp, _i64, _vp, _vp],
     "gm_tile_order": [_i32, _i32, _vp, _i64],
     "gm_ca_step2": [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _vp],
+    "gm_run_part2": [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, ctypes.c_uint32, ctypes.c_uint32, _vp],
     "gm_dev_alloc": [_i64, ctypes.POINTER(ctypes.c_void_p)],
     "gm_dev_free": [_vp],
     "gm_ipc_get_handle": [_vp, _vp],

@@ -67,6 +67,7 @@ class PartitionPlan:
     level: int
     world: int
     eight: bool = True
+    depth: int = 1  # CA steps per exchange (2: two fused steps per launch, gm_run_part2)
     ranges: list[tuple[int, int]] = field(init=False)
     halo: dict[int, np.ndarray] = field(init=False)  # sub-gasket -> linear indices of changing halo cells
 
@@ -77,7 +78,9 @@ class PartitionPlan:
         self.nsg = 3 ** self.level
         self.m = self.n >> self.level
         self.ranges = rank_ranges(self.nsg, self.world)
-        self.halo = {s: self._halo_cells(s) for s in range(self.nsg)}
+        if self.depth not in (1, 2):
+            raise ValueError("depth must be 1 or 2 (CA steps per halo exchange)")
+        self.halo = {s: self._halo_cells_depth(s) for s in range(self.nsg)}
 
     # -- ownership --------------------------------------------------------
     def owner_of_subgasket(self, s: int) -> int:
@@ -118,6 +121,35 @@ class PartitionPlan:
             inside = (ix >= 0) & (ix < m) & (iy >= 0) & (iy < m)
             read |= inside & _is_member(ox + np.clip(ix, 0, m - 1), oy + np.clip(iy, 0, m - 1), n)
         return np.unique(gy[read] * n + gx[read])
+
+    def _offsets(self) -> list[tuple[int, int]]:
+        offs = [(1, 0), (-1, 0), (0, 1), (0, -1)]
+        if self.eight:
+            offs += [(1, 1), (1, -1), (-1, 1), (-1, -1)]
+        return offs
+
+    def _halo_cells_depth(self, s: int) -> np.ndarray:
+        """Changing cells outside sub-gasket s that its next `depth` steps read: for two
+        steps, the one-step halo H1 plus every gasket cell outside s next to an H1 cell
+        (H1's step-t+1 values, recomputed locally, read those at step t).  Off-gasket
+        cells never change, and a rank holds them from the start."""
+        h1 = self._halo_cells(s)
+        if self.depth == 1 or h1.size == 0:
+            return h1
+        n, m = self.n, self.m
+        bx, by = subgasket_block(s, self.level)
+        ox, oy = bx * m, by * m
+        extra = set()
+        for c in h1.tolist():
+            y, x = divmod(c, n)
+            for dx, dy in self._offsets():
+                gx, gy = x + dx, y + dy
+                if not (0 <= gx < n and 0 <= gy < n) or (gx & (n - 1 - gy)) != 0:
+                    continue
+                if ox <= gx < ox + m and oy <= gy < oy + m:
+                    continue  # own cell
+                extra.add(gy * n + gx)
+        return np.unique(np.concatenate([h1, np.array(sorted(extra), dtype=np.int64)]))
 
     def exchange_slots(self) -> tuple[list[np.ndarray], int]:
         """Per owner rank, the sorted linear indices of its cells some other rank reads."""
@@ -352,6 +384,8 @@ class PartitionedCA:
                  group=None, loopback: Optional[LoopbackGroup] = None, step_fn: Optional[StepFn] = None,
                  adopt_init: bool = False, halo: str = "collective",
                  init_fill: Optional[Callable[[torch.Tensor], None]] = None) -> None:
+        """plan.depth = 2 makes every step() advance two CA steps with one fused launch
+        (gm_run_part2) and one halo exchange."""
         """`init_fill(t)` (peer halo only) writes the initial state into the first buffer in
         place; `init` then only gives shape and dtype (a meta tensor is enough), so a
         2^18 grid needs two full-size buffers, not three."""
@@ -382,6 +416,10 @@ class PartitionedCA:
         from . import device as dev
         from . import native
 
+        if self.plan.depth == 2:  # two fused steps over this rank's sub-gaskets
+            native.call("gm_run_part2", dst.data_ptr(), src.data_ptr(), self.plan.n, dst.element_size(), self.kind,
+                        int(np.int32(self.param)), 0, self.plan.level, lo, hi, dev.stream_handle())
+            return
         native.call("gm_run_part", dst.data_ptr(), src.data_ptr(), self.plan.n, dst.element_size(), self.kind,
                     int(np.int32(self.param)), native.FLAG_DST_FROM_SRC, self.plan.level, lo, hi,
                     dev.stream_handle())
@@ -428,7 +466,8 @@ class PartitionedCA:
 
 def run_loopback(plan: PartitionPlan, init: torch.Tensor, kind: int, steps: int, param: int = 1,
                  step_fn: Optional[StepFn] = None) -> torch.Tensor:
-    """All virtual ranks on one device; returns the assembled grid after `steps`."""
+    """All virtual ranks on one device; returns the assembled grid after `steps` exchange
+    rounds (each plan.depth CA steps)."""
     lb = LoopbackGroup(plan.world)
     ranks = [PartitionedCA(plan, r, init, kind, param, loopback=lb, step_fn=step_fn) for r in range(plan.world)]
     for _ in range(steps):

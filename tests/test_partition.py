@@ -49,12 +49,39 @@ def test_halo_cells_are_corner_cells(eight):
             assert len(rel) <= (5 if eight else 3)
 
 
+@pytest.mark.parametrize("kind", [1, 2])
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_depth2_partition_matches_full_steps_cpu(kind, world):
+    """Two CA steps per exchange: with the depth-2 halo (H1 plus the gasket cells next to
+    H1) every rank's own cells after k pairs equal 2k full-grid oracle steps."""
+    n, level = 1 << 8, 3
+    plan = P.PartitionPlan(n, level, world, eight=kind == 2, depth=2)
+    import oracle
+
+    init = oracle.fill_hash(n, np.int8, 21, 0)
+    got = P.run_loopback(plan, torch.from_numpy(init), kind, 3, step_fn=_oracle_step_fn(plan, kind, 1))
+    assert np.array_equal(got.numpy(), _reference_steps(init, kind, 1, 6))
+
+
+def test_depth2_halo_contains_depth1():
+    for eight in (False, True):
+        p1 = P.PartitionPlan(1 << 10, 4, 4, eight=eight)
+        p2 = P.PartitionPlan(1 << 10, 4, 4, eight=eight, depth=2)
+        for s in range(p1.nsg):
+            assert set(p1.halo[s].tolist()) <= set(p2.halo[s].tolist())
+            assert len(p2.halo[s]) <= (13 if eight else 8)
+
+
 def _oracle_step_fn(plan, kind, param):
     import oracle
 
     def step(dst, src, lo, hi):
         tmp = dst.numpy().copy()
         oracle.run_bounding_box(tmp, src.numpy(), 1, kind, param)
+        if plan.depth == 2:  # a second step on this rank's (halo-current) local copy
+            tmp2 = tmp.copy()
+            oracle.run_bounding_box(tmp2, tmp, 1, kind, param)
+            tmp = tmp2
         mask = np.zeros(tmp.shape, dtype=bool)
         m = plan.m
         for s in range(lo, hi):
@@ -151,6 +178,10 @@ def test_partition_loopback_gpu_matches_full_grid(gpu, kind):
             plan = P.PartitionPlan(n, level, world, eight=kind == 2)
             got = P.run_loopback(plan, init, kind, 4)
             assert gpu.device.count_mismatch(got, a) == 0, (n, level, world)
+            # two fused steps per launch (gm_run_part2) with the depth-2 halo: 2 pairs = 4 steps
+            plan2 = P.PartitionPlan(n, level, world, eight=kind == 2, depth=2)
+            got2 = P.run_loopback(plan2, init, kind, 2)
+            assert gpu.device.count_mismatch(got2, a) == 0, (n, level, world, "depth 2")
 
 
 def _peer_worker(rank, world, port, n, level, kind, steps, out):
