@@ -231,14 +231,22 @@ def _make_step(workload: str, grid, src, rho: int, flags: int):
     return step
 
 
+_STEP_LAUNCHES = [0]  # our kernels launched between the events of the last _time_steps call
+
+
 def _time_steps(step, flusher, steps: int) -> list[float]:
     import torch
 
+    from paper_1706_04552_b200 import native
+
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    _STEP_LAUNCHES[0] = 0
     for a, b in ev:
-        flusher()
+        flusher()  # (its own kernel, outside the events: not counted)
         a.record()
+        k0 = native.launch_count()
         step()
+        _STEP_LAUNCHES[0] += native.launch_count() - k0
         b.record()
     torch.cuda.synchronize()
     return [a.elapsed_time(b) for a, b in ev]
@@ -498,7 +506,7 @@ def run_ours(args) -> None:
         t_wall = time.perf_counter() - t_wall0
     torch.cuda.synchronize()
     _barrier(world)
-    launches = native.launch_count() - launches0
+    launches = _STEP_LAUNCHES[0]  # inside the timed (event-bracketed) region only
     total_ms = _max_over_ranks(sum(ms), world)
     ms_per_step = total_ms / args.steps
     ca_steps = args.temporal if part is not None else 1  # CA steps per timed step
