@@ -499,7 +499,6 @@ def run_ours(args) -> None:
 
     _barrier(world)
     torch.cuda.synchronize()
-    launches0 = native.launch_count()
     with ClockSampler(local) as clk:
         t_wall0 = time.perf_counter()
         ms = _time_steps(step, flusher, args.steps)
