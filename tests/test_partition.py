@@ -184,7 +184,7 @@ def test_partition_loopback_gpu_matches_full_grid(gpu, kind):
             assert gpu.device.count_mismatch(got2, a) == 0, (n, level, world, "depth 2")
 
 
-def _peer_worker(rank, world, port, n, level, kind, steps, out):
+def _peer_worker(rank, world, port, n, level, kind, steps, out, depth=1):
     """One rank of the partitioned CA with the peer-memory halo (peer.cu): both ranks
     share the one GPU of the test box and map each other's buffers with CUDA IPC."""
     import torch.distributed as dist
@@ -196,7 +196,7 @@ def _peer_worker(rank, world, port, n, level, kind, steps, out):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         torch.cuda.set_device(0)
-        plan = P.PartitionPlan(n, level, world, eight=kind == 2)
+        plan = P.PartitionPlan(n, level, world, eight=kind == 2, depth=depth)
         init = oracle.fill_hash(n, np.int8, 9, 0)
         ca = P.PartitionedCA(plan, rank, torch.from_numpy(init).cuda(), kind, 1, group=dist.group.WORLD, halo="peer")
         for _ in range(steps):
@@ -205,7 +205,7 @@ def _peer_worker(rank, world, port, n, level, kind, steps, out):
         ca.peer.check()
         mask = ca.owned_mask().cpu().numpy()
         got = ca.a.cpu().numpy()[mask]
-        want = _reference_steps(init, kind, 1, steps)[mask]
+        want = _reference_steps(init, kind, 1, steps * depth)[mask]
         out[rank] = bool(np.array_equal(got, want))
         out[f"bytes{rank}"] = ca.halo_bytes_per_step
         ca.close()
@@ -214,8 +214,9 @@ def _peer_worker(rank, world, port, n, level, kind, steps, out):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("depth", [1, 2])
 @pytest.mark.parametrize("kind", [1, 2])
-def test_peer_memory_halo_two_processes(gpu, kind):
+def test_peer_memory_halo_two_processes(gpu, kind, depth):
     """PartitionedCA(halo="peer"): no collective per step, halo cells written into the
     peer's buffer over CUDA IPC + release/acquire step flags == the oracle's steps."""
     import torch.multiprocessing as mp
@@ -224,7 +225,8 @@ def test_peer_memory_halo_two_processes(gpu, kind):
     ctx = mp.get_context("spawn")
     out = ctx.Manager().dict()
     port = _free_port()
-    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, 1 << 10, 3, kind, 5, out)) for r in range(world)]
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, 1 << 10, 3, kind, 5, out, depth))
+             for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
