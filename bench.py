@@ -2,7 +2,7 @@
 """Headline benchmark: lambda(omega) gasket passes on B200 (BASELINE.json).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload write16|write16-i32|stencil17|stencil17-nsum4]
+                    [--workload write16|write16-i32|write17|stencil16|stencil17|stencil17-nsum4|part18]
                     [--no-sweep] [--no-e2e] [--no-cpu]
 
 Default workload (BASELINE configs[1]): the n = 2^16 write pass ("write a
@@ -45,6 +45,8 @@ WORKLOADS = {
     # name: (r, cell dtype name, kind, rho, description)
     "write16": (16, "int8", 0, 32, "n=2^16 gasket write pass (const 1), int8 cells, lambda map"),
     "write16-i32": (16, "int32", 0, 32, "n=2^16 gasket write pass (const 1), int32 cells, lambda map"),
+    "write17": (17, "int8", 0, 32, "n=2^17 gasket write pass (const 1), int8 cells, lambda map"),
+    "stencil16": (16, "int8", 2, 64, "n=2^16 8-neighbour CA step, int8 states, lambda map"),
     "stencil17": (17, "int8", 2, 64, "n=2^17 8-neighbour CA step, int8 states, lambda map"),
     "stencil17-nsum4": (17, "int8", 1, 64, "n=2^17 4-neighbour CA step, int8 states, lambda map"),
     "part15": (15, "int8", 2, 0, "n=2^15 8-neighbour CA step, int8 states, level-5 sub-gasket partition (functional "
