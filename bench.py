@@ -306,8 +306,23 @@ def _sweep(r: int, dtype, flusher, budget_s: float = 3.0) -> dict:
         "speedup_rho32_subbox_vs_bb": float(out["32"]["bb"]["ms"]) / float(out["32"]["subbox"]["ms"]),
         "speedup_rho1_subbox_vs_bb": float(out["1"]["bb"]["ms"]) / float(out["1"]["subbox"]["ms"]),
     }
+    # fraction of launched threads that land on gasket cells (engine.work_counts;
+    # the tuned kernel launches warps over whole 128-byte tile rows, so its figure is per
+    # touched word rather than per thread)
+    from paper_1706_04552_b200.engine import Mapping, work_counts
+    from paper_1706_04552_b200.geometry import FractalSpec
+
+    useful = {}
+    for rho in (1, 2, 4, 8, 16, 32):
+        spec = FractalSpec(n=n, rho=rho)
+        row = {"bb": work_counts(spec, Mapping.BOUNDING_BOX).threads_useful
+               / work_counts(spec, Mapping.BOUNDING_BOX).threads_launched}
+        for s in (IntraStrategy.SUBBOX, IntraStrategy.TABLE, IntraStrategy.UNROLL):
+            w = work_counts(spec, Mapping.BLOCK_SPACE, s)
+            row[s.value] = w.threads_useful / w.threads_launched
+        useful[str(rho)] = row
     return {"per_rho_ms": {rho: {k: v["ms"] for k, v in row.items()} for rho, row in out.items()},
-            "summary": summary}
+            "summary": summary, "useful_thread_fraction": useful}
 
 
 def _multi_step(r: int, tdt, kind: int, flusher, steps: int = 40) -> dict:
