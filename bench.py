@@ -320,6 +320,8 @@ def _sweep(r: int, dtype, flusher, budget_s: float = 3.0) -> dict:
         for s in (IntraStrategy.SUBBOX, IntraStrategy.TABLE, IntraStrategy.UNROLL):
             w = work_counts(spec, Mapping.BLOCK_SPACE, s)
             row[s.value] = w.threads_useful / w.threads_launched
+        k3 = 3 ** (rho.bit_length() - 1)  # TABLE / UNROLL threads per block: lanes used of the launched warps
+        row["table_unroll_lane_utilisation"] = k3 / (32 * -(-k3 // 32))
         useful[str(rho)] = row
     return {"per_rho_ms": {rho: {k: v["ms"] for k, v in row.items()} for rho, row in out.items()},
             "summary": summary, "useful_thread_fraction": useful}
