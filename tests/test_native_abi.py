@@ -55,3 +55,18 @@ def test_errors_without_gpu_are_loud():
     g = np.zeros((8, 8), dtype=np.int32)
     with pytest.raises(native.GasketError):
         backends.run_bounding_box(g, g, 2, 0, 1)
+
+
+def test_product_never_imports_the_oracle():
+    """The oracle is test infrastructure: only tests/, __graft_entry__.smoke() and bench.py's
+    CPU legs may use it; the package itself must not import it (no CPU fallback)."""
+    import ast
+
+    pkg = ROOT / "paper_1706_04552_b200"
+    for path in pkg.rglob("*.py"):
+        tree = ast.parse(path.read_text())
+        for node in ast.walk(tree):
+            if isinstance(node, ast.Import):
+                assert all(not a.name.split(".")[0] == "oracle" for a in node.names), path
+            elif isinstance(node, ast.ImportFrom):
+                assert (node.module or "").split(".")[0] != "oracle", path
