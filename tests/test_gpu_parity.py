@@ -467,3 +467,27 @@ def test_fused_two_steps_equal_single_steps_large(gpu, dtype):
         native.call("gm_ca_step2", fused.data_ptr(), src.data_ptr(), n, src.element_size(), kind, 5, 0,
                     device.stream_handle())
         assert torch.equal(fused, two), (dtype, kind)
+
+
+def test_randomised_launches_vs_oracle(gpu, oracle):
+    """Seeded fuzz over (n, rho, cell type, kernel, param, strategy, tuned flags) -- every
+    launch cell-by-cell against the oracle."""
+    rng = np.random.default_rng(20261017)
+    be, S = gpu.backends, gpu.geometry.IntraStrategy
+    dtypes = list(DTYPES)
+    for _ in range(160):
+        r = int(rng.integers(0, 11))
+        n = 1 << r
+        rho = 1 << int(rng.integers(0, r + 1))
+        dtype = dtypes[int(rng.integers(0, len(dtypes)))]
+        kind = int(rng.integers(0, 3))
+        param = int(rng.integers(-(2**31), 2**31 - 1))
+        grid0 = oracle.fill_hash(n, dtype, int(rng.integers(0, 1 << 30)), int(rng.integers(0, 2)))
+        src = oracle.fill_hash(n, dtype, int(rng.integers(0, 1 << 30)), 0)
+        want = _oracle_result(oracle, grid0, src, rho, kind, param)
+        strat = [S.UNROLL, S.TABLE, S.SUBBOX, S.TUNED][int(rng.integers(0, 4))]
+        flags = int(TUNED_FLAGS[int(rng.integers(0, len(TUNED_FLAGS)))]) if strat is S.TUNED else 0
+        g = _to_dev(grid0)
+        lx, ly = be.local_cell_arrays(strat, rho)
+        be.run_block_space(g, _to_dev(src), rho, (n // rho).bit_length() - 1, strat, lx, ly, kind, param, flags=flags)
+        assert np.array_equal(g.cpu().numpy(), want), (n, rho, np.dtype(dtype).name, kind, param, strat, flags)
