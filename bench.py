@@ -47,6 +47,7 @@ WORKLOADS = {
     "write16-i32": (16, "int32", 0, 32, "n=2^16 gasket write pass (const 1), int32 cells, lambda map"),
     "write17": (17, "int8", 0, 32, "n=2^17 gasket write pass (const 1), int8 cells, lambda map"),
     "stencil16": (16, "int8", 2, 64, "n=2^16 8-neighbour CA step, int8 states, lambda map"),
+    "stencil16-i32-nsum4": (16, "int32", 1, 64, "n=2^16 4-neighbour CA step, int32 states (the reference's dtype), lambda map"),
     "stencil17": (17, "int8", 2, 64, "n=2^17 8-neighbour CA step, int8 states, lambda map"),
     "stencil17-nsum4": (17, "int8", 1, 64, "n=2^17 4-neighbour CA step, int8 states, lambda map"),
     "part15": (15, "int8", 2, 0, "n=2^15 8-neighbour CA step, int8 states, level-5 sub-gasket partition (functional "
