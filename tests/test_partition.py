@@ -214,14 +214,13 @@ def _peer_worker(rank, world, port, n, level, kind, steps, out, depth=1):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("depth", [1, 2])
-@pytest.mark.parametrize("kind", [1, 2])
-def test_peer_memory_halo_two_processes(gpu, kind, depth):
+@pytest.mark.parametrize("world,depth,kind", [(2, 1, 1), (2, 1, 2), (2, 2, 1), (2, 2, 2), (4, 1, 2), (4, 2, 2)])
+def test_peer_memory_halo_processes(gpu, world, depth, kind):
     """PartitionedCA(halo="peer"): no collective per step, halo cells written into the
-    peer's buffer over CUDA IPC + release/acquire step flags == the oracle's steps."""
+    peers' buffers over CUDA IPC + release/acquire step flags == the oracle's steps
+    (all ranks share the test box's GPU; 4 ranks exercise every-peer puts and waits)."""
     import torch.multiprocessing as mp
 
-    world = 2
     ctx = mp.get_context("spawn")
     out = ctx.Manager().dict()
     port = _free_port()
@@ -232,5 +231,5 @@ def test_peer_memory_halo_two_processes(gpu, kind, depth):
     for p in procs:
         p.join(timeout=300)
         assert p.exitcode == 0
-    assert out[0] is True and out[1] is True
-    assert out["bytes0"] > 0 and out["bytes1"] > 0
+    assert all(out[r] is True for r in range(world))
+    assert all(out[f"bytes{r}"] > 0 for r in range(world))
