@@ -1,3 +1,6 @@
+#include <tuple>
+#include <set>
+#include <mutex>
 #include <cstdlib>
 #include <algorithm>
 // capi.cu -- extern "C" drop-in boundary (include/gasket_b200.h).
@@ -131,6 +134,16 @@ int launch_cfg(const gm_cfg_t* c, void* grid, const void* src, const int32_t* tx
 }  // namespace
 
 namespace gm {
+void ensure_dynamic_smem(const void* kern, size_t smem) {
+    static std::mutex mu;
+    static std::set<std::tuple<const void*, int, size_t>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.insert(std::make_tuple(kern, dev, smem)).second)
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
 int order_level(const LaunchArgs& a, int r_t) {
     if (a.part_level >= 0) return a.part_level;
     static const int env = [] {

@@ -45,6 +45,10 @@ inline void tile_range(const LaunchArgs& a, int r_t, uint32_t& lo, uint32_t& hi)
 
 void note_launch();
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize for `kern` on the current device, set once
+// per (kernel, device) -- the attribute is per device context (capi.cu)
+void ensure_dynamic_smem(const void* kern, size_t smem);
+
 // Sub-gasket level whose groups the row-major tile order keeps together: the partition
 // level for partitioned launches (their tile ranges are digit-order sub-gasket ranges),
 // else 0 (one row-major sweep) -- or GASKET_TILE_ORDER_LEVEL for experiments.

@@ -322,11 +322,7 @@ cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
     const uint32_t ntiles = hi - lo;
     const size_t smem = 2 * S::BUF + 2 * S::ROWS * CHUNKS + 16;
     auto* kern = stencil_tile<C, KIND>;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-    }
+    ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -296,11 +296,7 @@ cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
     const uint32_t ntiles = hi - lo;
     const size_t smem = (size_t)NST * S::BUF + (NST == 2 ? 8 : 4) * S::ROWS * CHUNKS;
     auto* kern = stencil_v2<C, KIND, NST>;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-    }
+    ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -394,11 +394,7 @@ cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
     if (L == nullptr || order == nullptr) return cudaErrorMemoryAllocation;
     const size_t smem = (size_t)NST * S::SBUF + S::IBUF + 2 * (size_t)(L->ns + L->np1 + L->np2);
     auto* kern = stencil_tb2<C, KIND, NST>;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-    }
+    ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -281,11 +281,7 @@ cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
         return cudaErrorNotSupported;
     const size_t smem = (size_t)NSTAGE * S::STAGE;
     auto* kern = stencil_tma<C, KIND>;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-    }
+    ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
