@@ -190,6 +190,14 @@ int gm_peer_halo_put(const void* mine, const uint64_t* peers, const int64_t* idx
                      const uint64_t* peer_flags, int32_t rank, int32_t world, uint64_t epoch, void* stream);
 int gm_peer_halo_wait(const uint64_t* flags, int32_t rank, int32_t world, uint64_t epoch, uint64_t timeout_ns,
                       uint32_t* status, void* stream);
+/* gm_run_part with the halo exchange fused into the step kernel (peer_epilogue.cuh):
+ * `epilogue` = device descriptor (PartitionedCA(halo="peer", fused=True) builds it);
+ * every CTA first acquires the peers' flags >= wait_epoch (0: no wait), the last CTA
+ * to finish stores the rank's halo cells into the peers' buffers and releases
+ * signal_epoch.  Stream-ordered like every launch. */
+int gm_run_part_peer(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
+                     int32_t flags, int32_t level, uint32_t sg_begin, uint32_t sg_end, void* epilogue,
+                     uint64_t wait_epoch, uint64_t signal_epoch, void* stream);
 /* gm_ca_step2 restricted to the level-`level` sub-gaskets [sg_begin, sg_end) (digit
  * order), like gm_run_part: one rank's share of a partitioned CA, two steps per call.
  * The caller keeps the halo within two steps current (PartitionPlan(depth=2)). */

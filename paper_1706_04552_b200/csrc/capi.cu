@@ -430,6 +430,43 @@ int gm_run_part2(void* grid, const void* src, int64_t n, int32_t cell_bytes, int
     return cuda_rc(e, "partitioned two-step CA launch");
 }
 
+int gm_run_part_peer(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
+                     int32_t flags, int32_t level, uint32_t sg_begin, uint32_t sg_end, void* epilogue,
+                     uint64_t wait_epoch, uint64_t signal_epoch, void* stream) {
+    gm_cfg_t c{};
+    c.n = n;
+    c.rho = 1;
+    c.mapping = GM_MAP_LAMBDA;
+    c.strategy = GM_STRAT_TUNED;
+    c.kind = kind;
+    c.cell_bytes = cell_bytes;
+    c.param = param;
+    c.flags = flags & ~(GM_FLAG_OMEGA_ORDER | GM_FLAG_STENCIL_V1 | GM_FLAG_FORCE_TMA);
+    if (int rc = check_common(n, cell_bytes, 1, kind)) return rc;
+    if (kind != GM_KIND_NSUM4 && kind != GM_KIND_NSUM8) return fail(GM_EINVAL, "gm_run_part_peer: kind must be NSUM4 or NSUM8");
+    if (!grid || !src || src == grid || !epilogue) return fail(GM_EINVAL, "gm_run_part_peer: bad buffers or descriptor");
+    const int64_t tile = cell_bytes <= 4 ? 128 / cell_bytes : 32;
+    if (level < 0 || (n >> level) < tile) return fail(GM_EINVAL, "partition level %d too deep", level);
+    uint64_t nsg = 1;
+    for (int i = 0; i < level; ++i) nsg *= 3;
+    if (sg_begin > sg_end || sg_end > nsg) return fail(GM_EINVAL, "sub-gasket range [%u, %u) outside [0, %llu)",
+                                                       sg_begin, sg_end, (unsigned long long)nsg);
+    gm::LaunchArgs a = make_args(&c, grid, src, nullptr, nullptr, 0, stream);
+    a.part_level = level;
+    a.sg_begin = sg_begin;
+    a.sg_end = sg_end;
+    a.peer_epi = epilogue;
+    a.wait_epoch = wait_epoch;
+    a.signal_epoch = signal_epoch;
+    // only the v2 tile kernel carries the fused exchange: no silent fallback to a kernel without it
+    const cudaError_t e = gm::launch_stencil_v2(a);
+    if (e == cudaErrorNotSupported) {
+        cudaGetLastError();
+        return fail(GM_EINVAL, "gm_run_part_peer: needs 1-, 2- or 4-byte cells");
+    }
+    return cuda_rc(e, "partitioned CA step with fused peer exchange");
+}
+
 int gm_tile_order(int32_t q, int32_t level, uint32_t* out, int64_t capacity) {
     if (q < 0 || q > 15 || level < 0 || level > q || out == nullptr) return fail(GM_EINVAL, "gm_tile_order: bad q/level");
     std::vector<uint32_t> v;

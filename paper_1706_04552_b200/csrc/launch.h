@@ -28,6 +28,10 @@ struct LaunchArgs {
     // sub-gaskets [sg_begin, sg_end) in digit order; part_level < 0 = whole gasket
     int part_level = -1;
     uint32_t sg_begin = 0, sg_end = 0;
+    // fused peer halo exchange (gm_run_part_peer, peer_epilogue.cuh): device descriptor,
+    // the peers' epoch to wait for before reading, the epoch to signal after writing
+    void* peer_epi = nullptr;
+    uint64_t wait_epoch = 0, signal_epoch = 0;
 };
 
 // Tile-index range [lo, hi) of a launch whose kernel tiles the gasket at level r_t.

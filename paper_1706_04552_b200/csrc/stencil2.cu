@@ -37,6 +37,7 @@
 #include "gasket.cuh"
 #include "launch.h"
 #include "stencil_common.cuh"
+#include "peer_epilogue.cuh"
 #include "../../include/gasket_b200.h"
 
 namespace gm {
@@ -98,8 +99,10 @@ template <int C, int KIND, int NST>
 __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict__ grid, const uint8_t* __restrict__ src,
                                                              int64_t n, uint32_t tile_lo, uint32_t tile_hi, int r_t,
                                                              int part_level, uint64_t param, int flags,
-                                                             const uint32_t* __restrict__ order) {
+                                                             const uint32_t* __restrict__ order, PeerEpilogue* epi,
+                                                             uint64_t wait_epoch, uint64_t signal_epoch) {
     using S = T2<C>;
+    peer_prologue_wait(epi, wait_epoch);  // partitioned CA with the fused exchange only
     constexpr bool EIGHT = KIND == KIND_NSUM8;
     extern __shared__ __align__(128) uint8_t smem[];
     uint32_t* chunks = reinterpret_cast<uint32_t*>(smem + NST * S::BUF);  // needed chunks: smem off | j << 16 | q << 24
@@ -196,8 +199,8 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
     const uint32_t step = chunked ? 1u : gridDim.x;
     const uint32_t first = tile_lo + blockIdx.x * chunk;
     const uint32_t last = chunked ? min(tile_hi, first + chunk) : tile_hi;  // exclusive
-    if (first >= last) return;
-    const uint32_t count = (last - first + step - 1) / step;
+    // (a CTA without tiles still takes part in the fused exchange's completion count)
+    const uint32_t count = first >= last ? 0u : (last - first + step - 1) / step;
 
     auto stage = [&](uint32_t idx) {  // stage this CTA's tile #idx into ring slot idx % NST
         if (idx >= count || probe_noload) return;
@@ -285,6 +288,7 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
         }
     }
     cp_async_wait<0>();
+    peer_epilogue_signal(grid, epi, signal_epoch);  // partitioned CA with the fused exchange only
 }
 
 template <int C, int KIND, int NST>
@@ -308,7 +312,9 @@ cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
     if (!(a.flags & GM_FLAG_DIGIT_ORDER)) order = rowmajor_table(r_t, order_level(a, r_t));
     kern<<<(unsigned)blocks, S::THREADS, smem, a.stream>>>(reinterpret_cast<uint8_t*>(a.grid),
                                                           reinterpret_cast<const uint8_t*>(a.src), a.n, lo, hi, r_t,
-                                                          a.part_level, a.param, a.flags, order);
+                                                          a.part_level, a.param, a.flags, order,
+                                                          reinterpret_cast<PeerEpilogue*>(a.peer_epi), a.wait_epoch,
+                                                          a.signal_epoch);
     note_launch();
     return cudaGetLastError();
 }

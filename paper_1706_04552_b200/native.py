@@ -73,6 +73,8 @@ _SIGS = {
     "gm_tile_order": [_i32, _i32, _vp, _i64],
     "gm_ca_step2": [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _vp],
     "gm_run_part2": [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, ctypes.c_uint32, ctypes.c_uint32, _vp],
+    "gm_run_part_peer": [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, ctypes.c_uint32, ctypes.c_uint32, _vp, _u64,
+                         _u64, _vp],
     "gm_dev_alloc": [_i64, ctypes.POINTER(ctypes.c_void_p)],
     "gm_dev_free": [_vp],
     "gm_ipc_get_handle": [_vp, _vp],

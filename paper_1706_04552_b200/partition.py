@@ -341,7 +341,49 @@ class PeerHaloExchange:
         self.peer_flags = torch.tensor(ptrs[2], dtype=torch.int64).cuda()
         self.bufs = bufs
         self.epoch = 0
+        self._group = group
         dist.barrier(group=group)
+
+    # ---- the exchange fused into the step kernel (peer_epilogue.cuh, gm_run_part_peer) ----
+    MAX_PEERS = 16
+
+    def epilogue(self, which: int) -> torch.Tensor:
+        """Device descriptor (struct PeerEpilogue) for steps that write buffer `which`."""
+        if not hasattr(self, "_epi"):
+            import ctypes
+
+            class Epi(ctypes.Structure):
+                _fields_ = [("peers", ctypes.c_uint64 * self.MAX_PEERS), ("peer_flags", ctypes.c_uint64 * self.MAX_PEERS),
+                            ("own_flags", ctypes.c_uint64), ("idx", ctypes.c_uint64), ("count", ctypes.c_int64),
+                            ("cell_bytes", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+                            ("done", ctypes.c_uint32), ("status", ctypes.c_uint32)]
+
+            if self.world > self.MAX_PEERS:
+                raise ValueError(f"the fused exchange supports up to {self.MAX_PEERS} ranks")
+            pb = [t.cpu().tolist() for t in self.peer_bufs]
+            pf = self.peer_flags.cpu().tolist()
+            self._epi = []
+            for w in range(2):
+                e = Epi()
+                for q in range(self.world):
+                    e.peers[q] = pb[w][q]
+                    e.peer_flags[q] = pf[q]
+                e.own_flags = self.flags.ptr
+                e.idx = self.send_idx.data_ptr()
+                e.count = self.send_idx.numel()
+                e.cell_bytes, e.rank, e.world = self.cell_bytes, self.rank, self.world
+                raw = np.frombuffer(bytes(e), dtype=np.uint8).copy()
+                self._epi.append(torch.from_numpy(raw).cuda())
+            self._epi_status_off = Epi.status.offset
+        return self._epi[which]
+
+    def check_fused(self) -> None:
+        for t in getattr(self, "_epi", []):
+            st = int(t[self._epi_status_off:self._epi_status_off + 4].cpu().numpy().view(np.uint32)[0])
+            if st:
+                from .native import GasketError
+
+                raise GasketError(f"fused peer halo wait timed out (peer bitmask {st:#x})")
 
     def exchange(self, which: int) -> None:
         """After this rank wrote its new state into buffer `which`: put + wait (stream-ordered)."""
@@ -364,9 +406,12 @@ class PeerHaloExchange:
             raise GasketError(f"peer halo wait timed out (peer bitmask {bad:#x})")
 
     def close(self) -> None:
+        import torch.distributed as dist
+
         from . import native
 
         torch.cuda.synchronize()
+        dist.barrier(group=self._group)  # every peer is done storing into this rank's buffers
         for p in self._opened:
             native.call("gm_ipc_close", p)
         self._opened = []
@@ -383,7 +428,7 @@ class PartitionedCA:
     def __init__(self, plan: PartitionPlan, rank: int, init: torch.Tensor, kind: int, param: int = 1,
                  group=None, loopback: Optional[LoopbackGroup] = None, step_fn: Optional[StepFn] = None,
                  adopt_init: bool = False, halo: str = "collective",
-                 init_fill: Optional[Callable[[torch.Tensor], None]] = None) -> None:
+                 init_fill: Optional[Callable[[torch.Tensor], None]] = None, fused: bool = False) -> None:
         """plan.depth = 2 makes every step() advance two CA steps with one fused launch
         (gm_run_part2) and one halo exchange."""
         """`init_fill(t)` (peer halo only) writes the initial state into the first buffer in
@@ -411,6 +456,12 @@ class PartitionedCA:
             raise ValueError("halo must be 'collective' (all_gather) or 'peer' (peer memory)")
         self.step_fn = step_fn or self._gpu_step
         self.lo, self.hi = plan.ranges[rank]
+        # fused=True (peer halo, one step per exchange): the exchange runs inside the step
+        # kernel (gm_run_part_peer) -- one launch per step, no put/wait kernels
+        self.fused = bool(fused)
+        if self.fused and (self.peer is None or plan.depth != 1 or step_fn is not None):
+            raise ValueError("fused exchange needs halo='peer', plan.depth == 1 and the GPU step")
+        self._epoch = 0
 
     def _gpu_step(self, dst: torch.Tensor, src: torch.Tensor, lo: int, hi: int) -> None:
         from . import device as dev
@@ -434,6 +485,17 @@ class PartitionedCA:
 
     def step(self) -> None:
         """compute -> exchange halo of the new state -> swap (real process group)."""
+        if self.fused:
+            from . import device as dev
+            from . import native
+
+            self._epoch += 1
+            native.call("gm_run_part_peer", self.b.data_ptr(), self.a.data_ptr(), self.plan.n, self.b.element_size(),
+                        self.kind, int(np.int32(self.param)), native.FLAG_DST_FROM_SRC, self.plan.level, self.lo,
+                        self.hi, self.peer.epilogue(self._dst).data_ptr(), self._epoch - 1, self._epoch,
+                        dev.stream_handle())
+            self.finish()
+            return
         self.compute()
         if self.peer is not None:
             self.peer.exchange(self._dst)
@@ -448,6 +510,7 @@ class PartitionedCA:
     def close(self) -> None:
         if self.peer is not None:
             self.peer.check()
+            self.peer.check_fused()
             self.peer.close()
             self.a = self.b = None
             for d in self._dbufs:

@@ -184,7 +184,7 @@ def test_partition_loopback_gpu_matches_full_grid(gpu, kind):
             assert gpu.device.count_mismatch(got2, a) == 0, (n, level, world, "depth 2")
 
 
-def _peer_worker(rank, world, port, n, level, kind, steps, out, depth=1):
+def _peer_worker(rank, world, port, n, level, kind, steps, out, depth=1, fused=False):
     """One rank of the partitioned CA with the peer-memory halo (peer.cu): both ranks
     share the one GPU of the test box and map each other's buffers with CUDA IPC."""
     import torch.distributed as dist
@@ -198,7 +198,8 @@ def _peer_worker(rank, world, port, n, level, kind, steps, out, depth=1):
         torch.cuda.set_device(0)
         plan = P.PartitionPlan(n, level, world, eight=kind == 2, depth=depth)
         init = oracle.fill_hash(n, np.int8, 9, 0)
-        ca = P.PartitionedCA(plan, rank, torch.from_numpy(init).cuda(), kind, 1, group=dist.group.WORLD, halo="peer")
+        ca = P.PartitionedCA(plan, rank, torch.from_numpy(init).cuda(), kind, 1, group=dist.group.WORLD, halo="peer",
+                             fused=fused)
         for _ in range(steps):
             ca.step()
         torch.cuda.synchronize()
@@ -214,8 +215,10 @@ def _peer_worker(rank, world, port, n, level, kind, steps, out, depth=1):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,depth,kind", [(2, 1, 1), (2, 1, 2), (2, 2, 1), (2, 2, 2), (4, 1, 2), (4, 2, 2)])
-def test_peer_memory_halo_processes(gpu, world, depth, kind):
+@pytest.mark.parametrize("world,depth,kind,fused", [(2, 1, 1, False), (2, 1, 2, False), (2, 2, 1, False),
+                                                    (2, 2, 2, False), (4, 1, 2, False), (4, 2, 2, False),
+                                                    (2, 1, 1, True), (2, 1, 2, True), (4, 1, 2, True)])
+def test_peer_memory_halo_processes(gpu, world, depth, kind, fused):
     """PartitionedCA(halo="peer"): no collective per step, halo cells written into the
     peers' buffers over CUDA IPC + release/acquire step flags == the oracle's steps
     (all ranks share the test box's GPU; 4 ranks exercise every-peer puts and waits)."""
@@ -224,7 +227,7 @@ def test_peer_memory_halo_processes(gpu, world, depth, kind):
     ctx = mp.get_context("spawn")
     out = ctx.Manager().dict()
     port = _free_port()
-    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, 1 << 10, 3, kind, 5, out, depth))
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, 1 << 10, 3, kind, 5, out, depth, fused))
              for r in range(world)]
     for p in procs:
         p.start()
