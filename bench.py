@@ -486,13 +486,13 @@ def run_ours(args) -> None:
         # one exchange of the depth-2 halo; the line then reports per-CA-step figures
         plan = P.PartitionPlan(n, PART_LEVEL, world, eight=kind == 2, depth=args.temporal)
         group = dist.group.WORLD if world > 1 else None
-        if world > 1 and args.halo == "peer":
+        if world > 1 and args.halo in ("peer", "peer-fused"):
             # halo over peer memory (CUDA IPC + release/acquire flags): no collective per step
             def fill(t):
                 native.call("gm_fill_hash", t.data_ptr(), n, c, 1, 0, device.stream_handle())
 
             part = P.PartitionedCA(plan, rank, torch.empty((n, n), dtype=tdt, device="meta"), kind, 1,
-                                   group=group, halo="peer", init_fill=fill)
+                                   group=group, halo="peer", init_fill=fill, fused=args.halo == "peer-fused")
         else:
             init = device.fill_hash(n, tdt, 1, 0)  # every rank holds the same initial state
             part = P.PartitionedCA(plan, rank, init, kind, 1, group=group, adopt_init=True)
@@ -723,8 +723,9 @@ def main() -> None:
     ap.add_argument("--nsweep", action="store_true", help="BASELINE config 4: n sweep + crossover n0, CSV")
     ap.add_argument("--temporal", type=int, choices=(1, 2), default=1,
                     help="part* workloads: CA steps fused per launch and per halo exchange")
-    ap.add_argument("--halo", choices=("collective", "peer"), default="collective",
-                    help="part* workloads, N>1: NCCL all_gather of the halo cells, or peer-memory puts (CUDA IPC)")
+    ap.add_argument("--halo", choices=("collective", "peer", "peer-fused"), default="collective",
+                    help="part* workloads, N>1: NCCL all_gather of the halo cells, peer-memory puts (CUDA IPC), "
+                         "or the peer exchange fused into the step kernel (temporal 1)")
     ap.add_argument("--r-min", type=int, default=8)
     ap.add_argument("--r-max", type=int, default=18)
     ap.add_argument("--nsweep-out", default="profiles/r1_nsweep.csv")
