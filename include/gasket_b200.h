@@ -78,6 +78,7 @@ extern "C" {
 #define GM_FLAG_FETCH_MIXED 1048576   /* stencil v2 with FETCH_HALF: whole-line fetch for lines needed in both halves */
 #define GM_FLAG_FETCH_HALF 2097152    /* stencil v2: stage with the .L2::64B hint (64-byte halves) instead of whole lines */
 #define GM_FLAG_FETCH256 4194304      /* stencil v2: stage interior tiles with the .L2::256B prefetch-size hint */
+#define GM_FLAG_TWO_STEPS 8388608     /* gm_run_part_peer: two fused CA steps per launch (depth-2 halo) */
 
 #define GM_OK 0
 #define GM_EINVAL 1  /* bad shape / size / tag (the reference's ValueError) */
@@ -194,7 +195,8 @@ int gm_peer_halo_wait(const uint64_t* flags, int32_t rank, int32_t world, uint64
  * `epilogue` = device descriptor (PartitionedCA(halo="peer", fused=True) builds it);
  * every CTA first acquires the peers' flags >= wait_epoch (0: no wait), the last CTA
  * to finish stores the rank's halo cells into the peers' buffers and releases
- * signal_epoch.  Stream-ordered like every launch. */
+ * signal_epoch.  With GM_FLAG_TWO_STEPS the launch is gm_run_part2's two fused steps
+ * (the halo must then be the depth-2 one).  Stream-ordered like every launch. */
 int gm_run_part_peer(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
                      int32_t flags, int32_t level, uint32_t sg_begin, uint32_t sg_end, void* epilogue,
                      uint64_t wait_epoch, uint64_t signal_epoch, void* stream);

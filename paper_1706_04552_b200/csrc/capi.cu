@@ -458,8 +458,9 @@ int gm_run_part_peer(void* grid, const void* src, int64_t n, int32_t cell_bytes,
     a.peer_epi = epilogue;
     a.wait_epoch = wait_epoch;
     a.signal_epoch = signal_epoch;
-    // only the v2 tile kernel carries the fused exchange: no silent fallback to a kernel without it
-    const cudaError_t e = gm::launch_stencil_v2(a);
+    // only the v2 tile kernel (one step) and the fused two-step kernel (GM_FLAG_TWO_STEPS)
+    // carry the fused exchange: no silent fallback to a kernel without it
+    const cudaError_t e = (flags & GM_FLAG_TWO_STEPS) ? gm::launch_stencil_tb2(a) : gm::launch_stencil_v2(a);
     if (e == cudaErrorNotSupported) {
         cudaGetLastError();
         return fail(GM_EINVAL, "gm_run_part_peer: needs 1-, 2- or 4-byte cells");

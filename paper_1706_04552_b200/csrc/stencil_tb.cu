@@ -36,6 +36,7 @@
 #include "gasket.cuh"
 #include "launch.h"
 #include "stencil_common.cuh"
+#include "peer_epilogue.cuh"
 #include "../../include/gasket_b200.h"
 
 namespace gm {
@@ -124,8 +125,10 @@ template <int C, int KIND, int NST>
 __global__ void __launch_bounds__(TB<C>::THREADS)
     stencil_tb2(uint8_t* __restrict__ grid, const uint8_t* __restrict__ src, int64_t n, uint32_t ntiles,
                 uint64_t param, const uint32_t* __restrict__ order, const uint16_t* __restrict__ lists_g, int ns,
-                int np1, int ng1, int ni1, int np2, int flags) {
+                int np1, int ng1, int ni1, int np2, int flags, PeerEpilogue* epi, uint64_t wait_epoch,
+                uint64_t signal_epoch) {
     using S = TB<C>;
+    peer_prologue_wait(epi, wait_epoch);  // partitioned CA with the fused exchange only
     constexpr bool EIGHT = KIND == KIND_NSUM8;
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* ibuf = smem + NST * S::SBUF;          // state t+1, rows -1..TT
@@ -261,6 +264,7 @@ __global__ void __launch_bounds__(TB<C>::THREADS)
         }
     }
     cp_async_wait<0>();
+    peer_epilogue_signal(grid, epi, signal_epoch);  // partitioned CA with the fused exchange only
 }
 
 // ---- host: the work lists (tile-independent supersets) ----------------------
@@ -403,7 +407,9 @@ cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
     if (blocks > ntiles) blocks = ntiles;
     kern<<<(unsigned)blocks, S::THREADS, smem, a.stream>>>(reinterpret_cast<uint8_t*>(a.grid),
                                                           reinterpret_cast<const uint8_t*>(a.src), a.n, ntiles,
-                                                          a.param, order, L->lists, L->ns, L->np1, L->ng1, L->ni1, L->np2, a.flags);
+                                                          a.param, order, L->lists, L->ns, L->np1, L->ng1, L->ni1, L->np2, a.flags,
+                                                          reinterpret_cast<PeerEpilogue*>(a.peer_epi), a.wait_epoch,
+                                                          a.signal_epoch);
     note_launch();
     return cudaGetLastError();
 }

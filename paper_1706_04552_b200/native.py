@@ -28,6 +28,7 @@ FLAG_FETCH_LINE, FLAG_FETCH64, FLAG_STENCIL_V1, FLAG_STAGES2 = 512, 1024, 2048, 
 FLAG_PROBE_NOSTORE, FLAG_PROBE_NOLOAD, FLAG_PROBE_NOCOMPUTE = 8192, 16384, 32768
 FLAG_DIGIT_ORDER, FLAG_STORE_CS, FLAG_BAND_MAJOR = 65536, 131072, 262144
 FLAG_PREFETCH_AHEAD, FLAG_FETCH_MIXED, FLAG_FETCH_HALF, FLAG_FETCH256 = 524288, 1048576, 2097152, 4194304
+FLAG_TWO_STEPS = 8388608
 
 
 class GmCfg(ctypes.Structure):

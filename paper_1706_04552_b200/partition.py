@@ -456,11 +456,11 @@ class PartitionedCA:
             raise ValueError("halo must be 'collective' (all_gather) or 'peer' (peer memory)")
         self.step_fn = step_fn or self._gpu_step
         self.lo, self.hi = plan.ranges[rank]
-        # fused=True (peer halo, one step per exchange): the exchange runs inside the step
-        # kernel (gm_run_part_peer) -- one launch per step, no put/wait kernels
+        # fused=True (peer halo): the exchange runs inside the step kernel (gm_run_part_peer)
+        # -- one launch per step (per two steps with plan.depth == 2), no put/wait kernels
         self.fused = bool(fused)
-        if self.fused and (self.peer is None or plan.depth != 1 or step_fn is not None):
-            raise ValueError("fused exchange needs halo='peer', plan.depth == 1 and the GPU step")
+        if self.fused and (self.peer is None or step_fn is not None):
+            raise ValueError("fused exchange needs halo='peer' and the GPU step")
         self._epoch = 0
 
     def _gpu_step(self, dst: torch.Tensor, src: torch.Tensor, lo: int, hi: int) -> None:
@@ -490,8 +490,9 @@ class PartitionedCA:
             from . import native
 
             self._epoch += 1
+            fl = native.FLAG_TWO_STEPS if self.plan.depth == 2 else native.FLAG_DST_FROM_SRC
             native.call("gm_run_part_peer", self.b.data_ptr(), self.a.data_ptr(), self.plan.n, self.b.element_size(),
-                        self.kind, int(np.int32(self.param)), native.FLAG_DST_FROM_SRC, self.plan.level, self.lo,
+                        self.kind, int(np.int32(self.param)), fl, self.plan.level, self.lo,
                         self.hi, self.peer.epilogue(self._dst).data_ptr(), self._epoch - 1, self._epoch,
                         dev.stream_handle())
             self.finish()

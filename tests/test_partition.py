@@ -217,7 +217,8 @@ def _peer_worker(rank, world, port, n, level, kind, steps, out, depth=1, fused=F
 @pytest.mark.gpu
 @pytest.mark.parametrize("world,depth,kind,fused", [(2, 1, 1, False), (2, 1, 2, False), (2, 2, 1, False),
                                                     (2, 2, 2, False), (4, 1, 2, False), (4, 2, 2, False),
-                                                    (2, 1, 1, True), (2, 1, 2, True), (4, 1, 2, True)])
+                                                    (2, 1, 1, True), (2, 1, 2, True), (4, 1, 2, True),
+                                                    (2, 2, 2, True), (4, 2, 1, True)])
 def test_peer_memory_halo_processes(gpu, world, depth, kind, fused):
     """PartitionedCA(halo="peer"): no collective per step, halo cells written into the
     peers' buffers over CUDA IPC + release/acquire step flags == the oracle's steps
