@@ -10,8 +10,8 @@
 // horizontally neighbouring tiles (shared DRAM pages: 118 -> 104 us at n=2^16
 // against the lambda digit order, GM_FLAG_DIGIT_ORDER, which hands each warp a
 // contiguous run of units instead).  This kernel is the CONST write pass; the
-// neighbour sums of grids at least one tile wide run in stencil2.cu, and this
-// file's stencil path serves narrower grids and the coverage counters.
+// neighbour sums run in stencil2.cu, and this file's stencil path serves only
+// GM_FLAG_OMEGA_ORDER launches (b = wy*W + wx order); KIND_COUNT is the coverage audit.
 //
 // DRAM-traffic rules (measured with scripts/probe_partial.cu: a partial
 // 32-byte-sector write costs a full-sector DRAM read-modify-write):
