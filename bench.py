@@ -2,8 +2,10 @@
 """Headline benchmark: lambda(omega) gasket passes on B200 (BASELINE.json).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload write16|write16-i32|write17|stencil16|stencil17|stencil17-nsum4|part18]
-                    [--no-sweep] [--no-e2e] [--no-cpu]
+                    [--workload write16|write16-i32|write17|stencil16|stencil16-i32-nsum4|
+                                stencil17|stencil17-nsum4|part15|part18]
+                    [--halo collective|peer|peer-fused] [--temporal 1|2]   (part* workloads)
+                    [--no-sweep] [--no-e2e] [--no-cpu] [--nsweep]
 
 Default workload (BASELINE configs[1]): the n = 2^16 write pass ("write a
 constant value on all the elements") on int8 cells, lambda
@@ -15,8 +17,10 @@ its own independent grid: weak scaling, no collective on the data path).
 
 Extras on the same JSON line: the rho sweep of lambda vs bounding box at the
 headline size (paper-literal SUBBOX/TABLE/UNROLL and tuned lambda, paper-
-literal and block-early-exit BB) with the best-vs-best speedup; `roofline`
-(sector-minimum bytes / event time vs the measured HBM peak); `cpu_baseline`
+literal and block-early-exit BB) with the best-vs-best speedup and the useful-
+thread fractions; `roofline` (sector-minimum bytes / event time vs the measured
+HBM peak, plus `hw_model`: the bytes this memory system must move); for the
+stencils `multi_step` (the CA driver, one and two fused steps per launch); `cpu_baseline`
 (the C/OpenMP port of the reference numba kernels, all host threads, bounded
 sample); `e2e` (the reference-facing call with host numpy buffers); `clocks`
 (NVML sampled during the timed region); `gpu_launches`.
