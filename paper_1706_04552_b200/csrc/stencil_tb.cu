@@ -48,6 +48,18 @@ constexpr int ROWB = 128;
 constexpr int PITCH = ROWB + 48;  // 16 B halo | 128 B row | 16 B halo | 16 B pad
 constexpr int CHUNKS = 10;
 
+// Skewed row layout of the staged (S) and state-t+1 (I) buffers: the row of tile row r
+// starts at idx * PITCH + 16 * ((r + 4) >> 2) (idx = buffer row, r = idx - SHIFT >= -4):
+// 16 more bytes per 4-row quad (monotone, so rows never overlap).  The vertical-run
+// work items of a warp come from several quads; with a plain 176-byte pitch a quad
+// step moves the bank by 16, so items two quads apart with the same word collided.
+// The skew makes the quad step 20 banks: 8 consecutive quads land in 8 bank groups.
+constexpr int SKEW_BYTES = 16 * 36;  // >= 16 * (((TT + 1) + 4) >> 2) for TT <= 128
+template <int SHIFT>
+__device__ __host__ __forceinline__ int row_off(int idx) {
+    return idx * PITCH + 16 * ((idx - SHIFT + 4) >> 2);
+}
+
 template <int C>
 struct TB {
     static constexpr int V = 4 / C;
@@ -56,8 +68,8 @@ struct TB {
     static constexpr int CC = 16 / C;          // cells per chunk
     static constexpr int SROWS = TT + 4;       // state-t rows -2 .. TT+1
     static constexpr int IROWS = TT + 2;       // state-t+1 rows -1 .. TT
-    static constexpr int SBUF = SROWS * PITCH;
-    static constexpr int IBUF = IROWS * PITCH;
+    static constexpr int SBUF = SROWS * PITCH + SKEW_BYTES;
+    static constexpr int IBUF = IROWS * PITCH + SKEW_BYTES;
     static constexpr int NTOUCH = 9 * SC;
     // 4/3 threads per touched sector: the store pass uses the first NTOUCH, the work
     // lists of phases 1-2 all of them.  With 16-bit work lists and no offset table the
@@ -76,13 +88,13 @@ __device__ __forceinline__ uint32_t word_mask(int x, int y, int n) {
 }
 
 // word k (0..39, 4 halo words each side) of staged rows ji-1+0..2 -> one result word
-template <int C, bool EIGHT>
-__device__ __forceinline__ uint32_t word_sum(const uint8_t* rows, int k, uint32_t pv, uint32_t& centre) {
-    // rows points at row 0 of the three (k = word index relative to `rows`)
+template <int C, bool EIGHT, int SHIFT>
+__device__ __forceinline__ uint32_t word_sum(const uint8_t* buf, int row0, int k, uint32_t pv, uint32_t& centre) {
+    // rows row0 .. row0+2 of `buf` (skewed layout), word k
     uint32_t w[3][3];
 #pragma unroll
     for (int rr = 0; rr < 3; ++rr) {
-        const uint32_t* row = reinterpret_cast<const uint32_t*>(rows + rr * PITCH);
+        const uint32_t* row = reinterpret_cast<const uint32_t*>(buf + row_off<SHIFT>(row0 + rr));
         w[rr][0] = row[k - 1];
         w[rr][1] = row[k];
         w[rr][2] = row[k + 1];
@@ -93,18 +105,18 @@ __device__ __forceinline__ uint32_t word_sum(const uint8_t* rows, int k, uint32_
     return o[0];
 }
 
-// A vertical run of RUN words (word k of RUN consecutive rows) from RUN+2 staged rows
-// starting at `rows` (the row above the first output): row loads and lane splits
+// A vertical run of RUN words (word k of RUN consecutive rows) from RUN+2 rows of `buf`
+// starting at buffer row row0 (the row above the first output): row loads and lane splits
 // are shared between the outputs.  Word k of a tile row holds gasket cells for a
 // whole aligned run of V rows (its first cell k*V only constrains bits >= log2 V of
 // the row), and the cell pattern of run row j is member_mask(j).
-template <int C, bool EIGHT, int RUN>
-__device__ __forceinline__ void vstrip(const uint8_t* rows, uint32_t pv, uint32_t (&out)[RUN],
+template <int C, bool EIGHT, int RUN, int SHIFT>
+__device__ __forceinline__ void vstrip(const uint8_t* buf, int row0, int k, uint32_t pv, uint32_t (&out)[RUN],
                                        uint32_t (&centre)[RUN]) {
     uint32_t w[RUN + 2][3];
 #pragma unroll
     for (int i = 0; i < RUN + 2; ++i) {
-        const uint32_t* row = reinterpret_cast<const uint32_t*>(rows + i * PITCH);
+        const uint32_t* row = reinterpret_cast<const uint32_t*>(buf + row_off<SHIFT>(row0 + i)) + k;
         w[i][0] = row[-1];
         w[i][1] = row[0];
         w[i][2] = row[1];
@@ -132,7 +144,8 @@ __global__ void __launch_bounds__(TB<C>::THREADS)
     constexpr bool EIGHT = KIND == KIND_NSUM8;
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* ibuf = smem + NST * S::SBUF;          // state t+1, rows -1..TT
-    // work lists, all shared-memory byte offsets (row = o / PITCH, chunk / word from o % PITCH)
+    // work lists: staged chunks as j * 16 + q (buffer row j, chunk q); phase-1/2 items as
+    // row * 64 + k (buffer row, word k) -- offsets follow from the skewed row_off()
     uint16_t* slist = reinterpret_cast<uint16_t*>(ibuf + S::IBUF);
     uint16_t* p1list = slist + ns;                 // runs of inner gasket words, ring gasket words, copies
     uint16_t* p2list = p1list + np1;               // runs of the tile's gasket words
@@ -182,14 +195,15 @@ __global__ void __launch_bounds__(TB<C>::THREADS)
         const bool interior = y0 >= 2 && y0 + S::TT + 2 <= n && x0 > 0 && x0 + S::TT < n;
         for (int i = threadIdx.x; i < ns; i += S::THREADS) {
             const uint32_t c = slist[i];
-            const int j = (int)(c / PITCH), q = (int)(c % PITCH) / 16;
+            const int j = (int)(c >> 4), q = (int)(c & 15u);
+            const uint32_t so = sb + (uint32_t)(row_off<2>(j) + q * 16);
             if (interior) {
-                cp_async16(sb + c, base + (int64_t)j * rowstride + q * 16, 16, fetch_line);
+                cp_async16(so, base + (int64_t)j * rowstride + q * 16, 16, fetch_line);
             } else {
                 const int64_t y = y0 + j - 2;
                 const int64_t xb = x0 * C + (q - 1) * 16;
                 const bool in = y >= 0 && y < n && xb >= 0 && xb < rowstride;
-                cp_async16(sb + c, in ? src + y * rowstride + xb : src, in ? 16 : 0, fetch_line);
+                cp_async16(so, in ? src + y * rowstride + xb : src, in ? 16 : 0, fetch_line);
             }
         }
     };
@@ -209,44 +223,46 @@ __global__ void __launch_bounds__(TB<C>::THREADS)
         v_cur = v_next;
         const uint8_t* sbuf = smem + (idx % NST) * S::SBUF;
 
-        // ---- phase 1: state t+1 on rows -1..TT.  Entries: byte offset o of (I row ji, word k)
-        //      (| ji << 16 | k << 24 for single words); I row ji = S row ji + 1 = row ji - 1.
-        //      [0, ni1): runs of V tile rows of a word holding gasket cells, o = first row;
+        // ---- phase 1: state t+1 on rows -1..TT.  Item = ji * 64 + k: I row ji (tile row ji - 1,
+        //      S rows ji .. ji+2), word k.
+        //      [0, ni1): runs of V tile rows of a word holding gasket cells (first row);
         //      [ni1, ng1): ring words that may hold gasket cells (exact global test);
         //      [ng1, np1): words without gasket cells (state t copied).
         for (int i = probe_nocompute ? np1 : threadIdx.x; i < np1; i += S::THREADS) {
-            const int o = (int)p1list[i];
+            const int c = (int)p1list[i];
+            const int ji = c >> 6, k = c & 63;
             if (i < ni1) {
                 uint32_t sum[S::V], centre[S::V];
-                vstrip<C, EIGHT, S::V>(sbuf + o, pv, sum, centre);
+                vstrip<C, EIGHT, S::V, 2>(sbuf, ji, k, pv, sum, centre);
 #pragma unroll
                 for (int j = 0; j < S::V; ++j) {
                     const uint32_t m = member_mask<C>((uint32_t)j);
-                    *reinterpret_cast<uint32_t*>(ibuf + o + j * PITCH) = (sum[j] & m) | (centre[j] & ~m);
+                    reinterpret_cast<uint32_t*>(ibuf + row_off<1>(ji + j))[k] = (sum[j] & m) | (centre[j] & ~m);
                 }
             } else if (i < ng1) {
                 uint32_t centre;
-                const uint32_t sum = word_sum<C, EIGHT>(sbuf + o, 0, pv, centre);
-                const int ji = o / PITCH, k = (o % PITCH) / 4;
+                const uint32_t sum = word_sum<C, EIGHT, 2>(sbuf, ji, k, pv, centre);
                 const uint32_t m = word_mask<C>((int)x0 + (k - 4) * S::V, (int)y0 + ji - 1, (int)n);
-                *reinterpret_cast<uint32_t*>(ibuf + o) = (sum & m) | (centre & ~m);
+                reinterpret_cast<uint32_t*>(ibuf + row_off<1>(ji))[k] = (sum & m) | (centre & ~m);
             } else {
-                *reinterpret_cast<uint32_t*>(ibuf + o) = *reinterpret_cast<const uint32_t*>(sbuf + o + PITCH);
+                reinterpret_cast<uint32_t*>(ibuf + row_off<1>(ji))[k] =
+                    reinterpret_cast<const uint32_t*>(sbuf + row_off<2>(ji + 1))[k];
             }
         }
         __syncthreads();
 
         // ---- phase 2: state t+2 on the tile's gasket words, in runs of V rows (I rows t-1..t+V),
         //      blended with state t and written over state t in the staging slot (phase 1 is
-        //      done with it; the store pass below reads the slot).  Entry: byte offset of
-        //      (I row t, word k) for the run's first tile row t.
+        //      done with it; the store pass below reads the slot).  Item = t * 64 + k for the
+        //      run's first tile row t (I row t = tile row t - 1; S row t + 2 = tile row t).
         for (int i = probe_nocompute ? np2 : threadIdx.x; i < np2; i += S::THREADS) {
-            const int o = (int)p2list[i];
+            const int c = (int)p2list[i];
+            const int t0 = c >> 6, k = c & 63;
             uint32_t sum[S::V], centre[S::V];
-            vstrip<C, EIGHT, S::V>(ibuf + o, pv, sum, centre);
+            vstrip<C, EIGHT, S::V, 1>(ibuf, t0, k, pv, sum, centre);
 #pragma unroll
             for (int j = 0; j < S::V; ++j) {
-                uint32_t* sp = reinterpret_cast<uint32_t*>(const_cast<uint8_t*>(sbuf) + o + (j + 2) * PITCH);
+                uint32_t* sp = reinterpret_cast<uint32_t*>(const_cast<uint8_t*>(sbuf) + row_off<2>(t0 + j + 2)) + k;
                 const uint32_t m = member_mask<C>((uint32_t)j);
                 *sp = (sum[j] & m) | (*sp & ~m);
             }
@@ -256,7 +272,7 @@ __global__ void __launch_bounds__(TB<C>::THREADS)
         // ---- store: every touched sector whole (its slot row now holds state t+2)
         if (active && !probe_nostore) {
             const int k0 = 4 + 8 * g;
-            const uint32_t* srow = reinterpret_cast<const uint32_t*>(sbuf + (t + 2) * PITCH);
+            const uint32_t* srow = reinterpret_cast<const uint32_t*>(sbuf + row_off<2>(t + 2));
             const uint4 a = *reinterpret_cast<const uint4*>(srow + k0);
             const uint4 b = *reinterpret_cast<const uint4*>(srow + k0 + 4);
             const uint32_t out[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
@@ -316,7 +332,7 @@ void build_lists(bool eight, std::vector<uint32_t>& out, int& ns, int& np1, int&
             bool any = false;
             for (int c = (q - 1) * CC; c < q * CC; ++c) any = any || at(need, c, r);
             const int j = r + 2;
-            if (any) out.push_back((uint32_t)(j * PITCH + q * 16));
+            if (any) out.push_back((uint32_t)(j * 16 + q));
         }
     ns = (int)out.size();
     // phase 1: words of rows -1..TT holding a D1 cell.  The tile's own gasket words come
@@ -335,12 +351,12 @@ void build_lists(bool eight, std::vector<uint32_t>& out, int& ns, int& np1, int&
             }
             const bool in_tile = r >= 0 && r < TT && k >= 4 && k < 4 + TT / V;
             if (in_tile && gsk) {  // exact inside the tile: part of a run
-                if (r % V == 0) inner.push_back((uint32_t)((r + 1) * PITCH + k * 4));
+                if (r % V == 0) inner.push_back((uint32_t)((r + 1) * 64 + k));
                 continue;
             }
             if (!d) continue;
             const int ji = r + 1;
-            const uint32_t e = (uint32_t)(ji * PITCH + k * 4);
+            const uint32_t e = (uint32_t)(ji * 64 + k);
             (gsk ? ring : copy).push_back(e);
         }
     ni1 = (int)inner.size();
@@ -355,7 +371,7 @@ void build_lists(bool eight, std::vector<uint32_t>& out, int& ns, int& np1, int&
     for (int t = 0; t < TT; t += V)
         for (int w = 0; w < TT / V; ++w)
             if (((w * V) & ~t) == 0) {
-                out.push_back((uint32_t)(t * PITCH + (w + 4) * 4));
+                out.push_back((uint32_t)(t * 64 + w + 4));
                 ++np2;
             }
 }
