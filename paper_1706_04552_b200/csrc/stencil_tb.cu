@@ -114,9 +114,16 @@ template <int C, bool EIGHT, int RUN, int SHIFT>
 __device__ __forceinline__ void vstrip(const uint8_t* buf, int row0, int k, uint32_t pv, uint32_t (&out)[RUN],
                                        uint32_t (&centre)[RUN]) {
     uint32_t w[RUN + 2][3];
+    // the run's rows are the last row of one quad, the V rows of the next, and the first
+    // row of the one after (runs start at a tile row that is a multiple of V = 4 for
+    // byte cells): offsets relative to the second row step by PITCH, plus one skew step
+    // before it and one after the run
+    const uint8_t* r1 = buf + row_off<SHIFT>(row0 + 1) + 4 * k;
 #pragma unroll
     for (int i = 0; i < RUN + 2; ++i) {
-        const uint32_t* row = reinterpret_cast<const uint32_t*>(buf + row_off<SHIFT>(row0 + i)) + k;
+        const int skew = (RUN == 4) ? (i == 0 ? -16 : i == RUN + 1 ? 16 : 0) : 0;
+        const uint32_t* row = (RUN == 4) ? reinterpret_cast<const uint32_t*>(r1 + (i - 1) * PITCH + skew)
+                                         : reinterpret_cast<const uint32_t*>(buf + row_off<SHIFT>(row0 + i)) + k;
         w[i][0] = row[-1];
         w[i][1] = row[0];
         w[i][2] = row[1];
@@ -234,10 +241,11 @@ __global__ void __launch_bounds__(TB<C>::THREADS)
             if (i < ni1) {
                 uint32_t sum[S::V], centre[S::V];
                 vstrip<C, EIGHT, S::V, 2>(sbuf, ji, k, pv, sum, centre);
+                uint32_t* dst = reinterpret_cast<uint32_t*>(ibuf + row_off<1>(ji)) + k;  // V rows of one quad
 #pragma unroll
                 for (int j = 0; j < S::V; ++j) {
                     const uint32_t m = member_mask<C>((uint32_t)j);
-                    reinterpret_cast<uint32_t*>(ibuf + row_off<1>(ji + j))[k] = (sum[j] & m) | (centre[j] & ~m);
+                    dst[j * (PITCH / 4)] = (sum[j] & m) | (centre[j] & ~m);
                 }
             } else if (i < ng1) {
                 uint32_t centre;
@@ -260,9 +268,10 @@ __global__ void __launch_bounds__(TB<C>::THREADS)
             const int t0 = c >> 6, k = c & 63;
             uint32_t sum[S::V], centre[S::V];
             vstrip<C, EIGHT, S::V, 1>(ibuf, t0, k, pv, sum, centre);
+            uint32_t* sp0 = reinterpret_cast<uint32_t*>(const_cast<uint8_t*>(sbuf) + row_off<2>(t0 + 2)) + k;
 #pragma unroll
-            for (int j = 0; j < S::V; ++j) {
-                uint32_t* sp = reinterpret_cast<uint32_t*>(const_cast<uint8_t*>(sbuf) + row_off<2>(t0 + j + 2)) + k;
+            for (int j = 0; j < S::V; ++j) {  // tile rows t0 .. t0+V-1: one quad, one skew
+                uint32_t* sp = sp0 + j * (PITCH / 4);
                 const uint32_t m = member_mask<C>((uint32_t)j);
                 *sp = (sum[j] & m) | (*sp & ~m);
             }
