@@ -60,6 +60,9 @@ WORKLOADS = {
                                  "the ranks, NCCL all_gather of the changing halo cells"),
 }
 PART_LEVEL = 5
+# measured floor of each pass's exact DRAM access set moved in address order (the best
+# this memory system does with those accesses; scripts/probe_rmw.cu, profiles/r1_probes.md)
+PATTERN_CEILING_US = {"write16": 81.9, "stencil17": 344.0}
 FALLBACK_HBM_GBS = 6650.0
 
 
@@ -573,6 +576,11 @@ def run_ours(args) -> None:
         "gpu_launches": int(launches),
         "timed_region_wall_s": t_wall,
     }
+    if workload in PATTERN_CEILING_US and part is None:
+        fl = PATTERN_CEILING_US[workload]
+        line["roofline"]["pattern_ceiling"] = {
+            "us": fl, "frac": fl * 1e-3 / statistics.fmean(ms),
+            "note": "the same DRAM accesses in address order (scripts/probe_rmw.cu); frac = ceiling / measured"}
     if part is not None:
         line["config"]["halo_bytes_per_step"] = part.halo_bytes_per_step if world > 1 else 0
         line["config"]["halo"] = (args.halo if world > 1 else "none (one rank)")
