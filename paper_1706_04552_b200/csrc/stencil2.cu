@@ -202,10 +202,20 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
     // (a CTA without tiles still takes part in the fused exchange's completion count)
     const uint32_t count = first >= last ? 0u : (last - first + step - 1) / step;
 
-    auto stage = [&](uint32_t idx) {  // stage this CTA's tile #idx into ring slot idx % NST
+    // order-table entry of this CTA's tile #idx (loaded one tile before its staging, so
+    // the staging right after the barrier does not wait on a global load)
+    auto order_v = [&](uint32_t idx) -> uint32_t {
+        return (order != nullptr && idx < count) ? __ldg(order + first + idx * step) : 0u;
+    };
+    auto stage = [&](uint32_t idx, uint32_t v) {  // stage this CTA's tile #idx into ring slot idx % NST
         if (idx >= count || probe_noload) return;
         uint32_t bx, by;
-        tile_xy(first + idx * step, bx, by);
+        if (order == nullptr) {
+            lambda_digit_order(first + idx * step, tab, bx, by);
+        } else {
+            bx = v & 0xffffu;
+            by = v >> 16;
+        }
         const int64_t x0 = (int64_t)bx * S::TT, y0 = (int64_t)by * S::TT;
         const uint32_t sb = smem0 + (idx % NST) * S::BUF;
         const uint8_t* base = src + (y0 - 1) * rowstride + x0 * C - 16;  // staged (row 0, chunk 0)
@@ -237,14 +247,17 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
 
 #pragma unroll
     for (int s = 0; s < NST - 1; ++s) {
-        stage((uint32_t)s);
+        stage((uint32_t)s, order_v((uint32_t)s));
         cp_async_commit();
     }
+    uint32_t v_stage = order_v(NST - 1);
     for (uint32_t idx = 0; idx < count; ++idx) {
+        const uint32_t v_after = order_v(idx + NST);
         cp_async_wait<NST - 2>();  // this thread's copies of tile idx have landed
         __syncthreads();           // everyone's have; everyone is done with tile idx-1's slot
-        stage(idx + NST - 1);      // refill the slot tile idx-1 used
+        stage(idx + NST - 1, v_stage);  // refill the slot tile idx-1 used
         cp_async_commit();
+        v_stage = v_after;
         if (active) {
             uint32_t bx, by;
             tile_xy(first + idx * step, bx, by);

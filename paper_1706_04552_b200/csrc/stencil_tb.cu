@@ -140,6 +140,49 @@ __device__ __forceinline__ void vstrip(const uint8_t* buf, int row0, int k, uint
     }
 }
 
+// Phase 2's strip: state t+1 of tile rows t0-1 .. t0+RUN around word k.  Phase 1 wrote
+// state t+1 into I only for the words that can hold gasket cells (superset test, the
+// work lists' `gsk`); every other word has no gasket cell, so its state t+1 is its
+// state t, read from the staged S slot instead (same skew for the same tile row, so the
+// S address is the I address + dS).  Rows t0 .. t0+RUN-1 share one membership pattern
+// (t0 is a multiple of V = RUN), so 3 row classes x 3 columns of sources.
+template <int C, bool EIGHT, int RUN>
+__device__ __forceinline__ void vstrip_p2(const uint8_t* ibuf, const uint8_t* sbuf, int t0, int k, uint32_t pv,
+                                          uint32_t (&out)[RUN], uint32_t (&centre)[RUN]) {
+    using S = TB<C>;
+    const uint8_t* i1 = ibuf + row_off<1>(t0 + 1) + 4 * k;  // tile row t0, word k, in I
+    const int dS = (int)(sbuf - ibuf) + PITCH;               // -> the same word in S
+    const uint32_t rm[3] = {(uint32_t)(t0 - 1) & (S::TT - 1), (uint32_t)t0, (uint32_t)(t0 + RUN) & (S::TT - 1)};
+    int sel[3][3];
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc) {
+        const uint32_t xm = (uint32_t)((k - 5 + cc) * S::V) & (S::TT - 1);
+#pragma unroll
+        for (int rc = 0; rc < 3; ++rc) sel[rc][cc] = (xm & ~rm[rc]) == 0 ? 0 : dS;
+    }
+    uint32_t w[RUN + 2][3];
+#pragma unroll
+    for (int i = 0; i < RUN + 2; ++i) {
+        const int rc = i == 0 ? 0 : i == RUN + 1 ? 2 : 1;
+        // (RUN == 4: rows t0..t0+3 are one quad; one skew step before it and one after)
+        const int roff = (RUN == 4) ? (i - 1) * PITCH + (i == 0 ? -16 : i == RUN + 1 ? 16 : 0)
+                                    : row_off<1>(t0 + i) - row_off<1>(t0 + 1);
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc)
+            w[i][cc] = *reinterpret_cast<const uint32_t*>(i1 + roff + 4 * (cc - 1) + sel[rc][cc]);
+    }
+#pragma unroll
+    for (int j = 0; j < RUN; ++j) {
+        const uint32_t win[3][3] = {{w[j][0], w[j][1], w[j][2]},
+                                    {w[j + 1][0], w[j + 1][1], w[j + 1][2]},
+                                    {w[j + 2][0], w[j + 2][1], w[j + 2][2]}};
+        uint32_t o[1];
+        sector_sums<C, EIGHT, 1>(win, pv, o);
+        out[j] = o[0];
+        centre[j] = w[j + 1][1];
+    }
+}
+
 template <int C, int KIND, int NST>
 __global__ void __launch_bounds__(TB<C>::THREADS)
     stencil_tb2(uint8_t* __restrict__ grid, const uint8_t* __restrict__ src, int64_t n, uint32_t ntiles,
@@ -216,25 +259,28 @@ __global__ void __launch_bounds__(TB<C>::THREADS)
     };
 
     static_assert(NST == 2, "the tile-order registers below assume a 2-deep ring");
-    uint32_t v_cur = tile_v(0);
+    // order entries are loaded one tile ahead of their use: the staging of tile idx+1
+    // right after the barrier would otherwise wait on a global load every tile
+    uint32_t v_cur = tile_v(0), v_next = tile_v(1);
     stage(0, v_cur);
     cp_async_commit();
     for (uint32_t idx = 0; idx < count; ++idx) {
+        const uint32_t v_after = tile_v(idx + 2);
         cp_async_wait<NST - 2>();
         __syncthreads();  // state t of tile idx staged; tile idx-1 fully stored (I and its S slot free)
-        const uint32_t v_next = tile_v(idx + 1);
         stage(idx + 1, v_next);
         cp_async_commit();
         int64_t x0, y0;
         tile_xy(v_cur, x0, y0);
         v_cur = v_next;
+        v_next = v_after;
         const uint8_t* sbuf = smem + (idx % NST) * S::SBUF;
 
         // ---- phase 1: state t+1 on rows -1..TT.  Item = ji * 64 + k: I row ji (tile row ji - 1,
         //      S rows ji .. ji+2), word k.
         //      [0, ni1): runs of V tile rows of a word holding gasket cells (first row);
-        //      [ni1, ng1): ring words that may hold gasket cells (exact global test);
-        //      [ng1, np1): words without gasket cells (state t copied).
+        //      [ni1, np1): ring words that may hold gasket cells (exact global test).
+        //      Words that cannot hold gasket cells keep state t: phase 2 reads them from S.
         for (int i = probe_nocompute ? np1 : threadIdx.x; i < np1; i += S::THREADS) {
             const int c = (int)p1list[i];
             const int ji = c >> 6, k = c & 63;
@@ -247,14 +293,11 @@ __global__ void __launch_bounds__(TB<C>::THREADS)
                     const uint32_t m = member_mask<C>((uint32_t)j);
                     dst[j * (PITCH / 4)] = (sum[j] & m) | (centre[j] & ~m);
                 }
-            } else if (i < ng1) {
+            } else {
                 uint32_t centre;
                 const uint32_t sum = word_sum<C, EIGHT, 2>(sbuf, ji, k, pv, centre);
                 const uint32_t m = word_mask<C>((int)x0 + (k - 4) * S::V, (int)y0 + ji - 1, (int)n);
                 reinterpret_cast<uint32_t*>(ibuf + row_off<1>(ji))[k] = (sum & m) | (centre & ~m);
-            } else {
-                reinterpret_cast<uint32_t*>(ibuf + row_off<1>(ji))[k] =
-                    reinterpret_cast<const uint32_t*>(sbuf + row_off<2>(ji + 1))[k];
             }
         }
         __syncthreads();
@@ -267,7 +310,7 @@ __global__ void __launch_bounds__(TB<C>::THREADS)
             const int c = (int)p2list[i];
             const int t0 = c >> 6, k = c & 63;
             uint32_t sum[S::V], centre[S::V];
-            vstrip<C, EIGHT, S::V, 1>(ibuf, t0, k, pv, sum, centre);
+            vstrip_p2<C, EIGHT, S::V>(ibuf, sbuf, t0, k, pv, sum, centre);
             uint32_t* sp0 = reinterpret_cast<uint32_t*>(const_cast<uint8_t*>(sbuf) + row_off<2>(t0 + 2)) + k;
 #pragma unroll
             for (int j = 0; j < S::V; ++j) {  // tile rows t0 .. t0+V-1: one quad, one skew
@@ -370,10 +413,9 @@ void build_lists(bool eight, std::vector<uint32_t>& out, int& ns, int& np1, int&
         }
     ni1 = (int)inner.size();
     ng1 = ni1 + (int)ring.size();
-    np1 = ng1 + (int)copy.size();
+    np1 = ng1;  // (the `copy` words are read from S by phase 2, not copied into I)
     out.insert(out.end(), inner.begin(), inner.end());
     out.insert(out.end(), ring.begin(), ring.end());
-    out.insert(out.end(), copy.begin(), copy.end());
     // phase 2: the tile's gasket words, one entry per aligned run of V rows: the byte
     // offset of (I row t, word k) (I rows t..t+V+1 are tile rows t-1..t+V)
     np2 = 0;
