@@ -336,7 +336,7 @@ def _sweep(r: int, dtype, flusher, budget_s: float = 3.0) -> dict:
 
 
 def _multi_step(r: int, tdt, kind: int, flusher, steps: int = 40) -> dict:
-    """The multi-step CA driver (ca.CARunner): single-step launches vs two fused steps
+    """The multi-step CA driver (ca.CARunner): single-step launches vs 2 or 4 fused steps
     per launch (temporal blocking, stencil_tb.cu), CUDA graphs, L2 flushed once before
     the run.  Not the headline: `value` above is one step = one pass."""
     import torch
@@ -345,7 +345,7 @@ def _multi_step(r: int, tdt, kind: int, flusher, steps: int = 40) -> dict:
 
     n = 1 << r
     out = {"steps": steps, "l2": "flushed once before the run (the state never fits L2)"}
-    for temporal in (1, 2):
+    for temporal in (1, 2, 4):
         g = device.fill_hash(n, tdt, 1, 0)
         run = ca.CARunner(g, kind=kind, param=1, use_graph=True, temporal=temporal)
         run.run(8)  # warm-up + graph capture
@@ -362,6 +362,7 @@ def _multi_step(r: int, tdt, kind: int, flusher, steps: int = 40) -> dict:
         del run, g
         torch.cuda.empty_cache()
     out["speedup_fused"] = out["temporal1"]["ms_per_step"] / out["temporal2"]["ms_per_step"]
+    out["speedup_fused4"] = out["temporal1"]["ms_per_step"] / out["temporal4"]["ms_per_step"]
     # work-equivalent roofline: the §8d bytes of one single step per fused step time (the
     # fused pass moves about one step's bytes per two steps, so this can exceed what the
     # memory system moves; labelled "effective", not the kernel's own roofline)
@@ -369,8 +370,8 @@ def _multi_step(r: int, tdt, kind: int, flusher, steps: int = 40) -> dict:
 
     peak, _ = _peaks()
     c = torch.empty((), dtype=tdt).element_size()
-    out["temporal2"]["effective_frac"] = (R.pass_bytes(r, c, kind) / (out["temporal2"]["ms_per_step"] * 1e-3)
-                                          / 1e9 / peak)
+    for t in ("temporal2", "temporal4"):
+        out[t]["effective_frac"] = R.pass_bytes(r, c, kind) / (out[t]["ms_per_step"] * 1e-3) / 1e9 / peak
     return out
 
 

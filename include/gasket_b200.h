@@ -173,6 +173,10 @@ int gm_set_l2_fetch_granularity(int32_t bytes);
  * kind = GM_KIND_NSUM4 or GM_KIND_NSUM8; 1-, 2- or 4-byte cells; async on `stream`. */
 int gm_ca_step2(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
                 int32_t flags, void* stream);
+/* gm_ca_step2 with `steps` = 2 or 4 fused CA steps per launch (temporal blocking over a
+ * 4-cell-deep dependency cone for 4): grid <- step^steps(src), same preconditions. */
+int gm_ca_steps(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
+                int32_t steps, int32_t flags, void* stream);
 /* Peer-memory halo exchange of the partitioned CA (peer.cu).
  * gm_dev_alloc/free: plain cudaMalloc'd buffers (allocation bases, so they can be
  * exported); gm_ipc_get_handle writes a 64-byte cudaIpcMemHandle_t; gm_ipc_open_handle

@@ -10,10 +10,10 @@ so every step may write whole sectors blended from its source
 (A->B, B->A) is captured once into a CUDA graph and replayed, which removes
 the per-step Python/ctypes launch cost for long runs.
 
-``temporal=2`` (temporal blocking) advances pairs of steps
-with one fused launch (``gm_ca_step2``, stencil_tb.cu): state t is read once,
-state t+1 lives only in shared memory, state t+2 is written once -- half the
-DRAM traffic per step.  Results are bit-identical to single steps.
+``temporal=T`` (temporal blocking) advances T = 2 or 4 steps
+with one fused launch (``gm_ca_steps``, stencil_tb.cu): state t is read once, the
+intermediate states live only in shared memory, state t+T is written once -- 1/T
+of the DRAM traffic per step.  Results are bit-identical to single steps.
 """
 
 from __future__ import annotations
@@ -27,7 +27,7 @@ from .geometry import FractalSpec, IntraStrategy
 
 class CARunner:
     def __init__(self, grid: torch.Tensor, kind: int = backends.KERNEL_NEIGHBOR_SUM8, param: int = 1,
-                 rho: int = 64, use_graph: bool = True, temporal: int = 2) -> None:
+                 rho: int = 64, use_graph: bool = True, temporal: int = 4) -> None:
         device.require_cuda()
         if not device.is_device(grid):
             raise TypeError("CARunner works on a CUDA grid tensor")
@@ -40,8 +40,8 @@ class CARunner:
         self.bufs = (grid, grid.clone())  # fixed physical buffers (the graph captures their addresses)
         self.cur = 0                      # which buffer holds the current state
         self.use_graph = use_graph
-        if temporal not in (1, 2):
-            raise ValueError("temporal must be 1 (one step per launch) or 2 (two fused steps)")
+        if temporal not in (1, 2, 4):
+            raise ValueError("temporal must be 1 (one step per launch), 2 or 4 (fused steps per launch)")
         # the fused kernel needs whole 128-byte tiles of 1-, 2- or 4-byte cells
         self.temporal = temporal if (grid.element_size() in (1, 2, 4) and n * grid.element_size() >= 128) else 1
         self._graph = None
@@ -51,10 +51,10 @@ class CARunner:
         backends.run_block_space(dst, src, self.spec.rho, self.spec.r_b, IntraStrategy.TUNED, kind=self.kind,
                                  param=self.param, flags=native.FLAG_DST_FROM_SRC)
 
-    def _pair(self, dst: torch.Tensor, src: torch.Tensor) -> None:
-        """Two steps src -> dst (the intermediate state never leaves the SM)."""
-        native.call("gm_ca_step2", dst.data_ptr(), src.data_ptr(), self.spec.n, dst.element_size(), self.kind,
-                    int(np.int32(self.param)), 0, device.stream_handle())
+    def _fused(self, dst: torch.Tensor, src: torch.Tensor, steps: int) -> None:
+        """`steps` (2 or 4) steps src -> dst (the intermediate states never leave the SM)."""
+        native.call("gm_ca_steps", dst.data_ptr(), src.data_ptr(), self.spec.n, dst.element_size(), self.kind,
+                    int(np.int32(self.param)), steps, 0, device.stream_handle())
 
     def _single(self) -> None:
         src, dst = self.bufs[self.cur], self.bufs[1 - self.cur]
@@ -62,20 +62,15 @@ class CARunner:
         self.cur ^= 1
         self.steps_done += 1
 
-    def _two(self) -> None:
-        """Advance two steps from the current buffer (graph-free path)."""
+    def _advance(self, steps: int) -> None:
+        """Advance `steps` (2 or 4) fused steps from the current buffer (graph-free path)."""
         src, dst = self.bufs[self.cur], self.bufs[1 - self.cur]
-        if self.temporal == 2:
-            self._pair(dst, src)
-            self.cur ^= 1
-        else:
-            self._single()
-            self._single()
-            return
-        self.steps_done += 2
+        self._fused(dst, src, steps)
+        self.cur ^= 1
+        self.steps_done += steps
 
     def _capture(self) -> None:
-        if self.temporal == 2:
+        if self.temporal > 1:
             return self._capture_fused()
         a, b = self.bufs
         # warm up outside the capture (module load, tensor-map caches); advances two steps
@@ -93,19 +88,19 @@ class CARunner:
         self._graph = g
 
     def _capture_fused(self) -> None:
-        # fused pairs alternate A->B, B->A: one graph = 4 steps (two launches)
-        a, b = self.bufs
+        # fused launches alternate A->B, B->A: one graph = 2T steps (two launches)
+        a, b, T = self.bufs[0], self.bufs[1], self.temporal
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
-            self._pair(b, a)
-            self._pair(a, b)
+            self._fused(b, a, T)
+            self._fused(a, b, T)
         torch.cuda.current_stream().wait_stream(s)
-        self.steps_done += 4
+        self.steps_done += 2 * T
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            self._pair(b, a)
-            self._pair(a, b)
+            self._fused(b, a, T)
+            self._fused(a, b, T)
         self._graph = g
 
     @property
@@ -117,7 +112,7 @@ class CARunner:
         if steps < 0:
             raise ValueError("steps must be >= 0")
         left = steps
-        per_graph = 4 if self.temporal == 2 else 2  # steps one graph replay advances
+        per_graph = 2 * self.temporal  # steps one graph replay advances (two launches)
         if self.use_graph and left >= per_graph:
             if self.cur == 1:  # graphs start from buffer 0
                 self._single()
@@ -129,9 +124,10 @@ class CARunner:
                 self._graph.replay()
                 self.steps_done += per_graph
                 left -= per_graph
-        while left >= 2 and self.temporal == 2:
-            self._two()
-            left -= 2
+        for k in (4, 2):  # the remainder: fused launches no longer than `temporal`, then singles
+            while self.temporal >= k and left >= k:
+                self._advance(k)
+                left -= k
         while left > 0:
             self._single()
             left -= 1
@@ -139,7 +135,7 @@ class CARunner:
 
 
 def run_ca(grid: torch.Tensor, steps: int, kind: int = backends.KERNEL_NEIGHBOR_SUM8, param: int = 1,
-           use_graph: bool = True, temporal: int = 2) -> torch.Tensor:
+           use_graph: bool = True, temporal: int = 4) -> torch.Tensor:
     """`steps` CA steps starting from `grid`; the final state is copied back into `grid`."""
     runner = CARunner(grid, kind, param, use_graph=use_graph, temporal=temporal)
     out = runner.run(steps)

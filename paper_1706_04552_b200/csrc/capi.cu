@@ -140,8 +140,12 @@ void ensure_dynamic_smem(const void* kern, size_t smem) {
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lock(mu);
-    if (done.insert(std::make_tuple(kern, dev, smem)).second)
+    if (done.insert(std::make_tuple(kern, dev, smem)).second) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        // the largest shared-memory carveout: the tiled kernels size their CTAs so that
+        // several share an SM's shared memory (the driver's default choice may not)
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+    }
 }
 
 int order_level(const LaunchArgs& a, int r_t) {
@@ -333,6 +337,12 @@ int gm_set_l2_fetch_granularity(int32_t bytes) {
 
 int gm_ca_step2(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
                 int32_t flags, void* stream) {
+    return gm_ca_steps(grid, src, n, cell_bytes, kind, param, 2, flags, stream);
+}
+
+int gm_ca_steps(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
+                int32_t steps, int32_t flags, void* stream) {
+    if (steps != 2 && steps != 4) return fail(GM_EINVAL, "gm_ca_steps: steps must be 2 or 4");
     gm_cfg_t c{};
     c.n = n;
     c.rho = 1;
@@ -343,15 +353,15 @@ int gm_ca_step2(void* grid, const void* src, int64_t n, int32_t cell_bytes, int3
     c.param = param;
     c.flags = flags;
     if (int rc = check_common(n, cell_bytes, 1, kind)) return rc;
-    if (kind != GM_KIND_NSUM4 && kind != GM_KIND_NSUM8) return fail(GM_EINVAL, "gm_ca_step2: kind must be NSUM4 or NSUM8");
-    if (!grid || !src || src == grid) return fail(GM_EINVAL, "gm_ca_step2 needs distinct grid and src buffers");
+    if (kind != GM_KIND_NSUM4 && kind != GM_KIND_NSUM8) return fail(GM_EINVAL, "gm_ca_steps: kind must be NSUM4 or NSUM8");
+    if (!grid || !src || src == grid) return fail(GM_EINVAL, "gm_ca_steps needs distinct grid and src buffers");
     gm::LaunchArgs a = make_args(&c, grid, src, nullptr, nullptr, 0, stream);
-    const cudaError_t e = gm::launch_stencil_tb2(a);
+    const cudaError_t e = gm::launch_stencil_tb(a, steps);
     if (e == cudaErrorNotSupported) {
         cudaGetLastError();
-        return fail(GM_EINVAL, "gm_ca_step2: needs 1-, 2- or 4-byte cells and n >= one 128-byte tile (<= 2^15 tiles per edge)");
+        return fail(GM_EINVAL, "gm_ca_steps: needs 1-, 2- or 4-byte cells and n >= one 128-byte tile (<= 2^15 tiles per edge)");
     }
-    return cuda_rc(e, "two-step CA launch");
+    return cuda_rc(e, "fused multi-step CA launch");
 }
 
 int gm_dev_alloc(int64_t bytes, void** out) {

@@ -66,6 +66,7 @@ cudaError_t launch_host_rows(const LaunchArgs& a);
 cudaError_t launch_stencil_tma(const LaunchArgs& a);
 cudaError_t launch_stencil_v2(const LaunchArgs& a);
 cudaError_t launch_stencil_tb2(const LaunchArgs& a);
+cudaError_t launch_stencil_tb(const LaunchArgs& a, int steps);  // steps = 2 or 4
 // member tiles of a level-q gasket, row-major inside each level-L sub-gasket (stencil2.cu)
 const uint32_t* rowmajor_table(int q, int L);
 void rowmajor_order_host(int q, int L, std::vector<uint32_t>& v);

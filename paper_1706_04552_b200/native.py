@@ -73,6 +73,7 @@ _SIGS = {
     "gm_scatter_cells": [_vp, _i32, _vp, _i64, _vp, _vp],
     "gm_tile_order": [_i32, _i32, _vp, _i64],
     "gm_ca_step2": [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _vp],
+    "gm_ca_steps": [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _vp],
     "gm_run_part2": [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, ctypes.c_uint32, ctypes.c_uint32, _vp],
     "gm_run_part_peer": [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, ctypes.c_uint32, ctypes.c_uint32, _vp, _u64,
                          _u64, _vp],
@@ -102,7 +103,10 @@ def lib() -> ctypes.CDLL:
                 f"{LIB_PATH} is missing: build the sm_100a library first "
                 "(python -m paper_1706_04552_b200._build); there is no CPU fallback")
         L = ctypes.CDLL(str(LIB_PATH))
+        ab_build = bool(os.environ.get("GASKET_B200_LIB"))
         for name, args in _SIGS.items():
+            if ab_build and not hasattr(L, name):
+                continue  # an older build under A/B comparison: entry points it predates stay unbound
             fn = getattr(L, name)
             fn.argtypes = args
             fn.restype = ctypes.c_int

@@ -133,10 +133,48 @@ def ca_pairs(r=17):
             m, mn = timeit(fn, flush, k=10)
             print(f"ca r={r} nsum{4 * kind} {name:20s} mean {m * 1e3:8.1f} us  min {mn * 1e3:8.1f} us  "
                   f"per step {m * 1e3 / 2:8.1f} us", flush=True)
+        for name, fl in (("fused quad", 0), ("fused quad (again)", 0),
+                         ("quad probe no compute", native.FLAG_PROBE_NOCOMPUTE),
+                         ("quad probe no memory", native.FLAG_PROBE_NOLOAD | native.FLAG_PROBE_NOSTORE)):
+            fn = lambda: native.call("gm_ca_steps", dst.data_ptr(), src.data_ptr(), n, 1, kind, 1, 4, fl,  # noqa: E731
+                                     device.stream_handle())
+            m, mn = timeit(fn, flush, k=10)
+            print(f"ca r={r} nsum{4 * kind} {name:20s} mean {m * 1e3:8.1f} us  min {mn * 1e3:8.1f} us  "
+                  f"per step {m * 1e3 / 4:8.1f} us", flush=True)
         T = IntraStrategy.TUNED
         m, mn = timeit(lambda: backends.run_block_space(dst, src, 64, r - 6, T, kind=kind, param=1,
                                                         flags=native.FLAG_DST_FROM_SRC), flush, k=10)
         print(f"ca r={r} nsum{4 * kind} {'single step':20s} mean {m * 1e3:8.1f} us  min {mn * 1e3:8.1f} us", flush=True)
+
+
+def ca_pair_ab(r=17, reps=int(__import__("os").environ.get("CAPAIR_REPS", "4"))):
+    """Just the fused pair (gm_ca_step2, present in every build) with the SM clock read
+    after each timing: for A/B runs of stencil_tb.cu builds."""
+    import pynvml
+
+    pynvml.nvmlInit()
+    h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+    n = 1 << r
+    flush = device.L2Flusher()
+    src = device.fill_hash(n, torch.int8, 1, 0)
+    dst = src.clone()
+    import os
+
+    probes = (("", 0), (" no compute", native.FLAG_PROBE_NOCOMPUTE), (" no memory", native.FLAG_PROBE_NOLOAD |
+              native.FLAG_PROBE_NOSTORE)) if os.environ.get("CAPAIR_PROBES") else (("", 0),)
+    for _ in range(reps):
+        for kind in (2, 1):
+            for label, fl in probes:
+                if os.environ.get("CAPAIR_STEPS", "2") == "2":
+                    fn = lambda: native.call("gm_ca_step2", dst.data_ptr(), src.data_ptr(), n, 1, kind, 1,  # noqa: E731
+                                             fl, device.stream_handle())
+                else:
+                    fn = lambda: native.call("gm_ca_steps", dst.data_ptr(), src.data_ptr(), n, 1, kind, 1,  # noqa: E731
+                                             int(os.environ["CAPAIR_STEPS"]), fl, device.stream_handle())
+                m, mn = timeit(fn, flush, k=20)
+                mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                print(f"ca r={r} nsum{4 * kind} fused pair{label:12s} mean {m * 1e3:8.1f} us  min {mn * 1e3:8.1f} us  "
+                      f"sm {mhz} MHz", flush=True)
 
 
 if __name__ == "__main__":
@@ -144,5 +182,7 @@ if __name__ == "__main__":
         offsets()
     elif sys.argv[1:] == ["ca"]:
         ca_pairs()
+    elif sys.argv[1:] == ["capair"]:
+        ca_pair_ab()
     else:
         main()

@@ -368,20 +368,25 @@ def _oracle_steps(oracle, init, kind, param, steps):
 
 
 @pytest.mark.parametrize("kind", [1, 2])
-@pytest.mark.parametrize("temporal", [1, 2])
+@pytest.mark.parametrize("temporal", [1, 2, 4])
 def test_ca_runner_matches_oracle_steps(gpu, oracle, kind, temporal):
     from paper_1706_04552_b200 import ca
 
     for dtype, n in ((np.int8, 512), (np.int8, 128), (np.int16, 256), (np.int32, 64), (np.int32, 32)):
-        steps = 7
         init = oracle.fill_hash(n, dtype, 13, 0)
-        want = _oracle_steps(oracle, init, kind, 3, steps)
+        want7 = _oracle_steps(oracle, init, kind, 3, 7)
+        want20 = _oracle_steps(oracle, want7, kind, 3, 13)
         for use_graph in (False, True):
             g = torch.from_numpy(init.copy()).cuda()
             runner = ca.CARunner(g, kind=kind, param=3, use_graph=use_graph, temporal=temporal)
             out = runner.run(3)
             out = runner.run(4)
-            assert runner.steps_done == steps
+            assert runner.steps_done == 7
+            assert np.array_equal(out.cpu().numpy(), want7), (np.dtype(dtype).name, n, use_graph)
+            # a longer run: graph replays of 2 * temporal steps plus a remainder
+            out = runner.run(13)
+            assert runner.steps_done == 20
+            want = want20
             assert np.array_equal(out.cpu().numpy(), want), (np.dtype(dtype).name, n, use_graph)
         g = torch.from_numpy(init.copy()).cuda()
         ca.run_ca(g, 10, kind=kind, param=3, temporal=temporal)
@@ -389,9 +394,10 @@ def test_ca_runner_matches_oracle_steps(gpu, oracle, kind, temporal):
 
 
 @pytest.mark.parametrize("dtype", [np.int8, np.int16, np.int32])
-def test_fused_two_steps_vs_oracle(gpu, oracle, dtype):
-    """gm_ca_step2 (two CA steps per pass) == two oracle steps, cell by cell, incl.
-    grid-edge tiles and a 2^12 grid; also on a CA state that is 0 off the gasket."""
+@pytest.mark.parametrize("steps", [2, 4])
+def test_fused_steps_vs_oracle(gpu, oracle, dtype, steps):
+    """gm_ca_steps (2 or 4 CA steps per pass) == that many oracle steps, cell by cell,
+    incl. grid-edge tiles and a 2^12 grid; also on a CA state that is 0 off the gasket."""
     from paper_1706_04552_b200 import device, native
 
     n0 = 128 // np.dtype(dtype).itemsize
@@ -400,11 +406,15 @@ def test_fused_two_steps_vs_oracle(gpu, oracle, dtype):
             init = oracle.fill_hash(n, dtype, 41 + mode, mode)
             for kind in (1, 2):
                 for param in (1, -7):
-                    want = _oracle_steps(oracle, init, kind, param, 2)
+                    want = _oracle_steps(oracle, init, kind, param, steps)
                     src = torch.from_numpy(init.copy()).cuda()
                     dst = src.clone()
-                    native.call("gm_ca_step2", dst.data_ptr(), src.data_ptr(), n, src.element_size(), kind, param, 0,
-                                device.stream_handle())
+                    if steps == 2:
+                        native.call("gm_ca_step2", dst.data_ptr(), src.data_ptr(), n, src.element_size(), kind, param,
+                                    0, device.stream_handle())
+                    else:
+                        native.call("gm_ca_steps", dst.data_ptr(), src.data_ptr(), n, src.element_size(), kind, param,
+                                    steps, 0, device.stream_handle())
                     assert np.array_equal(dst.cpu().numpy(), want), (np.dtype(dtype).name, n, mode, kind, param)
                     assert np.array_equal(src.cpu().numpy(), init)
 
@@ -449,24 +459,25 @@ def test_whole_grid_tile_and_unit_grid(gpu, oracle):
 
 
 @pytest.mark.parametrize("dtype", [torch.int8, torch.int16, torch.int32])
-def test_fused_two_steps_equal_single_steps_large(gpu, dtype):
-    """At sizes past the oracle's reach: gm_ca_step2 == two single-step launches, bit for bit."""
+@pytest.mark.parametrize("steps", [2, 4])
+def test_fused_steps_equal_single_steps_large(gpu, dtype, steps):
+    """At sizes past the oracle's reach: gm_ca_steps == that many single-step launches,
+    bit for bit."""
     from paper_1706_04552_b200 import device, native
 
     be, S = gpu.backends, gpu.geometry.IntraStrategy
     n = 1 << 15 if dtype == torch.int8 else 1 << 14
     for kind in (1, 2):
         src = device.fill_hash(n, dtype, 77, 0)
-        mid = src.clone()
-        be.run_block_space(mid, src, 64, (n // 64).bit_length() - 1, S.TUNED, kind=kind, param=5,
-                           flags=native.FLAG_DST_FROM_SRC)
-        two = src.clone()
-        be.run_block_space(two, mid, 64, (n // 64).bit_length() - 1, S.TUNED, kind=kind, param=5,
-                           flags=native.FLAG_DST_FROM_SRC)
+        a, b = src.clone(), src.clone()
+        for _ in range(steps):
+            be.run_block_space(b, a, 64, (n // 64).bit_length() - 1, S.TUNED, kind=kind, param=5,
+                               flags=native.FLAG_DST_FROM_SRC)
+            a, b = b, a
         fused = src.clone()
-        native.call("gm_ca_step2", fused.data_ptr(), src.data_ptr(), n, src.element_size(), kind, 5, 0,
+        native.call("gm_ca_steps", fused.data_ptr(), src.data_ptr(), n, src.element_size(), kind, 5, steps, 0,
                     device.stream_handle())
-        assert torch.equal(fused, two), (dtype, kind)
+        assert torch.equal(fused, a), (dtype, kind)
 
 
 def test_randomised_launches_vs_oracle(gpu, oracle):
