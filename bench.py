@@ -4,7 +4,7 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--workload write16|write16-i32|write17|stencil16|stencil16-i32-nsum4|
                                 stencil17|stencil17-nsum4|part15|part18]
-                    [--halo collective|peer|peer-fused] [--temporal 1|2]   (part* workloads)
+                    [--halo collective|peer|peer-fused] [--temporal 1|2|4]   (part* workloads)
                     [--no-sweep] [--no-e2e] [--no-cpu] [--nsweep]
 
 Default workload (BASELINE configs[1]): the n = 2^16 write pass ("write a
@@ -490,8 +490,9 @@ def run_ours(args) -> None:
 
         from paper_1706_04552_b200 import partition as P
 
-        # --temporal 2: every timed step is one fused pair of CA steps (gm_run_part2) with
-        # one exchange of the depth-2 halo; the line then reports per-CA-step figures
+        # --temporal 2|4: every timed step is one fused launch of that many CA steps
+        # (gm_run_part_steps) with one exchange of the depth-2|4 halo; the line then
+        # reports per-CA-step figures
         plan = P.PartitionPlan(n, PART_LEVEL, world, eight=kind == 2, depth=args.temporal)
         group = dist.group.WORLD if world > 1 else None
         if world > 1 and args.halo in ("peer", "peer-fused"):
@@ -746,7 +747,7 @@ def main() -> None:
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--nsweep", action="store_true", help="BASELINE config 4: n sweep + crossover n0, CSV")
-    ap.add_argument("--temporal", type=int, choices=(1, 2), default=1,
+    ap.add_argument("--temporal", type=int, choices=(1, 2, 4), default=1,
                     help="part* workloads: CA steps fused per launch and per halo exchange")
     ap.add_argument("--halo", choices=("collective", "peer", "peer-fused"), default="collective",
                     help="part* workloads, N>1: NCCL all_gather of the halo cells, peer-memory puts (CUDA IPC), "

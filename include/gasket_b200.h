@@ -79,6 +79,7 @@ extern "C" {
 #define GM_FLAG_FETCH_HALF 2097152    /* stencil v2: stage with the .L2::64B hint (64-byte halves) instead of whole lines */
 #define GM_FLAG_FETCH256 4194304      /* stencil v2: stage interior tiles with the .L2::256B prefetch-size hint */
 #define GM_FLAG_TWO_STEPS 8388608     /* gm_run_part_peer: two fused CA steps per launch (depth-2 halo) */
+#define GM_FLAG_FOUR_STEPS 16777216   /* gm_run_part_peer: four fused CA steps per launch (depth-4 halo) */
 
 #define GM_OK 0
 #define GM_EINVAL 1  /* bad shape / size / tag (the reference's ValueError) */
@@ -209,6 +210,9 @@ int gm_run_part_peer(void* grid, const void* src, int64_t n, int32_t cell_bytes,
  * The caller keeps the halo within two steps current (PartitionPlan(depth=2)). */
 int gm_run_part2(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
                  int32_t flags, int32_t level, uint32_t sg_begin, uint32_t sg_end, void* stream);
+/* gm_run_part2 with `steps` = 2 or 4 fused steps per call (PartitionPlan(depth=steps)). */
+int gm_run_part_steps(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
+                      int32_t steps, int32_t flags, int32_t level, uint32_t sg_begin, uint32_t sg_end, void* stream);
 /* The tuned kernels' tile visiting order (host-side, no GPU needed): the 3^q
  * member tiles of a level-q gasket as bx | by << 16, level-`level` sub-gaskets in
  * lambda digit order, row-major inside each.  out must hold 3^q entries. */

@@ -408,6 +408,12 @@ int gm_peer_halo_wait(const uint64_t* flags, int32_t rank, int32_t world, uint64
 
 int gm_run_part2(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
                  int32_t flags, int32_t level, uint32_t sg_begin, uint32_t sg_end, void* stream) {
+    return gm_run_part_steps(grid, src, n, cell_bytes, kind, param, 2, flags, level, sg_begin, sg_end, stream);
+}
+
+int gm_run_part_steps(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
+                      int32_t steps, int32_t flags, int32_t level, uint32_t sg_begin, uint32_t sg_end, void* stream) {
+    if (steps != 2 && steps != 4) return fail(GM_EINVAL, "gm_run_part_steps: steps must be 2 or 4");
     gm_cfg_t c{};
     c.n = n;
     c.rho = 1;
@@ -418,8 +424,8 @@ int gm_run_part2(void* grid, const void* src, int64_t n, int32_t cell_bytes, int
     c.param = param;
     c.flags = flags;
     if (int rc = check_common(n, cell_bytes, 1, kind)) return rc;
-    if (kind != GM_KIND_NSUM4 && kind != GM_KIND_NSUM8) return fail(GM_EINVAL, "gm_run_part2: kind must be NSUM4 or NSUM8");
-    if (!grid || !src || src == grid) return fail(GM_EINVAL, "gm_run_part2 needs distinct grid and src buffers");
+    if (kind != GM_KIND_NSUM4 && kind != GM_KIND_NSUM8) return fail(GM_EINVAL, "gm_run_part_steps: kind must be NSUM4 or NSUM8");
+    if (!grid || !src || src == grid) return fail(GM_EINVAL, "gm_run_part_steps needs distinct grid and src buffers");
     const int r = log2i(n);
     const int64_t tile = cell_bytes <= 4 ? 128 / cell_bytes : 32;
     if (level < 0 || (n >> level) < tile)
@@ -432,12 +438,12 @@ int gm_run_part2(void* grid, const void* src, int64_t n, int32_t cell_bytes, int
     a.part_level = level;
     a.sg_begin = sg_begin;
     a.sg_end = sg_end;
-    const cudaError_t e = gm::launch_stencil_tb2(a);
+    const cudaError_t e = gm::launch_stencil_tb(a, steps);
     if (e == cudaErrorNotSupported) {
         cudaGetLastError();
-        return fail(GM_EINVAL, "gm_run_part2: needs 1-, 2- or 4-byte cells");
+        return fail(GM_EINVAL, "gm_run_part_steps: needs 1-, 2- or 4-byte cells");
     }
-    return cuda_rc(e, "partitioned two-step CA launch");
+    return cuda_rc(e, "partitioned fused multi-step CA launch");
 }
 
 int gm_run_part_peer(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
@@ -468,9 +474,11 @@ int gm_run_part_peer(void* grid, const void* src, int64_t n, int32_t cell_bytes,
     a.peer_epi = epilogue;
     a.wait_epoch = wait_epoch;
     a.signal_epoch = signal_epoch;
-    // only the v2 tile kernel (one step) and the fused two-step kernel (GM_FLAG_TWO_STEPS)
-    // carry the fused exchange: no silent fallback to a kernel without it
-    const cudaError_t e = (flags & GM_FLAG_TWO_STEPS) ? gm::launch_stencil_tb2(a) : gm::launch_stencil_v2(a);
+    // only the v2 tile kernel (one step) and the fused multi-step kernel (GM_FLAG_TWO_STEPS,
+    // GM_FLAG_FOUR_STEPS) carry the fused exchange: no silent fallback to a kernel without it
+    const cudaError_t e = (flags & GM_FLAG_FOUR_STEPS)  ? gm::launch_stencil_tb(a, 4)
+                          : (flags & GM_FLAG_TWO_STEPS) ? gm::launch_stencil_tb(a, 2)
+                                                        : gm::launch_stencil_v2(a);
     if (e == cudaErrorNotSupported) {
         cudaGetLastError();
         return fail(GM_EINVAL, "gm_run_part_peer: needs 1-, 2- or 4-byte cells");

@@ -29,6 +29,7 @@ FLAG_PROBE_NOSTORE, FLAG_PROBE_NOLOAD, FLAG_PROBE_NOCOMPUTE = 8192, 16384, 32768
 FLAG_DIGIT_ORDER, FLAG_STORE_CS, FLAG_BAND_MAJOR = 65536, 131072, 262144
 FLAG_PREFETCH_AHEAD, FLAG_FETCH_MIXED, FLAG_FETCH_HALF, FLAG_FETCH256 = 524288, 1048576, 2097152, 4194304
 FLAG_TWO_STEPS = 8388608
+FLAG_FOUR_STEPS = 16777216
 
 
 class GmCfg(ctypes.Structure):
@@ -75,6 +76,7 @@ _SIGS = {
     "gm_ca_step2": [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _vp],
     "gm_ca_steps": [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _vp],
     "gm_run_part2": [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, ctypes.c_uint32, ctypes.c_uint32, _vp],
+    "gm_run_part_steps": [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _i32, ctypes.c_uint32, ctypes.c_uint32, _vp],
     "gm_run_part_peer": [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, ctypes.c_uint32, ctypes.c_uint32, _vp, _u64,
                          _u64, _vp],
     "gm_dev_alloc": [_i64, ctypes.POINTER(ctypes.c_void_p)],

@@ -67,7 +67,7 @@ class PartitionPlan:
     level: int
     world: int
     eight: bool = True
-    depth: int = 1  # CA steps per exchange (2: two fused steps per launch, gm_run_part2)
+    depth: int = 1  # CA steps per exchange (2 or 4: fused steps per launch, gm_run_part_steps)
     ranges: list[tuple[int, int]] = field(init=False)
     halo: dict[int, np.ndarray] = field(init=False)  # sub-gasket -> linear indices of changing halo cells
 
@@ -78,8 +78,8 @@ class PartitionPlan:
         self.nsg = 3 ** self.level
         self.m = self.n >> self.level
         self.ranges = rank_ranges(self.nsg, self.world)
-        if self.depth not in (1, 2):
-            raise ValueError("depth must be 1 or 2 (CA steps per halo exchange)")
+        if self.depth not in (1, 2, 4):
+            raise ValueError("depth must be 1, 2 or 4 (CA steps per halo exchange)")
         self.halo = {s: self._halo_cells_depth(s) for s in range(self.nsg)}
 
     # -- ownership --------------------------------------------------------
@@ -129,27 +129,32 @@ class PartitionPlan:
         return offs
 
     def _halo_cells_depth(self, s: int) -> np.ndarray:
-        """Changing cells outside sub-gasket s that its next `depth` steps read: for two
-        steps, the one-step halo H1 plus every gasket cell outside s next to an H1 cell
-        (H1's step-t+1 values, recomputed locally, read those at step t).  Off-gasket
-        cells never change, and a rank holds them from the start."""
-        h1 = self._halo_cells(s)
-        if self.depth == 1 or h1.size == 0:
-            return h1
+        """Changing cells outside sub-gasket s that its next `depth` steps read: H_1 is the
+        one-step halo; H_{k+1} adds every gasket cell outside s next to an H_k cell (H_k's
+        later values, recomputed locally, read those one step earlier).  Off-gasket cells
+        never change, and a rank holds them from the start."""
+        h = self._halo_cells(s)
+        if self.depth == 1 or h.size == 0:
+            return h
         n, m = self.n, self.m
         bx, by = subgasket_block(s, self.level)
         ox, oy = bx * m, by * m
-        extra = set()
-        for c in h1.tolist():
-            y, x = divmod(c, n)
-            for dx, dy in self._offsets():
-                gx, gy = x + dx, y + dy
-                if not (0 <= gx < n and 0 <= gy < n) or (gx & (n - 1 - gy)) != 0:
-                    continue
-                if ox <= gx < ox + m and oy <= gy < oy + m:
-                    continue  # own cell
-                extra.add(gy * n + gx)
-        return np.unique(np.concatenate([h1, np.array(sorted(extra), dtype=np.int64)]))
+        cells, frontier = set(h.tolist()), set(h.tolist())
+        for _ in range(self.depth - 1):
+            grown = set()
+            for c in frontier:
+                y, x = divmod(c, n)
+                for dx, dy in self._offsets():
+                    gx, gy = x + dx, y + dy
+                    if not (0 <= gx < n and 0 <= gy < n) or (gx & (n - 1 - gy)) != 0:
+                        continue
+                    if ox <= gx < ox + m and oy <= gy < oy + m:
+                        continue  # own cell
+                    if gy * n + gx not in cells:
+                        grown.add(gy * n + gx)
+            cells |= grown
+            frontier = grown
+        return np.array(sorted(cells), dtype=np.int64)
 
     def exchange_slots(self) -> tuple[list[np.ndarray], int]:
         """Per owner rank, the sorted linear indices of its cells some other rank reads."""
@@ -429,8 +434,8 @@ class PartitionedCA:
                  group=None, loopback: Optional[LoopbackGroup] = None, step_fn: Optional[StepFn] = None,
                  adopt_init: bool = False, halo: str = "collective",
                  init_fill: Optional[Callable[[torch.Tensor], None]] = None, fused: bool = False) -> None:
-        """plan.depth = 2 makes every step() advance two CA steps with one fused launch
-        (gm_run_part2) and one halo exchange."""
+        """plan.depth = 2 or 4 makes every step() advance that many CA steps with one fused
+        launch (gm_run_part_steps) and one halo exchange."""
         """`init_fill(t)` (peer halo only) writes the initial state into the first buffer in
         place; `init` then only gives shape and dtype (a meta tensor is enough), so a
         2^18 grid needs two full-size buffers, not three."""
@@ -457,7 +462,7 @@ class PartitionedCA:
         self.step_fn = step_fn or self._gpu_step
         self.lo, self.hi = plan.ranges[rank]
         # fused=True (peer halo): the exchange runs inside the step kernel (gm_run_part_peer)
-        # -- one launch per step (per two steps with plan.depth == 2), no put/wait kernels
+        # -- one launch per step (per plan.depth steps), no put/wait kernels
         self.fused = bool(fused)
         if self.fused and (self.peer is None or step_fn is not None):
             raise ValueError("fused exchange needs halo='peer' and the GPU step")
@@ -467,9 +472,10 @@ class PartitionedCA:
         from . import device as dev
         from . import native
 
-        if self.plan.depth == 2:  # two fused steps over this rank's sub-gaskets
-            native.call("gm_run_part2", dst.data_ptr(), src.data_ptr(), self.plan.n, dst.element_size(), self.kind,
-                        int(np.int32(self.param)), 0, self.plan.level, lo, hi, dev.stream_handle())
+        if self.plan.depth > 1:  # depth fused steps over this rank's sub-gaskets
+            native.call("gm_run_part_steps", dst.data_ptr(), src.data_ptr(), self.plan.n, dst.element_size(),
+                        self.kind, int(np.int32(self.param)), self.plan.depth, 0, self.plan.level, lo, hi,
+                        dev.stream_handle())
             return
         native.call("gm_run_part", dst.data_ptr(), src.data_ptr(), self.plan.n, dst.element_size(), self.kind,
                     int(np.int32(self.param)), native.FLAG_DST_FROM_SRC, self.plan.level, lo, hi,
@@ -490,7 +496,7 @@ class PartitionedCA:
             from . import native
 
             self._epoch += 1
-            fl = native.FLAG_TWO_STEPS if self.plan.depth == 2 else native.FLAG_DST_FROM_SRC
+            fl = {1: native.FLAG_DST_FROM_SRC, 2: native.FLAG_TWO_STEPS, 4: native.FLAG_FOUR_STEPS}[self.plan.depth]
             native.call("gm_run_part_peer", self.b.data_ptr(), self.a.data_ptr(), self.plan.n, self.b.element_size(),
                         self.kind, int(np.int32(self.param)), fl, self.plan.level, self.lo,
                         self.hi, self.peer.epilogue(self._dst).data_ptr(), self._epoch - 1, self._epoch,

@@ -51,25 +51,29 @@ def test_halo_cells_are_corner_cells(eight):
 
 @pytest.mark.parametrize("kind", [1, 2])
 @pytest.mark.parametrize("world", [2, 3, 4])
-def test_depth2_partition_matches_full_steps_cpu(kind, world):
-    """Two CA steps per exchange: with the depth-2 halo (H1 plus the gasket cells next to
-    H1) every rank's own cells after k pairs equal 2k full-grid oracle steps."""
+@pytest.mark.parametrize("depth", [2, 4])
+def test_deep_partition_matches_full_steps_cpu(kind, world, depth):
+    """`depth` CA steps per exchange: with the depth-d halo (H1 grown by the gasket cells
+    next to it, d-1 times) every rank's own cells after k rounds equal d*k full-grid
+    oracle steps."""
     n, level = 1 << 8, 3
-    plan = P.PartitionPlan(n, level, world, eight=kind == 2, depth=2)
+    plan = P.PartitionPlan(n, level, world, eight=kind == 2, depth=depth)
     import oracle
 
     init = oracle.fill_hash(n, np.int8, 21, 0)
     got = P.run_loopback(plan, torch.from_numpy(init), kind, 3, step_fn=_oracle_step_fn(plan, kind, 1))
-    assert np.array_equal(got.numpy(), _reference_steps(init, kind, 1, 6))
+    assert np.array_equal(got.numpy(), _reference_steps(init, kind, 1, 3 * depth))
 
 
-def test_depth2_halo_contains_depth1():
+def test_deeper_halo_contains_shallower():
     for eight in (False, True):
         p1 = P.PartitionPlan(1 << 10, 4, 4, eight=eight)
         p2 = P.PartitionPlan(1 << 10, 4, 4, eight=eight, depth=2)
+        p4 = P.PartitionPlan(1 << 10, 4, 4, eight=eight, depth=4)
         for s in range(p1.nsg):
-            assert set(p1.halo[s].tolist()) <= set(p2.halo[s].tolist())
+            assert set(p1.halo[s].tolist()) <= set(p2.halo[s].tolist()) <= set(p4.halo[s].tolist())
             assert len(p2.halo[s]) <= (13 if eight else 8)
+            assert len(p4.halo[s]) <= (45 if eight else 24)
 
 
 def _oracle_step_fn(plan, kind, param):
@@ -78,7 +82,7 @@ def _oracle_step_fn(plan, kind, param):
     def step(dst, src, lo, hi):
         tmp = dst.numpy().copy()
         oracle.run_bounding_box(tmp, src.numpy(), 1, kind, param)
-        if plan.depth == 2:  # a second step on this rank's (halo-current) local copy
+        for _ in range(plan.depth - 1):  # further steps on this rank's (halo-current) local copy
             tmp2 = tmp.copy()
             oracle.run_bounding_box(tmp2, tmp, 1, kind, param)
             tmp = tmp2
@@ -178,10 +182,11 @@ def test_partition_loopback_gpu_matches_full_grid(gpu, kind):
             plan = P.PartitionPlan(n, level, world, eight=kind == 2)
             got = P.run_loopback(plan, init, kind, 4)
             assert gpu.device.count_mismatch(got, a) == 0, (n, level, world)
-            # two fused steps per launch (gm_run_part2) with the depth-2 halo: 2 pairs = 4 steps
-            plan2 = P.PartitionPlan(n, level, world, eight=kind == 2, depth=2)
-            got2 = P.run_loopback(plan2, init, kind, 2)
-            assert gpu.device.count_mismatch(got2, a) == 0, (n, level, world, "depth 2")
+            # fused steps per launch (gm_run_part_steps) with the depth-d halo: 4 steps
+            for depth in (2, 4):
+                plan_d = P.PartitionPlan(n, level, world, eight=kind == 2, depth=depth)
+                got_d = P.run_loopback(plan_d, init, kind, 4 // depth)
+                assert gpu.device.count_mismatch(got_d, a) == 0, (n, level, world, depth)
 
 
 def _peer_worker(rank, world, port, n, level, kind, steps, out, depth=1, fused=False):
@@ -218,7 +223,8 @@ def _peer_worker(rank, world, port, n, level, kind, steps, out, depth=1, fused=F
 @pytest.mark.parametrize("world,depth,kind,fused", [(2, 1, 1, False), (2, 1, 2, False), (2, 2, 1, False),
                                                     (2, 2, 2, False), (4, 1, 2, False), (4, 2, 2, False),
                                                     (2, 1, 1, True), (2, 1, 2, True), (4, 1, 2, True),
-                                                    (2, 2, 2, True), (4, 2, 1, True)])
+                                                    (2, 2, 2, True), (4, 2, 1, True), (2, 4, 2, False),
+                                                    (4, 4, 2, True), (2, 4, 1, True)])
 def test_peer_memory_halo_processes(gpu, world, depth, kind, fused):
     """PartitionedCA(halo="peer"): no collective per step, halo cells written into the
     peers' buffers over CUDA IPC + release/acquire step flags == the oracle's steps
