@@ -29,6 +29,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <exception>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -392,7 +393,11 @@ const uint32_t* rowmajor_table(int q, int L) {
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
     std::vector<uint32_t> v;
-    rowmajor_order_host(q, L, v);
+    try {
+        rowmajor_order_host(q, L, v);
+    } catch (const std::exception&) {  // (host allocation) -- no exception crosses the C ABI
+        return nullptr;
+    }
     uint32_t* d_tab = nullptr;
     if (cudaMalloc(&d_tab, v.size() * sizeof(uint32_t)) != cudaSuccess) {
         cudaGetLastError();

@@ -432,7 +432,11 @@ const TbLists* tb_lists(bool eight, int T) {
     if (it != cache.end()) return &it->second;
     std::vector<uint32_t> v;
     TbLists L;
-    build_lists<C>(eight, T, v, L.cnt);
+    try {
+        build_lists<C>(eight, T, v, L.cnt);
+    } catch (const std::exception&) {  // (a cone outside the window, host allocation) -- no
+        return nullptr;                 // exception crosses the C ABI: the launch reports an error
+    }
     std::vector<uint16_t> v16(v.begin(), v.end());  // every entry < 2^16
     if (cudaMalloc(&L.lists, v16.size() * 2) != cudaSuccess ||
         cudaMemcpy(L.lists, v16.data(), v16.size() * 2, cudaMemcpyHostToDevice) != cudaSuccess) {
