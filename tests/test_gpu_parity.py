@@ -502,3 +502,57 @@ def test_randomised_launches_vs_oracle(gpu, oracle):
         lx, ly = be.local_cell_arrays(strat, rho)
         be.run_block_space(g, _to_dev(src), rho, (n // rho).bit_length() - 1, strat, lx, ly, kind, param, flags=flags)
         assert np.array_equal(g.cpu().numpy(), want), (n, rho, np.dtype(dtype).name, kind, param, strat, flags)
+
+
+def test_randomised_fused_steps_vs_oracle(gpu, oracle):
+    """Seeded fuzz over the fused multi-step kernel (gm_ca_steps): grid size, cell type,
+    kernel, param, steps per launch, CA-mode or random off-gasket state -- every launch
+    cell by cell against that many oracle steps."""
+    from paper_1706_04552_b200 import device, native
+
+    rng = np.random.default_rng(20261018)
+    for _ in range(40):
+        dtype = [np.int8, np.uint8, np.int16, np.int32][int(rng.integers(0, 4))]
+        c = np.dtype(dtype).itemsize
+        n = (128 // c) << int(rng.integers(0, 4))  # one tile .. 8 tiles per edge
+        kind = int(rng.integers(1, 3))
+        steps = (2, 4)[int(rng.integers(0, 2))]
+        param = int(rng.integers(-(2**31), 2**31 - 1))
+        init = oracle.fill_hash(n, dtype, int(rng.integers(0, 1 << 30)), int(rng.integers(0, 2)))
+        want = _oracle_steps(oracle, init, kind, param, steps)
+        src = torch.from_numpy(init.copy()).cuda()
+        dst = src.clone()
+        native.call("gm_ca_steps", dst.data_ptr(), src.data_ptr(), n, c, kind, int(np.int32(param)), steps, 0,
+                    device.stream_handle())
+        assert np.array_equal(dst.cpu().numpy(), want), (n, np.dtype(dtype).name, kind, steps, param)
+
+
+def test_partitioned_fused_steps_random_ranges(gpu):
+    """gm_run_part_steps over random sub-gasket ranges [lo, hi) of a random level: the
+    cells of those sub-gaskets == the unpartitioned fused launch, everything else
+    untouched (the launch reads a halo-complete copy: here the whole previous state)."""
+    from paper_1706_04552_b200 import device, native
+    from paper_1706_04552_b200 import partition as P
+
+    rng = np.random.default_rng(7)
+    n = 1 << 12
+    for _ in range(12):
+        kind = int(rng.integers(1, 3))
+        steps = (2, 4)[int(rng.integers(0, 2))]
+        level = int(rng.integers(0, 6))  # sub-gaskets >= one 128-byte tile
+        nsg = 3**level
+        lo = int(rng.integers(0, nsg))
+        hi = int(rng.integers(lo, nsg + 1))
+        src = device.fill_hash(n, torch.int8, int(rng.integers(0, 1 << 30)), 0)
+        full = src.clone()
+        native.call("gm_ca_steps", full.data_ptr(), src.data_ptr(), n, 1, kind, 3, steps, 0, device.stream_handle())
+        part = src.clone()
+        native.call("gm_run_part_steps", part.data_ptr(), src.data_ptr(), n, 1, kind, 3, steps, 0, level, lo, hi,
+                    device.stream_handle())
+        m = n >> level
+        mask = torch.zeros((n, n), dtype=torch.bool, device="cuda")
+        for s in range(lo, hi):
+            bx, by = P.subgasket_block(s, level)
+            mask[by * m:(by + 1) * m, bx * m:(bx + 1) * m] = True
+        assert torch.equal(part[mask], full[mask]), (kind, steps, level, lo, hi)
+        assert torch.equal(part[~mask], src[~mask]), (kind, steps, level, lo, hi)
