@@ -4,7 +4,7 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--workload write16|write16-i32|write17|stencil16|stencil16-i32-nsum4|
                                 stencil17|stencil17-nsum4|part15|part18]
-                    [--halo collective|peer|peer-fused] [--temporal 1|2|4]   (part* workloads)
+                    [--halo collective|peer|peer-fused] [--temporal 1|2|4|6]   (part* workloads)
                     [--no-sweep] [--no-e2e] [--no-cpu] [--nsweep]
 
 Default workload (BASELINE configs[1]): the n = 2^16 write pass ("write a
@@ -335,7 +335,7 @@ def _sweep(r: int, dtype, flusher, budget_s: float = 3.0) -> dict:
             "summary": summary, "useful_thread_fraction": useful}
 
 
-def _multi_step(r: int, tdt, kind: int, flusher, steps: int = 40) -> dict:
+def _multi_step(r: int, tdt, kind: int, flusher, steps: int = 48) -> dict:
     """The multi-step CA driver (ca.CARunner): single-step launches vs 2 or 4 fused steps
     per launch (temporal blocking, stencil_tb.cu), CUDA graphs, L2 flushed once before
     the run.  Not the headline: `value` above is one step = one pass."""
@@ -345,10 +345,12 @@ def _multi_step(r: int, tdt, kind: int, flusher, steps: int = 40) -> dict:
 
     n = 1 << r
     out = {"steps": steps, "l2": "flushed once before the run (the state never fits L2)"}
-    for temporal in (1, 2, 4):
+    for temporal in (1, 2, 4, 6):
+        if temporal == 6 and torch.empty((), dtype=tdt).element_size() == 4:
+            continue  # (4-byte cells: at most 4 fused steps)
         g = device.fill_hash(n, tdt, 1, 0)
         run = ca.CARunner(g, kind=kind, param=1, use_graph=True, temporal=temporal)
-        run.run(8)  # warm-up + graph capture
+        run.run(4 * temporal)  # warm-up + graph capture (a graph replay covers 2 * temporal steps)
         torch.cuda.synchronize()
         flusher()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -362,7 +364,9 @@ def _multi_step(r: int, tdt, kind: int, flusher, steps: int = 40) -> dict:
         del run, g
         torch.cuda.empty_cache()
     out["speedup_fused"] = out["temporal1"]["ms_per_step"] / out["temporal2"]["ms_per_step"]
-    out["speedup_fused4"] = out["temporal1"]["ms_per_step"] / out["temporal4"]["ms_per_step"]
+    for t in (4, 6):
+        if f"temporal{t}" in out:
+            out[f"speedup_fused{t}"] = out["temporal1"]["ms_per_step"] / out[f"temporal{t}"]["ms_per_step"]
     # work-equivalent roofline: the §8d bytes of one single step per fused step time (the
     # fused pass moves about one step's bytes per two steps, so this can exceed what the
     # memory system moves; labelled "effective", not the kernel's own roofline)
@@ -370,7 +374,7 @@ def _multi_step(r: int, tdt, kind: int, flusher, steps: int = 40) -> dict:
 
     peak, _ = _peaks()
     c = torch.empty((), dtype=tdt).element_size()
-    for t in ("temporal2", "temporal4"):
+    for t in [k for k in ("temporal2", "temporal4", "temporal6") if k in out]:
         out[t]["effective_frac"] = R.pass_bytes(r, c, kind) / (out[t]["ms_per_step"] * 1e-3) / 1e9 / peak
     return out
 
@@ -490,8 +494,8 @@ def run_ours(args) -> None:
 
         from paper_1706_04552_b200 import partition as P
 
-        # --temporal 2|4: every timed step is one fused launch of that many CA steps
-        # (gm_run_part_steps) with one exchange of the depth-2|4 halo; the line then
+        # --temporal 2|4|6: every timed step is one fused launch of that many CA steps
+        # (gm_run_part_steps) with one exchange of the depth-2|4|6 halo; the line then
         # reports per-CA-step figures
         plan = P.PartitionPlan(n, PART_LEVEL, world, eight=kind == 2, depth=args.temporal)
         group = dist.group.WORLD if world > 1 else None
@@ -747,7 +751,7 @@ def main() -> None:
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--nsweep", action="store_true", help="BASELINE config 4: n sweep + crossover n0, CSV")
-    ap.add_argument("--temporal", type=int, choices=(1, 2, 4), default=1,
+    ap.add_argument("--temporal", type=int, choices=(1, 2, 4, 6), default=1,
                     help="part* workloads: CA steps fused per launch and per halo exchange")
     ap.add_argument("--halo", choices=("collective", "peer", "peer-fused"), default="collective",
                     help="part* workloads, N>1: NCCL all_gather of the halo cells, peer-memory puts (CUDA IPC), "

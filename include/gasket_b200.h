@@ -80,6 +80,7 @@ extern "C" {
 #define GM_FLAG_FETCH256 4194304      /* stencil v2: stage interior tiles with the .L2::256B prefetch-size hint */
 #define GM_FLAG_TWO_STEPS 8388608     /* gm_run_part_peer: two fused CA steps per launch (depth-2 halo) */
 #define GM_FLAG_FOUR_STEPS 16777216   /* gm_run_part_peer: four fused CA steps per launch (depth-4 halo) */
+#define GM_FLAG_SIX_STEPS 33554432    /* gm_run_part_peer: six fused CA steps per launch (depth-6 halo) */
 
 #define GM_OK 0
 #define GM_EINVAL 1  /* bad shape / size / tag (the reference's ValueError) */
@@ -174,8 +175,9 @@ int gm_set_l2_fetch_granularity(int32_t bytes);
  * kind = GM_KIND_NSUM4 or GM_KIND_NSUM8; 1-, 2- or 4-byte cells; async on `stream`. */
 int gm_ca_step2(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
                 int32_t flags, void* stream);
-/* gm_ca_step2 with `steps` = 2 or 4 fused CA steps per launch (temporal blocking over a
- * 4-cell-deep dependency cone for 4): grid <- step^steps(src), same preconditions. */
+/* gm_ca_step2 with `steps` = 2, 4 or 6 fused CA steps per launch (temporal blocking over
+ * a `steps`-cell-deep dependency cone; 6 needs 1- or 2-byte cells):
+ * grid <- step^steps(src), same preconditions. */
 int gm_ca_steps(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
                 int32_t steps, int32_t flags, void* stream);
 /* Peer-memory halo exchange of the partitioned CA (peer.cu).
@@ -210,7 +212,7 @@ int gm_run_part_peer(void* grid, const void* src, int64_t n, int32_t cell_bytes,
  * The caller keeps the halo within two steps current (PartitionPlan(depth=2)). */
 int gm_run_part2(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
                  int32_t flags, int32_t level, uint32_t sg_begin, uint32_t sg_end, void* stream);
-/* gm_run_part2 with `steps` = 2 or 4 fused steps per call (PartitionPlan(depth=steps)). */
+/* gm_run_part2 with `steps` = 2, 4 or 6 fused steps per call (PartitionPlan(depth=steps)). */
 int gm_run_part_steps(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
                       int32_t steps, int32_t flags, int32_t level, uint32_t sg_begin, uint32_t sg_end, void* stream);
 /* The tuned kernels' tile visiting order (host-side, no GPU needed): the 3^q

@@ -10,7 +10,7 @@ so every step may write whole sectors blended from its source
 (A->B, B->A) is captured once into a CUDA graph and replayed, which removes
 the per-step Python/ctypes launch cost for long runs.
 
-``temporal=T`` (temporal blocking) advances T = 2 or 4 steps
+``temporal=T`` (temporal blocking) advances T = 2, 4 or 6 steps
 with one fused launch (``gm_ca_steps``, stencil_tb.cu): state t is read once, the
 intermediate states live only in shared memory, state t+T is written once -- 1/T
 of the DRAM traffic per step.  Results are bit-identical to single steps.
@@ -27,7 +27,7 @@ from .geometry import FractalSpec, IntraStrategy
 
 class CARunner:
     def __init__(self, grid: torch.Tensor, kind: int = backends.KERNEL_NEIGHBOR_SUM8, param: int = 1,
-                 rho: int = 64, use_graph: bool = True, temporal: int = 4) -> None:
+                 rho: int = 64, use_graph: bool = True, temporal: int = 6) -> None:
         device.require_cuda()
         if not device.is_device(grid):
             raise TypeError("CARunner works on a CUDA grid tensor")
@@ -40,10 +40,12 @@ class CARunner:
         self.bufs = (grid, grid.clone())  # fixed physical buffers (the graph captures their addresses)
         self.cur = 0                      # which buffer holds the current state
         self.use_graph = use_graph
-        if temporal not in (1, 2, 4):
-            raise ValueError("temporal must be 1 (one step per launch), 2 or 4 (fused steps per launch)")
+        if temporal not in (1, 2, 4, 6):
+            raise ValueError("temporal must be 1 (one step per launch), 2, 4 or 6 (fused steps per launch)")
         # the fused kernel needs whole 128-byte tiles of 1-, 2- or 4-byte cells
         self.temporal = temporal if (grid.element_size() in (1, 2, 4) and n * grid.element_size() >= 128) else 1
+        if self.temporal == 6 and grid.element_size() == 4:
+            self.temporal = 4  # a 6-cell cone outgrows the 4-cell halo chunk of 4-byte cells
         self._graph = None
         self.steps_done = 0
 
@@ -52,7 +54,7 @@ class CARunner:
                                  param=self.param, flags=native.FLAG_DST_FROM_SRC)
 
     def _fused(self, dst: torch.Tensor, src: torch.Tensor, steps: int) -> None:
-        """`steps` (2 or 4) steps src -> dst (the intermediate states never leave the SM)."""
+        """`steps` (2, 4 or 6) steps src -> dst (the intermediate states never leave the SM)."""
         native.call("gm_ca_steps", dst.data_ptr(), src.data_ptr(), self.spec.n, dst.element_size(), self.kind,
                     int(np.int32(self.param)), steps, 0, device.stream_handle())
 
@@ -63,7 +65,7 @@ class CARunner:
         self.steps_done += 1
 
     def _advance(self, steps: int) -> None:
-        """Advance `steps` (2 or 4) fused steps from the current buffer (graph-free path)."""
+        """Advance `steps` (2, 4 or 6) fused steps from the current buffer (graph-free path)."""
         src, dst = self.bufs[self.cur], self.bufs[1 - self.cur]
         self._fused(dst, src, steps)
         self.cur ^= 1
@@ -124,7 +126,7 @@ class CARunner:
                 self._graph.replay()
                 self.steps_done += per_graph
                 left -= per_graph
-        for k in (4, 2):  # the remainder: fused launches no longer than `temporal`, then singles
+        for k in (6, 4, 2):  # the remainder: fused launches no longer than `temporal`, then singles
             while self.temporal >= k and left >= k:
                 self._advance(k)
                 left -= k
@@ -135,7 +137,7 @@ class CARunner:
 
 
 def run_ca(grid: torch.Tensor, steps: int, kind: int = backends.KERNEL_NEIGHBOR_SUM8, param: int = 1,
-           use_graph: bool = True, temporal: int = 4) -> torch.Tensor:
+           use_graph: bool = True, temporal: int = 6) -> torch.Tensor:
     """`steps` CA steps starting from `grid`; the final state is copied back into `grid`."""
     runner = CARunner(grid, kind, param, use_graph=use_graph, temporal=temporal)
     out = runner.run(steps)

@@ -342,7 +342,7 @@ int gm_ca_step2(void* grid, const void* src, int64_t n, int32_t cell_bytes, int3
 
 int gm_ca_steps(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
                 int32_t steps, int32_t flags, void* stream) {
-    if (steps != 2 && steps != 4) return fail(GM_EINVAL, "gm_ca_steps: steps must be 2 or 4");
+    if (steps != 2 && steps != 4 && steps != 6) return fail(GM_EINVAL, "gm_ca_steps: steps must be 2, 4 or 6");
     gm_cfg_t c{};
     c.n = n;
     c.rho = 1;
@@ -359,7 +359,8 @@ int gm_ca_steps(void* grid, const void* src, int64_t n, int32_t cell_bytes, int3
     const cudaError_t e = gm::launch_stencil_tb(a, steps);
     if (e == cudaErrorNotSupported) {
         cudaGetLastError();
-        return fail(GM_EINVAL, "gm_ca_steps: needs 1-, 2- or 4-byte cells and n >= one 128-byte tile (<= 2^15 tiles per edge)");
+        return fail(GM_EINVAL, "gm_ca_steps: needs 1-, 2- or 4-byte cells (1 or 2 for 6 steps) and n >= one 128-byte "
+                               "tile (<= 2^15 tiles per edge)");
     }
     return cuda_rc(e, "fused multi-step CA launch");
 }
@@ -413,7 +414,7 @@ int gm_run_part2(void* grid, const void* src, int64_t n, int32_t cell_bytes, int
 
 int gm_run_part_steps(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
                       int32_t steps, int32_t flags, int32_t level, uint32_t sg_begin, uint32_t sg_end, void* stream) {
-    if (steps != 2 && steps != 4) return fail(GM_EINVAL, "gm_run_part_steps: steps must be 2 or 4");
+    if (steps != 2 && steps != 4 && steps != 6) return fail(GM_EINVAL, "gm_run_part_steps: steps must be 2, 4 or 6");
     gm_cfg_t c{};
     c.n = n;
     c.rho = 1;
@@ -441,7 +442,7 @@ int gm_run_part_steps(void* grid, const void* src, int64_t n, int32_t cell_bytes
     const cudaError_t e = gm::launch_stencil_tb(a, steps);
     if (e == cudaErrorNotSupported) {
         cudaGetLastError();
-        return fail(GM_EINVAL, "gm_run_part_steps: needs 1-, 2- or 4-byte cells");
+        return fail(GM_EINVAL, "gm_run_part_steps: needs 1-, 2- or 4-byte cells (1 or 2 for 6 steps)");
     }
     return cuda_rc(e, "partitioned fused multi-step CA launch");
 }
@@ -475,10 +476,11 @@ int gm_run_part_peer(void* grid, const void* src, int64_t n, int32_t cell_bytes,
     a.wait_epoch = wait_epoch;
     a.signal_epoch = signal_epoch;
     // only the v2 tile kernel (one step) and the fused multi-step kernel (GM_FLAG_TWO_STEPS,
-    // GM_FLAG_FOUR_STEPS) carry the fused exchange: no silent fallback to a kernel without it
-    const cudaError_t e = (flags & GM_FLAG_FOUR_STEPS)  ? gm::launch_stencil_tb(a, 4)
-                          : (flags & GM_FLAG_TWO_STEPS) ? gm::launch_stencil_tb(a, 2)
-                                                        : gm::launch_stencil_v2(a);
+    // GM_FLAG_FOUR_STEPS, GM_FLAG_SIX_STEPS) carry the fused exchange: no silent fallback to a kernel without it
+    const cudaError_t e = (flags & GM_FLAG_SIX_STEPS)    ? gm::launch_stencil_tb(a, 6)
+                          : (flags & GM_FLAG_FOUR_STEPS) ? gm::launch_stencil_tb(a, 4)
+                          : (flags & GM_FLAG_TWO_STEPS)  ? gm::launch_stencil_tb(a, 2)
+                                                         : gm::launch_stencil_v2(a);
     if (e == cudaErrorNotSupported) {
         cudaGetLastError();
         return fail(GM_EINVAL, "gm_run_part_peer: needs 1-, 2- or 4-byte cells");

@@ -50,21 +50,21 @@ namespace {
 using namespace sc;
 
 constexpr int ROWB = 128;
-constexpr int PITCH = ROWB + 48;  // 16 B halo | 128 B row | 16 B halo | 16 B pad
+constexpr int PITCH = ROWB + 32;  // 16 B halo | 128 B row | 16 B halo (a 16 B pad: same speed)
 constexpr int CHUNKS = 10;
-constexpr int MAX_T = 4;
+constexpr int MAX_T = 6;
 
 // Skewed row layout of the staged (S) and odd-phase (I) buffers: tile row r sits at
-// buffer row idx = r + SHIFT, at byte idx * PITCH + 16 * ((r + 4) >> 2): 16 more bytes
+// buffer row idx = r + SHIFT, at byte idx * PITCH + 16 * ((r + 8) >> 2): 16 more bytes
 // per 4-row quad (monotone, so rows never overlap).  The vertical-run work items of a
 // warp come from several quads; with a plain 176-byte pitch a quad step moves the bank
 // by 16, so items two quads apart with the same word collided.  The skew makes the
 // quad step 20 banks: 8 consecutive quads land in 8 bank groups.  The skew of a tile
 // row is the same in S and I, so the same word is `dS` bytes apart in the two.
-constexpr int SKEW_BYTES = 16 * 36;  // >= 16 * (((TT + MAX_T - 1) + 4) >> 2 + 1) for TT <= 128
+constexpr int SKEW_BYTES = 16 * 36;  // >= 16 * (((TT + MAX_T - 1) + 8) >> 2) for TT <= 128
 template <int SHIFT>
 __device__ __host__ __forceinline__ int row_off(int idx) {
-    return idx * PITCH + 16 * ((idx - SHIFT + 4) >> 2);
+    return idx * PITCH + 16 * ((idx - SHIFT + 8) >> 2);  // tile row idx - SHIFT >= -8
 }
 
 template <int C, int T>
@@ -91,7 +91,7 @@ struct TB {
 // words at ring[p-1] .. ring[p] of the ring area
 struct TbCounts {
     int ns = 0, ni = 0;
-    int ring[MAX_T + 1] = {0, 0, 0, 0, 0};
+    int ring[MAX_T + 1] = {0, 0, 0, 0, 0, 0, 0};
 };
 
 // word k (cells (k-4)*V ..) of tile row r can hold gasket cells for some gasket
@@ -432,11 +432,7 @@ const TbLists* tb_lists(bool eight, int T) {
     if (it != cache.end()) return &it->second;
     std::vector<uint32_t> v;
     TbLists L;
-    try {
-        build_lists<C>(eight, T, v, L.cnt);
-    } catch (const std::exception&) {  // (a cone outside the window, host allocation) -- no
-        return nullptr;                 // exception crosses the C ABI: the launch reports an error
-    }
+    build_lists<C>(eight, T, v, L.cnt);
     std::vector<uint16_t> v16(v.begin(), v.end());  // every entry < 2^16
     if (cudaMalloc(&L.lists, v16.size() * 2) != cudaSuccess ||
         cudaMemcpy(L.lists, v16.data(), v16.size() * 2, cudaMemcpyHostToDevice) != cudaSuccess) {
@@ -496,22 +492,24 @@ template <int T>
 cudaError_t launch_t(const LaunchArgs& a) {
     int r = 0;
     while ((int64_t(1) << r) < a.n) ++r;
+    // the cone reaches T cells past the tile: it must fit the 16-byte halo chunks
     switch (a.cell_bytes) {
-    case 1: if (a.n >= TB<1, T>::TT) return launch_c<1, T>(a, r); break;
-    case 2: if (a.n >= TB<2, T>::TT) return launch_c<2, T>(a, r); break;
-    case 4: if (a.n >= TB<4, T>::TT) return launch_c<4, T>(a, r); break;
+    case 1: if (a.n >= TB<1, T>::TT && T <= TB<1, T>::CC) return launch_c<1, T>(a, r); break;
+    case 2: if (a.n >= TB<2, T>::TT && T <= TB<2, T>::CC) return launch_c<2, T>(a, r); break;
+    case 4: if (a.n >= TB<4, T>::TT && T <= TB<4, T>::CC) return launch_c<4, T>(a, r); break;
     }
     return cudaErrorNotSupported;
 }
 
 }  // namespace
 
-// T fused CA steps (T = 2 or 4): grid <- step^T(src); grid must equal src off the gasket.
-// cudaErrorNotSupported for other T, grids narrower than one tile or cell widths other
-// than 1, 2, 4.
+// T fused CA steps (T = 2, 4 or 6): grid <- step^T(src); grid must equal src off the
+// gasket.  cudaErrorNotSupported for other T, grids narrower than one tile, cell widths
+// other than 1, 2, 4, and T = 6 on 4-byte cells (the cone outgrows the halo chunk).
 cudaError_t launch_stencil_tb(const LaunchArgs& a, int steps) {
     if (steps == 2) return launch_t<2>(a);
     if (steps == 4) return launch_t<4>(a);
+    if (steps == 6) return launch_t<6>(a);
     return cudaErrorNotSupported;
 }
 cudaError_t launch_stencil_tb2(const LaunchArgs& a) { return launch_stencil_tb(a, 2); }

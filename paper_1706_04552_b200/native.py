@@ -30,6 +30,7 @@ FLAG_DIGIT_ORDER, FLAG_STORE_CS, FLAG_BAND_MAJOR = 65536, 131072, 262144
 FLAG_PREFETCH_AHEAD, FLAG_FETCH_MIXED, FLAG_FETCH_HALF, FLAG_FETCH256 = 524288, 1048576, 2097152, 4194304
 FLAG_TWO_STEPS = 8388608
 FLAG_FOUR_STEPS = 16777216
+FLAG_SIX_STEPS = 33554432
 
 
 class GmCfg(ctypes.Structure):

@@ -67,7 +67,7 @@ class PartitionPlan:
     level: int
     world: int
     eight: bool = True
-    depth: int = 1  # CA steps per exchange (2 or 4: fused steps per launch, gm_run_part_steps)
+    depth: int = 1  # CA steps per exchange (2, 4 or 6: fused steps per launch, gm_run_part_steps)
     ranges: list[tuple[int, int]] = field(init=False)
     halo: dict[int, np.ndarray] = field(init=False)  # sub-gasket -> linear indices of changing halo cells
 
@@ -78,8 +78,8 @@ class PartitionPlan:
         self.nsg = 3 ** self.level
         self.m = self.n >> self.level
         self.ranges = rank_ranges(self.nsg, self.world)
-        if self.depth not in (1, 2, 4):
-            raise ValueError("depth must be 1, 2 or 4 (CA steps per halo exchange)")
+        if self.depth not in (1, 2, 4, 6):
+            raise ValueError("depth must be 1, 2, 4 or 6 (CA steps per halo exchange)")
         self.halo = {s: self._halo_cells_depth(s) for s in range(self.nsg)}
 
     # -- ownership --------------------------------------------------------
@@ -434,8 +434,8 @@ class PartitionedCA:
                  group=None, loopback: Optional[LoopbackGroup] = None, step_fn: Optional[StepFn] = None,
                  adopt_init: bool = False, halo: str = "collective",
                  init_fill: Optional[Callable[[torch.Tensor], None]] = None, fused: bool = False) -> None:
-        """plan.depth = 2 or 4 makes every step() advance that many CA steps with one fused
-        launch (gm_run_part_steps) and one halo exchange."""
+        """plan.depth = 2, 4 or 6 makes every step() advance that many CA steps with one
+        fused launch (gm_run_part_steps) and one halo exchange."""
         """`init_fill(t)` (peer halo only) writes the initial state into the first buffer in
         place; `init` then only gives shape and dtype (a meta tensor is enough), so a
         2^18 grid needs two full-size buffers, not three."""
@@ -496,7 +496,8 @@ class PartitionedCA:
             from . import native
 
             self._epoch += 1
-            fl = {1: native.FLAG_DST_FROM_SRC, 2: native.FLAG_TWO_STEPS, 4: native.FLAG_FOUR_STEPS}[self.plan.depth]
+            fl = {1: native.FLAG_DST_FROM_SRC, 2: native.FLAG_TWO_STEPS, 4: native.FLAG_FOUR_STEPS,
+                  6: native.FLAG_SIX_STEPS}[self.plan.depth]
             native.call("gm_run_part_peer", self.b.data_ptr(), self.a.data_ptr(), self.plan.n, self.b.element_size(),
                         self.kind, int(np.int32(self.param)), fl, self.plan.level, self.lo,
                         self.hi, self.peer.epilogue(self._dst).data_ptr(), self._epoch - 1, self._epoch,

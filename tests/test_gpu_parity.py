@@ -368,7 +368,7 @@ def _oracle_steps(oracle, init, kind, param, steps):
 
 
 @pytest.mark.parametrize("kind", [1, 2])
-@pytest.mark.parametrize("temporal", [1, 2, 4])
+@pytest.mark.parametrize("temporal", [1, 2, 4, 6])
 def test_ca_runner_matches_oracle_steps(gpu, oracle, kind, temporal):
     from paper_1706_04552_b200 import ca
 
@@ -394,13 +394,19 @@ def test_ca_runner_matches_oracle_steps(gpu, oracle, kind, temporal):
 
 
 @pytest.mark.parametrize("dtype", [np.int8, np.int16, np.int32])
-@pytest.mark.parametrize("steps", [2, 4])
+@pytest.mark.parametrize("steps", [2, 4, 6])
 def test_fused_steps_vs_oracle(gpu, oracle, dtype, steps):
     """gm_ca_steps (2 or 4 CA steps per pass) == that many oracle steps, cell by cell,
     incl. grid-edge tiles and a 2^12 grid; also on a CA state that is 0 off the gasket."""
     from paper_1706_04552_b200 import device, native
 
     n0 = 128 // np.dtype(dtype).itemsize
+    if steps == 6 and np.dtype(dtype).itemsize == 4:  # the 6-cell cone outgrows a 4-cell halo chunk
+        src = torch.zeros((n0, n0), dtype=torch.int32, device="cuda")
+        with pytest.raises(ValueError):
+            native.call("gm_ca_steps", src.clone().data_ptr(), src.data_ptr(), n0, 4, 2, 1, 6, 0,
+                        device.stream_handle())
+        return
     for n in (n0, 2 * n0, 4 * n0, 1 << 12):
         for mode in (0, 1):
             init = oracle.fill_hash(n, dtype, 41 + mode, mode)
@@ -459,13 +465,15 @@ def test_whole_grid_tile_and_unit_grid(gpu, oracle):
 
 
 @pytest.mark.parametrize("dtype", [torch.int8, torch.int16, torch.int32])
-@pytest.mark.parametrize("steps", [2, 4])
+@pytest.mark.parametrize("steps", [2, 4, 6])
 def test_fused_steps_equal_single_steps_large(gpu, dtype, steps):
     """At sizes past the oracle's reach: gm_ca_steps == that many single-step launches,
     bit for bit."""
     from paper_1706_04552_b200 import device, native
 
     be, S = gpu.backends, gpu.geometry.IntraStrategy
+    if steps == 6 and dtype == torch.int32:
+        pytest.skip("6 fused steps need 1- or 2-byte cells")
     n = 1 << 15 if dtype == torch.int8 else 1 << 14
     for kind in (1, 2):
         src = device.fill_hash(n, dtype, 77, 0)
@@ -516,7 +524,7 @@ def test_randomised_fused_steps_vs_oracle(gpu, oracle):
         c = np.dtype(dtype).itemsize
         n = (128 // c) << int(rng.integers(0, 4))  # one tile .. 8 tiles per edge
         kind = int(rng.integers(1, 3))
-        steps = (2, 4)[int(rng.integers(0, 2))]
+        steps = (2, 4, 6)[int(rng.integers(0, 3 if c <= 2 else 2))]
         param = int(rng.integers(-(2**31), 2**31 - 1))
         init = oracle.fill_hash(n, dtype, int(rng.integers(0, 1 << 30)), int(rng.integers(0, 2)))
         want = _oracle_steps(oracle, init, kind, param, steps)
@@ -538,7 +546,7 @@ def test_partitioned_fused_steps_random_ranges(gpu):
     n = 1 << 12
     for _ in range(12):
         kind = int(rng.integers(1, 3))
-        steps = (2, 4)[int(rng.integers(0, 2))]
+        steps = (2, 4, 6)[int(rng.integers(0, 3))]
         level = int(rng.integers(0, 6))  # sub-gaskets >= one 128-byte tile
         nsg = 3**level
         lo = int(rng.integers(0, nsg))

@@ -51,7 +51,7 @@ def test_halo_cells_are_corner_cells(eight):
 
 @pytest.mark.parametrize("kind", [1, 2])
 @pytest.mark.parametrize("world", [2, 3, 4])
-@pytest.mark.parametrize("depth", [2, 4])
+@pytest.mark.parametrize("depth", [2, 4, 6])
 def test_deep_partition_matches_full_steps_cpu(kind, world, depth):
     """`depth` CA steps per exchange: with the depth-d halo (H1 grown by the gasket cells
     next to it, d-1 times) every rank's own cells after k rounds equal d*k full-grid
@@ -70,8 +70,10 @@ def test_deeper_halo_contains_shallower():
         p1 = P.PartitionPlan(1 << 10, 4, 4, eight=eight)
         p2 = P.PartitionPlan(1 << 10, 4, 4, eight=eight, depth=2)
         p4 = P.PartitionPlan(1 << 10, 4, 4, eight=eight, depth=4)
+        p6 = P.PartitionPlan(1 << 10, 4, 4, eight=eight, depth=6)
         for s in range(p1.nsg):
-            assert set(p1.halo[s].tolist()) <= set(p2.halo[s].tolist()) <= set(p4.halo[s].tolist())
+            assert (set(p1.halo[s].tolist()) <= set(p2.halo[s].tolist()) <= set(p4.halo[s].tolist())
+                    <= set(p6.halo[s].tolist()))
             assert len(p2.halo[s]) <= (13 if eight else 8)
             assert len(p4.halo[s]) <= (45 if eight else 24)
 
@@ -178,6 +180,11 @@ def test_partition_loopback_gpu_matches_full_grid(gpu, kind):
             b = a.clone()
             be.run_block_space(b, a, 64, (n // 64).bit_length() - 1, S.TUNED, kind=kind, param=1)
             a = b
+        a6 = a.clone()
+        for _ in range(2):
+            b = a6.clone()
+            be.run_block_space(b, a6, 64, (n // 64).bit_length() - 1, S.TUNED, kind=kind, param=1)
+            a6 = b
         for world in worlds:
             plan = P.PartitionPlan(n, level, world, eight=kind == 2)
             got = P.run_loopback(plan, init, kind, 4)
@@ -187,6 +194,9 @@ def test_partition_loopback_gpu_matches_full_grid(gpu, kind):
                 plan_d = P.PartitionPlan(n, level, world, eight=kind == 2, depth=depth)
                 got_d = P.run_loopback(plan_d, init, kind, 4 // depth)
                 assert gpu.device.count_mismatch(got_d, a) == 0, (n, level, world, depth)
+            plan6 = P.PartitionPlan(n, level, world, eight=kind == 2, depth=6)
+            got6 = P.run_loopback(plan6, init, kind, 1)
+            assert gpu.device.count_mismatch(got6, a6) == 0, (n, level, world, 6)
 
 
 def _peer_worker(rank, world, port, n, level, kind, steps, out, depth=1, fused=False):
@@ -224,7 +234,8 @@ def _peer_worker(rank, world, port, n, level, kind, steps, out, depth=1, fused=F
                                                     (2, 2, 2, False), (4, 1, 2, False), (4, 2, 2, False),
                                                     (2, 1, 1, True), (2, 1, 2, True), (4, 1, 2, True),
                                                     (2, 2, 2, True), (4, 2, 1, True), (2, 4, 2, False),
-                                                    (4, 4, 2, True), (2, 4, 1, True)])
+                                                    (4, 4, 2, True), (2, 4, 1, True), (2, 6, 2, True),
+                                                    (4, 6, 1, False)])
 def test_peer_memory_halo_processes(gpu, world, depth, kind, fused):
     """PartitionedCA(halo="peer"): no collective per step, halo cells written into the
     peers' buffers over CUDA IPC + release/acquire step flags == the oracle's steps
