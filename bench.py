@@ -594,6 +594,9 @@ def run_ours(args) -> None:
             line["config"]["ca_steps_per_launch"] = ca_steps
             line["config"]["timing"] = (f"{ca_steps} fused CA steps per timed launch; ms_per_step and value are per "
                                         f"CA step; roofline fracs are work-equivalent (one step's bytes per step)")
+        if args.project and world == 1:
+            line["projection"] = [_project(part, int(w), ms_per_step * ca_steps, ca_steps, flusher)
+                                  for w in args.project.split(",")]
         if hasattr(part, "close"):
             part.close()
         line["config"]["subgasket_ranges"] = part.plan.ranges
@@ -629,6 +632,37 @@ def run_ours(args) -> None:
         import torch.distributed as dist
 
         dist.destroy_process_group()
+
+
+def _project(part, world: int, ms_launch_1: float, ca_steps: int, flusher, reps: int = 10) -> dict:
+    """Multi-GPU projection on one GPU: time each of `world` ranks' sub-gasket ranges
+    (PartitionPlan(world)) alone, on the full-size buffers, without the halo exchange.
+    The slowest rank bounds an N-GPU step from below; the exchange adds a few hundred
+    bytes of NVLink traffic per step (latency).  Not a scaling measurement."""
+    import torch
+
+    from paper_1706_04552_b200 import partition as P
+
+    plan = P.PartitionPlan(part.plan.n, part.plan.level, world, eight=part.plan.eight, depth=part.plan.depth)
+    per_rank = []
+    for lo, hi in plan.ranges:
+        ts = []
+        for _ in range(reps):
+            flusher()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            part.step_fn(part.b, part.a, lo, hi)
+            b.record()
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        per_rank.append(statistics.fmean(ts) / ca_steps)
+    slots, width = plan.exchange_slots()
+    worst = max(per_rank)
+    return {"world": world, "per_rank_ms_per_step": per_rank, "max_rank_ms_per_step": worst,
+            "speedup_vs_one_gpu": ms_launch_1 / ca_steps / worst,
+            "halo_cells_per_rank_per_exchange": [int(len(x)) for x in slots],
+            "note": ("each rank's sub-gasket range timed alone on one GPU, no exchange: a compute-only "
+                     "bound on the N-GPU step, not a scaling measurement")}
 
 
 def run_reference(args) -> None:
@@ -753,6 +787,9 @@ def main() -> None:
     ap.add_argument("--nsweep", action="store_true", help="BASELINE config 4: n sweep + crossover n0, CSV")
     ap.add_argument("--temporal", type=int, choices=(1, 2, 4, 6), default=1,
                     help="part* workloads: CA steps fused per launch and per halo exchange")
+    ap.add_argument("--project", default="",
+                    help="part* workloads on one GPU, e.g. 2,4,8: also time each of N ranks' sub-gasket ranges "
+                         "alone (compute-only bound of an N-GPU step; 'projection' in the line)")
     ap.add_argument("--halo", choices=("collective", "peer", "peer-fused"), default="collective",
                     help="part* workloads, N>1: NCCL all_gather of the halo cells, peer-memory puts (CUDA IPC), "
                          "or the peer exchange fused into the step kernel (temporal 1)")
