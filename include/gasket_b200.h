@@ -149,6 +149,14 @@ int gm_coverage_blocks(const int64_t* bx, const int64_t* by, int64_t nblocks, co
 int gm_bijection_check(const int64_t* cx, const int64_t* cy, int64_t nblocks, int64_t n_b,
                        int64_t* owner, int64_t* result, void* stream);
 
+/* The pre-launch snapshot of a neighbour-sum launch (engine.py:201's grid.copy()),
+ * masked: copies into `snap` (n*n cells, distinct from grid) only what a one-step
+ * stencil over the gasket reads -- each member 128-byte tile's rows -1..TT and one
+ * 32-byte sector either side -- at the same positions; other cells of snap are left
+ * as they are.  Async on `stream`.  GM_EINVAL for other cell widths, edges that are
+ * not a power of two >= 128/cell_bytes, or more than 2^15 tiles per edge. */
+int gm_snapshot_stencil(void* snap, const void* grid, int64_t n, int32_t cell_bytes, void* stream);
+
 /* Synthetic inputs / checks shared with the CPU oracle (oracle/gasket_oracle.c). */
 int gm_fill_hash(void* buf, int64_t n, int32_t cell_bytes, uint64_t seed, int32_t mode, void* stream);
 int gm_checksum(const void* buf, int64_t count, int32_t cell_bytes, uint64_t* out_dev, void* stream);

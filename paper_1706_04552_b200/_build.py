@@ -13,7 +13,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libgasket_b200.so"
-SOURCES = ["literal.cu", "tuned.cu", "stream.cu", "stencil.cu", "stencil2.cu", "stencil_tb.cu", "stencil_tma.cu", "hostrows.cu", "maps.cu", "capi.cu", "part.cu", "peer.cu"]
+SOURCES = ["literal.cu", "tuned.cu", "stream.cu", "stencil.cu", "stencil2.cu", "stencil_tb.cu", "stencil_tma.cu", "hostrows.cu", "maps.cu", "capi.cu", "part.cu", "peer.cu", "snapshot.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
               "--expt-relaxed-constexpr"]

@@ -147,9 +147,7 @@ def _run(grid: Any, src: Any, kind: int, launch, *, mapped_ok: bool) -> None:
             if not device.is_device(src):
                 src_dev = torch.from_numpy(np.ascontiguousarray(src)).to(grid.device, non_blocking=True)
             elif _shares_memory(src, grid):
-                snap = device.scratch.get("snapshot", grid.numel(), grid.dtype, grid.device).view(n, n)
-                snap.copy_(grid)
-                src_dev = snap
+                src_dev = device.stencil_snapshot(grid)  # engine.py:201's snapshot, masked
             else:
                 device.check_square(src, "src")
         launch(device.data_ptr(grid), device.data_ptr(src_dev) if reads_src else 0, n, c, stream, 0)
@@ -177,10 +175,10 @@ def _run(grid: Any, src: Any, kind: int, launch, *, mapped_ok: bool) -> None:
     dev_grid.copy_(host_grid, non_blocking=True)
     src_ptr = 0
     if reads_src:
-        dev_src = device.scratch.get("host_src", n * n, tdtype).view(n, n)
         if _shares_memory(src, grid):
-            dev_src.copy_(dev_grid)
+            dev_src = device.stencil_snapshot(dev_grid)
         else:
+            dev_src = device.scratch.get("host_src", n * n, tdtype).view(n, n)
             dev_src.copy_(torch.from_numpy(np.ascontiguousarray(src)), non_blocking=True)
         src_ptr = dev_src.data_ptr()
     launch(dev_grid.data_ptr(), src_ptr, n, c, stream, 0)

@@ -277,6 +277,18 @@ int gm_bijection_check(const int64_t* cx, const int64_t* cy, int64_t nblocks, in
     return GM_OK;
 }
 
+int gm_snapshot_stencil(void* snap, const void* grid, int64_t n, int32_t cell_bytes, void* stream) {
+    if (!snap || !grid || snap == grid) return fail(GM_EINVAL, "gm_snapshot_stencil needs distinct buffers");
+    if (n < 1) return fail(GM_EINVAL, "bad edge");
+    const cudaError_t e = gm::launch_snapshot_stencil(snap, grid, n, cell_bytes, reinterpret_cast<cudaStream_t>(stream));
+    if (e == cudaErrorNotSupported) {
+        cudaGetLastError();
+        return fail(GM_EINVAL, "gm_snapshot_stencil: needs 1/2/4/8-byte cells, a power-of-two edge >= one 128-byte "
+                               "tile and <= 2^15 tiles per edge");
+    }
+    return cuda_rc(e, "masked snapshot");
+}
+
 int gm_fill_hash(void* buf, int64_t n, int32_t cell_bytes, uint64_t seed, int32_t mode, void* stream) {
     if (n < 1) return fail(GM_EINVAL, "bad edge");
     return cuda_rc(gm::launch_fill_hash(buf, n, cell_bytes, seed, mode, reinterpret_cast<cudaStream_t>(stream)),

@@ -1,0 +1,90 @@
+// snapshot.cu -- the pre-launch snapshot of a neighbour-sum launch, masked.
+//
+// engine.launch takes `src = grid.copy()` before every NEIGHBOR_SUM launch
+// (engine.py:201; a full n^2 copy, outside the reference's
+// timer) so that the launch reads the pre-launch state while it writes gasket
+// cells of `grid`.  Every stencil kernel here (literal, tuned, fused) reads `src`
+// only at gasket cells, their 4/8 neighbours, and -- for whole-sector stores --
+// the touched sectors of the gasket rows.  All of those lie in the window of some
+// member tile: rows -1..TT of the tile (TT = 128/C cells, one 128-byte line per
+// row) and one 32-byte sector either side.  So the snapshot copies exactly those
+// windows, at their own positions, into a grid-sized buffer; the rest of the buffer
+// is never read.  n = 2^17 int8: 59049 tiles x 130 rows x 192 B = 1.47 GB each way
+// instead of 16 GiB each way.  Whole sectors only (no partial-sector RMW).
+#include <cstdint>
+
+#include "gasket.cuh"
+#include "launch.h"
+
+namespace gm {
+namespace {
+
+constexpr int WIN_BYTES = 32 + 128 + 32;  // left sector | the tile's line | right sector
+constexpr int VEC_PER_ROW = WIN_BYTES / 16;
+
+// 16 bytes, streaming; `half`: fetch only the 64-byte half of the line on an L2 miss
+// (the halo sectors of a neighbouring line)
+__device__ __forceinline__ uint4 ld16(const uint8_t* p, bool half) {
+    uint4 v;
+    if (half)
+        asm volatile("ld.global.cs.L2::64B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    else
+        v = __ldcs(reinterpret_cast<const uint4*>(p));
+    return v;
+}
+
+__global__ void __launch_bounds__(256) snapshot_tiles(uint8_t* __restrict__ snap, const uint8_t* __restrict__ grid,
+                                                      int64_t n, int cell_bytes, const uint32_t* __restrict__ order,
+                                                      uint32_t ntiles, uint32_t nb) {
+    const int64_t rowbytes = n * cell_bytes;
+    const int tt = 128 / cell_bytes;  // tile rows (and cells per row)
+    const int per_tile = (tt + 2) * VEC_PER_ROW;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const uint32_t v = __ldg(order + t);
+        const uint32_t bx = v & 0xffffu, by = v >> 16;
+        // halo rows / sectors that a neighbouring member tile's window already covers are
+        // skipped (tile (X, Y) is a member iff X & ~Y == 0, X, Y < nb)
+        const bool up = by > 0 && (bx & ~(by - 1)) == 0;
+        const bool down = by + 1 < nb && (bx & ~(by + 1)) == 0;
+        const bool left = bx > 0 && ((bx - 1) & ~by) == 0;
+        const bool right = bx + 1 < nb && ((bx + 1) & ~by) == 0;
+        const int64_t xb0 = (int64_t)bx * 128 - 32;  // window's first byte
+        const int64_t y0 = (int64_t)by * tt - 1;     // window's first row
+        for (int i = threadIdx.x; i < per_tile; i += blockDim.x) {
+            const int row = i / VEC_PER_ROW, q = i - row * VEC_PER_ROW;
+            if ((row == 0 && up) || (row == tt + 1 && down) || (q < 2 && left) || (q >= 10 && right)) continue;
+            const int64_t y = y0 + row, xb = xb0 + q * 16;
+            if (y < 0 || y >= n || xb < 0 || xb >= rowbytes) continue;
+            const int64_t off = y * rowbytes + xb;
+            *reinterpret_cast<uint4*>(snap + off) = ld16(grid + off, q < 2 || q >= 10);
+        }
+    }
+}
+
+}  // namespace
+
+// cudaErrorNotSupported: cell widths other than 1/2/4/8, grids narrower than a tile or
+// with more than 2^15 tiles per edge (the caller then copies the whole grid).
+cudaError_t launch_snapshot_stencil(void* snap, const void* grid, int64_t n, int cell_bytes, cudaStream_t s) {
+    if (cell_bytes != 1 && cell_bytes != 2 && cell_bytes != 4 && cell_bytes != 8) return cudaErrorNotSupported;
+    const int64_t tt = 128 / cell_bytes;
+    if (n < tt || (n & (n - 1)) != 0) return cudaErrorNotSupported;
+    int r_t = 0;
+    while ((tt << r_t) < n) ++r_t;
+    const uint32_t* order = rowmajor_table(r_t, 0);  // neighbouring tiles together: shared halo lines hit L2
+    if (order == nullptr) return cudaErrorNotSupported;
+    uint32_t ntiles = 1;
+    for (int i = 0; i < r_t; ++i) ntiles *= 3u;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    uint32_t blocks = (uint32_t)sms * 8u;
+    if (blocks > ntiles) blocks = ntiles;
+    snapshot_tiles<<<blocks, 256, 0, s>>>(reinterpret_cast<uint8_t*>(snap), reinterpret_cast<const uint8_t*>(grid), n,
+                                          cell_bytes, order, ntiles, 1u << r_t);
+    note_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace gm

@@ -122,6 +122,24 @@ class _Scratch:
 scratch = _Scratch()
 
 
+def stencil_snapshot(grid: torch.Tensor) -> torch.Tensor:
+    """engine.launch's pre-launch copy of a neighbour-sum launch (engine.py:201), on the
+    device and masked: only the cells a one-step stencil over the gasket reads are
+    copied (gm_snapshot_stencil: each member tile's rows -1..TT plus a 32-byte sector
+    either side), into a reused scratch buffer whose other cells are never read.
+    Grids the masked copy does not cover (narrower than one 128-byte tile) are copied
+    whole, on the device."""
+    n = int(grid.shape[0])
+    snap = scratch.get("snapshot", grid.numel(), grid.dtype, grid.device).view(n, n)
+    c = grid.element_size()
+    tt = 128 // c if c in (1, 2, 4, 8) else 0
+    if tt and n >= tt and n & (n - 1) == 0 and n // tt <= 1 << 15:
+        native.call("gm_snapshot_stencil", snap.data_ptr(), grid.data_ptr(), n, c, stream_handle())
+    else:
+        snap.copy_(grid)
+    return snap
+
+
 # ---------------------------------------------------------------------------
 # mapped (zero-copy) host buffers
 # ---------------------------------------------------------------------------

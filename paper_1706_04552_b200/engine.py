@@ -189,7 +189,9 @@ def launch(config: LaunchConfig, grid, backend: Optional[str] = None) -> WorkMet
     plan = prepare(config, backend)
     neighbour = config.kernel.kind is not KernelKind.CONST
     if neighbour:
-        src = grid.clone() if isinstance(grid, torch.Tensor) else grid.copy()
+        # engine.py:201 (src = grid.copy()): on the device only the cells the launch reads
+        # are copied (device.stencil_snapshot), into a reused buffer
+        src = device.stencil_snapshot(grid) if isinstance(grid, torch.Tensor) else grid.copy()
         # grid and its snapshot agree off the gasket: stencils may blend from src
         plan.flags |= native.FLAG_DST_FROM_SRC
     else:

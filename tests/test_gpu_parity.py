@@ -564,3 +564,54 @@ def test_partitioned_fused_steps_random_ranges(gpu):
             mask[by * m:(by + 1) * m, bx * m:(bx + 1) * m] = True
         assert torch.equal(part[mask], full[mask]), (kind, steps, level, lo, hi)
         assert torch.equal(part[~mask], src[~mask]), (kind, steps, level, lo, hi)
+
+
+@pytest.mark.parametrize("dtype", [torch.int8, torch.int16, torch.int32, torch.int64])
+def test_masked_snapshot_serves_every_stencil(gpu, dtype):
+    """gm_snapshot_stencil (engine.launch's grid.copy(), masked): a snapshot buffer that
+    holds garbage outside the copied windows gives every neighbour-sum kernel the same
+    result as a full copy -- literal strategies, BB, the tuned kernel and its variants."""
+    from paper_1706_04552_b200 import device, native
+
+    be, S = gpu.backends, gpu.geometry.IntraStrategy
+    c = torch.empty((), dtype=dtype).element_size()
+    for n in (128 // c, 4 * (128 // c), 1 << 11):
+        grid0 = device.fill_hash(n, dtype, 91, 0)
+        snap = device.fill_hash(n, dtype, 92, 0)  # garbage outside the windows
+        native.call("gm_snapshot_stencil", snap.data_ptr(), grid0.data_ptr(), n, c, device.stream_handle())
+        for kind in (1, 2):
+            for rho, strat, flags in ((8, S.TUNED, 2), (8, S.TUNED, 0), (8, S.SUBBOX, 0), (8, S.TABLE, 0),
+                                      (16, S.UNROLL, 0), (8, S.TUNED, 2 | 2048), (8, S.TUNED, 2 | 4096)):
+                if rho > n:
+                    continue
+                r_b = (n // rho).bit_length() - 1
+                lx, ly = be.local_cell_arrays(strat, rho)
+                want = grid0.clone()
+                be.run_block_space(want, grid0.clone(), rho, r_b, strat, lx, ly, kind, 7, flags=flags)
+                got = grid0.clone()
+                be.run_block_space(got, snap, rho, r_b, strat, lx, ly, kind, 7, flags=flags)
+                assert torch.equal(got, want), (n, str(dtype), kind, rho, strat, flags)
+            want = grid0.clone()
+            be.run_bounding_box(want, grid0.clone(), 8, kind, 7)
+            got = grid0.clone()
+            be.run_bounding_box(got, snap, 8, kind, 7)
+            assert torch.equal(got, want), (n, str(dtype), kind, "bb")
+
+
+def test_engine_launch_neighbour_sum_uses_masked_snapshot(gpu, oracle):
+    """engine.launch (engine.py:193-211) on a device grid, NEIGHBOR_SUM: the result equals
+    the oracle's step (the masked snapshot replaces the full grid.copy())."""
+    eng = gpu.engine
+    from paper_1706_04552_b200.geometry import FractalSpec
+
+    for n, rho in ((256, 8), (1024, 16)):
+        init = oracle.fill_hash(n, np.int32, 5, 0)
+        want = init.copy()
+        oracle.run_bounding_box(want, init, 1, oracle.KIND_NSUM4, 1)
+        spec = FractalSpec(n=n, rho=rho)
+        for strat in (gpu.geometry.IntraStrategy.TUNED, gpu.geometry.IntraStrategy.TABLE):
+            g = torch.from_numpy(init.copy()).cuda()
+            cfg = eng.LaunchConfig(spec=spec, mapping=eng.Mapping.BLOCK_SPACE, strategy=strat,
+                                   kernel=eng.CellKernel(eng.KernelKind.NEIGHBOR_SUM, 1))
+            eng.launch(cfg, g)
+            assert np.array_equal(g.cpu().numpy(), want), (n, rho, strat)
