@@ -319,6 +319,25 @@ def test_numpy_host_path(gpu, oracle, monkeypatch, transport):
         assert np.array_equal(g, want)
 
 
+def test_mapped_write_pass_multi_chunk_rows(gpu, monkeypatch):
+    """The host-mapped write pass (hostrows.cu) at sizes whose rows span several K-line
+    work units: equal to the device write pass on the same grid, cell for cell."""
+    from paper_1706_04552_b200 import device
+
+    monkeypatch.setenv("GASKET_HOST_TRANSPORT", "mapped")
+    S = gpu.geometry.IntraStrategy
+    for n, dtype in ((1 << 14, torch.int8), (1 << 14, torch.int16), (1 << 13, torch.int32)):
+        dev = device.fill_hash(n, dtype, 17, 0)
+        host = torch.empty((n, n), dtype=dtype, pin_memory=True)
+        host.copy_(dev.cpu())
+        g = host.numpy()
+        rho = 32
+        r_b = (n // rho).bit_length() - 1
+        gpu.backends.run_block_space(g, g, rho, r_b, S.TUNED, kind=0, param=-3)
+        gpu.backends.run_block_space(dev, dev, rho, r_b, S.TUNED, kind=0, param=-3)
+        assert torch.equal(torch.from_numpy(g).cuda(), dev), (n, str(dtype))
+
+
 def test_src_alias_is_snapshotted(gpu, oracle):
     n = 256
     grid0 = oracle.fill_hash(n, np.int32, 4, 0)
