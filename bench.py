@@ -20,7 +20,7 @@ headline size (paper-literal SUBBOX/TABLE/UNROLL and tuned lambda, paper-
 literal and block-early-exit BB) with the best-vs-best speedup and the useful-
 thread fractions; `roofline` (sector-minimum bytes / event time vs the measured
 HBM peak, plus `hw_model`: the bytes this memory system must move); for the
-stencils `multi_step` (the CA driver, one and two fused steps per launch); `cpu_baseline`
+stencils `multi_step` (the CA driver, 1 / 2 / 4 / 6 fused steps per launch); `cpu_baseline`
 (the C/OpenMP port of the reference numba kernels, all host threads, bounded
 sample); `e2e` (the reference-facing call with host numpy buffers); `clocks`
 (NVML sampled during the timed region); `gpu_launches`.

@@ -210,8 +210,9 @@ int gm_peer_halo_wait(const uint64_t* flags, int32_t rank, int32_t world, uint64
  * `epilogue` = device descriptor (PartitionedCA(halo="peer", fused=True) builds it);
  * every CTA first acquires the peers' flags >= wait_epoch (0: no wait), the last CTA
  * to finish stores the rank's halo cells into the peers' buffers and releases
- * signal_epoch.  With GM_FLAG_TWO_STEPS the launch is gm_run_part2's two fused steps
- * (the halo must then be the depth-2 one).  Stream-ordered like every launch. */
+ * signal_epoch.  With GM_FLAG_TWO_STEPS / _FOUR_STEPS / _SIX_STEPS the launch is
+ * gm_run_part_steps' 2 / 4 / 6 fused steps (the halo must then be of that depth).
+ * Stream-ordered like every launch. */
 int gm_run_part_peer(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
                      int32_t flags, int32_t level, uint32_t sg_begin, uint32_t sg_end, void* epilogue,
                      uint64_t wait_epoch, uint64_t signal_epoch, void* stream);

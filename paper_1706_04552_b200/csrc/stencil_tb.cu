@@ -445,7 +445,7 @@ const TbLists* tb_lists(bool eight, int T) {
 template <int C, int KIND, int T>
 cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
     using S = TB<C, T>;
-    // tile range: the whole gasket, or (partitioned launches, gm_run_part2) the digit-order
+    // tile range: the whole gasket, or (partitioned launches, gm_run_part_steps) the digit-order
     // sub-gasket range [sg_begin, sg_end) of level part_level; the order table groups
     // tiles by those sub-gaskets, so the range is a contiguous run of it
     uint32_t lo, hi;
