@@ -34,13 +34,20 @@ __device__ __forceinline__ uint4 ld16(const uint8_t* p, bool half) {
     return v;
 }
 
+// one warp per member tile (tiles row-major, grid-stride over all warps); each lane moves
+// UNROLL 16-byte pieces per round with all its loads in flight before the stores
+constexpr int UNROLL = 8;
+
 __global__ void __launch_bounds__(256) snapshot_tiles(uint8_t* __restrict__ snap, const uint8_t* __restrict__ grid,
                                                       int64_t n, int cell_bytes, const uint32_t* __restrict__ order,
                                                       uint32_t ntiles, uint32_t nb) {
     const int64_t rowbytes = n * cell_bytes;
     const int tt = 128 / cell_bytes;  // tile rows (and cells per row)
     const int per_tile = (tt + 2) * VEC_PER_ROW;
-    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t t = warp; t < ntiles; t += nwarps) {
         const uint32_t v = __ldg(order + t);
         const uint32_t bx = v & 0xffffu, by = v >> 16;
         // halo rows / sectors that a neighbouring member tile's window already covers are
@@ -51,13 +58,23 @@ __global__ void __launch_bounds__(256) snapshot_tiles(uint8_t* __restrict__ snap
         const bool right = bx + 1 < nb && ((bx + 1) & ~by) == 0;
         const int64_t xb0 = (int64_t)bx * 128 - 32;  // window's first byte
         const int64_t y0 = (int64_t)by * tt - 1;     // window's first row
-        for (int i = threadIdx.x; i < per_tile; i += blockDim.x) {
-            const int row = i / VEC_PER_ROW, q = i - row * VEC_PER_ROW;
-            if ((row == 0 && up) || (row == tt + 1 && down) || (q < 2 && left) || (q >= 10 && right)) continue;
-            const int64_t y = y0 + row, xb = xb0 + q * 16;
-            if (y < 0 || y >= n || xb < 0 || xb >= rowbytes) continue;
-            const int64_t off = y * rowbytes + xb;
-            *reinterpret_cast<uint4*>(snap + off) = ld16(grid + off, q < 2 || q >= 10);
+        for (int base = 0; base < per_tile; base += 32 * UNROLL) {
+            uint4 val[UNROLL];
+            int64_t off[UNROLL];
+#pragma unroll
+            for (int k = 0; k < UNROLL; ++k) {
+                const int i = base + k * 32 + lane;
+                const int row = i / VEC_PER_ROW, q = i - row * VEC_PER_ROW;
+                const int64_t y = y0 + row, xb = xb0 + q * 16;
+                const bool skip = i >= per_tile || (row == 0 && up) || (row == tt + 1 && down) ||
+                                  (q < 2 && left) || (q >= 10 && right) || y < 0 || y >= n || xb < 0 ||
+                                  xb >= rowbytes;
+                off[k] = skip ? -1 : y * rowbytes + xb;
+                if (!skip) val[k] = ld16(grid + off[k], q < 2 || q >= 10);
+            }
+#pragma unroll
+            for (int k = 0; k < UNROLL; ++k)
+                if (off[k] >= 0) *reinterpret_cast<uint4*>(snap + off[k]) = val[k];
         }
     }
 }
@@ -79,8 +96,8 @@ cudaError_t launch_snapshot_stencil(void* snap, const void* grid, int64_t n, int
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    uint32_t blocks = (uint32_t)sms * 8u;
-    if (blocks > ntiles) blocks = ntiles;
+    uint32_t blocks = (uint32_t)sms * 8u;  // 64 warps per SM, a tile each
+    if (blocks > (ntiles + 7) / 8) blocks = (ntiles + 7) / 8;
     snapshot_tiles<<<blocks, 256, 0, s>>>(reinterpret_cast<uint8_t*>(snap), reinterpret_cast<const uint8_t*>(grid), n,
                                           cell_bytes, order, ntiles, 1u << r_t);
     note_launch();
