@@ -21,7 +21,9 @@ def main():
     dst = src.clone()
     D = native.FLAG_DST_FROM_SRC
     for kind in (2, 1):
-        for name, fl in (("full", D), ("no compute", D | native.FLAG_PROBE_NOCOMPUTE),
+        for name, fl in (("full", D), ("fetch half", D | native.FLAG_FETCH_HALF),
+                         ("fetch mixed", D | native.FLAG_FETCH_HALF | native.FLAG_FETCH_MIXED),
+                         ("stages2", D | native.FLAG_STAGES2), ("no compute", D | native.FLAG_PROBE_NOCOMPUTE),
                          ("reads only", D | native.FLAG_PROBE_NOSTORE), ("no memory", D | native.FLAG_PROBE_NOLOAD |
                                                                           native.FLAG_PROBE_NOSTORE)):
             fn = lambda: backends.run_block_space(dst, src, 64, 11, IntraStrategy.TUNED, kind=kind,  # noqa: E731
