@@ -53,6 +53,9 @@ constexpr int ROWB = 128;
 constexpr int PITCH = ROWB + 32;  // 16 B halo | 128 B row | 16 B halo (a 16 B pad: same speed)
 constexpr int CHUNKS = 10;
 constexpr int MAX_T = 6;
+#ifndef TB_ONE_SLOT_FROM_T
+#define TB_ONE_SLOT_FROM_T 6  // T = 6: one staging slot, 4 CTAs per SM (903 vs 916 us per launch; T = 4: 663 vs 652)
+#endif
 
 // Skewed row layout of the staged (S) and odd-phase (I) buffers: tile row r sits at
 // buffer row idx = r + SHIFT, at byte idx * PITCH + 16 * ((r + 8) >> 2): 16 more bytes
@@ -193,13 +196,15 @@ __device__ __forceinline__ void vstrip(const uint8_t* ibuf, const uint8_t* sbuf,
     }
 }
 
-template <int C, int KIND, int T>
+template <int C, int KIND, int T, int NST>
 __global__ void __launch_bounds__(TB<C, T>::THREADS)
     stencil_tb(uint8_t* __restrict__ grid, const uint8_t* __restrict__ src, int64_t n, uint32_t ntiles,
                uint64_t param, const uint32_t* __restrict__ order, const uint16_t* __restrict__ lists_g,
                TbCounts cnt, int flags, PeerEpilogue* epi, uint64_t wait_epoch, uint64_t signal_epoch) {
     using S = TB<C, T>;
-    constexpr int NST = 2;  // staging ring depth
+    // NST = staging slots: 2 (tile idx+1 staged while idx computes) or 1 (staged after
+    // tile idx is stored; a smaller CTA, so 4 instead of 3 share an SM)
+    static_assert(NST == 1 || NST == 2, "one or two staging slots");
     static_assert(T % 2 == 0 && T <= MAX_T, "an even number of fused steps leaves the result in S");
     peer_prologue_wait(epi, wait_epoch);  // partitioned CA with the fused exchange only
     constexpr bool EIGHT = KIND == KIND_NSUM8;
@@ -277,11 +282,13 @@ __global__ void __launch_bounds__(TB<C, T>::THREADS)
     cp_async_commit();
     for (uint32_t idx = 0; idx < count; ++idx) {
         const uint32_t v_after = AHEAD ? tile_v(idx + 2) : 0u;
-        cp_async_wait<NST - 2>();
+        cp_async_wait<0>();
         __syncthreads();  // state t of tile idx staged; tile idx-1 fully stored (I and its S slot free)
         if constexpr (!AHEAD) v_next = tile_v(idx + 1);
-        stage(idx + 1, v_next);
-        cp_async_commit();
+        if constexpr (NST == 2) {
+            stage(idx + 1, v_next);
+            cp_async_commit();
+        }
         int64_t x0, y0;
         tile_xy(v_cur, x0, y0);
         v_cur = v_next;
@@ -333,6 +340,11 @@ __global__ void __launch_bounds__(TB<C, T>::THREADS)
             const uint4 b = *reinterpret_cast<const uint4*>(srow + k0 + 4);
             const uint32_t out[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
             st_sector(grid + (y0 + t) * rowstride + x0 * C + g * 32, out, v8, false);
+        }
+        if constexpr (NST == 1) {  // the slot is free once every thread has read its sector
+            __syncthreads();
+            stage(idx + 1, v_cur);  // (v_cur already holds tile idx+1's order entry)
+            cp_async_commit();
         }
     }
     cp_async_wait<0>();
@@ -442,7 +454,7 @@ const TbLists* tb_lists(bool eight, int T) {
     return &(cache[key] = L);
 }
 
-template <int C, int KIND, int T>
+template <int C, int KIND, int T, int NST>
 cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
     using S = TB<C, T>;
     // tile range: the whole gasket, or (partitioned launches, gm_run_part_steps) the digit-order
@@ -457,8 +469,8 @@ cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
     if (order != nullptr) order += lo;
     if (L == nullptr || order == nullptr) return cudaErrorMemoryAllocation;
     const int entries = L->cnt.ns + L->cnt.ni + L->cnt.ring[T];
-    const size_t smem = 2 * (size_t)S::SBUF + S::IBUF + 2 * (size_t)entries;
-    auto* kern = stencil_tb<C, KIND, T>;
+    const size_t smem = (size_t)NST * S::SBUF + S::IBUF + 2 * (size_t)entries;
+    auto* kern = stencil_tb<C, KIND, T, NST>;
     ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
@@ -483,8 +495,9 @@ cudaError_t launch_c(const LaunchArgs& a, int r) {
     int k = 0;
     while ((1 << k) < TB<C, T>::TT) ++k;
     if (r - k > 15) return cudaErrorNotSupported;  // tile-order table limit
-    if (a.kind == KIND_NSUM4) return launch_ck<C, KIND_NSUM4, T>(a, r - k);
-    if (a.kind == KIND_NSUM8) return launch_ck<C, KIND_NSUM8, T>(a, r - k);
+    constexpr int NST = T >= TB_ONE_SLOT_FROM_T ? 1 : 2;
+    if (a.kind == KIND_NSUM4) return launch_ck<C, KIND_NSUM4, T, NST>(a, r - k);
+    if (a.kind == KIND_NSUM8) return launch_ck<C, KIND_NSUM8, T, NST>(a, r - k);
     return cudaErrorNotSupported;
 }
 
