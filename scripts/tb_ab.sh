@@ -1,4 +1,4 @@
-# usage (on the GPU box): LIBS="C F2" bash scripts/tb_ab.sh TAG -- fused CA, T = 2 and 4, per A/B build
+# usage (on the GPU box): LIBS="A B" TS="2 4 6" bash scripts/tb_ab.sh TAG -- fused CA launch times per A/B build (ab/libX.so)
 TAG=$1; mkdir -p gpurun_out/$TAG; O=gpurun_out/$TAG/ab.txt
 for rep in 1 2; do for L in ${LIBS:-C F2}; do for T in ${TS:-2 4}; do
   echo "== lib$L T=$T" >> $O
