@@ -378,6 +378,28 @@ def _multi_step(r: int, tdt, kind: int, flusher, steps: int = 48) -> dict:
     return out
 
 
+def _staged_bytes(r: int, c: int) -> tuple[int, int]:
+    """Host bytes of the staged mapped stencil (gm_snapshot_stencil + gm_writeback_tiles):
+    each member tile's rows -1..TT (128-byte line + a 32-byte sector either side, halos a
+    neighbouring member tile covers skipped, grid edges clipped) read, its own TT lines
+    written back."""
+    tt = 128 // c
+    nb = (1 << r) // tt
+    h2d = ntiles = 0
+    for Y in range(nb):
+        X = Y
+        while True:  # subsets of Y
+            member = lambda x, y: 0 <= x < nb and 0 <= y < nb and (x & ~y) == 0  # noqa: E731
+            rows = tt + (0 if (Y == 0 or member(X, Y - 1)) else 1) + (0 if (Y == nb - 1 or member(X, Y + 1)) else 1)
+            per_row = 128 + (0 if (X == 0 or member(X - 1, Y)) else 32) + (0 if (X == nb - 1 or member(X + 1, Y)) else 32)
+            h2d += rows * per_row
+            ntiles += 1
+            if X == 0:
+                break
+            X = (X - 1) & Y
+    return h2d, ntiles * tt * 128
+
+
 def _e2e(workload: str, rho: int, steps: int, transports: tuple = ("mapped", "copy")) -> dict:
     """The reference-facing call (backends.run_block_space on host numpy grids)."""
     import numpy as np
@@ -403,8 +425,10 @@ def _e2e(workload: str, rho: int, steps: int, transports: tuple = ("mapped", "co
         g[...] = src
     for transport in transports:
         os.environ[device.HOST_TRANSPORT_ENV] = transport
-        call = (lambda: backends.run_block_space(g, g if src is None else src, rho, r_b, IntraStrategy.TUNED,
-                                                 kind=kind, param=1))
+        # mapped stencils: engine.launch semantics (src is the grid's pre-launch snapshot),
+        # which the staged path serves (masked snapshot -> device kernel -> write-back)
+        s_arg = g if (src is None or transport == "mapped") else src
+        call = (lambda: backends.run_block_space(g, s_arg, rho, r_b, IntraStrategy.TUNED, kind=kind, param=1))
         call()  # warm-up (page-locks and maps the buffer once for "mapped")
         k = steps if transport == "mapped" else max(2, min(steps, 3))
         t0 = time.perf_counter()
@@ -423,8 +447,7 @@ def _e2e(workload: str, rho: int, steps: int, transports: tuple = ("mapped", "co
                 full = 3 ** (r - kh)  # halves made only of gasket cells need no read
                 h2d, d2h = (halves - full) * 64, halves * 64
             else:
-                touched = R.write_bytes(r, c)
-                h2d, d2h = R.stencil_read_bytes(r, c, kind == 2) + touched, touched
+                h2d, d2h = _staged_bytes(r, c)
         else:
             h2d = n * n * c * (1 if kind == 0 else 2)
             d2h = n * n * c

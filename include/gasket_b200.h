@@ -156,6 +156,10 @@ int gm_bijection_check(const int64_t* cx, const int64_t* cy, int64_t nblocks, in
  * as they are.  Async on `stream`.  GM_EINVAL for other cell widths, edges that are
  * not a power of two >= 128/cell_bytes, or more than 2^15 tiles per edge. */
 int gm_snapshot_stencil(void* snap, const void* grid, int64_t n, int32_t cell_bytes, void* stream);
+/* The write-back of a staged neighbour-sum launch (host-mapped grids): writes every
+ * member tile's own rows (128-byte lines) of `out` whole -- sectors holding gasket
+ * cells from `dst`, the others from `snap`.  out, dst, snap: n*n cells, distinct. */
+int gm_writeback_tiles(void* out, const void* dst, const void* snap, int64_t n, int32_t cell_bytes, void* stream);
 
 /* Synthetic inputs / checks shared with the CPU oracle (oracle/gasket_oracle.c). */
 int gm_fill_hash(void* buf, int64_t n, int32_t cell_bytes, uint64_t seed, int32_t mode, void* stream);

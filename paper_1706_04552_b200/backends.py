@@ -123,6 +123,12 @@ def _shares_memory(a: Any, b: Any) -> bool:
     return False
 
 
+def _same_array(a: Any, b: Any) -> bool:
+    """Both numpy arrays over exactly the same memory (same start, shape and strides)."""
+    return (isinstance(a, np.ndarray) and isinstance(b, np.ndarray) and a.ctypes.data == b.ctypes.data
+            and a.shape == b.shape and a.strides == b.strides)
+
+
 def _run(grid: Any, src: Any, kind: int, launch, *, mapped_ok: bool) -> None:
     """Route one launch: device tensors directly, numpy through a host transport.
 
@@ -158,6 +164,21 @@ def _run(grid: Any, src: Any, kind: int, launch, *, mapped_ok: bool) -> None:
     if not grid.flags.writeable:
         raise ValueError("grid is read-only")
     mode = device.host_transport()
+    if (mode == "mapped" and mapped_ok and reads_src and _same_array(src, grid)
+            and device.tile_staging_ok(n, c)):
+        # engine.launch semantics on a host grid (src is the grid: its pre-launch snapshot):
+        # stage only what the launch reads (the member tiles' windows) into the device,
+        # run the tuned kernel there, write the tiles' own lines back whole -- the host
+        # sees whole-line traffic for the dilated gasket instead of 16-byte pieces
+        tdtype = device._torch_dtype(grid.dtype)
+        snap = device.scratch.get("host_snap", n * n, tdtype).view(n, n)
+        dst = device.scratch.get("host_dst", n * n, tdtype).view(n, n)
+        with device.MappedHost(grid) as gptr:
+            native.call("gm_snapshot_stencil", snap.data_ptr(), gptr, n, c, stream)
+            launch(dst.data_ptr(), snap.data_ptr(), n, c, stream, native.FLAG_DST_FROM_SRC)
+            native.call("gm_writeback_tiles", gptr, dst.data_ptr(), snap.data_ptr(), n, c, stream)
+            torch.cuda.current_stream().synchronize()
+        return
     if mode == "mapped" and mapped_ok and not (reads_src and _shares_memory(src, grid)):
         src_host = np.ascontiguousarray(src) if reads_src else None
         with device.MappedHost(grid) as gptr:

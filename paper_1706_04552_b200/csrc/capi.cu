@@ -289,6 +289,18 @@ int gm_snapshot_stencil(void* snap, const void* grid, int64_t n, int32_t cell_by
     return cuda_rc(e, "masked snapshot");
 }
 
+int gm_writeback_tiles(void* out, const void* dst, const void* snap, int64_t n, int32_t cell_bytes, void* stream) {
+    if (!out || !dst || !snap || out == dst || out == snap) return fail(GM_EINVAL, "gm_writeback_tiles: bad buffers");
+    if (n < 1) return fail(GM_EINVAL, "bad edge");
+    const cudaError_t e = gm::launch_writeback_tiles(out, dst, snap, n, cell_bytes, reinterpret_cast<cudaStream_t>(stream));
+    if (e == cudaErrorNotSupported) {
+        cudaGetLastError();
+        return fail(GM_EINVAL, "gm_writeback_tiles: needs 1/2/4/8-byte cells, a power-of-two edge >= one 128-byte "
+                               "tile and <= 2^15 tiles per edge");
+    }
+    return cuda_rc(e, "tile write-back");
+}
+
 int gm_fill_hash(void* buf, int64_t n, int32_t cell_bytes, uint64_t seed, int32_t mode, void* stream) {
     if (n < 1) return fail(GM_EINVAL, "bad edge");
     return cuda_rc(gm::launch_fill_hash(buf, n, cell_bytes, seed, mode, reinterpret_cast<cudaStream_t>(stream)),

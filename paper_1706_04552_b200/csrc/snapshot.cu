@@ -79,7 +79,66 @@ __global__ void __launch_bounds__(256) snapshot_tiles(uint8_t* __restrict__ snap
     }
 }
 
+// The write-back half of a staged launch on a host-mapped grid: every member tile's own
+// rows (one 128-byte line each) go back whole -- the touched sectors from `dst` (the
+// stencil's whole-sector results), the other sectors from `snap` (the pre-launch state)
+// -- so the host sees whole-line writes only.
+__global__ void __launch_bounds__(256) writeback_tiles(uint8_t* __restrict__ out, const uint8_t* __restrict__ dst,
+                                                       const uint8_t* __restrict__ snap, int64_t n, int cell_bytes,
+                                                       const uint32_t* __restrict__ order, uint32_t ntiles) {
+    const int64_t rowbytes = n * cell_bytes;
+    const int tt = 128 / cell_bytes;
+    const int sc = 32 / cell_bytes;  // cells per sector
+    const int per_tile = tt * 8;     // 16-byte pieces of the tile's own lines
+    const int lane = threadIdx.x & 31;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t t = warp; t < ntiles; t += nwarps) {
+        const uint32_t v = __ldg(order + t);
+        const int64_t xb0 = (int64_t)(v & 0xffffu) * 128, y0 = (int64_t)(v >> 16) * tt;
+        for (int base = 0; base < per_tile; base += 32 * UNROLL) {
+            uint4 val[UNROLL];
+            int64_t off[UNROLL];
+#pragma unroll
+            for (int k = 0; k < UNROLL; ++k) {
+                const int i = base + k * 32 + lane;
+                const int row = i >> 3, q = i & 7;
+                off[k] = i < per_tile ? (y0 + row) * rowbytes + xb0 + q * 16 : -1;
+                if (off[k] >= 0) {
+                    const bool touched = (((q >> 1) * sc) & ~row) == 0;  // sector holds gasket cells
+                    val[k] = __ldcs(reinterpret_cast<const uint4*>((touched ? dst : snap) + off[k]));
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < UNROLL; ++k)
+                if (off[k] >= 0) *reinterpret_cast<uint4*>(out + off[k]) = val[k];
+        }
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_writeback_tiles(void* out, const void* dst, const void* snap, int64_t n, int cell_bytes,
+                                   cudaStream_t s) {
+    if (cell_bytes != 1 && cell_bytes != 2 && cell_bytes != 4 && cell_bytes != 8) return cudaErrorNotSupported;
+    const int64_t tt = 128 / cell_bytes;
+    if (n < tt || (n & (n - 1)) != 0) return cudaErrorNotSupported;
+    int r_t = 0;
+    while ((tt << r_t) < n) ++r_t;
+    const uint32_t* order = rowmajor_table(r_t, 0);
+    if (order == nullptr) return cudaErrorNotSupported;
+    uint32_t ntiles = 1;
+    for (int i = 0; i < r_t; ++i) ntiles *= 3u;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    uint32_t blocks = (uint32_t)sms * 8u;
+    if (blocks > (ntiles + 7) / 8) blocks = (ntiles + 7) / 8;
+    writeback_tiles<<<blocks, 256, 0, s>>>(reinterpret_cast<uint8_t*>(out), reinterpret_cast<const uint8_t*>(dst),
+                                           reinterpret_cast<const uint8_t*>(snap), n, cell_bytes, order, ntiles);
+    note_launch();
+    return cudaGetLastError();
+}
 
 // cudaErrorNotSupported: cell widths other than 1/2/4/8, grids narrower than a tile or
 // with more than 2^15 tiles per edge (the caller then copies the whole grid).

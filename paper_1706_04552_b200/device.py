@@ -122,6 +122,13 @@ class _Scratch:
 scratch = _Scratch()
 
 
+def tile_staging_ok(n: int, c: int) -> bool:
+    """Grids the tile-window kernels (gm_snapshot_stencil, gm_writeback_tiles) cover:
+    1/2/4/8-byte cells, a power-of-two edge of at least one 128-byte tile, <= 2^15 tiles."""
+    tt = 128 // c if c in (1, 2, 4, 8) else 0
+    return bool(tt) and n >= tt and n & (n - 1) == 0 and n // tt <= 1 << 15
+
+
 def stencil_snapshot(grid: torch.Tensor) -> torch.Tensor:
     """engine.launch's pre-launch copy of a neighbour-sum launch (engine.py:201), on the
     device and masked: only the cells a one-step stencil over the gasket reads are
@@ -132,8 +139,7 @@ def stencil_snapshot(grid: torch.Tensor) -> torch.Tensor:
     n = int(grid.shape[0])
     snap = scratch.get("snapshot", grid.numel(), grid.dtype, grid.device).view(n, n)
     c = grid.element_size()
-    tt = 128 // c if c in (1, 2, 4, 8) else 0
-    if tt and n >= tt and n & (n - 1) == 0 and n // tt <= 1 << 15:
+    if tile_staging_ok(n, c):
         native.call("gm_snapshot_stencil", snap.data_ptr(), grid.data_ptr(), n, c, stream_handle())
     else:
         snap.copy_(grid)

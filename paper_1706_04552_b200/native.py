@@ -64,6 +64,7 @@ _SIGS = {
     "gm_coverage_blocks": [_vp, _vp, _i64, _vp, _vp, _i32, _i32, _i64, _vp, _vp],
     "gm_bijection_check": [_vp, _vp, _i64, _i64, _vp, _vp, _vp],
     "gm_snapshot_stencil": [_vp, _vp, _i64, _i32, _vp],
+    "gm_writeback_tiles": [_vp, _vp, _vp, _i64, _i32, _vp],
     "gm_fill_hash": [_vp, _i64, _i32, _u64, _i32, _vp],
     "gm_checksum": [_vp, _i64, _i32, _vp, _vp],
     "gm_count_equal": [_vp, _vp, _i64, _i32, _vp, _vp],

@@ -634,3 +634,23 @@ def test_engine_launch_neighbour_sum_uses_masked_snapshot(gpu, oracle):
                                    kernel=eng.CellKernel(eng.KernelKind.NEIGHBOR_SUM, 1))
             eng.launch(cfg, g)
             assert np.array_equal(g.cpu().numpy(), want), (n, rho, strat)
+
+
+@pytest.mark.parametrize("dtype", [np.int8, np.int16, np.int32])
+def test_mapped_staged_neighbour_sum(gpu, oracle, monkeypatch, dtype):
+    """Host-mapped numpy grid, src is the grid (engine.launch semantics): the staged path
+    (masked snapshot -> device kernel -> whole-line write-back, gm_writeback_tiles) ==
+    the oracle's step, cell for cell, off-gasket cells untouched."""
+    monkeypatch.setenv("GASKET_HOST_TRANSPORT", "mapped")
+    S = gpu.geometry.IntraStrategy
+    c = np.dtype(dtype).itemsize
+    for n in (128 // c, 4 * (128 // c), 1 << 12):
+        for kind in (1, 2):
+            grid0 = oracle.fill_hash(n, dtype, 23 + kind, 0)
+            want = grid0.copy()
+            oracle.run_bounding_box(want, grid0.copy(), 1, kind, -4)
+            host = torch.from_numpy(grid0.copy()).pin_memory()
+            g = host.numpy()
+            rho = min(64, n)
+            gpu.backends.run_block_space(g, g, rho, (n // rho).bit_length() - 1, S.TUNED, kind=kind, param=-4)
+            assert np.array_equal(g, want), (n, np.dtype(dtype).name, kind)
