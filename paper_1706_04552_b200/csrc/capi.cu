@@ -292,7 +292,12 @@ int gm_snapshot_stencil(void* snap, const void* grid, int64_t n, int32_t cell_by
 int gm_writeback_tiles(void* out, const void* dst, const void* snap, int64_t n, int32_t cell_bytes, void* stream) {
     if (!out || !dst || !snap || out == dst || out == snap) return fail(GM_EINVAL, "gm_writeback_tiles: bad buffers");
     if (n < 1) return fail(GM_EINVAL, "bad edge");
-    const cudaError_t e = gm::launch_writeback_tiles(out, dst, snap, n, cell_bytes, reinterpret_cast<cudaStream_t>(stream));
+    // the row-ordered walk (host pages K lines at a time) for 1/2/4-byte cells, else per tile
+    cudaError_t e = gm::launch_host_rows_copyback(out, dst, snap, n, cell_bytes, reinterpret_cast<cudaStream_t>(stream));
+    if (e == cudaErrorNotSupported) {
+        cudaGetLastError();
+        e = gm::launch_writeback_tiles(out, dst, snap, n, cell_bytes, reinterpret_cast<cudaStream_t>(stream));
+    }
     if (e == cudaErrorNotSupported) {
         cudaGetLastError();
         return fail(GM_EINVAL, "gm_writeback_tiles: needs 1/2/4/8-byte cells, a power-of-two edge >= one 128-byte "

@@ -134,6 +134,49 @@ __global__ void __launch_bounds__(256) host_rows_write(uint8_t* __restrict__ gri
     }
 }
 
+// The write-back of a staged neighbour-sum launch (gm_writeback_tiles) in the same
+// row-major walk: the member lines of each row go to the host whole, sector by sector
+// from `dst` (sectors holding gasket cells: the kernel's results) or `snap` (the rest).
+template <int C>
+__global__ void __launch_bounds__(256) host_rows_copyback(uint8_t* __restrict__ out, const uint8_t* __restrict__ dst,
+                                                          const uint8_t* __restrict__ snap, int64_t n,
+                                                          const uint64_t* __restrict__ prefix, uint32_t nY) {
+    constexpr int TT = 128 / C;
+    constexpr int SC = 32 / C;  // cells per sector
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t total = prefix[nY];
+    const int64_t rowstride = n * C;
+    for (uint64_t u = warp0; u < total; u += nwarps) {
+        uint32_t lo = 0, hi = nY;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (__ldg(prefix + mid) <= u) lo = mid; else hi = mid;
+        }
+        const uint32_t Y = lo;
+        const uint32_t lines = 1u << __popc(Y);
+        const uint32_t chunks = (lines + K - 1) / K;
+        const uint64_t rem = u - __ldg(prefix + Y);
+        const uint32_t y_lo = (uint32_t)(rem / chunks);
+        const uint32_t j = (uint32_t)(rem - (uint64_t)y_lo * chunks);
+        const int64_t rowoff = ((int64_t)Y * TT + y_lo) * rowstride + lane * 4;
+        const uint32_t g = (uint32_t)(lane * 4 / 32);
+        const uint8_t* from = (((g * SC) & ~y_lo) == 0) ? dst : snap;
+        const uint32_t i0 = j * K;
+        const int cnt = (int)min((uint32_t)K, lines - i0);
+        uint32_t v[K], off[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            off[k] = pdep(i0 + k, Y) * 128u;
+            if (k < cnt) v[k] = __ldcs(reinterpret_cast<const unsigned int*>(from + rowoff + off[k]));
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+            if (k < cnt) *reinterpret_cast<uint32_t*>(out + rowoff + off[k]) = v[k];
+    }
+}
+
 std::mutex g_mu;
 std::map<std::pair<int, int>, uint64_t*> g_prefix;  // (device, nYbits*1024 + rows per block row) -> table
 
@@ -178,6 +221,39 @@ cudaError_t launch_c(const LaunchArgs& a, int r) {
 }
 
 }  // namespace
+
+template <int C>
+cudaError_t launch_copyback_c(void* out, const void* dst, const void* snap, int64_t n, int r, cudaStream_t s) {
+    constexpr int TT = 128 / C;
+    int k = 0;
+    while ((1 << k) < TT) ++k;
+    uint32_t nY;
+    uint64_t* pre = prefix_table(r - k, TT, nY);
+    if (!pre) return cudaErrorMemoryAllocation;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    host_rows_copyback<C><<<sms * 8, 256, 0, s>>>(reinterpret_cast<uint8_t*>(out),
+                                                  reinterpret_cast<const uint8_t*>(dst),
+                                                  reinterpret_cast<const uint8_t*>(snap), n, pre, nY);
+    note_launch();
+    return cudaGetLastError();
+}
+
+// Row-ordered write-back of the member tiles' own lines (1/2/4-byte cells, n >= one
+// 128-byte line, power of two); cudaErrorNotSupported otherwise.
+cudaError_t launch_host_rows_copyback(void* out, const void* dst, const void* snap, int64_t n, int cell_bytes,
+                                      cudaStream_t s) {
+    if (n < 1 || (n & (n - 1)) != 0) return cudaErrorNotSupported;
+    int r = 0;
+    while ((int64_t(1) << r) < n) ++r;
+    switch (cell_bytes) {
+    case 1: if (n >= 128) return launch_copyback_c<1>(out, dst, snap, n, r, s); break;
+    case 2: if (n >= 64) return launch_copyback_c<2>(out, dst, snap, n, r, s); break;
+    case 4: if (n >= 32) return launch_copyback_c<4>(out, dst, snap, n, r, s); break;
+    }
+    return cudaErrorNotSupported;
+}
 
 // CONST write pass on a grid at least one 128-byte line wide with 1/2/4-byte cells.
 cudaError_t launch_host_rows(const LaunchArgs& a) {

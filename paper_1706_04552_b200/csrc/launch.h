@@ -69,6 +69,8 @@ cudaError_t launch_stencil_tb2(const LaunchArgs& a);
 cudaError_t launch_stencil_tb(const LaunchArgs& a, int steps);  // steps = 2, 4 or 6
 cudaError_t launch_snapshot_stencil(void* snap, const void* grid, int64_t n, int cell_bytes, cudaStream_t s);
 cudaError_t launch_writeback_tiles(void* out, const void* dst, const void* snap, int64_t n, int cell_bytes, cudaStream_t s);
+cudaError_t launch_host_rows_copyback(void* out, const void* dst, const void* snap, int64_t n, int cell_bytes,
+                                      cudaStream_t s);
 // member tiles of a level-q gasket, row-major inside each level-L sub-gasket (stencil2.cu)
 const uint32_t* rowmajor_table(int q, int L);
 void rowmajor_order_host(int q, int L, std::vector<uint32_t>& v);
