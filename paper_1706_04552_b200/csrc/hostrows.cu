@@ -177,21 +177,82 @@ __global__ void __launch_bounds__(256) host_rows_copyback(uint8_t* __restrict__ 
     }
 }
 
+// MODE 0 with 16-byte lanes: 8 lanes per line, 4 lines per warp instruction, KL lines of
+// a row per unit -- twice the lines in flight per warp for the same registers
+constexpr int KL = 128;
+template <int C>
+__global__ void __launch_bounds__(256) host_rows_write16(uint8_t* __restrict__ grid, int64_t n,
+                                                         const uint64_t* __restrict__ prefix, uint32_t nY,
+                                                         uint64_t param) {
+    constexpr int TT = 128 / C;
+    constexpr int PER = KL / 4;  // lines per lane per unit
+    const int lane = threadIdx.x & 31;
+    const int sub = lane >> 3, q = lane & 7;  // line of the group of 4, 16-byte chunk of the line
+    const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t total = prefix[nY];
+    const uint32_t pv = splat4<C>(param);
+    const int64_t rowstride = n * C;
+    for (uint64_t u = warp0; u < total; u += nwarps) {
+        uint32_t lo = 0, hi = nY;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (__ldg(prefix + mid) <= u) lo = mid; else hi = mid;
+        }
+        const uint32_t Y = lo;
+        const uint32_t lines = 1u << __popc(Y);
+        const uint32_t chunks = (lines + KL - 1) / KL;
+        const uint64_t rem = u - __ldg(prefix + Y);
+        const uint32_t y_lo = (uint32_t)(rem / chunks);
+        const uint32_t j = (uint32_t)(rem - (uint64_t)y_lo * chunks);
+        uint8_t* row = grid + ((int64_t)Y * TT + y_lo) * rowstride + q * 16;
+        const uint32_t i0 = j * KL;
+        const int cnt = (int)min((uint32_t)KL, lines - i0);
+        // this lane's 4 words (cells 4q*V/4 ..) and its 64-byte half (the PCIe read unit)
+        uint32_t m[4];
+        bool full = true;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            m[w] = word_mask<C>(4 * q + w, y_lo);
+            full = full && m[w] == 0xffffffffu;
+        }
+        const bool half_touched = (((uint32_t)(q >> 2) * (64 / C)) & ~y_lo) == 0;
+        const bool do_load = half_touched && !full;
+        uint4 old[PER];
+        uint32_t off[PER];
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int k = 4 * i + sub;
+            off[i] = pdep(i0 + k, Y) * 128u;
+            old[i] = make_uint4(0, 0, 0, 0);
+            if (k < cnt && do_load) old[i] = __ldcv(reinterpret_cast<const uint4*>(row + off[i]));
+        }
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int k = 4 * i + sub;
+            if (k < cnt && half_touched)
+                *reinterpret_cast<uint4*>(row + off[i]) =
+                    make_uint4((pv & m[0]) | (old[i].x & ~m[0]), (pv & m[1]) | (old[i].y & ~m[1]),
+                               (pv & m[2]) | (old[i].z & ~m[2]), (pv & m[3]) | (old[i].w & ~m[3]));
+        }
+    }
+}
+
 std::mutex g_mu;
 std::map<std::pair<int, int>, uint64_t*> g_prefix;  // (device, nYbits*1024 + rows per block row) -> table
 
-uint64_t* prefix_table(int nYbits, int rows, uint32_t& nY) {
+uint64_t* prefix_table(int nYbits, int rows, uint32_t& nY, int kl = K) {
     nY = 1u << nYbits;
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lk(g_mu);
-    const int key = nYbits * 1024 + rows;
+    const int key = (kl * 64 + nYbits) * 1024 + rows;
     auto it = g_prefix.find({dev, key});
     if (it != g_prefix.end()) return it->second;
     std::vector<uint64_t> pre(nY + 1, 0);
     for (uint32_t Y = 0; Y < nY; ++Y) {
         const uint64_t lines = 1ull << __builtin_popcount(Y);
-        pre[Y + 1] = pre[Y] + (uint64_t)((lines + K - 1) / K) * rows;  // rows per block row = tile edge
+        pre[Y + 1] = pre[Y] + (uint64_t)((lines + kl - 1) / kl) * rows;  // rows per block row = tile edge
     }
     uint64_t* d = nullptr;
     if (cudaMalloc(&d, pre.size() * sizeof(uint64_t)) != cudaSuccess) return nullptr;
@@ -213,7 +274,12 @@ cudaError_t launch_c(const LaunchArgs& a, int r) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     uint8_t* g = reinterpret_cast<uint8_t*>(a.grid);
-    if (mode == 0) host_rows_write<C, 0><<<sms * 8, 256, 0, a.stream>>>(g, a.n, r, pre, nY, a.param);
+    if (mode == 0) {
+        uint32_t nY16;
+        uint64_t* pre16 = prefix_table(r - k, TT, nY16, KL);
+        if (!pre16) return cudaErrorMemoryAllocation;
+        host_rows_write16<C><<<sms * 8, 256, 0, a.stream>>>(g, a.n, pre16, nY16, a.param);
+    }
     else if (mode == 1) host_rows_write<C, 1><<<sms * 8, 256, 0, a.stream>>>(g, a.n, r, pre, nY, a.param);
     else host_rows_write<C, 2><<<sms * 8, 256, 0, a.stream>>>(g, a.n, r, pre, nY, a.param);
     note_launch();
