@@ -814,7 +814,7 @@ def main() -> None:
                          "alone (compute-only bound of an N-GPU step; 'projection' in the line)")
     ap.add_argument("--halo", choices=("collective", "peer", "peer-fused"), default="collective",
                     help="part* workloads, N>1: NCCL all_gather of the halo cells, peer-memory puts (CUDA IPC), "
-                         "or the peer exchange fused into the step kernel (temporal 1)")
+                         "or the peer exchange fused into the step kernel (any --temporal)")
     ap.add_argument("--r-min", type=int, default=8)
     ap.add_argument("--r-max", type=int, default=18)
     ap.add_argument("--nsweep-out", default="profiles/r1_nsweep.csv")
