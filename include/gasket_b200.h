@@ -81,6 +81,11 @@ extern "C" {
 #define GM_FLAG_TWO_STEPS 8388608     /* gm_run_part_peer: two fused CA steps per launch (depth-2 halo) */
 #define GM_FLAG_FOUR_STEPS 16777216   /* gm_run_part_peer: four fused CA steps per launch (depth-4 halo) */
 #define GM_FLAG_SIX_STEPS 33554432    /* gm_run_part_peer: six fused CA steps per launch (depth-6 halo) */
+#define GM_FLAG_ZERO_BACKGROUND 67108864 /* tuned write pass, opt-in: the caller asserts every off-gasket cell is 0
+                                            (PAPER.md:442-443's zero-filled matrix); touched 32-byte sectors are
+                                            stored whole (gasket cells = param, the rest 0), no DRAM read-modify-write */
+#define GM_FLAG_GRID_ROWS 536870912   /* tuned write pass: no blocks -- one warp per grid row, its member lines
+                                         left to right (the row enumeration; write.cu) */
 
 #define GM_OK 0
 #define GM_EINVAL 1  /* bad shape / size / tag (the reference's ValueError) */

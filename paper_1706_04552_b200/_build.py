@@ -13,7 +13,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libgasket_b200.so"
-SOURCES = ["literal.cu", "tuned.cu", "stream.cu", "stencil.cu", "stencil2.cu", "stencil_tb.cu", "stencil_tma.cu", "hostrows.cu", "maps.cu", "capi.cu", "part.cu", "peer.cu", "snapshot.cu"]
+SOURCES = ["literal.cu", "tuned.cu", "stream.cu", "write.cu", "stencil.cu", "stencil2.cu", "stencil_tb.cu", "stencil_tma.cu", "hostrows.cu", "maps.cu", "capi.cu", "peer.cu", "snapshot.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
               "--expt-relaxed-constexpr"]
@@ -24,19 +24,6 @@ def _nvcc() -> str:
     if not Path(cand).exists():
         raise RuntimeError("nvcc not found: cannot build the sm_100a library")
     return cand
-
-
-def _nccl_paths() -> tuple[str | None, str | None]:
-    try:
-        import nvidia.nccl as m  # type: ignore
-
-        root = Path(list(m.__path__)[0])
-        inc, lib = root / "include", root / "lib"
-        if (inc / "nccl.h").exists() and (lib / "libnccl.so.2").exists():
-            return str(inc), str(lib)
-    except Exception:
-        pass
-    return None, None
 
 
 def sources() -> list[Path]:
@@ -57,12 +44,8 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     nvcc = _nvcc()
     obj_dir = LIB_DIR / "obj"
     obj_dir.mkdir(parents=True, exist_ok=True)
-    inc_nccl, lib_nccl = _nccl_paths()
     extra_inc = ["-I", str(PKG.parent / "include")]
-    defines = []
-    if inc_nccl:
-        extra_inc += ["-I", inc_nccl]
-        defines += ["-DGM_HAVE_NCCL=1"]
+    defines: list[str] = []
 
     def compile_one(src: Path) -> Path:
         obj = obj_dir / (src.stem + ".o")
@@ -79,8 +62,6 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         objs = list(ex.map(compile_one, sources()))
     link = [nvcc, *ARCH, "-shared", "-o", str(LIB), *map(str, objs)]
-    if lib_nccl:
-        link += [f"-L{lib_nccl}", "-l:libnccl.so.2", "-Xlinker", f"-rpath={lib_nccl}"]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -227,14 +227,27 @@ def run_bounding_box(grid, src, rho: int, kind: int, param: int, backend: str = 
 
 def run_block_space(grid, src, rho: int, r_b: int, strategy, local_x: Optional[np.ndarray] = None,
                     local_y: Optional[np.ndarray] = None, kind: int = KERNEL_CONST, param: int = 1,
-                    backend: str = BACKEND, *, flags: int = 0) -> None:
+                    backend: str = BACKEND, *, flags: int = 0, assume_zero_background: bool = False) -> None:
     """backends.py:234-272: lambda over the packed rectangle of level r_b, then the
     intra-block strategy.  ``local_x/local_y`` are the TABLE lookup table
-    (ignored by the other strategies, as in the numba leg)."""
+    (ignored by the other strategies, as in the numba leg).
+
+    ``assume_zero_background`` (tuned constant write pass only, off by default): the
+    caller asserts that every off-gasket cell of ``grid`` is 0 -- the paper's
+    zero-filled matrix and the reference bench's ``make_grid``
+    zeros re-written in place (engine.py:88-90, bench.py:145-150).  The kernel then
+    stores every touched 32-byte sector whole (gasket cells = param, the rest 0),
+    which leaves the same grid without the DRAM read-modify-write of partial
+    sectors.  On a grid with a nonzero background the off-gasket cells of touched
+    sectors would be zeroed, so it is never implied."""
     resolve_backend(backend)
     tag = _strategy_tag(strategy)
     p = _param32(param)
     kind = int(kind)
+    if assume_zero_background:
+        if kind != KERNEL_CONST or tag != STRAT_TUNED:
+            raise ValueError("assume_zero_background applies to the tuned constant write pass only")
+        flags = int(flags) | native.FLAG_ZERO_BACKGROUND
     packing_dims(int(r_b))  # level range check
     tx = ty = 0
     ntab = 0

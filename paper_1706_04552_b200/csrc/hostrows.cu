@@ -183,7 +183,7 @@ constexpr int KL = 128;
 template <int C>
 __global__ void __launch_bounds__(256) host_rows_write16(uint8_t* __restrict__ grid, int64_t n,
                                                          const uint64_t* __restrict__ prefix, uint32_t nY,
-                                                         uint64_t param) {
+                                                         uint64_t param, int zero_bg) {
     constexpr int TT = 128 / C;
     constexpr int PER = KL / 4;  // lines per lane per unit
     const int lane = threadIdx.x & 31;
@@ -217,7 +217,8 @@ __global__ void __launch_bounds__(256) host_rows_write16(uint8_t* __restrict__ g
             full = full && m[w] == 0xffffffffu;
         }
         const bool half_touched = (((uint32_t)(q >> 2) * (64 / C)) & ~y_lo) == 0;
-        const bool do_load = half_touched && !full;
+        // GM_FLAG_ZERO_BACKGROUND: the off-gasket cells are 0, nothing to read back
+        const bool do_load = half_touched && !full && !zero_bg;
         uint4 old[PER];
         uint32_t off[PER];
 #pragma unroll
@@ -278,7 +279,8 @@ cudaError_t launch_c(const LaunchArgs& a, int r) {
         uint32_t nY16;
         uint64_t* pre16 = prefix_table(r - k, TT, nY16, KL);
         if (!pre16) return cudaErrorMemoryAllocation;
-        host_rows_write16<C><<<sms * 8, 256, 0, a.stream>>>(g, a.n, pre16, nY16, a.param);
+        host_rows_write16<C><<<sms * 8, 256, 0, a.stream>>>(g, a.n, pre16, nY16, a.param,
+                                                            (a.flags & GM_FLAG_ZERO_BACKGROUND) ? 1 : 0);
     }
     else if (mode == 1) host_rows_write<C, 1><<<sms * 8, 256, 0, a.stream>>>(g, a.n, r, pre, nY, a.param);
     else host_rows_write<C, 2><<<sms * 8, 256, 0, a.stream>>>(g, a.n, r, pre, nY, a.param);

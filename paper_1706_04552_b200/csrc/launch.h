@@ -61,6 +61,7 @@ int order_level(const LaunchArgs& a, int r_t);
 cudaError_t launch_literal(const LaunchArgs& a);
 cudaError_t launch_tuned(const LaunchArgs& a);
 cudaError_t launch_stream(const LaunchArgs& a);
+cudaError_t launch_write(const LaunchArgs& a);
 cudaError_t launch_stencil_tile(const LaunchArgs& a);
 cudaError_t launch_host_rows(const LaunchArgs& a);
 cudaError_t launch_stencil_tma(const LaunchArgs& a);

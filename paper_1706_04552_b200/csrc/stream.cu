@@ -1,4 +1,7 @@
-// stream.cu -- the B200 lambda kernel (strategy STRAT_TUNED, n*C >= 128 bytes).
+// stream.cu -- warp-per-tile-band lambda kernel (strategy STRAT_TUNED, n*C >= 128 bytes):
+// since round 2 only the paths the dedicated kernels do not take -- GM_FLAG_OMEGA_ORDER
+// launches (b = wy*W + wx order, every kind) and neighbour sums on 8-byte cells.  The
+// write pass and the coverage audit run in write.cu, neighbour sums in stencil2.cu.
 //
 // Decomposition.  lambda maps the compact tile index onto tiles of TT x TT
 // cells whose rows are exactly one 128-byte line (TT = 32 * WB / C, WB = 4-byte
@@ -9,9 +12,7 @@
 // over the warps, so the warps running together store the same rows of
 // horizontally neighbouring tiles (shared DRAM pages: 118 -> 104 us at n=2^16
 // against the lambda digit order, GM_FLAG_DIGIT_ORDER, which hands each warp a
-// contiguous run of units instead).  This kernel is the CONST write pass; the
-// neighbour sums run in stencil2.cu, and this file's stencil path serves only
-// GM_FLAG_OMEGA_ORDER launches (b = wy*W + wx order); KIND_COUNT is the coverage audit.
+// contiguous run of units instead).
 //
 // DRAM-traffic rules (measured with scripts/probe_partial.cu: a partial
 // 32-byte-sector write costs a full-sector DRAM read-modify-write):
@@ -97,36 +98,6 @@ __device__ __forceinline__ W shfl_dn1(W v) {
     }
 }
 
-// Loads with the .L2::64B fetch-size hint: an L2 miss brings in the 64-byte half
-// holding the word instead of the whole 128-byte line (scripts/probe_fetch.cu).
-template <class W>
-__device__ __forceinline__ W ld_half(const void* p) {
-    if constexpr (sizeof(W) == 8) {
-        uint64_t v;
-        asm volatile("ld.global.cg.L2::64B.u64 %0, [%1];" : "=l"(v) : "l"(p));
-        return v;
-    } else {
-        uint32_t v;
-        asm volatile("ld.global.cg.L2::64B.u32 %0, [%1];" : "=r"(v) : "l"(p));
-        return v;
-    }
-}
-__device__ __forceinline__ void touch_line(const void* p) {
-    uint32_t v;
-    asm volatile("ld.global.cg.L2::128B.u32 %0, [%1];" : "=r"(v) : "l"(p));
-}
-template <class W>
-__device__ __forceinline__ W ld_line(const void* p) {
-    return *reinterpret_cast<const volatile W*>(p);
-}
-
-// Plain store, or (GM_FLAG_STORE_CS) a streaming / evict-first store.
-template <class T>
-__device__ __forceinline__ void st_cell(void* p, T v, bool cs) {
-    if (cs) __stcs(reinterpret_cast<T*>(p), v);
-    else *reinterpret_cast<T*>(p) = v;
-}
-
 // Left / right neighbour cells of every cell of the word.
 template <int C>
 __device__ __forceinline__ typename WordT<C>::T left_of(typename WordT<C>::T prev, typename WordT<C>::T cur) {
@@ -204,22 +175,9 @@ __global__ void __launch_bounds__(256) lambda_stream(uint8_t* __restrict__ grid,
     uint32_t cur_tile = 0xffffffffu;
     int64_t x0 = 0, y0 = 0;
     int prev_t0 = -BAND;
-    // GM_FLAG_BAND_MAJOR (with a tile order table): unit = band * ntiles + tile, so the
-    // warps running together store the same rows of neighbouring tiles (DRAM pages)
-    const bool band_major = interleave && (flags & GM_FLAG_BAND_MAJOR) != 0;
-    const uint64_t ntl = (uint64_t)(tile_hi - tile_lo);
     for (uint64_t u = u_begin; u < u_end; u += u_step) {
-        uint32_t tile;
-        int t0;
-        if (band_major) {
-            const uint64_t v = u - u_lo;
-            const uint64_t b = v / ntl;
-            tile = tile_lo + (uint32_t)(v - b * ntl);
-            t0 = (int)b * BAND;
-        } else {
-            tile = (uint32_t)(u >> band_shift);
-            t0 = (int)(u & ((1u << band_shift) - 1u)) * BAND;
-        }
+        const uint32_t tile = (uint32_t)(u >> band_shift);
+        const int t0 = (int)(u & ((1u << band_shift) - 1u)) * BAND;
         const bool same_tile = tile == cur_tile;
         if (!same_tile) {
             uint32_t bx, by;
@@ -239,27 +197,6 @@ __global__ void __launch_bounds__(256) lambda_stream(uint8_t* __restrict__ grid,
         }
         uint8_t* drow = grid + (y0 + t0) * rowstride + x0 * C + lane * G::WB;
 
-        if constexpr (KIND == KIND_CONST) {
-            // GM_FLAG_PREFETCH_AHEAD (interleaved order): pull the lines this warp stores
-            // PF units from now into L2, so the partial-sector stores merge into resident
-            // sectors instead of each waiting for its own read-modify-write fill
-            if (interleave && (flags & GM_FLAG_PREFETCH_AHEAD)) {
-                constexpr int PF = 2;
-                const uint64_t uf = u + PF * u_step;
-                if (uf < u_end) {
-                    const uint32_t ftile = (uint32_t)(uf >> band_shift);
-                    const int ft0 = (int)(uf & ((1u << band_shift) - 1u)) * BAND;
-                    const uint32_t v = __ldg(order + ftile);
-                    const uint8_t* frow = grid + ((int64_t)(v >> 16) * G::TT + ft0) * rowstride +
-                                          (int64_t)(v & 0xffffu) * G::TT * C + lane * G::WB;
-#pragma unroll
-                    for (int i = 0; i < BAND; ++i)
-                        if ((c0 & ~(ft0 + i)) == 0)
-                            asm volatile("prefetch.global.L2 [%0];" ::"l"(frow + (int64_t)i * rowstride));
-                }
-            }
-        }
-
         if constexpr (KIND == KIND_COUNT) {
 #pragma unroll
             for (int i = 0; i < BAND; ++i) {
@@ -267,45 +204,6 @@ __global__ void __launch_bounds__(256) lambda_stream(uint8_t* __restrict__ grid,
                 if ((c0 & ~(t0 + i)) == 0) atomicAdd(reinterpret_cast<unsigned int*>(drow + (int64_t)i * rowstride), 1u);
             }
         } else if constexpr (KIND == KIND_CONST) {
-            if (flags & GM_FLAG_EXPLICIT_RMW) {
-                // whole-sector writes: load the partial touched sectors first (all rows of
-                // the band in flight), blend the gasket cells in, store every touched sector
-                // GM_FLAG_WHOLE_LINES (host-mapped grids): move whole 128-byte rows -- PCIe
-                // reads come in 64-byte units and small writes are TLP-rate bound
-                const bool lines = (flags & GM_FLAG_WHOLE_LINES) != 0;
-                WT old[BAND];
-#pragma unroll
-                for (int i = 0; i < BAND; ++i) {
-                    const int t = t0 + i;
-                    const bool full = ((g * G::SC + G::SC - 1) & ~t) == 0;
-                    const uint8_t* p = drow + (int64_t)i * rowstride;
-                    old[i] = ((sec_touched<C>(t, g) || lines) && !full)
-                                 ? ((flags & GM_FLAG_FETCH_LINE) ? ld_line<WT>(p) : ld_half<WT>(p))
-                                 : WT(0);
-                }
-#pragma unroll
-                for (int i = 0; i < BAND; ++i) {
-                    const int t = t0 + i;
-                    if (sec_touched<C>(t, g) || lines) {
-                        const WT m = (c0 & ~t) == 0 ? cell_mask<C>((uint32_t)t) : WT(0);
-                        *reinterpret_cast<WT*>(drow + (int64_t)i * rowstride) = (pv & m) | (old[i] & ~m);
-                    }
-                }
-            } else {
-            if (flags & GM_FLAG_FETCH64) {
-                // bring the touched 64-byte halves into L2 with plain reads first, so the
-                // partial stores below merge into valid sectors instead of each forcing
-                // its own DRAM read-modify-write fill
-#pragma unroll
-                for (int i = 0; i < BAND; ++i)
-                    if ((c0 & ~(t0 + i)) == 0) {  // asm volatile: kept
-                        if (flags & GM_FLAG_FETCH_LINE) {
-                            if (lane == 0) touch_line(drow - lane * G::WB + (int64_t)i * rowstride);
-                        } else {
-                            (void)ld_half<WT>(drow + (int64_t)i * rowstride);
-                        }
-                    }
-            }
             // rows come in groups of V (t0 is a multiple of V): within a group the word's
             // touched flag is constant and slot j's cell pattern is j (cells k subset of j)
 #pragma unroll
@@ -313,21 +211,19 @@ __global__ void __launch_bounds__(256) lambda_stream(uint8_t* __restrict__ grid,
                 const int tq = t0 + q * G::V;
                 if ((c0 & ~tq) == 0) {
                     uint8_t* p = drow + (int64_t)(q * G::V) * rowstride;
-                    const bool cs = (flags & GM_FLAG_STORE_CS) != 0;
                     if constexpr (G::V == 1) {
-                        st_cell<WT>(p, pv, cs);
+                        *reinterpret_cast<WT*>(p) = pv;
                     } else if constexpr (G::V == 2) {
-                        st_cell<uint16_t>(p, (uint16_t)pv, cs);
-                        st_cell<uint32_t>(p + rowstride, pv, cs);
+                        *reinterpret_cast<uint16_t*>(p) = (uint16_t)pv;
+                        *reinterpret_cast<uint32_t*>(p + rowstride) = (uint32_t)pv;
                     } else {
-                        st_cell<uint8_t>(p, (uint8_t)pv, cs);
-                        st_cell<uint16_t>(p + rowstride, (uint16_t)pv, cs);
-                        st_cell<uint8_t>(p + 2 * rowstride, (uint8_t)pv, cs);
-                        st_cell<uint8_t>(p + 2 * rowstride + 2, (uint8_t)pv, cs);
-                        st_cell<uint32_t>(p + 3 * rowstride, pv, cs);
+                        p[0] = (uint8_t)pv;
+                        *reinterpret_cast<uint16_t*>(p + rowstride) = (uint16_t)pv;
+                        p[2 * rowstride] = (uint8_t)pv;
+                        p[2 * rowstride + 2] = (uint8_t)pv;
+                        *reinterpret_cast<uint32_t*>(p + 3 * rowstride) = (uint32_t)pv;
                     }
                 }
-            }
             }
         } else {
             // ---- rows t0-1 .. t0+BAND (only sectors some neighbourhood needs); the two

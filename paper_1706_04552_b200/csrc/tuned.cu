@@ -280,6 +280,12 @@ cudaError_t launch_tuned(const LaunchArgs& a) {
         if (es != cudaErrorNotSupported) return es;
         cudaGetLastError();
     }
+    // the write pass: line-tile slabs, unit -> tile computed per unit (write.cu)
+    if (a.kind == KIND_CONST || a.kind == KIND_COUNT) {
+        const cudaError_t ew = launch_write(a);
+        if (ew != cudaErrorNotSupported) return ew;
+        cudaGetLastError();
+    }
     // otherwise the warp-per-tile-band kernel (stream.cu)
     const cudaError_t e = launch_stream(a);
     if (e != cudaErrorNotSupported) return e;

@@ -31,6 +31,7 @@ FLAG_PREFETCH_AHEAD, FLAG_FETCH_MIXED, FLAG_FETCH_HALF, FLAG_FETCH256 = 524288, 
 FLAG_TWO_STEPS = 8388608
 FLAG_FOUR_STEPS = 16777216
 FLAG_SIX_STEPS = 33554432
+FLAG_ZERO_BACKGROUND, FLAG_GRID_ROWS = 67108864, 536870912
 
 
 class GmCfg(ctypes.Structure):
