@@ -84,6 +84,8 @@ extern "C" {
 #define GM_FLAG_ZERO_BACKGROUND 67108864 /* tuned write pass, opt-in: the caller asserts every off-gasket cell is 0
                                             (PAPER.md:442-443's zero-filled matrix); touched 32-byte sectors are
                                             stored whole (gasket cells = param, the rest 0), no DRAM read-modify-write */
+#define GM_FLAG_WRITE_HALVES 134217728 /* zero-background write pass: store the touched 64-byte halves whole */
+#define GM_FLAG_WRITE_LINES 268435456  /* zero-background write pass: store the touched 128-byte lines whole */
 #define GM_FLAG_GRID_ROWS 536870912   /* tuned write pass: no blocks -- one warp per grid row, its member lines
                                          left to right (the row enumeration; write.cu) */
 

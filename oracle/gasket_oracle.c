@@ -302,3 +302,116 @@ void go_coverage_blocks(const int64_t* bx, const int64_t* by, int64_t nblocks, c
             if (x >= 0 && x < n && y >= 0 && y < n) counts[y * n + x] += 1;
         }
 }
+
+/* ------------------------------------------------------------------------ */
+/* Row bands of a multi-step CA run at sizes the full-grid oracle cannot     */
+/* hold (n = 2^17 int8 is 16 GiB per grid, 2^18 is 64 GiB).                  */
+/*                                                                          */
+/* Same arithmetic as bb_* / bs_* above: every step is one NEIGHBOR_SUM      */
+/* launch with engine.launch's snapshot semantics (engine.py:201, src = the  */
+/* pre-launch grid): each gasket cell x & (n-1-y) == 0 (backends.py:155-156) */
+/* gets _cell_value (backends.py:127-141) of the previous state, off-gasket  */
+/* cells never change.  Only the cell order differs (rows, the x that are    */
+/* bit-subsets of y ascending)   ; writes are disjoint, so order is moot.   */
+/*                                                                          */
+/* The input is the synthetic grid go_fill_hash(seed, mode) builds.  Rows     */
+/* [y0, y1) after s steps depend on rows [y0-s, y1+s) of the input, so the    */
+/* window is filled with `smax` extra rows on each side (clipped to the      */
+/* grid, where out-of-grid = 0 is exact); cells next to a window edge that    */
+/* is not a grid edge go stale one row per step and never reach the band.    */
+/* outs[i] receives rows [y0, y1) after steps[i] steps (0 = the input).      */
+/* ------------------------------------------------------------------------ */
+
+static void fill_rows(void* buf, int64_t n, int cell_bytes, uint64_t seed, int mode, int64_t w0, int64_t w1,
+                      int threads) {
+#pragma omp parallel for num_threads(nthr(threads)) schedule(static)
+    for (int64_t y = w0; y < w1; ++y) {
+        int64_t m = n - 1 - y;
+        for (int64_t x = 0; x < n; ++x) {
+            uint64_t v = splitmix64(seed ^ (((uint64_t)y << 32) | (uint64_t)x));
+            if (mode == 1 && (x & m) != 0) v = 0;
+            int64_t i = (y - w0) * n + x;
+            switch (cell_bytes) {
+            case 1: ((uint8_t*)buf)[i] = (uint8_t)v; break;
+            case 2: ((uint16_t*)buf)[i] = (uint16_t)v; break;
+            case 4: ((uint32_t*)buf)[i] = (uint32_t)v; break;
+            default: ((uint64_t*)buf)[i] = v; break;
+            }
+        }
+    }
+}
+
+#define DEFINE_BAND_STEP(T, SUF)                                                            \
+static void band_step_##SUF(T* dst, const T* src, int64_t n, int64_t w0, int64_t w1,       \
+                            int kind, int32_t param, int threads) {                        \
+    _Pragma("omp parallel for num_threads(nthr(threads)) schedule(dynamic, 16)")           \
+    for (int64_t y = w0; y < w1; ++y) {                                                    \
+        const T* r0 = src + (y - w0) * n;                                                  \
+        const T* rp = (y > w0) ? r0 - n : 0;          /* row y-1 (absent: grid or window edge) */ \
+        const T* rn = (y + 1 < w1) ? r0 + n : 0;      /* row y+1 */                        \
+        T* out = dst + (y - w0) * n;                                                       \
+        const int64_t m = y;   /* x & (n-1-y) == 0  <=>  x is a bit-subset of y */         \
+        int64_t x = 0;                                                                     \
+        if (kind == KIND_CONST) {                       /* the write pass: param */        \
+            do { out[x] = (T)(int64_t)param; x = (x - m) & m; } while (x != 0);            \
+            continue;                                                                      \
+        }                                                                                  \
+        do {                                                                               \
+            uint64_t t = (uint64_t)(int64_t)param;                                         \
+            if (x > 0) t += (uint64_t)(int64_t)r0[x - 1];                                  \
+            if (x < n - 1) t += (uint64_t)(int64_t)r0[x + 1];                              \
+            if (rp) t += (uint64_t)(int64_t)rp[x];                                         \
+            if (rn) t += (uint64_t)(int64_t)rn[x];                                         \
+            if (kind == KIND_NSUM8) {                                                      \
+                if (rp && x > 0) t += (uint64_t)(int64_t)rp[x - 1];                        \
+                if (rp && x < n - 1) t += (uint64_t)(int64_t)rp[x + 1];                    \
+                if (rn && x > 0) t += (uint64_t)(int64_t)rn[x - 1];                        \
+                if (rn && x < n - 1) t += (uint64_t)(int64_t)rn[x + 1];                    \
+            }                                                                              \
+            out[x] = (T)t;                                                                 \
+            x = (x - m) & m;                                                               \
+        } while (x != 0);                                                                  \
+    }                                                                                      \
+}
+
+DEFINE_BAND_STEP(int8_t, i8)
+DEFINE_BAND_STEP(int16_t, i16)
+DEFINE_BAND_STEP(int32_t, i32)
+DEFINE_BAND_STEP(int64_t, i64)
+
+int go_steps_band(void* const* outs, const int32_t* steps, int nouts, int64_t n, int cell_bytes, uint64_t seed,
+                  int mode, int kind, int32_t param, int64_t y0, int64_t y1, int threads) {
+    if (kind != KIND_CONST && kind != KIND_NSUM4 && kind != KIND_NSUM8) return -1;
+    if (y0 < 0 || y1 > n || y0 >= y1 || nouts < 1) return -1;
+    int smax = 0;
+    for (int i = 0; i < nouts; ++i) {
+        if (steps[i] < 0) return -1;
+        if (steps[i] > smax) smax = steps[i];
+    }
+    const int64_t w0 = y0 - smax < 0 ? 0 : y0 - smax, w1 = y1 + smax > n ? n : y1 + smax;
+    const size_t bytes = (size_t)(w1 - w0) * (size_t)n * (size_t)cell_bytes;
+    char* a = (char*)malloc(bytes);
+    char* b = (char*)malloc(bytes);
+    if (!a || !b) { free(a); free(b); return -2; }
+    fill_rows(a, n, cell_bytes, seed, mode, w0, w1, threads);
+    memcpy(b, a, bytes);  /* off-gasket cells: identical in both ping-pong buffers for ever */
+    const size_t off = (size_t)(y0 - w0) * (size_t)n * (size_t)cell_bytes;
+    const size_t len = (size_t)(y1 - y0) * (size_t)n * (size_t)cell_bytes;
+    for (int s = 0; s <= smax; ++s) {
+        if (s > 0) {
+            switch (cell_bytes) {
+            case 1: band_step_i8((int8_t*)b, (const int8_t*)a, n, w0, w1, kind, param, threads); break;
+            case 2: band_step_i16((int16_t*)b, (const int16_t*)a, n, w0, w1, kind, param, threads); break;
+            case 4: band_step_i32((int32_t*)b, (const int32_t*)a, n, w0, w1, kind, param, threads); break;
+            case 8: band_step_i64((int64_t*)b, (const int64_t*)a, n, w0, w1, kind, param, threads); break;
+            default: free(a); free(b); return -1;
+            }
+            char* t = a; a = b; b = t;
+        }
+        for (int i = 0; i < nouts; ++i)
+            if (steps[i] == s) memcpy(outs[i], a + off, len);
+    }
+    free(a);
+    free(b);
+    return 0;
+}

@@ -66,6 +66,9 @@ def lib() -> ctypes.CDLL:
         L.go_run_block_space.restype = c_int
         L.go_fill_hash.argtypes = [vp, i64, c_int, ctypes.c_uint64, c_int, c_int]
         L.go_checksum.argtypes = [vp, i64, c_int, c_int]
+        L.go_steps_band.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(i32), c_int, i64, c_int, ctypes.c_uint64,
+                                    c_int, c_int, i32, i64, i64, c_int]
+        L.go_steps_band.restype = c_int
         L.go_checksum.restype = ctypes.c_uint64
         L.go_coverage_blocks.argtypes = [_i64p, _i64p, i64, _i64p, _i64p, i64, i64, i64, _i64p]
         _lib = L
@@ -200,6 +203,25 @@ def fill_hash(n: int, dtype, seed: int, mode: int = 0, threads: int = 0) -> np.n
     return a
 
 
+def steps_band(n: int, dtype, seed: int, mode: int, kind: int, param: int, y0: int, y1: int,
+               steps, threads: int = 0) -> list[np.ndarray]:
+    """Rows [y0, y1) of fill_hash(n, dtype, seed, mode) after each count in ``steps`` of
+    engine.launch NEIGHBOR_SUM steps (engine.py:201 snapshot semantics, _cell_value
+    backends.py:127-141 on the gasket cells, backends.py:155-156) -- the band restatement
+    in gasket_oracle.c, for grids too large to hold whole on the host."""
+    steps = [int(s) for s in steps]
+    outs = [np.empty((y1 - y0, n), dtype=dtype) for _ in steps]
+    ptrs = (ctypes.c_void_p * len(outs))(*[o.ctypes.data for o in outs])
+    st = (ctypes.c_int32 * len(steps))(*steps)
+    rc = lib().go_steps_band(ptrs, st, len(steps), n, np.dtype(dtype).itemsize, seed & (2**64 - 1), mode, kind,
+                             int(np.int32(param)), y0, y1, threads)
+    if rc == -2:
+        raise MemoryError("steps_band window")
+    if rc:
+        raise ValueError("steps_band: bad arguments")
+    return outs
+
+
 def checksum(a: np.ndarray, threads: int = 0) -> int:
     a = np.ascontiguousarray(a)
     return int(lib().go_checksum(a.ctypes.data, a.size, a.dtype.itemsize, threads))
@@ -241,5 +263,5 @@ __all__ = [
     "KIND_CONST", "KIND_NSUM4", "KIND_NSUM8", "STRAT_UNROLL", "STRAT_TABLE", "STRAT_SUBBOX",
     "build", "lib", "max_threads", "packing_dims", "member_mask", "enumerate_cells",
     "map_block_scalar", "local_cells", "map_blocks", "map_rectangle", "run_bounding_box",
-    "run_block_space", "fill_hash", "checksum", "coverage_counts", "nsum_reference_numpy",
+    "run_block_space", "fill_hash", "steps_band", "checksum", "coverage_counts", "nsum_reference_numpy",
 ]

@@ -97,6 +97,10 @@ def _device_table(local_x, local_y, rho: int) -> tuple[int, int, int]:
         if len(_table_cache) > 64:
             _table_cache.clear()
         _table_cache[key] = hit
+    # a table dropped from the cache later must outlive the launches that read it
+    cur = torch.cuda.current_stream()
+    hit[0].record_stream(cur)
+    hit[1].record_stream(cur)
     return int(hit[0].data_ptr()), int(hit[1].data_ptr()), int(lx.size)
 
 
@@ -165,7 +169,7 @@ def _run(grid: Any, src: Any, kind: int, launch, *, mapped_ok: bool) -> None:
         raise ValueError("grid is read-only")
     mode = device.host_transport()
     if (mode == "mapped" and mapped_ok and reads_src and _same_array(src, grid)
-            and device.tile_staging_ok(n, c)):
+            and device.staged_writeback_ok(n, c)):
         # engine.launch semantics on a host grid (src is the grid: its pre-launch snapshot):
         # stage only what the launch reads (the member tiles' windows) into the device,
         # run the tuned kernel there, write the tiles' own lines back whole -- the host

@@ -40,6 +40,7 @@
 //     sector is stored whole (gasket cells = param, the rest 0): the same final grid,
 //     no DRAM read.
 #include <algorithm>
+#include <cstdlib>
 
 #include "gasket.cuh"
 #include "launch.h"
@@ -93,6 +94,12 @@ __device__ __forceinline__ uint32_t splat_w(uint64_t p, int w) {
 
 __device__ __forceinline__ void st_v4(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
     asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
+__device__ __forceinline__ void st_v8(void* p, const uint32_t (&v)[8]) {
+    asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),
+                 "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
 }
 
 // The gasket cells of one lane word of a row with in-line pattern t (general mode):
@@ -195,7 +202,7 @@ __global__ void __launch_bounds__(256) gasket_write(uint8_t* __restrict__ grid, 
 // 16-byte lanes, 4 lines per instruction -- lane group g owns the lines whose index k
 // has low bits g: X = pdep(g, the two lowest bits of Y) | S, S over the subsets of Y's
 // other bits in increasing order.  General: 4-byte lanes, one line per instruction.
-template <int C, bool ZERO, bool COUNT = false>
+template <int C, bool ZERO, int GRAN, bool COUNT = false>
 __global__ void __launch_bounds__(256) gasket_write_rows(uint8_t* __restrict__ grid, int64_t n, uint64_t param) {
     using G = WGeo<C>;
     const int lane = threadIdx.x & 31;
@@ -216,12 +223,40 @@ __global__ void __launch_bounds__(256) gasket_write_rows(uint8_t* __restrict__ g
                 else st_members<C>(row + (int64_t)X * 128, v, t);
                 X = (X - Y) & Y;
             } while (X != 0);
+        } else if constexpr (GRAN == 3) {
+            // 32-byte lanes (one sector each, 256-bit stores): 8 lines per instruction
+            const int p = lane & 3;
+            const uint32_t g = (uint32_t)(lane >> 2);
+            const int lb = min(__popc(Y), 3);
+            if (g >= (1u << lb)) continue;
+            if (((uint32_t)p * (32u / C)) & ~t) continue;  // sector without gasket cells
+            uint32_t rem = Y, base = 0;
+            for (int i = 0; i < lb; ++i) {
+                const uint32_t b = rem & (0u - rem);
+                rem ^= b;
+                if ((g >> i) & 1u) base |= b;
+            }
+            uint32_t v[8];
+#pragma unroll
+            for (int w = 0; w < 8; ++w) v[w] = splat_w<C>(param, w) & word_mask<C>(2 * p + (w >> 2), w & 3, t);
+            uint8_t* row = grid + (int64_t)y * rowstride + p * 32;
+            uint32_t S = 0;
+            do {
+                st_v8(row + (int64_t)(base | S) * 128, v);
+                S = (S - rem) & rem;
+            } while (S != 0);
         } else {
             const int p = lane & 7;
             const uint32_t g = (uint32_t)(lane >> 3);
             const int pc = __popc(Y);
             if (g >= (1u << (pc < 2 ? pc : 2))) continue;
-            if ((((uint32_t)(p & ~1) * G::P16) & ~t) != 0) continue;  // sector without gasket cells
+            // store granularity: GRAN 0 = the touched 32-byte sectors, 1 = the touched
+            // 64-byte halves, 2 = whole lines (zeros included)
+            if constexpr (GRAN == 0) {
+                if ((((uint32_t)(p & ~1) * G::P16) & ~t) != 0) continue;
+            } else if constexpr (GRAN == 1) {
+                if ((((uint32_t)(p & ~3) * G::P16) & ~t) != 0) continue;
+            }
             const uint32_t b0 = Y & (0u - Y), Y1 = Y ^ b0, b1 = Y1 & (0u - Y1), Yh = Y1 ^ b1;
             const uint32_t base = ((g & 1u) ? b0 : 0u) | ((g & 2u) ? b1 : 0u);
             uint32_t v[4];
@@ -237,6 +272,14 @@ __global__ void __launch_bounds__(256) gasket_write_rows(uint8_t* __restrict__ g
     }
 }
 
+int rows_ctas_per_sm() {
+    static int v = [] {
+        const char* e = getenv("GASKET_WRITE_ROWS_CTAS");
+        return e ? atoi(e) : 8;
+    }();
+    return v;
+}
+
 int sm_count() {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -249,9 +292,16 @@ cudaError_t launch_c(const LaunchArgs& a, int q) {
     using G = WGeo<C>;
     if ((a.flags & GM_FLAG_GRID_ROWS) && a.part_level < 0) {
         // 8 CTAs of 256 threads per SM (the row walk wants many rows in flight)
-        const uint64_t blocks = std::min<uint64_t>((uint64_t)sm_count() * 8, ((uint64_t)a.n * 32 + 255) / 256);
-        gasket_write_rows<C, ZERO, COUNT><<<(unsigned)blocks, 256, 0, a.stream>>>(reinterpret_cast<uint8_t*>(a.grid), a.n,
-                                                                           a.param);
+        const uint64_t blocks = std::min<uint64_t>((uint64_t)sm_count() * rows_ctas_per_sm(), ((uint64_t)a.n * 32 + 255) / 256);
+        const int gran = (a.flags & GM_FLAG_WRITE_LINES) && (a.flags & GM_FLAG_WRITE_HALVES) ? 3
+                         : (a.flags & GM_FLAG_WRITE_LINES)                                ? 2
+                         : (a.flags & GM_FLAG_WRITE_HALVES)                               ? 1
+                                                                                          : 0;
+        auto* kr = !ZERO || gran == 0 ? gasket_write_rows<C, ZERO, 0, COUNT>
+                   : gran == 1        ? gasket_write_rows<C, ZERO, 1, COUNT>
+                   : gran == 2        ? gasket_write_rows<C, ZERO, 2, COUNT>
+                                      : gasket_write_rows<C, ZERO, 3, COUNT>;
+        kr<<<(unsigned)blocks, 256, 0, a.stream>>>(reinterpret_cast<uint8_t*>(a.grid), a.n, a.param);
         note_launch();
         return cudaGetLastError();
     }

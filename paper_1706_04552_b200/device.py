@@ -5,12 +5,12 @@ every computation is a call into libgasket_b200.so through ``native``.
 
 Host (numpy) arrays follow the reference's synchronous semantics: the call
 returns after the result is back in the caller's array.  Two host transports:
-  * "copy"   (default): H2D of the needed inputs into a cached device buffer,
-               kernel, D2H of the grid;
-  * "mapped": the numpy buffer is page-locked and mapped once
-               (cudaHostRegister, cached per buffer) and the kernel reads and
-               writes it in place over PCIe, so only the 16-byte row segments
-               the gasket touches cross the bus (tuned strategy only).
+  * "mapped" (default): the numpy buffer is page-locked and mapped once per
+               owning array (cudaHostRegister, ``pinned``) and the tuned kernels
+               read and write it in place over PCIe, so only the lines the gasket
+               touches cross the bus (tuned strategy; others use "copy");
+  * "copy":   H2D of the whole grid into a cached device buffer, kernel, D2H of
+               the whole grid.
 """
 
 from __future__ import annotations
@@ -129,6 +129,18 @@ def tile_staging_ok(n: int, c: int) -> bool:
     return bool(tt) and n >= tt and n & (n - 1) == 0 and n // tt <= 1 << 15
 
 
+def staged_writeback_ok(n: int, c: int) -> bool:
+    """Grids whose staged host neighbour-sum launch is exact: the snapshot and write-back
+    kernels cover them (tile_staging_ok) AND the tuned stencil that runs in between stores
+    whole 32-byte sectors (stencil v2 for 1/2/4-byte cells, the stream kernel for 8-byte
+    cells on grids of at least 256 bytes per row).  gm_writeback_tiles copies every
+    touched sector whole from the result, so a kernel that only stored the gasket cells
+    would leave unwritten scratch bytes in the off-gasket cells of those sectors."""
+    if not tile_staging_ok(n, c):
+        return False
+    return n * c >= 256 if c == 8 else True
+
+
 def stencil_snapshot(grid: torch.Tensor) -> torch.Tensor:
     """engine.launch's pre-launch copy of a neighbour-sum launch (engine.py:201), on the
     device and masked: only the cells a one-step stencil over the gasket reads are
@@ -137,7 +149,9 @@ def stencil_snapshot(grid: torch.Tensor) -> torch.Tensor:
     Grids the masked copy does not cover (narrower than one 128-byte tile) are copied
     whole, on the device."""
     n = int(grid.shape[0])
-    snap = scratch.get("snapshot", grid.numel(), grid.dtype, grid.device).view(n, n)
+    # one buffer per stream: launches queued on different streams must not share it
+    key = f"snapshot:{torch.cuda.current_stream(grid.device).cuda_stream}"
+    snap = scratch.get(key, grid.numel(), grid.dtype, grid.device).view(n, n)
     c = grid.element_size()
     if tile_staging_ok(n, c):
         native.call("gm_snapshot_stencil", snap.data_ptr(), grid.data_ptr(), n, c, stream_handle())
@@ -150,21 +164,130 @@ def stencil_snapshot(grid: torch.Tensor) -> torch.Tensor:
 # mapped (zero-copy) host buffers
 # ---------------------------------------------------------------------------
 
+def _root_array(a: np.ndarray) -> np.ndarray:
+    while isinstance(a.base, np.ndarray):
+        a = a.base
+    return a
+
+
+class _PinCache:
+    """Page-locked registrations of pageable numpy buffers, one per owning array.
+
+    The reference's callers re-run launches on the same ``make_grid`` array
+    (bench.py:145-150 re-runs ``plan.run(grid, grid)`` reps x inner times), so the
+    buffer that owns a pageable grid is registered (cudaHostRegister, mapped) on
+    its first use and stays registered until that array is garbage-collected
+    (``weakref.finalize``: numpy clears weak references before it frees the data),
+    or until the cache has to make room.  Every later call on the array or on a view
+    of it maps it for free.  Total pinned bytes are capped (``GASKET_HOST_PIN_CAP_GB``,
+    default half of physical memory); least recently used registrations are dropped
+    first, and a buffer that does not fit is registered for the one call only."""
+
+    def __init__(self) -> None:
+        self._lock = threading.Lock()
+        self._regs: dict[int, list] = {}  # root ptr -> [nbytes, last use tick, finalizer]
+        self._tick = 0
+
+    @staticmethod
+    def cap_bytes() -> int:
+        v = os.environ.get("GASKET_HOST_PIN_CAP_GB")
+        if v:
+            return int(float(v) * (1 << 30))
+        try:
+            return int(os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")) // 2
+        except (ValueError, OSError):
+            return 16 << 30
+
+    def _drop(self, ptr: int) -> None:
+        ent = self._regs.pop(ptr, None)
+        if ent is not None:
+            ent[2].detach()
+            _unregister(ptr)
+
+    def pin(self, a: np.ndarray) -> bool:
+        """Make sure the array owning ``a``'s memory is registered; False if it was not
+        cached (memory owned by a non-numpy object, or larger than the cap)."""
+        import weakref
+
+        root = _root_array(a)
+        if not root.flags.owndata:
+            return False
+        ptr, nbytes = int(root.ctypes.data), int(root.nbytes)
+        cap = self.cap_bytes()
+        with self._lock:
+            self._tick += 1
+            ent = self._regs.get(ptr)
+            if ent is not None and ent[0] == nbytes:
+                ent[1] = self._tick
+                return True
+            if ent is not None:
+                self._drop(ptr)
+            if nbytes > cap:
+                return False
+            used = sum(e[0] for e in self._regs.values())
+            for old in sorted(self._regs, key=lambda k: self._regs[k][1]):
+                if used + nbytes <= cap:
+                    break
+                used -= self._regs[old][0]
+                self._drop(old)
+            out = ctypes.c_void_p()
+            reg = ctypes.c_int32(0)
+            native.call("gm_host_map", ptr, nbytes, 1, ctypes.byref(out), ctypes.byref(reg))
+            if not reg.value:
+                return True  # already page-locked by its owner (e.g. torch pin_memory)
+            fin = weakref.finalize(root, _unregister_finalizer, self, ptr)
+            self._regs[ptr] = [nbytes, self._tick, fin]
+            return True
+
+    def forget(self, ptr: int) -> None:
+        with self._lock:
+            ent = self._regs.pop(ptr, None)
+        if ent is not None:
+            _unregister(ptr)
+
+    def pinned_bytes(self) -> int:
+        with self._lock:
+            return sum(e[0] for e in self._regs.values())
+
+    def clear(self) -> None:
+        with self._lock:
+            for ptr in list(self._regs):
+                self._drop(ptr)
+
+
+def _unregister(ptr: int) -> None:
+    try:
+        if torch.cuda.is_available():
+            torch.cuda.synchronize()
+        native.call("gm_host_unmap", ptr)
+    except Exception:  # interpreter shutdown: the driver releases the pages with the context
+        pass
+
+
+def _unregister_finalizer(cache: "_PinCache", ptr: int) -> None:
+    cache.forget(ptr)
+
+
+pinned = _PinCache()
+
+
 class MappedHost:
     """Device-visible view of a numpy buffer for one call (context manager).
 
-    Already page-locked memory (e.g. a view of a torch ``pin_memory`` tensor,
-    the fast path) is used in place; pageable memory is page-locked and mapped
-    for the duration of the call and released afterwards, so no registration
-    outlives the array it belongs to."""
+    Already page-locked memory (e.g. a view of a torch ``pin_memory`` tensor) is
+    used in place.  Pageable memory is registered through ``pinned`` (once per
+    owning array, released with it); a buffer the cache does not hold is
+    page-locked for the duration of the call and released afterwards."""
 
     def __init__(self, a: np.ndarray) -> None:
+        self.array = a
         self.host = int(a.ctypes.data)
         self.nbytes = int(a.nbytes)
         self.ptr = 0
         self._owned = False
 
     def __enter__(self) -> int:
+        pinned.pin(self.array)
         out = ctypes.c_void_p()
         reg = ctypes.c_int32(0)
         native.call("gm_host_map", self.host, self.nbytes, 1, ctypes.byref(out), ctypes.byref(reg))
@@ -178,7 +301,7 @@ class MappedHost:
 
 
 def host_transport() -> str:
-    mode = os.environ.get(HOST_TRANSPORT_ENV, "copy").strip().lower()
+    mode = os.environ.get(HOST_TRANSPORT_ENV, "mapped").strip().lower()
     if mode not in ("copy", "mapped"):
         raise ValueError(f"{HOST_TRANSPORT_ENV} must be 'copy' or 'mapped', got {mode!r}")
     return mode

@@ -32,6 +32,7 @@ FLAG_TWO_STEPS = 8388608
 FLAG_FOUR_STEPS = 16777216
 FLAG_SIX_STEPS = 33554432
 FLAG_ZERO_BACKGROUND, FLAG_GRID_ROWS = 67108864, 536870912
+FLAG_WRITE_HALVES, FLAG_WRITE_LINES = 134217728, 268435456
 
 
 class GmCfg(ctypes.Structure):

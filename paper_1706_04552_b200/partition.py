@@ -77,6 +77,10 @@ class PartitionPlan:
             raise ValueError(f"partition level {self.level} outside [0, {r}]")
         self.nsg = 3 ** self.level
         self.m = self.n >> self.level
+        if self.world > self.nsg:
+            # a rank without sub-gaskets would never launch, so on the fused peer path it
+            # would never release its step flag and its peers would wait for it
+            raise ValueError(f"{self.world} ranks exceed the {self.nsg} level-{self.level} sub-gaskets")
         self.ranges = rank_ranges(self.nsg, self.world)
         if self.depth not in (1, 2, 4, 6):
             raise ValueError("depth must be 1, 2, 4 or 6 (CA steps per halo exchange)")

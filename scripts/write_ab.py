@@ -21,10 +21,22 @@ from paper_1706_04552_b200 import roofline as R  # noqa: E402
 from paper_1706_04552_b200.geometry import IntraStrategy  # noqa: E402
 
 T = IntraStrategy.TUNED
+Z = native.FLAG_ZERO_BACKGROUND
 VARIANTS = (
-    ("tiles-lambda", native.FLAG_DIGIT_ORDER | native.FLAG_NARROW_TILES),
-    ("tiles-lambda-zero", native.FLAG_ZERO_BACKGROUND | native.FLAG_DIGIT_ORDER | native.FLAG_NARROW_TILES),
+    ("lambda", 0),
+    ("rowmajor", native.FLAG_ROWMAJOR),
+    ("gridrows", native.FLAG_GRID_ROWS),
+    ("lambda-zero", Z),
+    ("rowmajor-zero", Z | native.FLAG_ROWMAJOR),
+    ("gridrows-zero", Z | native.FLAG_GRID_ROWS),
+    ("gridrows-zero-halves", Z | native.FLAG_GRID_ROWS | native.FLAG_WRITE_HALVES),
+    ("gridrows-zero-lines", Z | native.FLAG_GRID_ROWS | native.FLAG_WRITE_LINES),
+    ("gridrows-zero-v8", Z | native.FLAG_GRID_ROWS | native.FLAG_WRITE_LINES | native.FLAG_WRITE_HALVES),
+    ("hostrows-zero", Z | native.FLAG_HOST_ROWS | native.FLAG_EXPLICIT_RMW | native.FLAG_WHOLE_LINES),
 )
+if len(sys.argv) > 1 and sys.argv[1].startswith("only="):
+    keep = sys.argv.pop(1)[5:].split(",")
+    VARIANTS = tuple(v for v in VARIANTS if v[0] in keep)
 
 
 def member(n, dt):
@@ -43,7 +55,7 @@ def check():
                 if "probe" in name:
                     continue
                 for bg in (0, 5):
-                    if bg and "zero" in name or bg and "zlines" in name:
+                    if bg and "zero" in name:
                         continue
                     g = torch.full((n, n), bg, dtype=dt, device="cuda")
                     backends.run_block_space(g, g, 1, r, T, kind=0, param=-3, flags=fl)
@@ -91,7 +103,7 @@ def main():
                     b.synchronize()
                     bb = a.elapsed_time(b) / K
                     m = statistics.fmean(ts)
-                    print(f"write r={r} c={c} {name:14s} flushed {m * 1e3:7.1f} us (min {min(ts) * 1e3:6.1f})  "
+                    print(f"write r={r} c={c} {name:22s} flushed {m * 1e3:7.1f} us (min {min(ts) * 1e3:6.1f})  "
                           f"b2b {bb * 1e3:7.1f} us  frac {alg / (m * 1e-3) / 1e9 / 6548.5:5.3f} / "
                           f"{alg / (bb * 1e-3) / 1e9 / 6548.5:5.3f}", flush=True)
             del g

@@ -636,21 +636,49 @@ def test_engine_launch_neighbour_sum_uses_masked_snapshot(gpu, oracle):
             assert np.array_equal(g.cpu().numpy(), want), (n, rho, strat)
 
 
-@pytest.mark.parametrize("dtype", [np.int8, np.int16, np.int32])
-def test_mapped_staged_neighbour_sum(gpu, oracle, monkeypatch, dtype):
+@pytest.mark.parametrize("dtype", [np.int8, np.int16, np.int32, np.int64])
+@pytest.mark.parametrize("pinned", [True, False])
+def test_mapped_staged_neighbour_sum(gpu, oracle, monkeypatch, dtype, pinned):
     """Host-mapped numpy grid, src is the grid (engine.launch semantics): the staged path
     (masked snapshot -> device kernel -> whole-line write-back, gm_writeback_tiles) ==
-    the oracle's step, cell for cell, off-gasket cells untouched."""
+    the oracle's step, cell for cell, off-gasket cells untouched.  Pinned (torch
+    pin_memory) and pageable (plain numpy, registered once by the pin cache) grids;
+    int64 covers the grids whose stencil kernel does not store whole sectors (16 <= n <
+    32), which must not take the staged path."""
     monkeypatch.setenv("GASKET_HOST_TRANSPORT", "mapped")
     S = gpu.geometry.IntraStrategy
     c = np.dtype(dtype).itemsize
-    for n in (128 // c, 4 * (128 // c), 1 << 12):
+    for n in sorted({128 // c, 2 * (128 // c), 4 * (128 // c), 1 << 12}):
         for kind in (1, 2):
             grid0 = oracle.fill_hash(n, dtype, 23 + kind, 0)
             want = grid0.copy()
             oracle.run_bounding_box(want, grid0.copy(), 1, kind, -4)
-            host = torch.from_numpy(grid0.copy()).pin_memory()
-            g = host.numpy()
+            g = torch.from_numpy(grid0.copy()).pin_memory().numpy() if pinned else grid0.copy()
             rho = min(64, n)
-            gpu.backends.run_block_space(g, g, rho, (n // rho).bit_length() - 1, S.TUNED, kind=kind, param=-4)
-            assert np.array_equal(g, want), (n, np.dtype(dtype).name, kind)
+            for _ in range(2):  # the second call reuses the cached registration
+                gpu.backends.run_block_space(g, g, rho, (n // rho).bit_length() - 1, S.TUNED, kind=kind, param=-4)
+                assert np.array_equal(g, want), (n, np.dtype(dtype).name, kind, pinned)
+                g[...] = grid0
+
+
+def test_pin_cache_registers_once_and_releases(gpu, monkeypatch):
+    """Pageable numpy grids are registered once per owning array and unregistered when
+    the array is collected; views share the owner's registration."""
+    import gc
+
+    monkeypatch.setenv("GASKET_HOST_TRANSPORT", "mapped")
+    dev = gpu.device
+    dev.pinned.clear()
+    n = 1 << 10
+    g = np.zeros((n, n), dtype=np.int8)
+    S = gpu.geometry.IntraStrategy
+    gpu.backends.run_block_space(g, g, 32, 5, S.TUNED, kind=0, param=3)
+    assert dev.pinned.pinned_bytes() == g.nbytes
+    v = g[: n // 2]
+    assert dev.pinned.pin(v) and dev.pinned.pinned_bytes() == g.nbytes
+    y = np.arange(n).reshape(n, 1)
+    x = np.arange(n).reshape(1, n)
+    assert np.array_equal(g, np.where((x & (n - 1 - y)) == 0, 3, 0).astype(np.int8))
+    del v, g
+    gc.collect()
+    assert dev.pinned.pinned_bytes() == 0

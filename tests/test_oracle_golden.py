@@ -143,3 +143,25 @@ def test_mutations_break_elementwise_lambda(oracle):
             lx, ly = oracle.map_rectangle(r_b)
             got = [fn((b % w, b // w), r_b).coord for b in range(w * h)]
             assert any((gx, gy) != (int(x), int(y)) for (gx, gy), x, y in zip(got, lx, ly)), (defect, r_b)
+
+
+@pytest.mark.parametrize("dtype", [np.int8, np.int16, np.int32, np.int64])
+@pytest.mark.parametrize("kind", [0, 1, 2])
+def test_steps_band_equals_full_grid_steps(oracle, dtype, kind):
+    """The row-band restatement (go_steps_band, used by the GPU tests at n = 2^17 / 2^18
+    where whole grids do not fit the host) == repeated full-grid oracle steps (the
+    golden-pinned bb_* kernel, each step reading the previous state: engine.py:201),
+    for every band placement: touching the top/bottom grid edge, interior, whole grid."""
+    for n in (1, 2, 16, 64, 256):
+        for mode in (0, 1):
+            states = [oracle.fill_hash(n, dtype, 77, mode)]
+            for _ in range(7):
+                nxt = states[-1].copy()
+                oracle.run_bounding_box(nxt, states[-1], 1, kind, -5)
+                states.append(nxt)
+            bands = {(0, n), (0, max(1, n // 4)), (n - max(1, n // 4), n), (n // 3, max(n // 3 + 1, n // 2))}
+            for y0, y1 in bands:
+                steps = [0, 1, 2, 4, 6, 7]
+                outs = oracle.steps_band(n, dtype, 77, mode, kind, -5, y0, y1, steps)
+                for s, o in zip(steps, outs):
+                    assert np.array_equal(o, states[s][y0:y1]), (n, mode, y0, y1, s)
