@@ -73,13 +73,23 @@ def _metric(workload: str) -> str:
 
 
 def _config(workload: str, rho: int, world: int, partitioned: bool) -> dict:
-    """The workload description both arms print."""
-    r, _, kind, _, desc = WORKLOADS[workload]
-    return {"workload": workload, "description": desc, "n": 1 << r, "rho": rho, "mapping": "lambda",
-            "strategy": "tuned", "kind": ["const", "nsum4", "nsum8"][kind], "cells_per_step": 3**r,
+    """The workload description both arms print.  The tuned kernels do not take the
+    paper's block size rho: their blocks are 128-byte-line tiles (128 / cell-bytes cells
+    square); rho shapes only the paper-literal launches of the sweep."""
+    r, dname, kind, _, desc = WORKLOADS[workload]
+    c = {"int8": 1, "int16": 2, "int32": 4, "int64": 8}[dname]
+    tile = 128 // c
+    return {"workload": workload, "description": desc, "n": 1 << r, "mapping": "lambda",
+            "strategy": "tuned",
+            "blocks": (f"lambda tiles of {tile}x{tile} cells (one 128-byte line per row), lambda(omega) "
+                       f"computed per tile on the warp (one lane per level, two ballots)" if kind == 0 else
+                       f"lambda tiles of {tile}x{tile} cells in row-major tile order"),
+            "kind": ["const", "nsum4", "nsum8"][kind], "cells_per_step": 3**r,
             "parallelism": (f"subgasket-partition{world} (level {PART_LEVEL})" if partitioned
                             else f"replicas{world}" if world > 1 else "single"),
-            "l2": "flushed before every timed step (4x L2 read, outside the events)"}
+            "l2": ("not flushed: every step touches several times the 126 MB L2 (the write pass's member "
+                   "lines alone are 2.6x L2 at n=2^16), and the K timed steps run back to back between two "
+                   "events, so each step's dirty-line write-back lands inside the timed region")}
 
 
 def _host_threads() -> int:
@@ -210,12 +220,15 @@ def _max_over_ranks(v: float, world: int) -> float:
 # our arm
 # ---------------------------------------------------------------------------
 
-def _traffic_from_profiles(workload: str) -> float | None:
+def _traffic_from_profiles(workload: str) -> tuple[float | None, str | None]:
+    """(DRAM bytes per launch, where they were measured): ncu cannot run inside the timed
+    process, so `traffic` comes from the committed capture of the same kernel."""
     p = ROOT / "profiles" / "traffic.json"
     try:
-        return float(json.loads(p.read_text())[workload]["dram_bytes_per_launch"])
+        d = json.loads(p.read_text())[workload]
+        return float(d["dram_bytes_per_launch"]), d.get("source")
     except Exception:
-        return None
+        return None, None
 
 
 def _make_step(workload: str, grid, src, rho: int, flags: int):
@@ -292,6 +305,8 @@ def _sweep(r: int, dtype, flusher, budget_s: float = 3.0) -> dict:
         for s in (IntraStrategy.SUBBOX, IntraStrategy.TABLE, IntraStrategy.UNROLL, IntraStrategy.TUNED):
             row[s.value] = timed(lambda: backends.run_block_space(grid, grid, rho, r_b, s, kind=0, param=1))
         out[str(rho)] = {k: {"ms": round(v, 5), "cells_per_s": cells / (v * 1e-3)} for k, v in row.items()}
+    # the vectorised bounding box (rho does not shape it): the competent BB baseline
+    bbv = timed(lambda: backends.run_bounding_box(grid, grid, 32, 0, 1, vectorized=True))
     del grid
     torch.cuda.empty_cache()
 
@@ -312,6 +327,10 @@ def _sweep(r: int, dtype, flusher, budget_s: float = 3.0) -> dict:
         "speedup_best_lambda_vs_best_bb_any": bbx[0] / tun[0],
         "speedup_rho32_subbox_vs_bb": float(out["32"]["bb"]["ms"]) / float(out["32"]["subbox"]["ms"]),
         "speedup_rho1_subbox_vs_bb": float(out["1"]["bb"]["ms"]) / float(out["1"]["subbox"]["ms"]),
+        "bb_vectorised_ms": bbv,
+        "speedup_tuned_lambda_vs_bb_vectorised": bbv / tun[0],
+        "bb_vectorised_note": ("the bounding box written like the tuned kernels (one lane per 16-byte segment "
+                               "of all n^2 cells, the same stores): lambda's gain over a competent BB"),
     }
     # fraction of launched threads that land on gasket cells (engine.work_counts;
     # the tuned kernel launches warps over whole 128-byte tile rows, so its figure is per
@@ -378,6 +397,62 @@ def _multi_step(r: int, tdt, kind: int, flusher, steps: int = 48) -> dict:
     return out
 
 
+def _time_b2b(step, steps: int) -> float:
+    """ms per step of `steps` steps back to back between two CUDA events on the launching
+    stream (synchronised on both sides; no L2 flush: the inputs exceed L2)."""
+    import torch
+
+    from paper_1706_04552_b200 import native
+
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k0 = native.launch_count()
+    a.record()
+    for _ in range(steps):
+        step()
+    b.record()
+    torch.cuda.synchronize()
+    _STEP_LAUNCHES[0] = native.launch_count() - k0
+    return a.elapsed_time(b) / steps
+
+
+def _zero_background(r: int, tdt, flusher, steps: int = 20) -> dict:
+    """The opt-in zero-background write pass (assume_zero_background=True: the paper's
+    zero-filled matrix; the reference bench's make_grid zeros,
+    engine.py:88-90): touched 32-byte sectors stored whole, no DRAM read-modify-write.
+    Same cells and values as the headline on that grid (tests/test_baseline_sizes.py)."""
+    import torch
+
+    from paper_1706_04552_b200 import backends, native
+    from paper_1706_04552_b200 import roofline as R
+    from paper_1706_04552_b200.geometry import IntraStrategy
+
+    n = 1 << r
+    c = torch.empty((), dtype=tdt).element_size()
+    grid = torch.zeros((n, n), dtype=tdt, device="cuda")
+    peak, _ = _peaks()
+    alg = R.write_bytes(r, c)
+    out = {}
+    for name, flags in (("grid rows (default)", 0), ("lambda tiles", native.FLAG_DIGIT_ORDER),
+                        ("address sweep", native.FLAG_WRITE_SWEEP)):
+        def step():
+            backends.run_block_space(grid, grid, 32, r - 5, IntraStrategy.TUNED, kind=0, param=1, flags=flags,
+                                     assume_zero_background=True)
+
+        for _ in range(3):
+            step()
+        ms = _time_b2b(step, steps)
+        fl_ms = statistics.fmean(_time_steps(step, flusher, 10))
+        out[name] = {"ms_per_step": ms, "cells_per_s": 3**r / (ms * 1e-3), "frac": alg / (ms * 1e-3) / 1e9 / peak,
+                     "flushed_ms_per_launch": fl_ms}
+    del grid
+    torch.cuda.empty_cache()
+    best = min(out, key=lambda k: out[k]["ms_per_step"])
+    return {"api": "backends.run_block_space(..., assume_zero_background=True)", "best": best,
+            "frac": out[best]["frac"], "value": out[best]["cells_per_s"], "schedules": out,
+            "bytes": alg, "note": "off-gasket cells must be 0 (opt-in); no DRAM reads"}
+
+
 def _staged_bytes(r: int, c: int) -> tuple[int, int]:
     """Host bytes of the staged mapped stencil (gm_snapshot_stencil + gm_writeback_tiles):
     each member tile's rows -1..TT (128-byte line + a 32-byte sector either side, halos a
@@ -400,48 +475,53 @@ def _staged_bytes(r: int, c: int) -> tuple[int, int]:
     return h2d, ntiles * tt * 128
 
 
-def _e2e(workload: str, rho: int, steps: int, transports: tuple = ("mapped", "copy")) -> dict:
-    """The reference-facing call (backends.run_block_space on host numpy grids)."""
+def _e2e(workload: str, rho: int, steps: int, transports: tuple = ("mapped", "mapped-pinned", "copy")) -> dict:
+    """The reference-facing call (backends.run_block_space on host numpy grids).
+
+    "mapped": a plain pageable numpy grid (what the reference's make_grid returns,
+    engine.py:88-90); the first call registers it (cudaHostRegister, kept until the
+    array dies: device.pinned) and is reported on its own, the timed steps reuse the
+    mapping.  "mapped-pinned": the same on a torch pin_memory grid.  "copy": whole-grid
+    H2D / D2H through a device buffer."""
     import numpy as np
     import torch
 
     from paper_1706_04552_b200 import backends, device
-    from paper_1706_04552_b200 import roofline as R
     from paper_1706_04552_b200.geometry import IntraStrategy
 
     r, dname, kind, _, _ = WORKLOADS[workload]
     n = 1 << r
     c = np.dtype(dname).itemsize
+    rho = 32
     r_b = r - (rho.bit_length() - 1)
+    tdt = getattr(torch, dname)
+    init = device.fill_hash(n, tdt, 1, 0).cpu().numpy() if kind != 0 else None
     res = {}
-    # pinned host grid (the contract's "pinned host memory"); numpy view for the public API
-    host = torch.zeros((n, n), dtype=getattr(torch, dname), pin_memory=True)
-    g = host.numpy()
-    src = None
-    if kind != 0:
-        srct = torch.empty((n, n), dtype=getattr(torch, dname), pin_memory=True)
-        srct.copy_(device.fill_hash(n, getattr(torch, dname), 1, 0).cpu())
-        src = srct.numpy()
-        g[...] = src
     for transport in transports:
-        os.environ[device.HOST_TRANSPORT_ENV] = transport
-        # mapped stencils: engine.launch semantics (src is the grid's pre-launch snapshot),
-        # which the staged path serves (masked snapshot -> device kernel -> write-back)
-        s_arg = g if (src is None or transport == "mapped") else src
-        call = (lambda: backends.run_block_space(g, s_arg, rho, r_b, IntraStrategy.TUNED, kind=kind, param=1))
-        call()  # warm-up (page-locks and maps the buffer once for "mapped")
-        k = steps if transport == "mapped" else max(2, min(steps, 3))
+        if transport == "mapped-pinned":
+            host = torch.zeros((n, n), dtype=tdt, pin_memory=True)
+            g = host.numpy()
+        else:
+            g = np.zeros((n, n), dtype=np.dtype(dname))
+        if init is not None:
+            g[...] = init
+        os.environ[device.HOST_TRANSPORT_ENV] = "copy" if transport == "copy" else "mapped"
+        # neighbour sums: engine.launch semantics (src is the grid's pre-launch snapshot),
+        # which the staged mapped path serves (masked snapshot -> device kernel -> write-back)
+        call = (lambda: backends.run_block_space(g, g, rho, r_b, IntraStrategy.TUNED, kind=kind, param=1))
+        t0 = time.perf_counter()
+        call()  # first call ("mapped": registers and maps the pageable buffer once)
+        first = time.perf_counter() - t0
+        k = steps if transport != "copy" else max(2, min(steps, 3))
         t0 = time.perf_counter()
         for _ in range(k):
             call()
         dt = (time.perf_counter() - t0) / k
-        if transport == "mapped":
+        if transport != "copy":
             # zero-copy: only what the kernel touches crosses PCIe.  Write pass (row-ordered
-            # schedule): every 128-byte line holding gasket cells is read (unless all its
-            # cells are gasket cells) and written back whole.  Stencils: the neighbour
-            # sectors of the snapshot are read, touched sectors read-modified-written.
+            # schedule): the 64-byte halves holding gasket cells are read (unless all their
+            # cells are gasket cells) and written back whole.  Stencils: the staged windows.
             if kind == 0:
-                # 64-byte halves of 128-byte lines that hold gasket cells (halves: k = log2(64/c))
                 kh = (64 // c).bit_length() - 1
                 halves = (1 << kh) * 3 ** (r - kh)
                 full = 3 ** (r - kh)  # halves made only of gasket cells need no read
@@ -449,16 +529,22 @@ def _e2e(workload: str, rho: int, steps: int, transports: tuple = ("mapped", "co
             else:
                 h2d, d2h = _staged_bytes(r, c)
         else:
-            h2d = n * n * c * (1 if kind == 0 else 2)
+            h2d = n * n * c
             d2h = n * n * c
         res[transport] = {"s_per_step": dt, "cells_per_s": 3**r / dt, "h2d_bytes_per_step": int(h2d),
-                          "d2h_bytes_per_step": int(d2h), "steps": k}
+                          "d2h_bytes_per_step": int(d2h), "steps": k, "first_call_s": first}
+        del g
+        if transport == "mapped-pinned":
+            del host
     os.environ.pop(device.HOST_TRANSPORT_ENV, None)
-    best = min(res.values(), key=lambda v: v["s_per_step"])
-    which = [k for k, v in res.items() if v is best][0]
-    return {"value": best["cells_per_s"], "unit": "cells/s", "h2d_bytes_per_step": best["h2d_bytes_per_step"],
-            "d2h_bytes_per_step": best["d2h_bytes_per_step"], "transport": which, "api": "backends.run_block_space(numpy)",
-            "timer": "host wall clock around the synchronous call", "variants": res}
+    device.pinned.clear()
+    head = res["mapped"] if "mapped" in res else min(res.values(), key=lambda v: v["s_per_step"])
+    return {"value": head["cells_per_s"], "unit": "cells/s", "h2d_bytes_per_step": head["h2d_bytes_per_step"],
+            "d2h_bytes_per_step": head["d2h_bytes_per_step"], "transport": "mapped (pageable numpy grid)",
+            "api": "backends.run_block_space(numpy grid, numpy grid, ...)",
+            "timer": "host wall clock around the synchronous call; first call (buffer registration) reported "
+                     "separately as variants.mapped.first_call_s",
+            "variants": res}
 
 
 def _cpu_baseline(workload: str, budget_s: float = 12.0) -> dict:
@@ -555,14 +641,25 @@ def run_ours(args) -> None:
     _barrier(world)
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
+        # the same steps for ~60 ms right before the timed region, so that the clock sampler
+        # sees the GPU under this load (the timed region itself lasts only milliseconds)
+        t_busy = time.perf_counter() + 0.06
+        while time.perf_counter() < t_busy:
+            for _ in range(8):
+                step()
+            torch.cuda.synchronize()
+        _barrier(world)
         t_wall0 = time.perf_counter()
-        ms = _time_steps(step, flusher, args.steps)
+        per = _time_b2b(step, args.steps)
         t_wall = time.perf_counter() - t_wall0
     torch.cuda.synchronize()
     _barrier(world)
     launches = _STEP_LAUNCHES[0]  # inside the timed (event-bracketed) region only
-    total_ms = _max_over_ranks(sum(ms), world)
+    ms = [per] * args.steps
+    total_ms = _max_over_ranks(per * args.steps, world)
     ms_per_step = total_ms / args.steps
+    # the same launch after an L2 flush (outside the events): the cold-L2 single-launch time
+    flushed = statistics.fmean(_time_steps(step, flusher, min(args.steps, 10)))
     ca_steps = args.temporal if part is not None else 1  # CA steps per timed step
     if ca_steps > 1:
         ms = [t / ca_steps for t in ms]
@@ -573,7 +670,7 @@ def run_ours(args) -> None:
     peak, peak_src = _peaks()
     alg_bytes = R.pass_bytes(r, c, kind)
     achieved = alg_bytes / (statistics.fmean(ms) * 1e-3) / 1e9
-    traffic = _traffic_from_profiles(workload)
+    traffic, traffic_src = _traffic_from_profiles(workload)
     line = {
         "metric": _metric(workload),
         "value": value,
@@ -589,7 +686,7 @@ def run_ours(args) -> None:
         "data": "synthetic (zero grid, param=1)" if kind == 0 else "synthetic (splitmix64 hash states, all cells)",
         "config": _config(workload, rho, world, part is not None),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "peak_source": peak_src, "algorithmic_bytes_per_launch": alg_bytes,
+                     "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src, "algorithmic_bytes_per_launch": alg_bytes,
                      "bytes_model": "exact 32-byte-sector minimum on the dense row-major grid (SURVEY §8d)",
                      "element_bytes_frac": R.element_bytes(r, c, kind) / (statistics.fmean(ms) * 1e-3) / 1e9 / peak,
                      # what DRAM must move on this layout (roofline.hw_bytes): a write pass's
@@ -600,8 +697,9 @@ def run_ours(args) -> None:
                                   "note": ("sector writes + forced RMW re-read" if kind == 0 else
                                            "64-byte-half reads of the dilated gasket + sector writes"),
                                   "frac": R.hw_bytes(r, c, kind) / (statistics.fmean(ms) * 1e-3) / 1e9 / peak}},
-        "clocks": clk.summary(),
+        "clocks": dict(clk.summary(), window="the last ~60 ms of warm-up (same steps) and the timed region"),
         "gpu_launches": int(launches),
+        "flushed_ms_per_launch": flushed / (args.temporal if part is not None else 1),
         "timed_region_wall_s": t_wall,
     }
     if workload in PATTERN_CEILING_US and part is None:
@@ -628,6 +726,8 @@ def run_ours(args) -> None:
     if rank == 0 and world == 1 and not workload.startswith("part"):
         if not args.no_sweep and kind == 0:
             line["sweep"] = _sweep(r, tdt, flusher)
+        if kind == 0:
+            line["zero_background"] = _zero_background(r, tdt, flusher, steps=args.steps)
         if kind != 0 and c in (1, 2, 4):
             line["multi_step"] = _multi_step(r, tdt, kind, flusher)
         if not args.no_e2e:
@@ -759,38 +859,8 @@ def run_nsweep(args) -> None:
     out = Path(args.nsweep_out)
     out.parent.mkdir(parents=True, exist_ok=True)
     B.write_csv(recs, out)
-    # speedup of the best lambda row over BB per (r, rho); n0 = smallest n from which it stays > 1
-    table: dict = {}
-    for rec in recs:
-        if not rec.status.startswith("ok"):
-            continue
-        row = table.setdefault(rec.rho, {}).setdefault(rec.r, {})
-        if rec.mapping == "bb":
-            row["bb"] = rec.wall_ns_mean
-        else:
-            row[rec.strategy] = rec.wall_ns_mean
-    summary = {}
-    for rho, rows in sorted(table.items()):
-        curve = {}
-        for r, row in sorted(rows.items()):
-            if "bb" not in row:
-                continue
-            lit = min(v for k, v in row.items() if k in ("subbox", "table", "unroll"))
-            curve[r] = {"paper_literal": row["bb"] / lit, "best": row["bb"] / min(v for k, v in row.items() if k != "bb")}
-        n0 = None
-        for r in sorted(curve):
-            if all(curve[q]["paper_literal"] > 1 for q in curve if q >= r):
-                n0 = 1 << r
-                break
-        summary[str(rho)] = {"n0_paper_literal": n0, "speedup_by_r": curve}
-    # best-vs-best per n
-    best = {}
-    for r in sorted({r for rows in table.values() for r in rows}):
-        bb = [rows[r]["bb"] for rows in table.values() if r in rows and "bb" in rows[r]]
-        lam = [v for rows in table.values() if r in rows for k, v in rows[r].items() if k in ("subbox", "table", "unroll")]
-        if bb and lam:
-            best[r] = min(bb) / min(lam)
-    n0_best = next((1 << r for r in sorted(best) if all(best[q] > 1 for q in best if q >= r)), None)
+    cross = B.crossover(recs)
+    summary, best, n0_best = cross["per_rho"], cross["best_vs_best_paper_literal_by_r"], cross["n0_best_vs_best"]
     print(json.dumps({"nsweep_csv": str(out), "rows": len(recs), "per_rho": summary,
                       "best_vs_best_paper_literal_by_r": best, "n0_best_vs_best": n0_best}), flush=True)
 

@@ -49,6 +49,7 @@ extern "C" {
 #define GM_MAP_BB 0       /* engine.Mapping.BOUNDING_BOX (paper-literal) */
 #define GM_MAP_LAMBDA 1   /* engine.Mapping.BLOCK_SPACE */
 #define GM_MAP_BB_EXIT 2  /* bounding box with block-level early exit */
+#define GM_MAP_BB_VEC 3   /* bounding box, vectorised: one lane per 16-byte segment of all n*n cells (write pass) */
 
 /* Launch flags.  All but GM_FLAG_DST_FROM_SRC and GM_FLAG_HOST_ROWS select kernel
  * variants kept for A/B measurement (scripts/variants.py; results in
@@ -61,16 +62,16 @@ extern "C" {
 #define GM_FLAG_HOST_ROWS 16   /* write pass on a host-mapped grid: row-ordered whole-line schedule */
 #define GM_FLAG_ROWMAJOR 32    /* tuned: visit tiles row-major per sub-gasket (the default since v2; kept for ABI) */
 #define GM_FLAG_CHUNKED 64     /* tuned stencil: contiguous tile run per CTA instead of interleaved */
-#define GM_FLAG_NO_TMA 128     /* tuned stencil: always stage tiles with cp.async */
-#define GM_FLAG_FORCE_TMA 256  /* tuned stencil: always stage tiles with TMA */
+#define GM_FLAG_NO_TMA 128     /* A/B builds only (GASKET_AB_BUILD=1): never the TMA-staged stencil */
+#define GM_FLAG_FORCE_TMA 256  /* A/B builds only: the superseded TMA-staged stencil (stencil_tma.cu) */
 #define GM_FLAG_FETCH_LINE 512 /* tuned kernels: whole-line (.L2::128B) loads (stencil v2: the default since round 1d) */
 #define GM_FLAG_FETCH64 1024   /* tuned write: touch each written 64-byte half with an .L2::64B load first
                                   (with GM_FLAG_FETCH_LINE: touch the whole line) */
-#define GM_FLAG_STENCIL_V1 2048 /* tuned stencil: the v1 kernel (stencil.cu) instead of v2 (stencil2.cu) */
+#define GM_FLAG_STENCIL_V1 2048 /* A/B builds only: the superseded v1 stencil (stencil.cu) instead of v2 */
 #define GM_FLAG_STAGES2 4096   /* tuned stencil v2: 2-deep staging ring instead of 3/4 */
-#define GM_FLAG_PROBE_NOSTORE 8192  /* design probe, stencil v2 / gm_ca_step2: no stores (result undefined) */
-#define GM_FLAG_PROBE_NOLOAD 16384  /* design probe, stencil v2 / gm_ca_step2: no staging (result undefined) */
-#define GM_FLAG_PROBE_NOCOMPUTE 32768 /* design probe, stencil v2 / gm_ca_step2: no arithmetic (result undefined) */
+#define GM_FLAG_PROBE_NOSTORE 8192  /* A/B builds only: design probe, no stores (result undefined) */
+#define GM_FLAG_PROBE_NOLOAD 16384  /* A/B builds only: design probe, no staging (result undefined) */
+#define GM_FLAG_PROBE_NOCOMPUTE 32768 /* A/B builds only: design probe, no arithmetic (result undefined) */
 #define GM_FLAG_DIGIT_ORDER 65536 /* tuned: visit tiles in lambda digit order instead of row-major per sub-gasket */
 #define GM_FLAG_STORE_CS 131072   /* tuned write pass / stencil v2: streaming (evict-first) stores */
 #define GM_FLAG_BAND_MAJOR 262144 /* tuned write pass: hand out (band, tile) units band-major */
@@ -86,6 +87,8 @@ extern "C" {
                                             stored whole (gasket cells = param, the rest 0), no DRAM read-modify-write */
 #define GM_FLAG_WRITE_HALVES 134217728 /* zero-background write pass: store the touched 64-byte halves whole */
 #define GM_FLAG_WRITE_LINES 268435456  /* zero-background write pass: store the touched 128-byte lines whole */
+#define GM_FLAG_WRITE_SWEEP 1073741824 /* tuned write pass: the grid's member lines in address order, chunks of
+                                          32 lines dealt round-robin over all warps (write.cu) */
 #define GM_FLAG_GRID_ROWS 536870912   /* tuned write pass: no blocks -- one warp per grid row, its member lines
                                          left to right (the row enumeration; write.cu) */
 
@@ -106,7 +109,9 @@ typedef struct gm_cfg {
     int32_t reserved;
 } gm_cfg_t;
 
-/* backends.py:225-231.  grid/src: n*n cells. */
+/* backends.py:225-231.  grid/src: n*n cells.  early_exit: 0 = the paper-literal kernel,
+ * 1 = off-gasket blocks exit first (GM_MAP_BB_EXIT), 2 = vectorised (GM_MAP_BB_VEC, write
+ * pass only: GM_EINVAL for neighbour sums). */
 int gm_run_bounding_box(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t rho,
                         int32_t kind, int32_t param, int32_t early_exit, void* stream);
 
@@ -217,6 +222,33 @@ int gm_peer_halo_put(const void* mine, const uint64_t* peers, const int64_t* idx
                      const uint64_t* peer_flags, int32_t rank, int32_t world, uint64_t epoch, void* stream);
 int gm_peer_halo_wait(const uint64_t* flags, int32_t rank, int32_t world, uint64_t epoch, uint64_t timeout_ns,
                       uint32_t* status, void* stream);
+/* gm_peer_halo_put with a destination per entry (tiled partition storage): entry i copies
+ * cell idx[i] of `mine` to cell (didx[i] & (2^56-1)) of rank (didx[i] >> 56)'s buffer --
+ * the own rank's entries are ring copies inside `mine` -- then releases `epoch` as above. */
+int gm_peer_halo_put_to(const void* mine, const uint64_t* peers, const int64_t* idx, const int64_t* didx,
+                        int64_t count, int32_t cell_bytes, const uint64_t* peer_flags, int32_t rank, int32_t world,
+                        uint64_t epoch, void* stream);
+/* Tiled partition storage (per-rank storage = the owned level-`level`
+ * sub-gaskets plus a ring, not two n x n grids).  Each owned sub-gasket is one block of
+ * (m + 2R) rows x `pitch` bytes (m = n >> level; R ring rows; `pitch` >= m*cell_bytes plus
+ * the ring columns, a multiple of 32); the global cell (x, y) of sub-gasket sg_begin + k
+ * lives at byte sg_off[k] + y*pitch + x*cell_bytes of the buffer (sg_off: device int64[],
+ * the block's virtual origin).  Rings hold the neighbours' cells (static off-gasket
+ * values once, changing halo cells per exchange).
+ * gm_run_part_tiled: `steps` (1, 2, 4 or 6) CA steps src -> grid over the rank's blocks
+ * (one step: whole-sector blend from src; the blocks of src and grid agree off the gasket);
+ * epilogue/wait/signal: the fused peer exchange of gm_run_part_peer (NULL: none; the
+ * descriptor's didx then lists per-entry destinations, gm_peer_halo_put_to's format).
+ * gm_copy_cells: dst[dst_idx[i]] = src[src_idx[i]] (cell indices).  gm_fill_hash_window:
+ * the synthetic grid's cells [x0, x0+w) x [y0, y0+h) (0 outside n x n) into a pitched
+ * block. */
+int gm_run_part_tiled(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
+                      int32_t steps, int32_t level, uint32_t sg_begin, uint32_t sg_end, const int64_t* sg_off,
+                      int64_t pitch, void* epilogue, uint64_t wait_epoch, uint64_t signal_epoch, void* stream);
+int gm_copy_cells(void* dst, const void* src, int32_t cell_bytes, const int64_t* dst_idx, const int64_t* src_idx,
+                  int64_t count, void* stream);
+int gm_fill_hash_window(void* out, int64_t pitch, int64_t n, int32_t cell_bytes, int64_t x0, int64_t y0, int64_t w,
+                        int64_t h, uint64_t seed, int32_t mode, void* stream);
 /* gm_run_part with the halo exchange fused into the step kernel (peer_epilogue.cuh):
  * `epilogue` = device descriptor (PartitionedCA(halo="peer", fused=True) builds it);
  * every CTA first acquires the peers' flags >= wait_epoch (0: no wait), the last CTA

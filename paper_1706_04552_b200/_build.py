@@ -12,8 +12,14 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
-LIB = LIB_DIR / "libgasket_b200.so"
-SOURCES = ["literal.cu", "tuned.cu", "stream.cu", "write.cu", "stencil.cu", "stencil2.cu", "stencil_tb.cu", "stencil_tma.cu", "hostrows.cu", "maps.cu", "capi.cu", "peer.cu", "snapshot.cu"]
+# A/B builds (GASKET_AB_BUILD=1, scripts/ only): the superseded stencil variants (v1,
+# TMA-staged) and the design-probe flags are compiled in, into a separate library that
+# scripts load with GASKET_B200_LIB; the product library carries neither.
+AB_BUILD = os.environ.get("GASKET_AB_BUILD", "") == "1"
+LIB = LIB_DIR / ("libgasket_b200_ab.so" if AB_BUILD else "libgasket_b200.so")
+SOURCES = ["literal.cu", "tuned.cu", "stream.cu", "write.cu", "stencil2.cu", "stencil_tb.cu", "hostrows.cu",
+           "maps.cu", "capi.cu", "peer.cu", "snapshot.cu"]
+AB_SOURCES = ["stencil.cu", "stencil_tma.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
               "--expt-relaxed-constexpr"]
@@ -27,7 +33,7 @@ def _nvcc() -> str:
 
 
 def sources() -> list[Path]:
-    return [CSRC / s for s in SOURCES if (CSRC / s).exists()]
+    return [CSRC / s for s in SOURCES + (AB_SOURCES if AB_BUILD else [])]
 
 
 def needs_build() -> bool:
@@ -42,10 +48,10 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     if not force and not needs_build():
         return LIB
     nvcc = _nvcc()
-    obj_dir = LIB_DIR / "obj"
+    obj_dir = LIB_DIR / ("obj_ab" if AB_BUILD else "obj")
     obj_dir.mkdir(parents=True, exist_ok=True)
     extra_inc = ["-I", str(PKG.parent / "include")]
-    defines: list[str] = []
+    defines: list[str] = ["-DGM_AB_VARIANTS=1"] if AB_BUILD else []
 
     def compile_one(src: Path) -> Path:
         obj = obj_dir / (src.stem + ".o")

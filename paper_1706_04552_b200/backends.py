@@ -216,15 +216,23 @@ def _run(grid: Any, src: Any, kind: int, launch, *, mapped_ok: bool) -> None:
 # ---------------------------------------------------------------------------
 
 def run_bounding_box(grid, src, rho: int, kind: int, param: int, backend: str = BACKEND, *,
-                     early_exit: bool = False) -> None:
+                     early_exit: bool = False, vectorized: bool = False) -> None:
     """backends.py:225-231: identity map over n_b x n_b blocks of rho x rho threads,
-    each thread testing x & (n-1-y) (``early_exit``: whole tiles off the gasket exit first)."""
+    each thread testing x & (n-1-y) (``early_exit``: whole tiles off the gasket exit first).
+
+    ``vectorized`` (write pass only): the bounding box written like the tuned lambda
+    kernels -- one lane per 16-byte segment of all n x n cells, the same membership test
+    and the same vectorised stores -- the competent BB baseline of the lambda-vs-BB
+    speed-up (rho does not shape this launch)."""
     resolve_backend(backend)
     p = _param32(param)
     kind = int(kind)
+    if vectorized and kind != KERNEL_CONST:
+        raise ValueError("the vectorised bounding box runs the write pass (KERNEL_CONST) only")
+    variant = 2 if vectorized else (1 if early_exit else 0)
 
     def launch(gp, sp, n, c, stream, extra_flags):
-        native.call("gm_run_bounding_box", gp, sp, n, c, int(rho), kind, p, 1 if early_exit else 0, stream)
+        native.call("gm_run_bounding_box", gp, sp, n, c, int(rho), kind, p, variant, stream)
 
     _run(grid, src, kind, launch, mapped_ok=False)
 

@@ -221,3 +221,37 @@ def run_sweep(cfg: SweepConfig) -> list[BenchRecord]:
             del grid
             torch.cuda.empty_cache()
     return records
+
+
+def crossover(records: Sequence[BenchRecord]) -> dict:
+    """The lambda-vs-BB speed-up curve of a sweep and its crossover n0 (the paper's Fig. 7
+    reading): per rho, speedup(r) = BB time / best paper-literal lambda
+    time (SUBBOX / TABLE / UNROLL) and BB / best of any lambda row; n0 = the smallest n
+    from which the paper-literal speed-up stays > 1.  Also best-vs-best over every rho."""
+    table: dict = {}
+    for rec in records:
+        if not rec.status.startswith("ok") or rec.wall_ns_mean is None:
+            continue
+        row = table.setdefault(rec.rho, {}).setdefault(rec.r, {})
+        row["bb" if rec.mapping == Mapping.BOUNDING_BOX.value else rec.strategy] = rec.wall_ns_mean
+    literal = ("subbox", "table", "unroll")
+    per_rho = {}
+    for rho, rows in sorted(table.items()):
+        curve = {}
+        for r, row in sorted(rows.items()):
+            lit = [v for k, v in row.items() if k in literal]
+            if "bb" not in row or not lit:
+                continue
+            curve[r] = {"paper_literal": row["bb"] / min(lit),
+                        "best": row["bb"] / min(v for k, v in row.items() if k != "bb")}
+        n0 = next((1 << r for r in sorted(curve) if all(curve[q]["paper_literal"] > 1 for q in curve if q >= r)), None)
+        per_rho[str(rho)] = {"n0_paper_literal": n0, "speedup_by_r": curve}
+    best = {}
+    for r in sorted({r for rows in table.values() for r in rows}):
+        bb = [rows[r]["bb"] for rows in table.values() if r in rows and "bb" in rows[r]]
+        lam = [v for rows in table.values() if r in rows for k, v in rows[r].items() if k in literal]
+        if bb and lam:
+            best[r] = min(bb) / min(lam)
+    n0_best = next((1 << r for r in sorted(best) if all(best[q] > 1 for q in best if q >= r)), None)
+    return {"per_rho": per_rho, "best_vs_best_paper_literal_by_r": best, "n0_best_vs_best": n0_best}
+

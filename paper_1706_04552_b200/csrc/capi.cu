@@ -30,6 +30,9 @@ cudaError_t launch_count_equal(const void*, const void*, int64_t, unsigned long 
 cudaError_t launch_l2_flush(const void*, int64_t, uint64_t*, cudaStream_t);
 cudaError_t launch_gather(const void*, int, const int64_t*, int64_t, void*, cudaStream_t);
 cudaError_t launch_scatter(void*, int, const int64_t*, int64_t, const void*, cudaStream_t);
+cudaError_t launch_copy_cells(void*, const void*, int, const int64_t*, const int64_t*, int64_t, cudaStream_t);
+cudaError_t launch_fill_hash_window(void*, int64_t, int64_t, int, int64_t, int64_t, int64_t, int64_t, uint64_t, int,
+                                    cudaStream_t);
 
 static std::atomic<uint64_t> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
@@ -116,7 +119,8 @@ int launch_cfg(const gm_cfg_t* c, void* grid, const void* src, const int32_t* tx
         if (src == grid)
             return fail(GM_EINVAL, "neighbour kernels read the pre-launch snapshot: src must not alias grid");
     }
-    if (c->mapping != GM_MAP_BB && c->mapping != GM_MAP_LAMBDA && c->mapping != GM_MAP_BB_EXIT)
+    if (c->mapping != GM_MAP_BB && c->mapping != GM_MAP_LAMBDA && c->mapping != GM_MAP_BB_EXIT &&
+        c->mapping != GM_MAP_BB_VEC)
         return fail(GM_EINVAL, "unknown mapping %d", c->mapping);
     const int r_b = log2i(c->n / c->rho);
     if (c->mapping == GM_MAP_LAMBDA) {
@@ -170,7 +174,9 @@ int gm_run_bounding_box(void* grid, const void* src, int64_t n, int32_t cell_byt
     gm_cfg_t c{};
     c.n = n;
     c.rho = rho;
-    c.mapping = early_exit ? GM_MAP_BB_EXIT : GM_MAP_BB;
+    if (early_exit == 2 && kind != GM_KIND_CONST)
+        return fail(GM_EINVAL, "the vectorised bounding box runs the write pass (kind %d) only", GM_KIND_CONST);
+    c.mapping = early_exit == 2 ? GM_MAP_BB_VEC : early_exit ? GM_MAP_BB_EXIT : GM_MAP_BB;
     c.strategy = GM_STRAT_SUBBOX;
     c.kind = kind;
     c.cell_bytes = cell_bytes;
@@ -424,8 +430,79 @@ int gm_peer_halo_put(const void* mine, const uint64_t* peers, const int64_t* idx
     if (world < 1 || rank < 0 || rank >= world) return fail(GM_EINVAL, "gm_peer_halo_put: rank %d outside world %d", rank, world);
     if (cell_bytes != 1 && cell_bytes != 2 && cell_bytes != 4 && cell_bytes != 8)
         return fail(GM_EINVAL, "gm_peer_halo_put: cell_bytes must be 1, 2, 4 or 8");
-    return cuda_rc(gm::launch_peer_put(mine, peers, idx, count, cell_bytes, peer_flags, rank, world, epoch,
+    return cuda_rc(gm::launch_peer_put(mine, peers, idx, nullptr, count, cell_bytes, peer_flags, rank, world, epoch,
                                        reinterpret_cast<cudaStream_t>(stream)), "peer_halo_put");
+}
+
+int gm_peer_halo_put_to(const void* mine, const uint64_t* peers, const int64_t* idx, const int64_t* didx,
+                        int64_t count, int32_t cell_bytes, const uint64_t* peer_flags, int32_t rank, int32_t world,
+                        uint64_t epoch, void* stream) {
+    if (!mine || !peers || !peer_flags || (count && (!idx || !didx)) || count < 0)
+        return fail(GM_EINVAL, "gm_peer_halo_put_to: bad arguments");
+    if (world < 1 || world > 255 || rank < 0 || rank >= world)
+        return fail(GM_EINVAL, "gm_peer_halo_put_to: rank %d outside world %d", rank, world);
+    if (cell_bytes != 1 && cell_bytes != 2 && cell_bytes != 4 && cell_bytes != 8)
+        return fail(GM_EINVAL, "gm_peer_halo_put_to: cell_bytes must be 1, 2, 4 or 8");
+    return cuda_rc(gm::launch_peer_put(mine, peers, idx, didx, count, cell_bytes, peer_flags, rank, world, epoch,
+                                       reinterpret_cast<cudaStream_t>(stream)), "peer_halo_put_to");
+}
+
+int gm_copy_cells(void* dst, const void* src, int32_t cell_bytes, const int64_t* dst_idx, const int64_t* src_idx,
+                  int64_t count, void* stream) {
+    if (count < 0 || (count && (!dst || !src || !dst_idx || !src_idx))) return fail(GM_EINVAL, "gm_copy_cells: bad arguments");
+    return cuda_rc(gm::launch_copy_cells(dst, src, cell_bytes, dst_idx, src_idx, count,
+                                         reinterpret_cast<cudaStream_t>(stream)), "copy_cells");
+}
+
+int gm_fill_hash_window(void* out, int64_t pitch, int64_t n, int32_t cell_bytes, int64_t x0, int64_t y0, int64_t w,
+                        int64_t h, uint64_t seed, int32_t mode, void* stream) {
+    if (!out || n < 1 || pitch < w * cell_bytes) return fail(GM_EINVAL, "gm_fill_hash_window: bad arguments");
+    return cuda_rc(gm::launch_fill_hash_window(out, pitch, n, cell_bytes, x0, y0, w, h, seed, mode,
+                                               reinterpret_cast<cudaStream_t>(stream)), "fill_hash_window");
+}
+
+int gm_run_part_tiled(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
+                      int32_t steps, int32_t level, uint32_t sg_begin, uint32_t sg_end, const int64_t* sg_off,
+                      int64_t pitch, void* epilogue, uint64_t wait_epoch, uint64_t signal_epoch, void* stream) {
+    if (steps != 1 && steps != 2 && steps != 4 && steps != 6)
+        return fail(GM_EINVAL, "gm_run_part_tiled: steps must be 1, 2, 4 or 6");
+    gm_cfg_t c{};
+    c.n = n;
+    c.rho = 1;
+    c.mapping = GM_MAP_LAMBDA;
+    c.strategy = GM_STRAT_TUNED;
+    c.kind = kind;
+    c.cell_bytes = cell_bytes;
+    c.param = param;
+    c.flags = steps == 1 ? GM_FLAG_DST_FROM_SRC : 0;
+    if (int rc = check_common(n, cell_bytes, 1, kind)) return rc;
+    if (kind != GM_KIND_NSUM4 && kind != GM_KIND_NSUM8) return fail(GM_EINVAL, "gm_run_part_tiled: kind must be NSUM4 or NSUM8");
+    if (!grid || !src || src == grid || !sg_off) return fail(GM_EINVAL, "gm_run_part_tiled: bad buffers");
+    if (cell_bytes != 1 && cell_bytes != 2 && cell_bytes != 4) return fail(GM_EINVAL, "gm_run_part_tiled: 1-, 2- or 4-byte cells");
+    const int64_t tile = 128 / cell_bytes;
+    if (level < 0 || (n >> level) < tile) return fail(GM_EINVAL, "partition level %d too deep", level);
+    if (pitch < (n >> level) * cell_bytes + 32 || pitch % 32 != 0)
+        return fail(GM_EINVAL, "gm_run_part_tiled: pitch %lld must cover a sub-gasket row plus its ring, a multiple of 32",
+                    (long long)pitch);
+    uint64_t nsg = 1;
+    for (int i = 0; i < level; ++i) nsg *= 3;
+    if (sg_begin > sg_end || sg_end > nsg) return fail(GM_EINVAL, "sub-gasket range [%u, %u) outside [0, %llu)",
+                                                       sg_begin, sg_end, (unsigned long long)nsg);
+    gm::LaunchArgs a = make_args(&c, grid, src, nullptr, nullptr, 0, stream);
+    a.part_level = level;
+    a.sg_begin = sg_begin;
+    a.sg_end = sg_end;
+    a.sg_off = sg_off;
+    a.pitch = pitch;
+    a.peer_epi = epilogue;
+    a.wait_epoch = epilogue ? wait_epoch : 0;
+    a.signal_epoch = epilogue ? signal_epoch : 0;
+    const cudaError_t e = steps == 1 ? gm::launch_stencil_v2(a) : gm::launch_stencil_tb(a, steps);
+    if (e == cudaErrorNotSupported) {
+        cudaGetLastError();
+        return fail(GM_EINVAL, "gm_run_part_tiled: no tiled kernel for these cells (6 steps: 1- or 2-byte cells)");
+    }
+    return cuda_rc(e, "tiled partition launch");
 }
 
 int gm_peer_halo_wait(const uint64_t* flags, int32_t rank, int32_t world, uint64_t epoch, uint64_t timeout_ns,

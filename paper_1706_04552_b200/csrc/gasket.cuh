@@ -16,7 +16,7 @@ namespace gm {
 
 enum Kind { KIND_CONST = 0, KIND_NSUM4 = 1, KIND_NSUM8 = 2, KIND_COUNT = 3 };
 enum Strategy { STRAT_UNROLL = 0, STRAT_TABLE = 1, STRAT_SUBBOX = 2, STRAT_TUNED = 3 };
-enum Mapping { MAP_BB = 0, MAP_LAMBDA = 1, MAP_BB_EXIT = 2 };
+enum Mapping { MAP_BB = 0, MAP_LAMBDA = 1, MAP_BB_EXIT = 2, MAP_BB_VEC = 3 };
 
 template <int C> struct CellT;
 template <> struct CellT<1> { using T = uint8_t; };

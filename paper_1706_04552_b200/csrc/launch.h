@@ -32,7 +32,24 @@ struct LaunchArgs {
     // the peers' epoch to wait for before reading, the epoch to signal after writing
     void* peer_epi = nullptr;
     uint64_t wait_epoch = 0, signal_epoch = 0;
+    // tiled partition storage (gm_run_part_tiled): the rank's sub-gaskets [sg_begin, sg_end)
+    // each in its own ringed block; sg_off[k] = byte offset from grid / src to the virtual
+    // origin of sub-gasket sg_begin + k (where global cell (0, 0) would sit), pitch = row
+    // bytes of those blocks.  nullptr = the dense n x n layout (pitch n * cell_bytes).
+    const int64_t* sg_off = nullptr;
+    int64_t pitch = 0;
 };
+
+// row pitch in bytes of a launch's buffers
+inline int64_t row_pitch(const LaunchArgs& a) { return a.pitch > 0 ? a.pitch : a.n * a.cell_bytes; }
+
+// tiles per sub-gasket of a partitioned launch tiled at level r_t (3^(r_t - part_level))
+inline uint32_t tiles_per_subgasket(const LaunchArgs& a, int r_t) {
+    uint32_t per = 1;
+    if (a.part_level >= 0)
+        for (int i = 0; i < r_t - a.part_level; ++i) per *= 3u;
+    return per;
+}
 
 // Tile-index range [lo, hi) of a launch whose kernel tiles the gasket at level r_t.
 inline void tile_range(const LaunchArgs& a, int r_t, uint32_t& lo, uint32_t& hi) {
@@ -62,6 +79,7 @@ cudaError_t launch_literal(const LaunchArgs& a);
 cudaError_t launch_tuned(const LaunchArgs& a);
 cudaError_t launch_stream(const LaunchArgs& a);
 cudaError_t launch_write(const LaunchArgs& a);
+cudaError_t launch_bb_vector(const LaunchArgs& a);  // GM_MAP_BB_VEC (write.cu)
 cudaError_t launch_stencil_tile(const LaunchArgs& a);
 cudaError_t launch_host_rows(const LaunchArgs& a);
 cudaError_t launch_stencil_tma(const LaunchArgs& a);
@@ -75,7 +93,8 @@ cudaError_t launch_host_rows_copyback(void* out, const void* dst, const void* sn
 // member tiles of a level-q gasket, row-major inside each level-L sub-gasket (stencil2.cu)
 const uint32_t* rowmajor_table(int q, int L);
 void rowmajor_order_host(int q, int L, std::vector<uint32_t>& v);
-cudaError_t launch_peer_put(const void* mine, const uint64_t* peers, const int64_t* idx, int64_t k, int cell_bytes,
+cudaError_t launch_peer_put(const void* mine, const uint64_t* peers, const int64_t* idx, const int64_t* didx,
+                            int64_t k, int cell_bytes,
                             const uint64_t* peer_flags, int rank, int world, uint64_t epoch, cudaStream_t s);
 cudaError_t launch_peer_wait(const uint64_t* flags, int rank, int world, uint64_t epoch, uint64_t timeout_ns,
                              uint32_t* status, cudaStream_t s);

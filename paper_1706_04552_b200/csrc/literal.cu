@@ -176,7 +176,12 @@ template <int C>
 static cudaError_t launch_lambda_c(const LaunchArgs& a) { GM_DISPATCH_KIND(launch_lambda_t, C, a) }
 
 cudaError_t launch_literal(const LaunchArgs& a) {
-    const bool bb = a.mapping == MAP_BB || a.mapping == MAP_BB_EXIT;
+    if (a.mapping == MAP_BB_VEC) {  // grids under one 16-byte segment per row: the literal bounding box
+        const cudaError_t e = launch_bb_vector(a);
+        if (e != cudaErrorNotSupported) return e;
+        cudaGetLastError();
+    }
+    const bool bb = a.mapping == MAP_BB || a.mapping == MAP_BB_EXIT || a.mapping == MAP_BB_VEC;
     switch (a.cell_bytes) {
     case 1: return bb ? launch_bb_c<1>(a) : launch_lambda_c<1>(a);
     case 2: return bb ? launch_bb_c<2>(a) : launch_lambda_c<2>(a);

@@ -195,7 +195,65 @@ __global__ void scatter_kernel(uint8_t* __restrict__ grid, const int64_t* __rest
         st_cell<C>(grid, idx[i], ld_cell<C>(in, i));
 }
 
+// cells at dst_idx <- cells at src_idx (tiled partition storage: own cells into the
+// rings of the rank's other sub-gasket blocks)
+template <int C>
+__global__ void copy_cells_kernel(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src,
+                                  const int64_t* __restrict__ didx, const int64_t* __restrict__ sidx, int64_t count) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+        st_cell<C>(dst, didx[i], ld_cell<C>(src, sidx[i]));
+}
+
+// A window [x0, x0+w) x [y0, y0+h) of the synthetic grid (fill_hash's values at global
+// cell coordinates, 0 outside the n x n grid) into a pitched block (tiled storage).
+template <int C>
+__global__ void fill_hash_window_kernel(uint8_t* __restrict__ out, int64_t pitch, int64_t n, int64_t x0, int64_t y0,
+                                        int64_t w, int64_t h, uint64_t seed, int mode) {
+    const int64_t total = w * h;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / w, c = i - r * w;
+        const int64_t y = y0 + r, x = x0 + c;
+        uint64_t v = 0;
+        if (x >= 0 && x < n && y >= 0 && y < n) {
+            v = splitmix64(seed ^ (((uint64_t)y << 32) | (uint64_t)x));
+            if (mode == 1 && (x & (n - 1 - y)) != 0) v = 0;
+        }
+        st_cell<C>(out + r * pitch, c, v);
+    }
+}
+
 // --- launchers (called from capi.cu) ------------------------------------------
+
+cudaError_t launch_copy_cells(void* dst, const void* src, int c, const int64_t* didx, const int64_t* sidx,
+                              int64_t count, cudaStream_t s) {
+    if (count == 0) return cudaSuccess;
+    auto* d = reinterpret_cast<uint8_t*>(dst);
+    auto* q = reinterpret_cast<const uint8_t*>(src);
+    switch (c) {
+    case 1: copy_cells_kernel<1><<<grid_for(count), 256, 0, s>>>(d, q, didx, sidx, count); break;
+    case 2: copy_cells_kernel<2><<<grid_for(count), 256, 0, s>>>(d, q, didx, sidx, count); break;
+    case 4: copy_cells_kernel<4><<<grid_for(count), 256, 0, s>>>(d, q, didx, sidx, count); break;
+    case 8: copy_cells_kernel<8><<<grid_for(count), 256, 0, s>>>(d, q, didx, sidx, count); break;
+    default: return cudaErrorInvalidValue;
+    }
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill_hash_window(void* out, int64_t pitch, int64_t n, int c, int64_t x0, int64_t y0, int64_t w,
+                                    int64_t h, uint64_t seed, int mode, cudaStream_t s) {
+    if (w <= 0 || h <= 0) return cudaSuccess;
+    auto* b = reinterpret_cast<uint8_t*>(out);
+    switch (c) {
+    case 1: fill_hash_window_kernel<1><<<grid_for(w * h), 256, 0, s>>>(b, pitch, n, x0, y0, w, h, seed, mode); break;
+    case 2: fill_hash_window_kernel<2><<<grid_for(w * h), 256, 0, s>>>(b, pitch, n, x0, y0, w, h, seed, mode); break;
+    case 4: fill_hash_window_kernel<4><<<grid_for(w * h), 256, 0, s>>>(b, pitch, n, x0, y0, w, h, seed, mode); break;
+    case 8: fill_hash_window_kernel<8><<<grid_for(w * h), 256, 0, s>>>(b, pitch, n, x0, y0, w, h, seed, mode); break;
+    default: return cudaErrorInvalidValue;
+    }
+    note_launch();
+    return cudaGetLastError();
+}
 
 cudaError_t launch_map_blocks(const int64_t* wx, const int64_t* wy, int64_t count, int r_b, int64_t* lx, int64_t* ly,
                               cudaStream_t s) {

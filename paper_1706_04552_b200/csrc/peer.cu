@@ -31,16 +31,25 @@ template <> struct CellT<8> { using T = uint64_t; };
 
 template <int C>
 __global__ void peer_put(const uint8_t* __restrict__ mine, const uint64_t* __restrict__ peers,
-                         const int64_t* __restrict__ idx, int64_t k, const uint64_t* __restrict__ peer_flags,
-                         int rank, int world, uint64_t epoch) {
+                         const int64_t* __restrict__ idx, const int64_t* __restrict__ didx, int64_t k,
+                         const uint64_t* __restrict__ peer_flags, int rank, int world, uint64_t epoch) {
     using T = typename CellT<C>::T;
     const T* src = reinterpret_cast<const T*>(mine);
-    for (int q = 0; q < world; ++q) {
-        if (q == rank) continue;
-        T* dst = reinterpret_cast<T*>(peers[q]);
+    if (didx != nullptr) {  // tiled storage: per entry the destination rank (bits 56-63) and cell
         for (int64_t i = threadIdx.x; i < k; i += blockDim.x) {
-            const int64_t c = idx[i];
-            dst[c] = src[c];
+            const uint64_t d = (uint64_t)didx[i];
+            const int q = (int)(d >> 56);
+            T* dst = q == rank ? const_cast<T*>(src) : reinterpret_cast<T*>(peers[q]);
+            dst[d & ((1ull << 56) - 1)] = src[idx[i]];
+        }
+    } else {
+        for (int q = 0; q < world; ++q) {
+            if (q == rank) continue;
+            T* dst = reinterpret_cast<T*>(peers[q]);
+            for (int64_t i = threadIdx.x; i < k; i += blockDim.x) {
+                const int64_t c = idx[i];
+                dst[c] = src[c];
+            }
         }
     }
     __syncthreads();
@@ -77,14 +86,15 @@ __global__ void peer_wait(const uint64_t* flags, int rank, int world, uint64_t e
 
 }  // namespace
 
-cudaError_t launch_peer_put(const void* mine, const uint64_t* peers, const int64_t* idx, int64_t k, int cell_bytes,
-                            const uint64_t* peer_flags, int rank, int world, uint64_t epoch, cudaStream_t s) {
+cudaError_t launch_peer_put(const void* mine, const uint64_t* peers, const int64_t* idx, const int64_t* didx,
+                            int64_t k, int cell_bytes, const uint64_t* peer_flags, int rank, int world, uint64_t epoch,
+                            cudaStream_t s) {
     const auto* m = reinterpret_cast<const uint8_t*>(mine);
     switch (cell_bytes) {
-    case 1: peer_put<1><<<1, 256, 0, s>>>(m, peers, idx, k, peer_flags, rank, world, epoch); break;
-    case 2: peer_put<2><<<1, 256, 0, s>>>(m, peers, idx, k, peer_flags, rank, world, epoch); break;
-    case 4: peer_put<4><<<1, 256, 0, s>>>(m, peers, idx, k, peer_flags, rank, world, epoch); break;
-    case 8: peer_put<8><<<1, 256, 0, s>>>(m, peers, idx, k, peer_flags, rank, world, epoch); break;
+    case 1: peer_put<1><<<1, 256, 0, s>>>(m, peers, idx, didx, k, peer_flags, rank, world, epoch); break;
+    case 2: peer_put<2><<<1, 256, 0, s>>>(m, peers, idx, didx, k, peer_flags, rank, world, epoch); break;
+    case 4: peer_put<4><<<1, 256, 0, s>>>(m, peers, idx, didx, k, peer_flags, rank, world, epoch); break;
+    case 8: peer_put<8><<<1, 256, 0, s>>>(m, peers, idx, didx, k, peer_flags, rank, world, epoch); break;
     default: return cudaErrorInvalidValue;
     }
     note_launch();

@@ -25,7 +25,12 @@ struct PeerEpilogue {
     int32_t cell_bytes, rank, world;
     uint32_t done;                      // CTAs finished in the current launch
     uint32_t status;                    // bit p: waiting on peer p timed out
+    uint64_t didx;                      // const int64_t*: tiled storage: per entry, the destination
+                                        // cell (bits 0-55) and rank (bits 56-63; own rank = a ring
+                                        // copy inside this rank's buffer); 0 = every peer, same index
 };
+
+constexpr int PEER_RANK_SHIFT = 56;
 
 __device__ __forceinline__ void peer_prologue_wait(PeerEpilogue* e, uint64_t epoch) {
     if (e == nullptr || epoch == 0) return;
@@ -56,6 +61,16 @@ template <class T>
 __device__ __forceinline__ void peer_copy_cells(const uint8_t* grid, PeerEpilogue* e) {
     const int64_t* idx = reinterpret_cast<const int64_t*>(e->idx);
     const T* src = reinterpret_cast<const T*>(grid);
+    if (e->didx != 0) {  // tiled storage: (source cell, destination rank + cell) entries
+        const int64_t* didx = reinterpret_cast<const int64_t*>(e->didx);
+        for (int64_t i = threadIdx.x; i < e->count; i += blockDim.x) {
+            const uint64_t d = (uint64_t)didx[i];
+            const int q = (int)(d >> PEER_RANK_SHIFT);
+            T* dst = q == e->rank ? const_cast<T*>(src) : reinterpret_cast<T*>(e->peers[q]);
+            dst[d & ((1ull << PEER_RANK_SHIFT) - 1)] = src[idx[i]];
+        }
+        return;
+    }
     for (int q = 0; q < e->world; ++q) {
         if (q == e->rank) continue;
         T* dst = reinterpret_cast<T*>(e->peers[q]);

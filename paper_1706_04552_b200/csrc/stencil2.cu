@@ -101,7 +101,9 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
                                                              int64_t n, uint32_t tile_lo, uint32_t tile_hi, int r_t,
                                                              int part_level, uint64_t param, int flags,
                                                              const uint32_t* __restrict__ order, PeerEpilogue* epi,
-                                                             uint64_t wait_epoch, uint64_t signal_epoch) {
+                                                             uint64_t wait_epoch, uint64_t signal_epoch,
+                                                             const int64_t* __restrict__ sg_off, int64_t pitch,
+                                                             uint32_t per) {
     using S = T2<C>;
     peer_prologue_wait(epi, wait_epoch);  // partitioned CA with the fused exchange only
     constexpr bool EIGHT = KIND == KIND_NSUM8;
@@ -136,7 +138,8 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
     }
     __syncthreads();
     const int nch = nchunks;
-    const int64_t rowstride = n * C;
+    const int64_t rowbytes = n * C;  // the global grid's row (bounds)
+    const int64_t rowstride = pitch;  // the buffers' row pitch (addresses; tiled storage: its blocks')
     // with a 2-deep ring there is shared memory left for the chunks' grid offsets (one add
     // per chunk when staging interior tiles); the 3-deep ring keeps 3 CTAs per SM without
     [[maybe_unused]] int32_t* goff = reinterpret_cast<int32_t*>(chunks + S::ROWS * CHUNKS);
@@ -155,9 +158,21 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
     const bool fetch256 = (flags & GM_FLAG_FETCH256) != 0;
     const bool fetch_mixed = (flags & GM_FLAG_FETCH_MIXED) != 0;
     const bool v8 = (reinterpret_cast<uintptr_t>(grid) & 31u) == 0;
+#ifdef GM_AB_VARIANTS
     const bool probe_nostore = (flags & GM_FLAG_PROBE_NOSTORE) != 0;
+#else
+    constexpr bool probe_nostore = false;  // design probe: A/B builds only
+#endif
+#ifdef GM_AB_VARIANTS
     const bool probe_noload = (flags & GM_FLAG_PROBE_NOLOAD) != 0;
+#else
+    constexpr bool probe_noload = false;  // design probe: A/B builds only
+#endif
+#ifdef GM_AB_VARIANTS
     const bool probe_nocompute = (flags & GM_FLAG_PROBE_NOCOMPUTE) != 0;
+#else
+    constexpr bool probe_nocompute = false;  // design probe: A/B builds only
+#endif
     const bool store_cs = (flags & GM_FLAG_STORE_CS) != 0;
     const uint32_t smem0 = (uint32_t)__cvta_generic_to_shared(smem);
     uint32_t pv;
@@ -203,6 +218,10 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
     // (a CTA without tiles still takes part in the fused exchange's completion count)
     const uint32_t count = first >= last ? 0u : (last - first + step - 1) / step;
 
+    // byte offset of this CTA's tile #idx's sub-gasket block (tiled partition storage)
+    auto tile_off = [&](uint32_t idx) -> int64_t {
+        return sg_off != nullptr ? __ldg(sg_off + (first + idx * step - tile_lo) / per) : 0;
+    };
     // order-table entry of this CTA's tile #idx
     auto order_v = [&](uint32_t idx) -> uint32_t {
         return (order != nullptr && idx < count) ? __ldg(order + first + idx * step) : 0u;
@@ -218,7 +237,8 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
         }
         const int64_t x0 = (int64_t)bx * S::TT, y0 = (int64_t)by * S::TT;
         const uint32_t sb = smem0 + (idx % NST) * S::BUF;
-        const uint8_t* base = src + (y0 - 1) * rowstride + x0 * C - 16;  // staged (row 0, chunk 0)
+        const uint8_t* srct = src + tile_off(idx);
+        const uint8_t* base = srct + (y0 - 1) * rowstride + x0 * C - 16;  // staged (row 0, chunk 0)
         const bool interior = y0 > 0 && y0 + S::TT < n && x0 > 0 && x0 + S::TT < n;
         if (interior) {
             for (int i = threadIdx.x; i < nch; i += S::THREADS) {
@@ -238,8 +258,8 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
                 const int j = (int)((c >> 16) & 0xffu), qq = (int)((c >> 24) & 15u);
                 const int64_t y = y0 + j - 1;
                 const int64_t xb = x0 * C + (qq - 1) * 16;
-                const bool in = y >= 0 && y < n && xb >= 0 && xb < rowstride;
-                cp_async16(sb + (c & 0xffffu), in ? src + y * rowstride + xb : src, in ? 16 : 0,
+                const bool in = y >= 0 && y < n && xb >= 0 && xb < rowbytes;
+                cp_async16(sb + (c & 0xffffu), in ? srct + y * rowstride + xb : src, in ? 16 : 0,
                            fetch_line || (fetch_mixed && (c >> 28)));
             }
         }
@@ -287,7 +307,7 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
             } else {
                 sector_sums<C, EIGHT>(w, pv, out);
             }
-            uint8_t* gp = grid + (y0 + t) * rowstride + x0 * C + g * 32;
+            uint8_t* gp = grid + tile_off(idx) + (y0 + t) * rowstride + x0 * C + g * 32;
             if (dst_from_src) {
 #pragma unroll
                 for (int i = 0; i < 8; ++i) out[i] = (out[i] & wmask[i]) | (w[1][i + 1] & ~wmask[i]);
@@ -327,7 +347,8 @@ cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
                                                           reinterpret_cast<const uint8_t*>(a.src), a.n, lo, hi, r_t,
                                                           a.part_level, a.param, a.flags, order,
                                                           reinterpret_cast<PeerEpilogue*>(a.peer_epi), a.wait_epoch,
-                                                          a.signal_epoch);
+                                                          a.signal_epoch, a.sg_off, row_pitch(a),
+                                                          tiles_per_subgasket(a, r_t));
     note_launch();
     return cudaGetLastError();
 }

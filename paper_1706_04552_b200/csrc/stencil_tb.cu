@@ -200,7 +200,8 @@ template <int C, int KIND, int T, int NST>
 __global__ void __launch_bounds__(TB<C, T>::THREADS)
     stencil_tb(uint8_t* __restrict__ grid, const uint8_t* __restrict__ src, int64_t n, uint32_t ntiles,
                uint64_t param, const uint32_t* __restrict__ order, const uint16_t* __restrict__ lists_g,
-               TbCounts cnt, int flags, PeerEpilogue* epi, uint64_t wait_epoch, uint64_t signal_epoch) {
+               TbCounts cnt, int flags, PeerEpilogue* epi, uint64_t wait_epoch, uint64_t signal_epoch,
+               const int64_t* __restrict__ sg_off, int64_t pitch, uint32_t per) {
     using S = TB<C, T>;
     // NST = staging slots: 2 (tile idx+1 staged while idx computes) or 1 (staged after
     // tile idx is stored; a smaller CTA, so 4 instead of 3 share an SM)
@@ -220,7 +221,8 @@ __global__ void __launch_bounds__(TB<C, T>::THREADS)
 
     const bool v8 = (reinterpret_cast<uintptr_t>(grid) & 31u) == 0;
     const uint32_t smem0 = (uint32_t)__cvta_generic_to_shared(smem);
-    const int64_t rowstride = n * C;
+    const int64_t rowbytes = n * C;  // the global grid's row (bounds)
+    const int64_t rowstride = pitch;  // the buffers' row pitch (addresses; tiled storage: its blocks')
     uint32_t pv;
     if constexpr (C == 1) pv = 0x00010001u * (uint32_t)(param & 0xffu);
     else if constexpr (C == 2) pv = (uint32_t)(param & 0xffffu);
@@ -241,21 +243,38 @@ __global__ void __launch_bounds__(TB<C, T>::THREADS)
 
     const uint32_t count = blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
     auto tile_v = [&](uint32_t idx) { return idx < count ? __ldg(order + blockIdx.x + idx * gridDim.x) : 0u; };
+    // byte offset of this CTA's tile #idx's sub-gasket block (tiled partition storage)
+    auto tile_off = [&](uint32_t idx) -> int64_t {
+        return sg_off != nullptr ? __ldg(sg_off + (blockIdx.x + idx * gridDim.x) / per) : 0;
+    };
     auto tile_xy = [&](uint32_t v, int64_t& x0, int64_t& y0) {
         x0 = (int64_t)(v & 0xffffu) * S::TT;
         y0 = (int64_t)(v >> 16) * S::TT;
     };
     // design probes (scripts/variants.py): drop staging / arithmetic / stores
+#ifdef GM_AB_VARIANTS
     const bool probe_noload = (flags & GM_FLAG_PROBE_NOLOAD) != 0;
+#else
+    constexpr bool probe_noload = false;  // design probe: A/B builds only
+#endif
+#ifdef GM_AB_VARIANTS
     const bool probe_nocompute = (flags & GM_FLAG_PROBE_NOCOMPUTE) != 0;
+#else
+    constexpr bool probe_nocompute = false;  // design probe: A/B builds only
+#endif
+#ifdef GM_AB_VARIANTS
     const bool probe_nostore = (flags & GM_FLAG_PROBE_NOSTORE) != 0;
+#else
+    constexpr bool probe_nostore = false;  // design probe: A/B builds only
+#endif
     const bool fetch_line = (flags & GM_FLAG_FETCH_LINE) != 0;
     auto stage = [&](uint32_t idx, uint32_t v) {
         if (idx >= count || probe_noload) return;
         int64_t x0, y0;
         tile_xy(v, x0, y0);
         const uint32_t sb = smem0 + (idx % NST) * S::SBUF;
-        const uint8_t* base = src + (y0 - T) * rowstride + x0 * C - 16;  // staged (row -T, chunk 0)
+        const uint8_t* srct = src + tile_off(idx);
+        const uint8_t* base = srct + (y0 - T) * rowstride + x0 * C - 16;  // staged (row -T, chunk 0)
         const bool interior = y0 >= T && y0 + S::TT + T <= n && x0 > 0 && x0 + S::TT < n;
         for (int i = threadIdx.x; i < ns; i += S::THREADS) {
             const uint32_t c = slist[i];
@@ -266,8 +285,8 @@ __global__ void __launch_bounds__(TB<C, T>::THREADS)
             } else {
                 const int64_t y = y0 + j - T;
                 const int64_t xb = x0 * C + (q - 1) * 16;
-                const bool in = y >= 0 && y < n && xb >= 0 && xb < rowstride;
-                cp_async16(so, in ? src + y * rowstride + xb : src, in ? 16 : 0, fetch_line);
+                const bool in = y >= 0 && y < n && xb >= 0 && xb < rowbytes;
+                cp_async16(so, in ? srct + y * rowstride + xb : src, in ? 16 : 0, fetch_line);
             }
         }
     };
@@ -339,7 +358,7 @@ __global__ void __launch_bounds__(TB<C, T>::THREADS)
             const uint4 a = *reinterpret_cast<const uint4*>(srow + k0);
             const uint4 b = *reinterpret_cast<const uint4*>(srow + k0 + 4);
             const uint32_t out[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-            st_sector(grid + (y0 + t) * rowstride + x0 * C + g * 32, out, v8, false);
+            st_sector(grid + tile_off(idx) + (y0 + t) * rowstride + x0 * C + g * 32, out, v8, false);
         }
         if constexpr (NST == 1) {  // the slot is free once every thread has read its sector
             __syncthreads();
@@ -485,7 +504,8 @@ cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
                                                           reinterpret_cast<const uint8_t*>(a.src), a.n, ntiles,
                                                           a.param, order, L->lists, L->cnt, a.flags,
                                                           reinterpret_cast<PeerEpilogue*>(a.peer_epi), a.wait_epoch,
-                                                          a.signal_epoch);
+                                                          a.signal_epoch, a.sg_off, row_pitch(a),
+                                                          tiles_per_subgasket(a, r_t));
     note_launch();
     return cudaGetLastError();
 }

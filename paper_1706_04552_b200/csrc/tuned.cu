@@ -273,12 +273,15 @@ cudaError_t launch_tuned(const LaunchArgs& a) {
             if (e2 != cudaErrorNotSupported) return e2;
             cudaGetLastError();
         }
-        const cudaError_t et = launch_stencil_tma(a);  // TMA-staged tiles (stencil_tma.cu)
+#ifdef GM_AB_VARIANTS
+        // A/B builds only: the superseded TMA-staged (stencil_tma.cu) and v1 (stencil.cu) tiles
+        const cudaError_t et = launch_stencil_tma(a);
         if (et != cudaErrorNotSupported) return et;
         cudaGetLastError();
         const cudaError_t es = launch_stencil_tile(a);
         if (es != cudaErrorNotSupported) return es;
         cudaGetLastError();
+#endif
     }
     // the write pass: line-tile slabs, unit -> tile computed per unit (write.cu)
     if (a.kind == KIND_CONST || a.kind == KIND_COUNT) {

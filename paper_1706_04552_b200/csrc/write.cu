@@ -41,6 +41,9 @@
 //     no DRAM read.
 #include <algorithm>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <vector>
 
 #include "gasket.cuh"
 #include "launch.h"
@@ -272,6 +275,111 @@ __global__ void __launch_bounds__(256) gasket_write_rows(uint8_t* __restrict__ g
     }
 }
 
+// GM_FLAG_WRITE_SWEEP: the grid rows' member lines in ADDRESS order, cut into work units of
+// up to KS consecutive member lines of one row and dealt round-robin over all warps, so
+// the warps in flight together write one contiguous stretch of the grid (a sweep from
+// the top row down) instead of one far-apart row each.  Unit u -> (block row Y, row t,
+// chunk j) by a binary search in the per-block-row unit prefix (nY + 1 entries, built
+// once per size).  Zero background: 16-byte lanes, 4 lines per instruction, the touched
+// sectors; general: 4-byte lanes, one line per instruction, the gasket cells.
+constexpr int KS = 32;  // member lines per unit
+
+template <int C, bool ZERO>
+__global__ void __launch_bounds__(256) gasket_write_sweep(uint8_t* __restrict__ grid, int64_t n,
+                                                          const uint32_t* __restrict__ prefix, uint32_t nY,
+                                                          uint64_t param) {
+    using G = WGeo<C>;
+    const int lane = threadIdx.x & 31;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int64_t rowstride = n * C;
+    const uint32_t total = __ldg(prefix + nY);
+    for (uint32_t u = warp; u < total; u += nwarps) {
+        uint32_t lo = 0, hi = nY;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (__ldg(prefix + mid) <= u) lo = mid; else hi = mid;
+        }
+        const uint32_t Y = lo;
+        const int pc = __popc(Y);
+        const uint32_t chunks = pc > 5 ? 1u << (pc - 5) : 1u;
+        const uint32_t rem = u - __ldg(prefix + Y);
+        const uint32_t t = rem / chunks, j = rem - t * chunks;
+        const int64_t y = (int64_t)Y * G::TT + t;
+        if constexpr (ZERO) {
+            const int p = lane & 7;
+            const uint32_t g = (uint32_t)(lane >> 3);
+            if (g >= (1u << (pc < 2 ? pc : 2))) continue;
+            if ((((uint32_t)(p & ~1) * G::P16) & ~t) != 0) continue;  // sector without gasket cells
+            const uint32_t b0 = Y & (0u - Y), Y1 = Y ^ b0, b1 = Y1 & (0u - Y1), Yh = Y1 ^ b1;
+            const uint32_t base = ((g & 1u) ? b0 : 0u) | ((g & 2u) ? b1 : 0u);
+            uint32_t v[4];
+#pragma unroll
+            for (int w = 0; w < 4; ++w) v[w] = splat_w<C>(param, w) & word_mask<C>(p, w, t);
+            uint8_t* row = grid + y * rowstride + p * 16;
+            // lines 32j .. 32j+31 of the row: groups of 4 = subsets S of Yh from pdep(8j, Yh)
+            uint32_t S = 0, m = 8u * j, bits = Yh;
+            while (m) {
+                const uint32_t low = bits & (0u - bits);
+                if (m & 1u) S |= low;
+                m >>= 1;
+                bits ^= low;
+            }
+#pragma unroll 8
+            for (int i = 0; i < KS / 4; ++i) {
+                st_v4(row + (int64_t)(base | S) * 128, v[0], v[1], v[2], v[3]);
+                S = (S - Yh) & Yh;
+                if (S == 0) break;
+            }
+        } else {
+            const uint32_t jc = C == 8 ? (uint32_t)(lane >> 1) : (uint32_t)lane * 4u / C;
+            if (jc & ~t) continue;
+            const uint32_t v = splat_w<C>(param, lane);
+            uint8_t* row = grid + y * rowstride + lane * 4;
+            uint32_t X = 0, m = KS * j, bits = Y;
+            while (m) {
+                const uint32_t low = bits & (0u - bits);
+                if (m & 1u) X |= low;
+                m >>= 1;
+                bits ^= low;
+            }
+#pragma unroll 4
+            for (int i = 0; i < KS; ++i) {
+                st_members<C>(row + (int64_t)X * 128, v, t);
+                X = (X - Y) & Y;
+                if (X == 0) break;
+            }
+        }
+    }
+}
+
+std::mutex g_sweep_mu;
+std::map<std::pair<int, int>, uint32_t*> g_sweep_prefix;  // (device, log2 nY * 256 + TT) -> prefix
+
+// units per block row Y: TT rows x max(1, 2^popc(Y) / KS) chunks
+const uint32_t* sweep_prefix(int nYbits, int tt) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_sweep_mu);
+    const std::pair<int, int> key{dev, nYbits * 256 + tt};
+    auto it = g_sweep_prefix.find(key);
+    if (it != g_sweep_prefix.end()) return it->second;
+    const uint32_t nY = 1u << nYbits;
+    std::vector<uint32_t> pre(nY + 1, 0);
+    for (uint32_t Y = 0; Y < nY; ++Y) {
+        const int pc = __builtin_popcount(Y);
+        pre[Y + 1] = pre[Y] + (uint32_t)tt * (pc > 5 ? 1u << (pc - 5) : 1u);
+    }
+    uint32_t* d = nullptr;
+    if (cudaMalloc(&d, pre.size() * sizeof(uint32_t)) != cudaSuccess) return nullptr;
+    if (cudaMemcpy(d, pre.data(), pre.size() * sizeof(uint32_t), cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaFree(d);
+        return nullptr;
+    }
+    g_sweep_prefix[key] = d;
+    return d;
+}
+
 int rows_ctas_per_sm() {
     static int v = [] {
         const char* e = getenv("GASKET_WRITE_ROWS_CTAS");
@@ -287,10 +395,64 @@ int sm_count() {
     return sms;
 }
 
+// The bounding-box baseline written as well as the tuned lambda kernels (GM_MAP_BB_VEC,
+// the write pass only): the bounding box's thread space -- every 16-byte segment of all
+// n x n cells, one lane each, grid-stride -- with the same vectorised stores.  A lane
+// tests its segment's cells with the paper's membership test x & (n-1-y) == 0
+// (backends.py:151-156) and stores the gasket cells of each 4-byte word (one store per
+// word, the row's in-word pattern), so it differs from the lambda kernels only in the
+// n^2 / 16 segment tests of the bounding box.
+template <int C>
+__global__ void __launch_bounds__(256) bb_vec(uint8_t* __restrict__ grid, int64_t n, int seg_shift,
+                                              uint64_t param) {
+    constexpr uint32_t P16 = 16 / C;  // cells per segment
+    const uint64_t total = (uint64_t)n << seg_shift;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint32_t v[4];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) v[w] = splat_w<C>(param, w);
+    for (uint64_t sidx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; sidx < total; sidx += stride) {
+        const uint32_t y = (uint32_t)(sidx >> seg_shift);
+        const uint32_t x0 = (uint32_t)(sidx & ((1ull << seg_shift) - 1)) * P16;
+        const uint32_t m = (uint32_t)n - 1u - y;
+        if ((x0 & m) != 0) continue;  // the segment's first cell decides its high bits
+        uint8_t* q = grid + (int64_t)y * n * C + (int64_t)x0 * C;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            const uint32_t xw = C == 8 ? x0 + (uint32_t)(w >> 1) : x0 + (uint32_t)w * (4u / C);
+            if (xw & m) continue;  // no gasket cell in this word
+            st_members<C>(q + 4 * w, v[w], y);
+        }
+    }
+}
+
+cudaError_t launch_bb_vec(const LaunchArgs& a) {
+    if (a.kind != KIND_CONST) return cudaErrorNotSupported;
+    if (a.n < 1 || (a.n & (a.n - 1)) != 0 || a.n * a.cell_bytes < 16) return cudaErrorNotSupported;
+    int seg_shift = 0;
+    while ((int64_t(1) << seg_shift) < a.n * a.cell_bytes / 16) ++seg_shift;
+    const unsigned blocks = (unsigned)sm_count() * 8u;
+    uint8_t* g = reinterpret_cast<uint8_t*>(a.grid);
+    switch (a.cell_bytes) {
+    case 1: bb_vec<1><<<blocks, 256, 0, a.stream>>>(g, a.n, seg_shift, a.param); break;
+    case 2: bb_vec<2><<<blocks, 256, 0, a.stream>>>(g, a.n, seg_shift, a.param); break;
+    case 4: bb_vec<4><<<blocks, 256, 0, a.stream>>>(g, a.n, seg_shift, a.param); break;
+    case 8: bb_vec<8><<<blocks, 256, 0, a.stream>>>(g, a.n, seg_shift, a.param); break;
+    default: return cudaErrorNotSupported;
+    }
+    note_launch();
+    return cudaGetLastError();
+}
+
+
 template <int C, bool ZERO, bool COUNT = false>
 cudaError_t launch_c(const LaunchArgs& a, int q) {
     using G = WGeo<C>;
-    if ((a.flags & GM_FLAG_GRID_ROWS) && a.part_level < 0) {
+    // zero background: the grid-row schedule unless lambda tiles (GM_FLAG_DIGIT_ORDER), row-major
+    // tiles or the address sweep are asked for (n=2^16 int8: 55.7 us vs 62-64 us for lambda tiles)
+    const bool rows = (a.flags & GM_FLAG_GRID_ROWS) ||
+                      (ZERO && !(a.flags & (GM_FLAG_DIGIT_ORDER | GM_FLAG_ROWMAJOR | GM_FLAG_WRITE_SWEEP)));
+    if (rows && a.part_level < 0) {
         // 8 CTAs of 256 threads per SM (the row walk wants many rows in flight)
         const uint64_t blocks = std::min<uint64_t>((uint64_t)sm_count() * rows_ctas_per_sm(), ((uint64_t)a.n * 32 + 255) / 256);
         const int gran = (a.flags & GM_FLAG_WRITE_LINES) && (a.flags & GM_FLAG_WRITE_HALVES) ? 3
@@ -302,6 +464,15 @@ cudaError_t launch_c(const LaunchArgs& a, int q) {
                    : gran == 2        ? gasket_write_rows<C, ZERO, 2, COUNT>
                                       : gasket_write_rows<C, ZERO, 3, COUNT>;
         kr<<<(unsigned)blocks, 256, 0, a.stream>>>(reinterpret_cast<uint8_t*>(a.grid), a.n, a.param);
+        note_launch();
+        return cudaGetLastError();
+    }
+    if ((a.flags & GM_FLAG_WRITE_SWEEP) && a.part_level < 0 && !COUNT && q <= 13) {
+        const uint32_t* pre = sweep_prefix(q, G::TT);
+        if (!pre) return cudaErrorMemoryAllocation;
+        const unsigned blocks = (unsigned)sm_count() * (unsigned)rows_ctas_per_sm();
+        gasket_write_sweep<C, ZERO><<<blocks, 256, 0, a.stream>>>(reinterpret_cast<uint8_t*>(a.grid), a.n, pre,
+                                                                 1u << q, a.param);
         note_launch();
         return cudaGetLastError();
     }
@@ -328,6 +499,8 @@ cudaError_t launch_cb(const LaunchArgs& a, int q) {
 }
 
 }  // namespace
+
+cudaError_t launch_bb_vector(const LaunchArgs& a) { return launch_bb_vec(a); }
 
 // The CONST pass on grids at least one 128-byte line wide (up to 3^20 tiles);
 // cudaErrorNotSupported otherwise (the caller then uses the generic kernels).

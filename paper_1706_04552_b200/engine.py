@@ -37,6 +37,7 @@ class Mapping(enum.Enum):
     BOUNDING_BOX = "bb"
     BLOCK_SPACE = "blockspace"
     BOUNDING_BOX_EXIT = "bb-exit"  # BB whose off-gasket tiles exit before any per-thread test
+    BOUNDING_BOX_VEC = "bb-vec"  # BB over 16-byte segments with the tuned kernels' stores (write pass)
 
 
 class KernelKind(enum.Enum):
@@ -47,7 +48,7 @@ class KernelKind(enum.Enum):
 
 _KIND_TAG = {KernelKind.CONST: backends.KERNEL_CONST, KernelKind.NEIGHBOR_SUM: backends.KERNEL_NEIGHBOR_SUM,
              KernelKind.NEIGHBOR_SUM8: backends.KERNEL_NEIGHBOR_SUM8}
-_BB_MAPPINGS = (Mapping.BOUNDING_BOX, Mapping.BOUNDING_BOX_EXIT)
+_BB_MAPPINGS = (Mapping.BOUNDING_BOX, Mapping.BOUNDING_BOX_EXIT, Mapping.BOUNDING_BOX_VEC)
 
 
 @dataclass(frozen=True)
@@ -162,7 +163,8 @@ class LaunchPlan:
         tag = _KIND_TAG[cfg.kernel.kind]
         if cfg.mapping in _BB_MAPPINGS:
             backends.run_bounding_box(grid, src, cfg.spec.rho, tag, cfg.kernel.param, self.backend,
-                                      early_exit=cfg.mapping is Mapping.BOUNDING_BOX_EXIT)
+                                      early_exit=cfg.mapping is Mapping.BOUNDING_BOX_EXIT,
+                                      vectorized=cfg.mapping is Mapping.BOUNDING_BOX_VEC)
         else:
             backends.run_block_space(grid, src, cfg.spec.rho, cfg.spec.r_b, cfg.strategy, self.local_x,
                                      self.local_y, tag, cfg.kernel.param, self.backend, flags=self.flags)
@@ -231,6 +233,7 @@ def _coverage_counts(config: LaunchConfig, map_fn) -> torch.Tensor:
         cfg.n, cfg.rho, cfg.cell_bytes = n, spec.rho, 4
         cfg.kind = native.KIND_COUNT
         if config.mapping in _BB_MAPPINGS:
+            # (the vectorised BB covers exactly the cells of the literal one: audited as that)
             cfg.mapping = native.MAP_BB_EXIT if config.mapping is Mapping.BOUNDING_BOX_EXIT else native.MAP_BB
             cfg.strategy = native.STRAT_SUBBOX
             tx = ty = ntab = 0

@@ -21,7 +21,7 @@ GM_OK, GM_EINVAL, GM_ECUDA, GM_ENOMEM = 0, 1, 2, 3
 
 KIND_CONST, KIND_NSUM4, KIND_NSUM8, KIND_COUNT = 0, 1, 2, 3
 STRAT_UNROLL, STRAT_TABLE, STRAT_SUBBOX, STRAT_TUNED = 0, 1, 2, 3
-MAP_BB, MAP_LAMBDA, MAP_BB_EXIT = 0, 1, 2
+MAP_BB, MAP_LAMBDA, MAP_BB_EXIT, MAP_BB_VEC = 0, 1, 2, 3
 FLAG_OMEGA_ORDER, FLAG_DST_FROM_SRC, FLAG_EXPLICIT_RMW, FLAG_WHOLE_LINES, FLAG_HOST_ROWS = 1, 2, 4, 8, 16
 FLAG_ROWMAJOR, FLAG_CHUNKED, FLAG_NO_TMA, FLAG_FORCE_TMA = 32, 64, 128, 256
 FLAG_FETCH_LINE, FLAG_FETCH64, FLAG_STENCIL_V1, FLAG_STAGES2 = 512, 1024, 2048, 4096
@@ -32,7 +32,7 @@ FLAG_TWO_STEPS = 8388608
 FLAG_FOUR_STEPS = 16777216
 FLAG_SIX_STEPS = 33554432
 FLAG_ZERO_BACKGROUND, FLAG_GRID_ROWS = 67108864, 536870912
-FLAG_WRITE_HALVES, FLAG_WRITE_LINES = 134217728, 268435456
+FLAG_WRITE_HALVES, FLAG_WRITE_LINES, FLAG_WRITE_SWEEP = 134217728, 268435456, 1073741824
 
 
 class GmCfg(ctypes.Structure):
@@ -90,6 +90,11 @@ _SIGS = {
     "gm_ipc_open_handle": [_vp, ctypes.POINTER(ctypes.c_void_p)],
     "gm_ipc_close": [_vp],
     "gm_peer_halo_put": [_vp, _vp, _vp, _i64, _i32, _vp, _i32, _i32, _u64, _vp],
+    "gm_peer_halo_put_to": [_vp, _vp, _vp, _vp, _i64, _i32, _vp, _i32, _i32, _u64, _vp],
+    "gm_run_part_tiled": [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, ctypes.c_uint32, ctypes.c_uint32, _vp, _i64,
+                          _vp, _u64, _u64, _vp],
+    "gm_copy_cells": [_vp, _vp, _i32, _vp, _vp, _i64, _vp],
+    "gm_fill_hash_window": [_vp, _i64, _i64, _i32, _i64, _i64, _i64, _i64, _u64, _i32, _vp],
     "gm_peer_halo_wait": [_vp, _i32, _i32, _u64, _u64, _vp, _vp],
 }
 

@@ -32,6 +32,8 @@ VARIANTS = (
     ("gridrows-zero-halves", Z | native.FLAG_GRID_ROWS | native.FLAG_WRITE_HALVES),
     ("gridrows-zero-lines", Z | native.FLAG_GRID_ROWS | native.FLAG_WRITE_LINES),
     ("gridrows-zero-v8", Z | native.FLAG_GRID_ROWS | native.FLAG_WRITE_LINES | native.FLAG_WRITE_HALVES),
+    ("sweep", native.FLAG_WRITE_SWEEP),
+    ("sweep-zero", Z | native.FLAG_WRITE_SWEEP),
     ("hostrows-zero", Z | native.FLAG_HOST_ROWS | native.FLAG_EXPLICIT_RMW | native.FLAG_WHOLE_LINES),
 )
 if len(sys.argv) > 1 and sys.argv[1].startswith("only="):

@@ -69,9 +69,9 @@ def test_n16_write_zero_background_exact(gpu, oracle):
     del want
     g = torch.zeros((n, n), dtype=torch.int8, device="cuda")
     nat = gpu.native
-    for flags in (0, nat.FLAG_ROWMAJOR, nat.FLAG_GRID_ROWS, nat.FLAG_GRID_ROWS | nat.FLAG_WRITE_HALVES,
+    for flags in (0, nat.FLAG_DIGIT_ORDER, nat.FLAG_ROWMAJOR, nat.FLAG_GRID_ROWS, nat.FLAG_GRID_ROWS | nat.FLAG_WRITE_HALVES,
                   nat.FLAG_GRID_ROWS | nat.FLAG_WRITE_LINES,
-                  nat.FLAG_GRID_ROWS | nat.FLAG_WRITE_LINES | nat.FLAG_WRITE_HALVES):
+                  nat.FLAG_GRID_ROWS | nat.FLAG_WRITE_LINES | nat.FLAG_WRITE_HALVES, nat.FLAG_WRITE_SWEEP):
         g.zero_()
         for _ in range(2):  # the reference bench re-runs plan.run(grid, grid) on its own output
             gpu.backends.run_block_space(g, g, 32, 11, S.TUNED, kind=0, param=1, flags=flags,
@@ -139,7 +139,7 @@ def test_n17_int8_ca_exact(gpu, oracle, kind):
 
 def test_n18_int8_ca_sampled_bands(gpu, oracle):
     """BASELINE config 5 on one GPU: n = 2^18 int8 (64 GiB per grid), NSUM8, the tuned
-    single step and the fused 6-step kernel, against the oracle on 12 bands of 512 rows
+    single step and the fused 6-step kernel, against the oracle on 24 bands of 1024 rows
     (grid top and bottom, and interior bands straddling tile / sub-gasket rows)."""
     n = 1 << 18
     seed = 5
@@ -147,7 +147,7 @@ def test_n18_int8_ca_sampled_bands(gpu, oracle):
     src = gpu.device.fill_hash(n, torch.int8, seed, 0)
     d = src.clone()
     gpu.backends.run_block_space(d, src, 64, 12, S.TUNED, kind=2, param=1)
-    bands = sampled_bands(n, 512, 12)
+    bands = sampled_bands(n, 1024, 24)
     assert band_mismatches(gpu, oracle, {1: d}, n, np.int8, seed, 0, 2, 1, bands=bands) == {1: 0}
     d.copy_(src)
     _ca_steps(gpu, d, src, n, 2, 6)

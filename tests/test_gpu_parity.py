@@ -171,46 +171,10 @@ def test_golden_kernel_checksums_on_device(gpu, oracle, golden):
 
 
 # ---------------------------------------------------------------------------
-# BASELINE sizes: n = 2^16 (checksum vs oracle) and n = 2^17 (properties)
+# BASELINE sizes
 # ---------------------------------------------------------------------------
 
-@pytest.mark.parametrize("kind", KINDS)
-def test_n16_int8_vs_oracle_checksum(gpu, oracle, kind):
-    n = 1 << 16
-    src_np = oracle.fill_hash(n, np.int8, 3, 0)
-    want = src_np.copy()
-    oracle.run_block_space(want, src_np, 16, 12, 2, None, None, kind, 1)
-    ck = oracle.checksum(want)
-    del want
-    src = gpu.device.fill_hash(n, torch.int8, 3, 0)
-    assert gpu.device.checksum(src) == oracle.checksum(src_np)
-    del src_np
-    S = gpu.geometry.IntraStrategy
-    g = torch.empty_like(src)
-    for rho, strat in [(16, S.TUNED), (32, S.TUNED), (64, S.TUNED), (8, S.TUNED), (16, S.SUBBOX), (32, S.TABLE)]:
-        g.copy_(src)
-        gpu.backends.run_block_space(g, src, rho, 16 - rho.bit_length() + 1, strat, kind=kind, param=1)
-        assert gpu.device.checksum(g) == ck, (rho, strat, kind)
-    g.copy_(src)
-    gpu.backends.run_bounding_box(g, src, 32, kind, 1, early_exit=True)
-    assert gpu.device.checksum(g) == ck
-
-
-def test_n16_int32_nsum4_vs_oracle(gpu, oracle):
-    """full grid at n=2^16 int32 (16 GiB per host grid) -- checksum vs the oracle."""
-    n = 1 << 16
-    src_np = oracle.fill_hash(n, np.int32, 21, 0)
-    want = src_np.copy()
-    oracle.run_block_space(want, src_np, 16, 12, oracle.STRAT_SUBBOX, None, None, 1, 1)
-    ck = oracle.checksum(want)
-    del want, src_np
-    src = gpu.device.fill_hash(n, torch.int32, 21, 0)
-    g = src.clone()
-    gpu.backends.run_block_space(g, src, 16, 12, gpu.geometry.IntraStrategy.TUNED, kind=1, param=1)
-    assert gpu.device.checksum(g) == ck
-    g.copy_(src)
-    gpu.backends.run_block_space(g, src, 16, 12, gpu.geometry.IntraStrategy.TUNED, kind=1, param=1, flags=2)
-    assert gpu.device.checksum(g) == ck
+# n = 2^16 / 2^17 / 2^18 against the oracle cell for cell: tests/test_baseline_sizes.py
 
 
 def test_n16_int32_const_write_counts(gpu):
@@ -223,30 +187,6 @@ def test_n16_int32_const_write_counts(gpu):
         assert int((g == 7).sum()) == 3**16
         assert int((g == -5).sum()) == n * n - 3**16
         del g
-
-
-@pytest.mark.parametrize("kind", [1, 2])
-def test_n17_int8_stencil_properties(gpu, kind):
-    """2^17 int8 (16 GiB per grid): tuned == paper-literal SUBBOX bit for bit, and
-    linearity: out(param=a) - out(param=b) == a-b on gasket cells, 0 elsewhere."""
-    n = 1 << 17
-    S = gpu.geometry.IntraStrategy
-    src = gpu.device.fill_hash(n, torch.int8, 9, 0)
-    a = src.clone()
-    gpu.backends.run_block_space(a, src, 32, 12, S.TUNED, kind=kind, param=1, flags=2)
-    b = src.clone()
-    gpu.backends.run_block_space(b, src, 32, 12, S.SUBBOX, kind=kind, param=1)
-    assert gpu.device.count_mismatch(a, b) == 0
-    b.copy_(src)
-    gpu.backends.run_block_space(b, src, 64, 11, S.TUNED, kind=kind, param=4)
-    # (b - a) on gasket cells == 3 (mod 256), elsewhere 0; counted in row chunks
-    threes = zeros = 0
-    for y in range(0, n, 8192):
-        d = b[y:y + 8192].view(torch.uint8) - a[y:y + 8192].view(torch.uint8)
-        threes += int((d == 3).sum())
-        zeros += int((d == 0).sum())
-    assert threes == 3**17
-    assert zeros == n * n - 3**17
 
 
 # ---------------------------------------------------------------------------

@@ -2,7 +2,7 @@
 
 Reference semantics: _block_space_nb with KERNEL_CONST (backends.py:158-222,
 _cell_value backends.py:127-141) -- every gasket cell gets `param`, nothing else
-changes (backends.py:155-156).  Three schedules (lambda digit order = default,
+changes (backends.py:155-156).  Four schedules (lambda digit order = default, address sweep,
 row-major tiles, grid rows) x two store modes (general; opt-in zero background,
 valid on the paper's zero-filled matrix).
 """
@@ -16,8 +16,9 @@ from tests.gpu_compare import first_mismatch, mismatches
 pytestmark = pytest.mark.gpu
 
 DTYPES = (np.int8, np.int16, np.int32, np.int64)
-# schedules: lambda digit order (default), row-major tiles (GM_FLAG_ROWMAJOR), grid rows (GM_FLAG_GRID_ROWS)
-SCHEDULES = {"lambda": 0, "rowmajor": 32, "gridrows": 536870912}
+# schedules: the default (lambda tiles; zero background: grid rows), lambda digit-order tiles, row-major tiles (GM_FLAG_ROWMAJOR), grid rows (GM_FLAG_GRID_ROWS),
+# address-ordered sweep of the member lines (GM_FLAG_WRITE_SWEEP)
+SCHEDULES = {"default": 0, "lambda": 65536, "rowmajor": 32, "gridrows": 536870912, "sweep": 1073741824}
 
 
 def _want(oracle, grid0, param):
