@@ -239,6 +239,109 @@ __global__ void __launch_bounds__(256) host_rows_write16(uint8_t* __restrict__ g
     }
 }
 
+// host_rows_write16 for a grid whose base is not 128-byte aligned (a plain numpy array:
+// malloc puts the data 16 bytes into a page).  PCIe moves host-aligned 64-byte units, so a
+// grid line that straddles two host lines would cost two reads and two writes per half.
+// Here every job is one HOST-aligned 128-byte line, decoded chunk by chunk (16-byte lanes,
+// flat chunk index f from the array start; a host line starts where f = -s16 mod 8):
+//   job A of member line X of row y: host line [128X - s, 128X - s + 128) of the row -- the
+//     first 128 - s bytes of line X and the last s bytes of the line before it (previous
+//     row's last line when X = 0);
+//   job B: host line X + 1, only when it holds bytes of line X that no job A covers (line
+//     X + 1 of the row is not a member line; the grid's very last line).
+// Each host line is written by exactly one job; chunks outside the array are never read
+// or written.  Per host 64-byte half: stored whole (reading the chunks that are not all
+// gasket cells) when any of its chunks holds gasket cells.
+constexpr int KLS = 64;  // member lines per unit (two host lines each: half of KL's registers)
+template <int C>
+__global__ void __launch_bounds__(256) host_rows_write16_shift(uint8_t* __restrict__ grid, int64_t n,
+                                                               const uint64_t* __restrict__ prefix, uint32_t nY,
+                                                               uint64_t param, int zero_bg, int s16) {
+    constexpr int TT = 128 / C;
+    constexpr int PER = KLS / 4;
+    const int lane = threadIdx.x & 31;
+    const int sub = lane >> 3, j = lane & 7;
+    const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t total = prefix[nY];
+    const uint32_t pv = splat4<C>(param);
+    const int64_t cpr = n * C / 16;          // chunks per row
+    const int64_t nchunks = cpr * n;
+    int cpr_shift = 0;
+    while ((int64_t(1) << cpr_shift) < cpr) ++cpr_shift;
+    const uint32_t nL = (uint32_t)(n / TT);  // lines per row
+    // chunk f (flat) -> 4 word masks of its gasket cells; false if outside the array
+    auto decode = [&](int64_t f, uint32_t (&m)[4]) -> bool {
+        if (f < 0 || f >= nchunks) return false;
+        const int64_t y = f >> cpr_shift;
+        const uint32_t cidx = (uint32_t)(f & (cpr - 1));
+        const uint32_t L = cidx >> 3, q = cidx & 7u;
+        const uint32_t Yr = (uint32_t)(y >> (__ffs(TT) - 1)), yl = (uint32_t)(y & (TT - 1));
+        const bool mem = (L & ~Yr) == 0;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) m[w] = mem ? word_mask<C>(4 * (int)q + w, yl) : 0u;
+        return true;
+    };
+    for (uint64_t u = warp0; u < total; u += nwarps) {
+        uint32_t lo = 0, hi = nY;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (__ldg(prefix + mid) <= u) lo = mid; else hi = mid;
+        }
+        const uint32_t Y = lo;
+        const uint32_t lines = 1u << __popc(Y);
+        const uint32_t chunks = (lines + KLS - 1) / KLS;
+        const uint64_t rem = u - __ldg(prefix + Y);
+        const uint32_t y_lo = (uint32_t)(rem / chunks);
+        const uint32_t jj = (uint32_t)(rem - (uint64_t)y_lo * chunks);
+        const int64_t y = (int64_t)Y * TT + y_lo;
+        const uint32_t i0 = jj * KLS;
+        const int cnt = (int)min((uint32_t)KLS, lines - i0);
+        uint4 oldA[PER], oldB[PER];
+        uint32_t mA[PER][4], mB[PER][4];
+        int64_t fA[PER];
+        bool stA[PER], stB[PER];
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int k = 4 * i + sub;
+            const uint32_t X = pdep(i0 + (uint32_t)k, Y);
+            const bool valid = k < cnt;
+            fA[i] = y * cpr + 8 * (int64_t)X - s16 + j;
+            const bool inA = valid && decode(fA[i], mA[i]);
+            // job B: host line X + 1 holds the tail of line X that no job A covers
+            const bool needB = valid && (((X + 1) & ~Y) != 0 || X + 1 == nL) && !(X + 1 == nL && y + 1 < n);
+            const bool inB = needB && j < s16 && decode(fA[i] + 8, mB[i]);
+            if (!inB) mB[i][0] = mB[i][1] = mB[i][2] = mB[i][3] = 0u;
+            if (!inA) mA[i][0] = mA[i][1] = mA[i][2] = mA[i][3] = 0u;
+            // host 64-byte half (4 lanes) holds gasket cells -> stored whole
+            const bool tA = (mA[i][0] | mA[i][1] | mA[i][2] | mA[i][3]) != 0;
+            const bool tB = (mB[i][0] | mB[i][1] | mB[i][2] | mB[i][3]) != 0;
+            const unsigned ba = __ballot_sync(0xffffffffu, tA), bb = __ballot_sync(0xffffffffu, tB);
+            const unsigned hm = 0xfu << (lane & ~3);
+            stA[i] = inA && (ba & hm) != 0;
+            // job B: only the chunks of line X (j < s16) of the host line's first half(s)
+            stB[i] = inB && (bb & hm) != 0;
+            const bool fullA = (mA[i][0] & mA[i][1] & mA[i][2] & mA[i][3]) == 0xffffffffu;
+            const bool fullB = (mB[i][0] & mB[i][1] & mB[i][2] & mB[i][3]) == 0xffffffffu;
+            oldA[i] = make_uint4(0, 0, 0, 0);
+            oldB[i] = make_uint4(0, 0, 0, 0);
+            if (stA[i] && !fullA && !zero_bg) oldA[i] = __ldcv(reinterpret_cast<const uint4*>(grid + fA[i] * 16));
+            if (stB[i] && !fullB && !zero_bg) oldB[i] = __ldcv(reinterpret_cast<const uint4*>(grid + (fA[i] + 8) * 16));
+        }
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            if (stA[i])
+                *reinterpret_cast<uint4*>(grid + fA[i] * 16) =
+                    make_uint4((pv & mA[i][0]) | (oldA[i].x & ~mA[i][0]), (pv & mA[i][1]) | (oldA[i].y & ~mA[i][1]),
+                               (pv & mA[i][2]) | (oldA[i].z & ~mA[i][2]), (pv & mA[i][3]) | (oldA[i].w & ~mA[i][3]));
+            if (stB[i])
+                *reinterpret_cast<uint4*>(grid + (fA[i] + 8) * 16) =
+                    make_uint4((pv & mB[i][0]) | (oldB[i].x & ~mB[i][0]), (pv & mB[i][1]) | (oldB[i].y & ~mB[i][1]),
+                               (pv & mB[i][2]) | (oldB[i].z & ~mB[i][2]), (pv & mB[i][3]) | (oldB[i].w & ~mB[i][3]));
+        }
+    }
+}
+
 std::mutex g_mu;
 std::map<std::pair<int, int>, uint64_t*> g_prefix;  // (device, nYbits*1024 + rows per block row) -> table
 
@@ -275,7 +378,16 @@ cudaError_t launch_c(const LaunchArgs& a, int r) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     uint8_t* g = reinterpret_cast<uint8_t*>(a.grid);
-    if (mode == 0) {
+    const int shift = (int)(reinterpret_cast<uintptr_t>(a.grid) & 127u);
+    if (mode == 0 && shift != 0 && shift % 16 == 0 && C <= 4) {
+        // a grid that does not start on a 128-byte boundary: host-aligned jobs
+        uint32_t nYs;
+        uint64_t* pres = prefix_table(r - k, TT, nYs, KLS);
+        if (!pres) return cudaErrorMemoryAllocation;
+        host_rows_write16_shift<C><<<sms * 8, 256, 0, a.stream>>>(g, a.n, pres, nYs, a.param,
+                                                                  (a.flags & GM_FLAG_ZERO_BACKGROUND) ? 1 : 0,
+                                                                  shift / 16);
+    } else if (mode == 0) {
         uint32_t nY16;
         uint64_t* pre16 = prefix_table(r - k, TT, nY16, KL);
         if (!pre16) return cudaErrorMemoryAllocation;

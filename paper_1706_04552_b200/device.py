@@ -230,6 +230,7 @@ class _PinCache:
                     break
                 used -= self._regs[old][0]
                 self._drop(old)
+            _huge_pages(ptr, nbytes)
             out = ctypes.c_void_p()
             reg = ctypes.c_int32(0)
             native.call("gm_host_map", ptr, nbytes, 1, ctypes.byref(out), ctypes.byref(reg))
@@ -253,6 +254,30 @@ class _PinCache:
         with self._lock:
             for ptr in list(self._regs):
                 self._drop(ptr)
+
+
+_MADV_HUGEPAGE, _MADV_COLLAPSE = 14, 25
+
+
+def _huge_pages(ptr: int, nbytes: int) -> None:
+    """Back a pageable buffer with 2 MB pages before it is registered (transparent huge
+    pages: MADV_HUGEPAGE, then MADV_COLLAPSE where the kernel has it).  The GPU reaches
+    mapped host memory through the IOMMU; with 4 KB pages the write pass over a pageable
+    n=2^16 grid ran at 14.4 ms per call against 8.3 ms on cudaHostAlloc'd memory.  Best
+    effort: a kernel without THP leaves the pages as they are.  GASKET_HOST_HUGEPAGES=0
+    turns it off."""
+    if os.environ.get("GASKET_HOST_HUGEPAGES", "1") == "0" or nbytes < (4 << 20):
+        return
+    try:
+        libc = ctypes.CDLL(None, use_errno=True)
+        libc.madvise.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]
+        page = 4096
+        start = ptr & ~(page - 1)
+        length = ((ptr + nbytes + page - 1) & ~(page - 1)) - start
+        libc.madvise(start, length, _MADV_HUGEPAGE)
+        libc.madvise(start, length, _MADV_COLLAPSE)
+    except Exception:  # pragma: no cover - non-Linux hosts
+        pass
 
 
 def _unregister(ptr: int) -> None:

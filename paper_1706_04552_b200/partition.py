@@ -315,16 +315,27 @@ class PeerHaloExchange:
 
     TIMEOUT_NS = 10_000_000_000
 
-    def __init__(self, plan: PartitionPlan, rank: int, bufs: Sequence[DeviceBuffer], group=None) -> None:
+    def __init__(self, plan: PartitionPlan, rank: int, bufs: Sequence[DeviceBuffer], group=None,
+                 entries: Optional[tuple[np.ndarray, np.ndarray]] = None) -> None:
+        """entries (tiled storage): (source cells, destination rank << 56 | cell) per copy,
+        own-rank destinations being ring copies; default: the dense layout's slots, each
+        cell stored at the same index in every peer."""
         import torch.distributed as dist
 
         from . import native
 
         self.plan, self.rank, self.world = plan, rank, plan.world
         self.cell_bytes = bufs[0].tensor.element_size()
-        slots, _ = plan.exchange_slots()
-        self.send_idx = torch.from_numpy(slots[rank]).cuda()
-        self.bytes_per_step = int(self.send_idx.numel() * self.cell_bytes * (self.world - 1))
+        if entries is None:
+            slots, _ = plan.exchange_slots()
+            self.send_idx = torch.from_numpy(slots[rank]).cuda()
+            self.didx = None
+            self.bytes_per_step = int(self.send_idx.numel() * self.cell_bytes * (self.world - 1))
+        else:
+            self.send_idx = torch.from_numpy(entries[0]).cuda()
+            self.didx = torch.from_numpy(entries[1]).cuda()
+            remote = int(((entries[1] >> 56) != rank).sum())
+            self.bytes_per_step = remote * self.cell_bytes
         self.flags = DeviceBuffer((self.world,), torch.uint64)
         self.flags.tensor.zero_()
         self.status = torch.zeros(1, dtype=torch.int32, device="cuda")
@@ -365,7 +376,7 @@ class PeerHaloExchange:
                 _fields_ = [("peers", ctypes.c_uint64 * self.MAX_PEERS), ("peer_flags", ctypes.c_uint64 * self.MAX_PEERS),
                             ("own_flags", ctypes.c_uint64), ("idx", ctypes.c_uint64), ("count", ctypes.c_int64),
                             ("cell_bytes", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
-                            ("done", ctypes.c_uint32), ("status", ctypes.c_uint32)]
+                            ("done", ctypes.c_uint32), ("status", ctypes.c_uint32), ("didx", ctypes.c_uint64)]
 
             if self.world > self.MAX_PEERS:
                 raise ValueError(f"the fused exchange supports up to {self.MAX_PEERS} ranks")
@@ -381,6 +392,7 @@ class PeerHaloExchange:
                 e.idx = self.send_idx.data_ptr()
                 e.count = self.send_idx.numel()
                 e.cell_bytes, e.rank, e.world = self.cell_bytes, self.rank, self.world
+                e.didx = self.didx.data_ptr() if self.didx is not None else 0
                 raw = np.frombuffer(bytes(e), dtype=np.uint8).copy()
                 self._epi.append(torch.from_numpy(raw).cuda())
             self._epi_status_off = Epi.status.offset
@@ -401,9 +413,14 @@ class PeerHaloExchange:
 
         self.epoch += 1
         s = dev.stream_handle()
-        native.call("gm_peer_halo_put", self.bufs[which].ptr, self.peer_bufs[which].data_ptr(),
-                    self.send_idx.data_ptr(), self.send_idx.numel(), self.cell_bytes, self.peer_flags.data_ptr(),
-                    self.rank, self.world, self.epoch, s)
+        if self.didx is not None:
+            native.call("gm_peer_halo_put_to", self.bufs[which].ptr, self.peer_bufs[which].data_ptr(),
+                        self.send_idx.data_ptr(), self.didx.data_ptr(), self.send_idx.numel(), self.cell_bytes,
+                        self.peer_flags.data_ptr(), self.rank, self.world, self.epoch, s)
+        else:
+            native.call("gm_peer_halo_put", self.bufs[which].ptr, self.peer_bufs[which].data_ptr(),
+                        self.send_idx.data_ptr(), self.send_idx.numel(), self.cell_bytes, self.peer_flags.data_ptr(),
+                        self.rank, self.world, self.epoch, s)
         native.call("gm_peer_halo_wait", self.flags.ptr, self.rank, self.world, self.epoch, self.TIMEOUT_NS,
                     self.status.data_ptr(), s)
 
@@ -539,6 +556,323 @@ class PartitionedCA:
         return mask
 
 
+# ---------------------------------------------------------------------------
+# tiled storage: each rank holds only its sub-gaskets, each in a ringed block
+# ---------------------------------------------------------------------------
+
+RING_ROWS = 8     # >= the deepest fused kernel's reach (6 rows) -- the staged window of a tile
+RING_BYTES = 128  # one line either side: the blocks' tile lines stay 128-byte aligned
+
+
+class TiledLayout:
+    """Per-rank storage of SURVEY §8e: the rank's level-L sub-gaskets, each one block of
+    (m + 2R) rows x pitch bytes (m = n >> L, R = RING_ROWS, pitch = m*C + 2*RING_BYTES)
+    holding the sub-gasket and a ring of its neighbours' cells -- not two n x n grids.
+    A sub-gasket of level L is itself an edge-m gasket (its cell (x, y) is a gasket cell
+    iff x is a bit-subset of y), so the tuned kernels run on a block unchanged, addressing
+    it through the block's virtual origin sg_off[k] (where global cell (0, 0) would sit):
+    global cell (x, y) of block k is at byte sg_off[k] + y*pitch + x*C.
+
+    n = 2^18 int8 at L = 5: 243 blocks of 69.3 MB = 16.8 GB for the whole gasket per
+    ping-pong buffer (the dense grid is 64 GiB), 2.2 GB per rank at 8 ranks."""
+
+    def __init__(self, plan: "PartitionPlan", rank: int, cell_bytes: int) -> None:
+        self.plan, self.rank, self.c = plan, rank, int(cell_bytes)
+        if self.c not in (1, 2, 4):
+            raise ValueError("tiled storage runs the tuned tile kernels: 1-, 2- or 4-byte cells")
+        self.m = plan.m
+        if self.m * self.c < 128:
+            raise ValueError(f"sub-gaskets of edge {self.m} are narrower than one 128-byte tile")
+        self.lo, self.hi = plan.ranges[rank]
+        self.count = self.hi - self.lo
+        self.R, self.P = RING_ROWS, RING_BYTES
+        self.pc = self.P // self.c  # ring cells either side
+        self.pitch = self.m * self.c + 2 * self.P
+        self.rows = self.m + 2 * self.R
+        self.block = self.rows * self.pitch
+        self.nbytes = self.count * self.block
+        self.origins = [tuple(v * self.m for v in subgasket_block(s, plan.level)) for s in range(self.lo, self.hi)]
+        self.sg_off = np.array([k * self.block + self.R * self.pitch + self.P - oy * self.pitch - ox * self.c
+                                for k, (ox, oy) in enumerate(self.origins)], dtype=np.int64)
+
+    def cell_index(self, k: int, x, y):
+        """Cell index (byte offset / C) of global cell (x, y) in block k (x, y may be arrays)."""
+        return (self.sg_off[k] + np.asarray(y, dtype=np.int64) * self.pitch
+                + np.asarray(x, dtype=np.int64) * self.c) // self.c
+
+    def block_of(self, s: int) -> int:
+        return s - self.lo
+
+    def window(self, k: int) -> tuple[int, int, int, int]:
+        """Global cells [x0, x1) x [y0, y1) block k holds (sub-gasket plus ring)."""
+        ox, oy = self.origins[k]
+        return ox - self.pc, ox + self.m + self.pc, oy - self.R, oy + self.m + self.R
+
+    def block_view(self, buf: torch.Tensor, k: int) -> torch.Tensor:
+        """Block k of a flat buffer as a (rows, pitch / C) tensor."""
+        w = self.pitch // self.c
+        return buf[k * (self.block // self.c):(k + 1) * (self.block // self.c)].view(self.rows, w)
+
+    # -- filling and reading -------------------------------------------------
+    def load_dense(self, buf: torch.Tensor, dense: torch.Tensor) -> None:
+        """Every block's window from a dense n x n grid (0 outside the grid)."""
+        n = self.plan.n
+        buf.zero_()
+        for k in range(self.count):
+            x0, x1, y0, y1 = self.window(k)
+            cx0, cx1, cy0, cy1 = max(x0, 0), min(x1, n), max(y0, 0), min(y1, n)
+            v = self.block_view(buf, k)
+            v[cy0 - y0:cy1 - y0, cx0 - x0:cx1 - x0].copy_(dense[cy0:cy1, cx0:cx1])
+
+    def fill_hash(self, buf: torch.Tensor, seed: int, mode: int = 0) -> None:
+        """Every block's window from the synthetic grid fill_hash(seed, mode) (no dense copy)."""
+        from . import device as dev
+        from . import native
+
+        for k in range(self.count):
+            x0, x1, y0, y1 = self.window(k)
+            v = self.block_view(buf, k)
+            native.call("gm_fill_hash_window", v.data_ptr(), self.pitch, self.plan.n, self.c, x0, y0, x1 - x0,
+                        y1 - y0, seed & (2**64 - 1), mode, dev.stream_handle())
+
+    def store_dense(self, buf: torch.Tensor, dense: torch.Tensor) -> None:
+        """The rank's sub-gaskets (block interiors) into a dense n x n grid."""
+        m = self.m
+        for k in range(self.count):
+            ox, oy = self.origins[k]
+            v = self.block_view(buf, k)
+            dense[oy:oy + m, ox:ox + m].copy_(v[self.R:self.R + m, self.pc:self.pc + m])
+
+
+def tiled_exchange(plan: "PartitionPlan", cell_bytes: int) -> list[tuple[np.ndarray, np.ndarray]]:
+    """Per SOURCE rank: (source cells in its layout, destination rank << 56 | destination
+    cell) for every copy a step needs -- each changing halo cell of a sub-gasket
+    (plan.halo, depth-aware) from its owner's block into the ring of the reading block;
+    a destination rank equal to the source is a ring copy inside the same buffer."""
+    layouts = [TiledLayout(plan, r, cell_bytes) for r in range(plan.world)]
+    src: list[list[int]] = [[] for _ in range(plan.world)]
+    dst: list[list[int]] = [[] for _ in range(plan.world)]
+    n = plan.n
+    for reader_rank, lay in enumerate(layouts):
+        for k in range(lay.count):
+            s = lay.lo + k
+            cells = plan.halo[s]
+            if cells.size == 0:
+                continue
+            y, x = np.divmod(cells, n)
+            owners_sg = [subgasket_index(int(a) // plan.m, int(b) // plan.m, plan.level) for a, b in zip(x, y)]
+            d_idx = lay.cell_index(k, x, y)
+            for i, s2 in enumerate(owners_sg):
+                if s2 is None:  # (never: halo cells are gasket cells)
+                    continue
+                o = plan.owner_of_subgasket(s2)
+                src_lay = layouts[o]
+                src[o].append(int(src_lay.cell_index(src_lay.block_of(s2), x[i], y[i])))
+                dst[o].append(int(d_idx[i]) | (reader_rank << 56))
+    return [(np.array(a, dtype=np.int64), np.array(b, dtype=np.int64)) for a, b in zip(src, dst)]
+
+
+class TiledCA:
+    """One rank of the partitioned CA on tiled storage (TiledLayout): two flat buffers of
+    the rank's blocks, `plan.depth` steps per launch (gm_run_part_tiled), then the halo
+    copies of tiled_exchange: over NCCL / gloo all_gather ("collective", the received
+    values scattered into the rings plus the rank's own ring copies), over peer memory
+    ("peer": gm_peer_halo_put_to), or inside the step kernel ("peer" + fused)."""
+
+    def __init__(self, plan: "PartitionPlan", rank: int, kind: int, param: int = 1, dtype=torch.int8,
+                 init: Optional[torch.Tensor] = None, seed: Optional[int] = None, group=None,
+                 loopback: Optional["LoopbackGroup"] = None, halo: str = "collective", fused: bool = False) -> None:
+        from . import device as dev
+
+        dev.require_cuda()
+        self.plan, self.rank, self.kind, self.param = plan, rank, kind, param
+        c = torch.empty((), dtype=dtype).element_size()
+        self.layout = L = TiledLayout(plan, rank, c)
+        self.sg_off = torch.from_numpy(L.sg_off).cuda()
+        entries = tiled_exchange(plan, c)
+        self.peer = None
+        numel = max(1, L.nbytes // c)
+        if halo == "peer":
+            self._dbufs = [DeviceBuffer((numel,), dtype) for _ in range(2)]
+            self.a, self.b = self._dbufs[0].tensor, self._dbufs[1].tensor
+        elif halo == "collective":
+            self.a = torch.empty(numel, dtype=dtype, device="cuda")
+            self.b = torch.empty(numel, dtype=dtype, device="cuda")
+        else:
+            raise ValueError("halo must be 'collective' or 'peer'")
+        if init is not None:
+            L.load_dense(self.a, init)
+        elif seed is not None:
+            self.a.zero_()
+            L.fill_hash(self.a, seed)
+        else:
+            raise ValueError("pass the initial state: a dense grid (init) or a synthetic seed")
+        self.b.copy_(self.a)  # both buffers agree off the gasket (rings included)
+        self.lo, self.hi = L.lo, L.hi
+        self.fused = bool(fused)
+        if halo == "peer":
+            self.peer = PeerHaloExchange(plan, rank, self._dbufs, group=group, entries=entries[rank])
+            self._dst = 1
+        else:
+            if self.fused:
+                raise ValueError("the fused exchange needs halo='peer'")
+            self._coll = _TiledCollective(plan, rank, entries, dtype, group=group, loopback=loopback)
+        self._epoch = 0
+
+    # -- one exchange round ---------------------------------------------------
+    def _launch(self, epi: int = 0, wait: int = 0, signal: int = 0) -> None:
+        from . import device as dev
+        from . import native
+
+        native.call("gm_run_part_tiled", self.b.data_ptr(), self.a.data_ptr(), self.plan.n, self.a.element_size(),
+                    self.kind, int(np.int32(self.param)), self.plan.depth, self.plan.level, self.lo, self.hi,
+                    self.sg_off.data_ptr(), self.layout.pitch, epi, wait, signal, dev.stream_handle())
+
+    def compute(self) -> None:
+        if self.hi > self.lo:
+            self._launch()
+
+    def finish(self) -> None:
+        self.a, self.b = self.b, self.a
+        if self.peer is not None:
+            self._dst ^= 1
+
+    def step(self) -> None:
+        """depth CA steps on the rank's blocks, then the halo copies of the new state."""
+        if self.fused:
+            self._epoch += 1
+            self._launch(self.peer.epilogue(self._dst).data_ptr(), self._epoch - 1, self._epoch)
+            self.finish()
+            return
+        self.compute()
+        if self.peer is not None:
+            self.peer.exchange(self._dst)
+        else:
+            self._coll.exchange(self.b)
+        self.finish()
+
+    @property
+    def halo_bytes_per_step(self) -> int:
+        return self.peer.bytes_per_step if self.peer is not None else self._coll.bytes_per_step
+
+    @property
+    def storage_bytes(self) -> int:
+        return 2 * self.layout.nbytes
+
+    def store_dense(self, dense: torch.Tensor) -> None:
+        torch.cuda.synchronize()
+        self.layout.store_dense(self.a, dense)
+
+    def close(self) -> None:
+        if self.peer is not None:
+            self.peer.check()
+            self.peer.check_fused()
+            self.peer.close()
+            self.a = self.b = None
+            for d in self._dbufs:
+                d.free()
+            self.peer = None
+
+
+class _TiledCollective:
+    """The tiled halo copies over a process group (all_gather) or a loopback group: the
+    rank's cells other ranks read go out in one fixed-size all_gather, the received
+    values are scattered into this rank's rings, and the rank's own ring copies run as
+    one gm_copy_cells."""
+
+    def __init__(self, plan, rank, entries, dtype, group=None, loopback=None) -> None:
+        self.plan, self.rank, self.group, self.loopback = plan, rank, group, loopback
+        W = plan.world
+        # per source rank o: its unique cells read by other ranks, in a fixed order
+        sends = []
+        for o in range(W):
+            srcs, dsts = entries[o]
+            remote = (dsts >> 56) != o
+            sends.append(np.unique(srcs[remote]))
+        self.width = max([1] + [len(v) for v in sends])
+        srcs, dsts = entries[rank]
+        local = (dsts >> 56) == rank
+        dev = torch.device("cuda")
+        self.send_idx = torch.from_numpy(sends[rank]).to(dev)
+        self.local_src = torch.from_numpy(srcs[local]).to(dev)
+        self.local_dst = torch.from_numpy(dsts[local] & ((1 << 56) - 1)).to(dev)
+        pos, cells = [], []
+        for o in range(W):
+            if o == rank:
+                continue
+            so, do = entries[o]
+            mine = (do >> 56) == rank
+            if not mine.any():
+                continue
+            slot = np.searchsorted(sends[o], so[mine])
+            pos.append(o * self.width + slot)
+            cells.append(do[mine] & ((1 << 56) - 1))
+        self.recv_pos = torch.from_numpy(np.concatenate(pos) if pos else np.zeros(0, np.int64)).to(dev)
+        self.recv_idx = torch.from_numpy(np.concatenate(cells) if cells else np.zeros(0, np.int64)).to(dev)
+        self.sendbuf = torch.zeros(self.width, dtype=dtype, device=dev)
+        self.gathered = torch.zeros(self.width * W, dtype=dtype, device=dev)
+        self.bytes_per_step = int(self.width * W * self.sendbuf.element_size())
+
+    def post(self, buf: torch.Tensor) -> None:
+        from . import device as dev
+        from . import native
+
+        k = self.send_idx.numel()
+        if k:
+            native.call("gm_gather_cells", buf.data_ptr(), buf.element_size(), self.send_idx.data_ptr(), k,
+                        self.sendbuf.data_ptr(), dev.stream_handle())
+        if self.loopback is not None:
+            self.loopback.contribute(self.rank, self.sendbuf)
+        else:
+            import torch.distributed as dist
+
+            dist.all_gather_into_tensor(self.gathered, self.sendbuf, group=self.group)
+
+    def complete(self, buf: torch.Tensor) -> None:
+        from . import device as dev
+        from . import native
+
+        if self.loopback is not None:
+            self.gathered.copy_(self.loopback.gathered())
+        k = self.recv_idx.numel()
+        if k:
+            vals = self.gathered[self.recv_pos].contiguous()
+            native.call("gm_scatter_cells", buf.data_ptr(), buf.element_size(), self.recv_idx.data_ptr(), k,
+                        vals.data_ptr(), dev.stream_handle())
+        k = self.local_src.numel()
+        if k:
+            native.call("gm_copy_cells", buf.data_ptr(), buf.data_ptr(), buf.element_size(), self.local_dst.data_ptr(),
+                        self.local_src.data_ptr(), k, dev.stream_handle())
+
+    def exchange(self, buf: torch.Tensor) -> None:
+        self.post(buf)
+        self.complete(buf)
+
+
+def run_loopback_tiled(plan: "PartitionPlan", kind: int, rounds: int, param: int = 1, dtype=torch.int8,
+                       init: Optional[torch.Tensor] = None, seed: Optional[int] = None,
+                       out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """All virtual ranks' tiled storage on one device; after `rounds` exchange rounds
+    (each plan.depth CA steps) the sub-gaskets are written into `out` (a dense grid:
+    a copy of init, or fill_hash(seed) -- off-gasket cells never change)."""
+    lb = LoopbackGroup(plan.world)
+    ranks = [TiledCA(plan, r, kind, param, dtype=dtype, init=init, seed=seed, loopback=lb) for r in range(plan.world)]
+    for _ in range(rounds):
+        for ca in ranks:
+            ca.compute()
+        for ca in ranks:
+            ca._coll.post(ca.b)
+        for ca in ranks:
+            ca._coll.complete(ca.b)
+        for ca in ranks:
+            ca.finish()
+    if out is None:
+        out = init.clone()
+    for ca in ranks:
+        ca.store_dense(out)
+    return out
+
+
 def run_loopback(plan: PartitionPlan, init: torch.Tensor, kind: int, steps: int, param: int = 1,
                  step_fn: Optional[StepFn] = None) -> torch.Tensor:
     """All virtual ranks on one device; returns the assembled grid after `steps` exchange
@@ -562,4 +896,5 @@ def run_loopback(plan: PartitionPlan, init: torch.Tensor, kind: int, steps: int,
 
 
 __all__: Sequence[str] = ("subgasket_block", "subgasket_index", "rank_ranges", "PartitionPlan", "LoopbackGroup",
-                          "HaloExchange", "DeviceBuffer", "PeerHaloExchange", "PartitionedCA", "run_loopback")
+                          "HaloExchange", "DeviceBuffer", "PeerHaloExchange", "PartitionedCA", "run_loopback",
+                          "TiledLayout", "tiled_exchange", "TiledCA", "run_loopback_tiled")

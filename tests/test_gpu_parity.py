@@ -622,3 +622,32 @@ def test_pin_cache_registers_once_and_releases(gpu, monkeypatch):
     del v, g
     gc.collect()
     assert dev.pinned.pinned_bytes() == 0
+
+
+@pytest.mark.parametrize("dtype", [np.int8, np.int16, np.int32])
+def test_mapped_write_misaligned_host_grids(gpu, oracle, monkeypatch, dtype):
+    """The mapped write pass on host grids that do not start on a 128-byte boundary (a
+    plain numpy array sits 16 bytes into its pages): the host-aligned kernel
+    (host_rows_write16_shift) == the oracle for every 16-byte shift, the bytes around the
+    array (another owner's memory) untouched, zero-background mode included."""
+    monkeypatch.setenv("GASKET_HOST_TRANSPORT", "mapped")
+    S = gpu.geometry.IntraStrategy
+    c = np.dtype(dtype).itemsize
+    for n in (128 // c, 2 * (128 // c), 1024):
+        nbytes = n * n * c
+        for shift in range(0, 128, 16):
+            for zero in (False, True):
+                raw = np.zeros(nbytes + 512, dtype=np.uint8)
+                base = (-raw.ctypes.data) % 128 + 128 + shift
+                raw[:] = 0xA5
+                g = raw[base:base + nbytes].view(dtype).reshape(n, n)
+                g0 = np.zeros((n, n), dtype) if zero else oracle.fill_hash(n, dtype, 3 + shift, 0)
+                g[...] = g0
+                want = g0.copy()
+                oracle.run_bounding_box(want, want, 1, 0, -7)
+                gpu.backends.run_block_space(g, g, min(32, n), (n // min(32, n)).bit_length() - 1, S.TUNED, kind=0,
+                                             param=-7, assume_zero_background=zero)
+                assert np.array_equal(g, want), (n, shift, zero)
+                assert (raw[:base] == 0xA5).all() and (raw[base + nbytes:] == 0xA5).all(), (n, shift, "guard")
+                del g
+    gpu.device.pinned.clear()

@@ -254,3 +254,192 @@ def test_peer_memory_halo_processes(gpu, world, depth, kind, fused):
         assert p.exitcode == 0
     assert all(out[r] is True for r in range(world))
     assert all(out[f"bytes{r}"] > 0 for r in range(world))
+
+
+# ---------------------------------------------------------------------------
+# tiled storage (per-rank blocks with a ring)
+# ---------------------------------------------------------------------------
+
+def _window_steps(win: np.ndarray, x0: int, y0: int, n: int, kind: int, param: int, steps: int) -> np.ndarray:
+    """`steps` CA steps on a window of the global grid, what a tiled block's kernel sees:
+    gasket cells (global test, in-grid) get param + neighbours, neighbours outside the
+    window read 0 (the window reaches past the block's sub-gasket by its ring)."""
+    h, w = win.shape
+    ys = np.arange(y0, y0 + h).reshape(h, 1)
+    xs = np.arange(x0, x0 + w).reshape(1, w)
+    member = (xs >= 0) & (xs < n) & (ys >= 0) & (ys < n) & ((xs & ~ys) == 0)
+    offs = [(1, 0), (-1, 0), (0, 1), (0, -1)] + ([(1, 1), (1, -1), (-1, 1), (-1, -1)] if kind == 2 else [])
+    a = win.astype(np.int64)
+    for _ in range(steps):
+        pad = np.zeros((h + 2, w + 2), dtype=np.int64)
+        pad[1:-1, 1:-1] = a
+        tot = np.full((h, w), param, dtype=np.int64)
+        for dx, dy in offs:
+            tot += pad[1 + dy:1 + dy + h, 1 + dx:1 + dx + w]
+        a = np.where(member, tot, a)
+    return a.astype(win.dtype)
+
+
+@pytest.mark.parametrize("kind", [1, 2])
+@pytest.mark.parametrize("world,level,depth", [(1, 2, 1), (2, 2, 1), (3, 3, 2), (4, 3, 6), (4, 2, 4), (8, 3, 1)])
+def test_tiled_protocol_matches_full_steps_cpu(oracle, kind, world, level, depth):
+    """The tiled storage end to end on CPU: every rank's blocks (sub-gasket + ring) loaded
+    from the initial grid, each block advanced `depth` steps from its window alone (the
+    numpy stand-in for gm_run_part_tiled), then the copies of tiled_exchange applied
+    (remote entries into the other ranks' rings, own entries into own rings); after 3
+    rounds every sub-gasket equals 3*depth full-grid oracle steps.  This pins the ring
+    depth, the halo lists and the block addressing the GPU kernels use."""
+    n = 1024
+    plan = P.PartitionPlan(n, level, world, eight=kind == 2, depth=depth)
+    init = oracle.fill_hash(n, np.int8, 17, 0)
+    lays = [P.TiledLayout(plan, r, 1) for r in range(world)]
+    bufs = []
+    for L in lays:
+        b = torch.zeros(L.nbytes, dtype=torch.int8)
+        L.load_dense(b, torch.from_numpy(init))
+        bufs.append(b)
+    ent = P.tiled_exchange(plan, 1)
+    for _ in range(3):
+        new = []
+        for L, b in zip(lays, bufs):
+            nb = b.clone()
+            for k in range(L.count):
+                x0, x1, y0, y1 = L.window(k)
+                v = L.block_view(b, k).numpy()
+                out = _window_steps(v[:, :x1 - x0], x0, y0, n, kind, 1, depth)
+                L.block_view(nb, k).numpy()[L.R:L.R + L.m, L.pc:L.pc + L.m] = out[L.R:L.R + L.m, L.pc:L.pc + L.m]
+            new.append(nb)
+        for o, (src, dst) in enumerate(ent):
+            vals = new[o].numpy()[src]
+            for q in range(world):
+                sel = (dst >> 56) == q
+                new[q].numpy()[dst[sel] & ((1 << 56) - 1)] = vals[sel]
+        bufs = new
+    want = init.copy()
+    for _ in range(3 * depth):
+        nxt = want.copy()
+        oracle.run_bounding_box(nxt, want, 1, kind, 1)
+        want = nxt
+    got = torch.from_numpy(init.copy())
+    for L, b in zip(lays, bufs):
+        L.store_dense(b, got)
+    assert np.array_equal(got.numpy(), want)
+
+
+def test_tiled_storage_shrinks_with_ranks():
+    """Per-rank storage = its sub-gasket blocks + rings: ~1/N of the whole gasket's blocks,
+    which is itself ~1/4 of the dense grid at level 5 (243 of 1024 blocks)."""
+    n, level = 1 << 18, 5
+    whole = P.TiledLayout(P.PartitionPlan(n, level, 1, eight=True), 0, 1).nbytes
+    assert whole < 0.27 * n * n
+    for world in (2, 4, 8):
+        plan = P.PartitionPlan(n, level, world, eight=True)
+        per = [P.TiledLayout(plan, r, 1).nbytes for r in range(world)]
+        assert max(per) <= (whole / world) * 1.04  # 243 blocks split as evenly as they go
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", [1, 2])
+def test_tiled_loopback_gpu_matches_full_grid(gpu, kind):
+    """gm_run_part_tiled + the tiled halo copies (loopback virtual ranks on one GPU) ==
+    the unpartitioned tuned kernel, bit for bit: depth 1 (single-step kernel on the
+    blocks) and 2 / 4 / 6 (fused kernel), several worlds, 1/2/4-byte cells."""
+    be = gpu.backends
+    S = gpu.geometry.IntraStrategy
+    for n, level, worlds, dt in ((1 << 12, 3, (1, 2, 3, 8), torch.int8), (1 << 14, 5, (8,), torch.int8),
+                                 (1 << 12, 2, (2,), torch.int16), (1 << 12, 2, (3,), torch.int32)):
+        init = gpu.device.fill_hash(n, dt, 5, 0)
+        ref = {0: init}
+        a = init
+        for s in range(1, 13):
+            b = a.clone()
+            be.run_block_space(b, a, 64, (n // 64).bit_length() - 1, S.TUNED, kind=kind, param=1)
+            a = b
+            ref[s] = a
+        for world in worlds:
+            for depth, rounds in ((1, 3), (2, 2), (4, 2), (6, 2)):
+                if depth == 6 and dt == torch.int32:
+                    continue
+                plan = P.PartitionPlan(n, level, world, eight=kind == 2, depth=depth)
+                got = P.run_loopback_tiled(plan, kind, rounds, dtype=dt, init=init)
+                assert gpu.device.count_mismatch(got, ref[depth * rounds]) == 0, (n, level, world, depth, str(dt))
+                got = P.run_loopback_tiled(plan, kind, rounds, dtype=dt, seed=5, out=init.clone())
+                assert gpu.device.count_mismatch(got, ref[depth * rounds]) == 0, ("seed", n, level, world, depth)
+
+
+@pytest.mark.gpu
+def test_tiled_n18_eight_ranks_vs_oracle(gpu, oracle):
+    """BASELINE config 5 at its size: n = 2^18 int8, NSUM8, the level-5 partition over 8
+    virtual ranks on tiled storage (the blocks of all 8 ranks: 2 x 16.8 GB instead of
+    8 x 2 x 64 GiB), depth 1 (3 exchange rounds) and depth 6 (one round), against the
+    oracle on sampled row bands that straddle sub-gasket boundaries."""
+    from tests.gpu_compare import band_mismatches, sampled_bands
+
+    n, seed = 1 << 18, 7
+    bands = sampled_bands(n, 512, 16)
+    for depth, rounds in ((1, 3), (6, 1)):
+        plan = P.PartitionPlan(n, 5, 8, eight=True, depth=depth)
+        out = gpu.device.fill_hash(n, torch.int8, seed, 0)
+        got = P.run_loopback_tiled(plan, 2, rounds, seed=seed, out=out)
+        torch.cuda.synchronize()
+        bad = band_mismatches(gpu, oracle, {depth * rounds: got}, n, np.int8, seed, 0, 2, 1, bands=bands)
+        assert bad == {depth * rounds: 0}, (depth, bad)
+        del got, out
+        torch.cuda.empty_cache()
+
+
+def _tiled_peer_worker(rank, world, port, n, level, kind, rounds, out, depth=1, fused=False):
+    import torch.distributed as dist
+
+    import oracle
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        plan = P.PartitionPlan(n, level, world, eight=kind == 2, depth=depth)
+        init = oracle.fill_hash(n, np.int8, 9, 0)
+        ca = P.TiledCA(plan, rank, kind, 1, init=torch.from_numpy(init).cuda(), group=dist.group.WORLD, halo="peer",
+                       fused=fused)
+        for _ in range(rounds):
+            ca.step()
+        got = torch.from_numpy(init.copy()).cuda()
+        ca.store_dense(got)
+        ca.peer.check()
+        lo, hi = plan.ranges[rank]
+        want = _reference_steps(init, kind, 1, rounds * depth)
+        ok = True
+        for s in range(lo, hi):
+            bx, by = P.subgasket_block(s, level)
+            m = plan.m
+            ok &= bool(np.array_equal(got[by * m:(by + 1) * m, bx * m:(bx + 1) * m].cpu().numpy(),
+                                      want[by * m:(by + 1) * m, bx * m:(bx + 1) * m]))
+        out[rank] = ok
+        out[f"bytes{rank}"] = ca.storage_bytes
+        ca.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,depth,kind,fused", [(2, 1, 2, False), (2, 1, 1, True), (4, 2, 2, True),
+                                                    (4, 6, 2, False), (2, 6, 1, True), (3, 4, 2, True)])
+def test_tiled_peer_memory_processes(gpu, world, depth, kind, fused):
+    """TiledCA(halo="peer"): per-entry destinations (gm_peer_halo_put_to / the fused
+    epilogue's didx) into the peers' rings and the rank's own rings, processes sharing
+    the test GPU; every rank's sub-gaskets equal the oracle's steps."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    mgr = ctx.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    ps = [ctx.Process(target=_tiled_peer_worker, args=(r, world, port, 1 << 10, 3, kind, 3, out, depth, fused))
+          for r in range(world)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    assert all(out[r] for r in range(world)), dict(out)
