@@ -607,7 +607,12 @@ def run_ours(args) -> None:
         # reports per-CA-step figures
         plan = P.PartitionPlan(n, PART_LEVEL, world, eight=kind == 2, depth=args.temporal)
         group = dist.group.WORLD if world > 1 else None
-        if world > 1 and args.halo in ("peer", "peer-fused"):
+        if args.storage == "tiled":
+            # each rank holds only its sub-gaskets, each a block with a ring (TiledLayout)
+            peer = world > 1 and args.halo in ("peer", "peer-fused")
+            part = P.TiledCA(plan, rank, kind, 1, dtype=tdt, seed=1, group=group,
+                             halo="peer" if peer else "collective", fused=args.halo == "peer-fused" and peer)
+        elif world > 1 and args.halo in ("peer", "peer-fused"):
             # halo over peer memory (CUDA IPC + release/acquire flags): no collective per step
             def fill(t):
                 native.call("gm_fill_hash", t.data_ptr(), n, c, 1, 0, device.stream_handle())
@@ -619,10 +624,10 @@ def run_ours(args) -> None:
             part = P.PartitionedCA(plan, rank, init, kind, 1, group=group, adopt_init=True)
             del init
         torch.cuda.empty_cache()
-        if world == 1:
+        if world == 1 and args.storage != "tiled":
             step = lambda: (part.compute(), part.finish())  # noqa: E731  (no peers: nothing to exchange)
         else:
-            step = part.step
+            step = part.step  # (tiled, one rank: the blocks' own ring copies every round)
         grid = src = None
     else:
         grid = torch.zeros((n, n), dtype=tdt, device="cuda")
@@ -710,12 +715,18 @@ def run_ours(args) -> None:
     if part is not None:
         line["config"]["halo_bytes_per_step"] = part.halo_bytes_per_step if world > 1 else 0
         line["config"]["halo"] = (args.halo if world > 1 else "none (one rank)")
+        line["config"]["storage"] = args.storage
+        if args.storage == "tiled":
+            line["config"]["storage_bytes_per_rank"] = part.storage_bytes
+            line["config"]["storage_note"] = ("the rank's level-5 sub-gaskets as ringed blocks, two ping-pong "
+                                              "buffers (the dense layout: two n x n grids per rank)")
         if ca_steps > 1:
             line["config"]["ca_steps_per_launch"] = ca_steps
             line["config"]["timing"] = (f"{ca_steps} fused CA steps per timed launch; ms_per_step and value are per "
                                         f"CA step; roofline fracs are work-equivalent (one step's bytes per step)")
         if args.project and world == 1:
-            line["projection"] = [_project(part, int(w), ms_per_step * ca_steps, ca_steps, flusher)
+            proj = _project_tiled if args.storage == "tiled" else _project
+            line["projection"] = [proj(part, int(w), ms_per_step * ca_steps, ca_steps, flusher)
                                   for w in args.project.split(",")]
         if hasattr(part, "close"):
             part.close()
@@ -768,16 +779,9 @@ def _project(part, world: int, ms_launch_1: float, ca_steps: int, flusher, reps:
     plan = P.PartitionPlan(part.plan.n, part.plan.level, world, eight=part.plan.eight, depth=part.plan.depth)
     per_rank = []
     for lo, hi in plan.ranges:
-        ts = []
-        for _ in range(reps):
-            flusher()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            part.step_fn(part.b, part.a, lo, hi)
-            b.record()
-            b.synchronize()
-            ts.append(a.elapsed_time(b))
-        per_rank.append(statistics.fmean(ts) / ca_steps)
+        part.step_fn(part.b, part.a, lo, hi)
+        # back to back, like the one-GPU line it is compared with
+        per_rank.append(_time_b2b(lambda: part.step_fn(part.b, part.a, lo, hi), reps * 5) / ca_steps)
     slots, width = plan.exchange_slots()
     worst = max(per_rank)
     return {"world": world, "per_rank_ms_per_step": per_rank, "max_rank_ms_per_step": worst,
@@ -785,6 +789,40 @@ def _project(part, world: int, ms_launch_1: float, ca_steps: int, flusher, reps:
             "halo_cells_per_rank_per_exchange": [int(len(x)) for x in slots],
             "note": ("each rank's sub-gasket range timed alone on one GPU, no exchange: a compute-only "
                      "bound on the N-GPU step, not a scaling measurement")}
+
+
+def _project_tiled(part, world: int, ms_launch_1: float, ca_steps: int, flusher, reps: int = 10) -> dict:
+    """_project on tiled storage: each of `world` ranks built alone (its own blocks, rings
+    loaded from the synthetic grid) and timed for one round -- its launch plus its own ring
+    copies, no peer traffic.  A compute-only bound on the N-GPU step."""
+    import torch
+
+    from paper_1706_04552_b200 import partition as P
+
+    plan = P.PartitionPlan(part.plan.n, part.plan.level, world, eight=part.plan.eight, depth=part.plan.depth)
+    per_rank, storage = [], []
+    for r in range(world):
+        ca = P.TiledCA(plan, r, part.kind, part.param, dtype=part.a.dtype, seed=1,
+                       loopback=P.LoopbackGroup(world))
+        storage.append(ca.storage_bytes)
+
+        def one():
+            ca.compute()
+            ca._coll.complete(ca.b)  # (own ring copies; the loopback values of the others are stale)
+            ca.finish()
+
+        ca._coll.post(ca.b)  # one contribution so complete() has a gathered buffer
+        for _ in range(3):
+            one()
+        # back to back, like the one-GPU line it is compared with
+        per_rank.append(_time_b2b(one, reps * 5) / ca_steps)
+        del ca
+        torch.cuda.empty_cache()
+    worst = max(per_rank)
+    return {"world": world, "per_rank_ms_per_step": per_rank, "max_rank_ms_per_step": worst,
+            "speedup_vs_one_gpu": ms_launch_1 / ca_steps / worst, "storage_bytes_per_rank": storage,
+            "note": ("each rank's blocks built and timed alone on one GPU (launch + own ring copies, no peer "
+                     "traffic): a compute-only bound on the N-GPU step, not a scaling measurement")}
 
 
 def run_reference(args) -> None:
@@ -885,6 +923,9 @@ def main() -> None:
     ap.add_argument("--halo", choices=("collective", "peer", "peer-fused"), default="collective",
                     help="part* workloads, N>1: NCCL all_gather of the halo cells, peer-memory puts (CUDA IPC), "
                          "or the peer exchange fused into the step kernel (any --temporal)")
+    ap.add_argument("--storage", choices=("tiled", "dense"), default="tiled",
+                    help="part* workloads: per-rank sub-gasket blocks with a ring (tiled) or two n x n grids per "
+                         "rank (dense)")
     ap.add_argument("--r-min", type=int, default=8)
     ap.add_argument("--r-max", type=int, default=18)
     ap.add_argument("--nsweep-out", default="profiles/r1_nsweep.csv")

@@ -811,12 +811,14 @@ class _TiledCollective:
         self.recv_idx = torch.from_numpy(np.concatenate(cells) if cells else np.zeros(0, np.int64)).to(dev)
         self.sendbuf = torch.zeros(self.width, dtype=dtype, device=dev)
         self.gathered = torch.zeros(self.width * W, dtype=dtype, device=dev)
-        self.bytes_per_step = int(self.width * W * self.sendbuf.element_size())
+        self.bytes_per_step = int(self.width * W * self.sendbuf.element_size()) if W > 1 else 0
 
     def post(self, buf: torch.Tensor) -> None:
         from . import device as dev
         from . import native
 
+        if self.plan.world == 1:
+            return  # one rank: only its own ring copies (complete)
         k = self.send_idx.numel()
         if k:
             native.call("gm_gather_cells", buf.data_ptr(), buf.element_size(), self.send_idx.data_ptr(), k,
@@ -832,7 +834,7 @@ class _TiledCollective:
         from . import device as dev
         from . import native
 
-        if self.loopback is not None:
+        if self.loopback is not None and self.plan.world > 1 and len(self.loopback._parts) == self.plan.world:
             self.gathered.copy_(self.loopback.gathered())
         k = self.recv_idx.numel()
         if k:
