@@ -87,6 +87,8 @@ extern "C" {
                                             stored whole (gasket cells = param, the rest 0), no DRAM read-modify-write */
 #define GM_FLAG_WRITE_HALVES 134217728 /* zero-background write pass: store the touched 64-byte halves whole */
 #define GM_FLAG_WRITE_LINES 268435456  /* zero-background write pass: store the touched 128-byte lines whole */
+#define GM_FLAG_STATIC_SCHEDULE 4096 /* tuned write pass: static round-robin units instead of the ticket queue
+                                       (A/B; shares its value with the stencil-only GM_FLAG_STAGES2) */
 #define GM_FLAG_WRITE_SWEEP 1073741824 /* tuned write pass: the grid's member lines in address order, chunks of
                                           32 lines dealt round-robin over all warps (write.cu) */
 #define GM_FLAG_GRID_ROWS 536870912   /* tuned write pass: no blocks -- one warp per grid row, its member lines

@@ -298,8 +298,12 @@ int gm_snapshot_stencil(void* snap, const void* grid, int64_t n, int32_t cell_by
 int gm_writeback_tiles(void* out, const void* dst, const void* snap, int64_t n, int32_t cell_bytes, void* stream) {
     if (!out || !dst || !snap || out == dst || out == snap) return fail(GM_EINVAL, "gm_writeback_tiles: bad buffers");
     if (n < 1) return fail(GM_EINVAL, "bad edge");
-    // the row-ordered walk (host pages K lines at a time) for 1/2/4-byte cells, else per tile
-    cudaError_t e = gm::launch_host_rows_copyback(out, dst, snap, n, cell_bytes, reinterpret_cast<cudaStream_t>(stream));
+    // the row-ordered walk (host pages K lines at a time) for 1/2/4-byte cells on 64-byte
+    // aligned grids, else per tile (host grids off a 64-byte boundary: in host-aligned units)
+    const bool aligned = (reinterpret_cast<uintptr_t>(out) & 63u) == 0;
+    cudaError_t e = aligned ? gm::launch_host_rows_copyback(out, dst, snap, n, cell_bytes,
+                                                            reinterpret_cast<cudaStream_t>(stream))
+                            : cudaErrorNotSupported;
     if (e == cudaErrorNotSupported) {
         cudaGetLastError();
         e = gm::launch_writeback_tiles(out, dst, snap, n, cell_bytes, reinterpret_cast<cudaStream_t>(stream));

@@ -38,12 +38,21 @@ __device__ __forceinline__ uint4 ld16(const uint8_t* p, bool half) {
 // UNROLL 16-byte pieces per round with all its loads in flight before the stores
 constexpr int UNROLL = 8;
 
+// s64 != 0 (a host grid that starts s64 bytes past a 64-byte boundary, e.g. a plain numpy
+// array): each window row is widened to the host-aligned 64-byte units that cover it
+// (PCIe reads whole units; 16 pieces per row instead of 12), so that the write-back can
+// store whole host units too; pieces outside the array are skipped.
 __global__ void __launch_bounds__(256) snapshot_tiles(uint8_t* __restrict__ snap, const uint8_t* __restrict__ grid,
                                                       int64_t n, int cell_bytes, const uint32_t* __restrict__ order,
-                                                      uint32_t ntiles, uint32_t nb) {
+                                                      uint32_t ntiles, uint32_t nb, int s64) {
     const int64_t rowbytes = n * cell_bytes;
+    const int64_t total = rowbytes * n;
     const int tt = 128 / cell_bytes;  // tile rows (and cells per row)
-    const int per_tile = (tt + 2) * VEC_PER_ROW;
+    const int vpr = s64 ? 16 : VEC_PER_ROW;  // pieces per window row
+    const int per_tile = (tt + 2) * vpr;
+    // first piece of a window row relative to the tile's line: -32 aligned, else the host
+    // unit holding byte -32 (unit boundaries at grid offsets g with (g + s64) % 64 == 0)
+    const int64_t lead = s64 ? 32 + ((s64 - 32) & 63) : 32;
     const int lane = threadIdx.x & 31;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -56,7 +65,8 @@ __global__ void __launch_bounds__(256) snapshot_tiles(uint8_t* __restrict__ snap
         const bool down = by + 1 < nb && (bx & ~(by + 1)) == 0;
         const bool left = bx > 0 && ((bx - 1) & ~by) == 0;
         const bool right = bx + 1 < nb && ((bx + 1) & ~by) == 0;
-        const int64_t xb0 = (int64_t)bx * 128 - 32;  // window's first byte
+        const int64_t line0 = (int64_t)bx * 128;    // the tile's line
+        const int64_t xb0 = line0 - lead;            // window's first byte
         const int64_t y0 = (int64_t)by * tt - 1;     // window's first row
         for (int base = 0; base < per_tile; base += 32 * UNROLL) {
             uint4 val[UNROLL];
@@ -64,13 +74,19 @@ __global__ void __launch_bounds__(256) snapshot_tiles(uint8_t* __restrict__ snap
 #pragma unroll
             for (int k = 0; k < UNROLL; ++k) {
                 const int i = base + k * 32 + lane;
-                const int row = i / VEC_PER_ROW, q = i - row * VEC_PER_ROW;
+                const int row = i / vpr, q = i - row * vpr;
                 const int64_t y = y0 + row, xb = xb0 + q * 16;
-                const bool skip = i >= per_tile || (row == 0 && up) || (row == tt + 1 && down) ||
-                                  (q < 2 && left) || (q >= 10 && right) || y < 0 || y >= n || xb < 0 ||
-                                  xb >= rowbytes;
+                const bool lpart = xb < line0, rpart = xb >= line0 + 128;
+                bool skip = i >= per_tile || (row == 0 && up) || (row == tt + 1 && down) || (lpart && left) ||
+                            (rpart && right) || y < 0 || y >= n;
+                if (s64 == 0) {
+                    skip = skip || xb < 0 || xb >= rowbytes;
+                } else {  // host units may run into the neighbouring rows: only the array's bytes
+                    const int64_t f = y * rowbytes + xb;
+                    skip = skip || f < 0 || f >= total;
+                }
                 off[k] = skip ? -1 : y * rowbytes + xb;
-                if (!skip) val[k] = ld16(grid + off[k], q < 2 || q >= 10);
+                if (!skip) val[k] = ld16(grid + off[k], lpart || rpart);
             }
 #pragma unroll
             for (int k = 0; k < UNROLL; ++k)
@@ -83,13 +99,19 @@ __global__ void __launch_bounds__(256) snapshot_tiles(uint8_t* __restrict__ snap
 // rows (one 128-byte line each) go back whole -- the touched sectors from `dst` (the
 // stencil's whole-sector results), the other sectors from `snap` (the pre-launch state)
 // -- so the host sees whole-line writes only.
+// s64 != 0 (host grid s64 bytes past a 64-byte boundary): each line goes back as the
+// host-aligned 64-byte units that cover it (12 pieces; the bytes of the neighbouring
+// lines they include come, by the same rule, from `dst` or `snap`, whose host-aligned
+// windows hold them; two tiles may store the same unit with the same bytes).
 __global__ void __launch_bounds__(256) writeback_tiles(uint8_t* __restrict__ out, const uint8_t* __restrict__ dst,
                                                        const uint8_t* __restrict__ snap, int64_t n, int cell_bytes,
-                                                       const uint32_t* __restrict__ order, uint32_t ntiles) {
+                                                       const uint32_t* __restrict__ order, uint32_t ntiles, int s64) {
     const int64_t rowbytes = n * cell_bytes;
+    const int64_t total = rowbytes * n;
     const int tt = 128 / cell_bytes;
     const int sc = 32 / cell_bytes;  // cells per sector
-    const int per_tile = tt * 8;     // 16-byte pieces of the tile's own lines
+    const int vpr = s64 ? 12 : 8;    // pieces per line (host units covering it)
+    const int per_tile = tt * vpr;   // 16-byte pieces of the tile's own lines
     const int lane = threadIdx.x & 31;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -102,11 +124,25 @@ __global__ void __launch_bounds__(256) writeback_tiles(uint8_t* __restrict__ out
 #pragma unroll
             for (int k = 0; k < UNROLL; ++k) {
                 const int i = base + k * 32 + lane;
-                const int row = i >> 3, q = i & 7;
-                off[k] = i < per_tile ? (y0 + row) * rowbytes + xb0 + q * 16 : -1;
-                if (off[k] >= 0) {
-                    const bool touched = (((q >> 1) * sc) & ~row) == 0;  // sector holds gasket cells
-                    val[k] = __ldcs(reinterpret_cast<const uint4*>((touched ? dst : snap) + off[k]));
+                if (s64 == 0) {
+                    const int row = i >> 3, q = i & 7;
+                    off[k] = i < per_tile ? (y0 + row) * rowbytes + xb0 + q * 16 : -1;
+                    if (off[k] >= 0) {
+                        const bool touched = (((q >> 1) * sc) & ~row) == 0;  // sector holds gasket cells
+                        val[k] = __ldcs(reinterpret_cast<const uint4*>((touched ? dst : snap) + off[k]));
+                    }
+                } else {
+                    const int row = i / vpr, q = i - row * vpr;
+                    const int64_t f = (y0 + row) * rowbytes + xb0 - s64 + q * 16;
+                    off[k] = (i < per_tile && f >= 0 && f < total) ? f : -1;
+                    if (off[k] >= 0) {
+                        // the piece's own row, line and sector decide where its bytes come from
+                        const int64_t yy = f / rowbytes, col = f - yy * rowbytes;
+                        const int64_t X = col >> 7, Yb = yy / tt, t = yy - Yb * tt;
+                        const int g = (int)((col & 127) >> 5);
+                        const bool touched = (X & ~Yb) == 0 && (((int64_t)g * sc) & ~t) == 0;
+                        val[k] = __ldcs(reinterpret_cast<const uint4*>((touched ? dst : snap) + off[k]));
+                    }
                 }
             }
 #pragma unroll
@@ -134,8 +170,10 @@ cudaError_t launch_writeback_tiles(void* out, const void* dst, const void* snap,
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     uint32_t blocks = (uint32_t)sms * 8u;
     if (blocks > (ntiles + 7) / 8) blocks = (ntiles + 7) / 8;
+    const int s64 = (int)(reinterpret_cast<uintptr_t>(out) & 63u);
+    if (s64 % 16 != 0) return cudaErrorNotSupported;  // (numpy data is at least 16-byte aligned)
     writeback_tiles<<<blocks, 256, 0, s>>>(reinterpret_cast<uint8_t*>(out), reinterpret_cast<const uint8_t*>(dst),
-                                           reinterpret_cast<const uint8_t*>(snap), n, cell_bytes, order, ntiles);
+                                           reinterpret_cast<const uint8_t*>(snap), n, cell_bytes, order, ntiles, s64);
     note_launch();
     return cudaGetLastError();
 }
@@ -157,8 +195,11 @@ cudaError_t launch_snapshot_stencil(void* snap, const void* grid, int64_t n, int
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     uint32_t blocks = (uint32_t)sms * 8u;  // 64 warps per SM, a tile each
     if (blocks > (ntiles + 7) / 8) blocks = (ntiles + 7) / 8;
+    // a grid that is not 64-byte aligned (a host numpy array) is read in host-aligned units
+    const int s64 = (int)(reinterpret_cast<uintptr_t>(grid) & 63u);
+    if (s64 % 16 != 0) return cudaErrorNotSupported;
     snapshot_tiles<<<blocks, 256, 0, s>>>(reinterpret_cast<uint8_t*>(snap), reinterpret_cast<const uint8_t*>(grid), n,
-                                          cell_bytes, order, ntiles, 1u << r_t);
+                                          cell_bytes, order, ntiles, 1u << r_t, s64);
     note_launch();
     return cudaGetLastError();
 }

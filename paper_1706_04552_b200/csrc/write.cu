@@ -131,6 +131,27 @@ __device__ __forceinline__ uint64_t lambda_lane_reciprocal(int lane) {
     return ~0ull / p3 + 1ull;  // floor(c / 3^lane) = umulhi(c, this) for c < 2^32
 }
 
+// Dynamic work distribution.  Warps take units from a ticket counter instead of a
+// static round-robin: the SMs do not run at the same speed (ncu, n=2^16 int8: SM active
+// cycles from 57 K to 98 K within one 111 K-cycle launch of the grid-row kernel -- the
+// SMs nearer the DRAM and L2 they write finish early), so a static split leaves the
+// fast SMs idle for the tail.  q[0] = next ticket, q[1] = warps retired; the last warp
+// to retire zeroes both for the next launch on the stream.
+__device__ __forceinline__ uint32_t grab(uint32_t* q, int lane, uint32_t step) {
+    uint32_t t = 0;
+    if (lane == 0) t = atomicAdd(q, step);
+    return __shfl_sync(0xffffffffu, t, 0);
+}
+__device__ __forceinline__ void retire(uint32_t* q, int lane, uint32_t nwarps) {
+    if (q == nullptr || lane != 0) return;
+    __threadfence();
+    if (atomicAdd(q + 1, 1u) == nwarps - 1) {
+        q[0] = 0u;
+        q[1] = 0u;
+        __threadfence();
+    }
+}
+
 // lambda of compact tile index c at level q (q <= 20): every lane returns (X, Y).
 __device__ __forceinline__ void lambda_lanes(uint32_t c, int q, int lane, uint64_t inv, uint32_t& X, uint32_t& Y) {
     const uint32_t qd = lane == 0 ? c : (uint32_t)__umul64hi((uint64_t)c, inv);
@@ -164,7 +185,8 @@ __device__ __forceinline__ void tile_rows(uint32_t k, int q, int lane, uint32_t&
 // lane l holds word l of the row.
 template <int C, bool ZERO, bool ROWMAJOR, bool COUNT = false>
 __global__ void __launch_bounds__(256) gasket_write(uint8_t* __restrict__ grid, int64_t n, int q, uint32_t u_lo,
-                                                    uint32_t u_hi, uint64_t param) {
+                                                    uint32_t u_hi, uint64_t param, uint32_t* __restrict__ wq,
+                                                    int tshift) {
     using G = WGeo<C>;
     const int lane = threadIdx.x & 31;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -174,7 +196,14 @@ __global__ void __launch_bounds__(256) gasket_write(uint8_t* __restrict__ grid, 
     const uint32_t js = (uint32_t)(lane & ~7) * 4u / C;                            // first cell of its sector
     const uint32_t v = splat_w<C>(param, lane);
     const uint64_t inv = lambda_lane_reciprocal(lane);
-    for (uint32_t u = u_lo + warp; u < u_hi; u += nwarps) {
+    // units come 1 << tshift per ticket (consecutive bands of one tile) when the queue is there
+    uint32_t u = u_lo + warp, u_end = u + 1;
+    if (wq != nullptr) {
+        u = u_lo + (grab(wq, lane, 1u) << tshift);
+        u_end = u + (1u << tshift);
+    }
+    for (;;) {
+        if (u >= u_hi) break;
         const uint32_t tile = u >> G::LB;
         uint32_t X, Y;
         if constexpr (ROWMAJOR) tile_rows(tile, q, lane, X, Y);
@@ -197,7 +226,16 @@ __global__ void __launch_bounds__(256) gasket_write(uint8_t* __restrict__ grid, 
                 }
             }
         }
+        if (wq != nullptr) {
+            if (++u == u_end) {
+                u = u_lo + (grab(wq, lane, 1u) << tshift);
+                u_end = u + (1u << tshift);
+            }
+        } else {
+            u += nwarps;
+        }
     }
+    retire(wq, lane, nwarps);
 }
 
 // GM_FLAG_GRID_ROWS: one warp per grid row y (bottom row first: the heaviest rows
@@ -206,13 +244,28 @@ __global__ void __launch_bounds__(256) gasket_write(uint8_t* __restrict__ grid, 
 // has low bits g: X = pdep(g, the two lowest bits of Y) | S, S over the subsets of Y's
 // other bits in increasing order.  General: 4-byte lanes, one line per instruction.
 template <int C, bool ZERO, int GRAN, bool COUNT = false>
-__global__ void __launch_bounds__(256) gasket_write_rows(uint8_t* __restrict__ grid, int64_t n, uint64_t param) {
+__global__ void __launch_bounds__(256) gasket_write_rows(uint8_t* __restrict__ grid, int64_t n, uint64_t param,
+                                                         uint32_t* __restrict__ wq) {
     using G = WGeo<C>;
     const int lane = threadIdx.x & 31;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     const int64_t rowstride = n * C;
-    for (uint32_t yy = warp; yy < (uint32_t)n; yy += nwarps) {
+    constexpr uint32_t RPT = 4;  // rows per ticket
+    uint32_t yy = warp, yy_end = yy + 1;
+    if (wq != nullptr) {
+        yy = grab(wq, lane, 1u) * RPT;
+        yy_end = yy + RPT;
+    }
+    auto advance = [&] {
+        if (wq == nullptr) {
+            yy += nwarps;
+        } else if (++yy == yy_end) {
+            yy = grab(wq, lane, 1u) * RPT;
+            yy_end = yy + RPT;
+        }
+    };
+    for (; yy < (uint32_t)n; advance()) {
         const uint32_t y = (uint32_t)n - 1u - yy;
         const uint32_t Y = y >> G::LT, t = y & (G::TT - 1);
         if constexpr (!ZERO) {
@@ -273,6 +326,7 @@ __global__ void __launch_bounds__(256) gasket_write_rows(uint8_t* __restrict__ g
             } while (S != 0);
         }
     }
+    retire(wq, lane, nwarps);
 }
 
 // GM_FLAG_WRITE_SWEEP: the grid rows' member lines in ADDRESS order, cut into work units of
@@ -445,6 +499,50 @@ cudaError_t launch_bb_vec(const LaunchArgs& a) {
 }
 
 
+// units per ticket of the lambda-tile write pass (log2): one band per ticket -- concurrently
+// running warps then hold consecutive bands of a tile (n=2^16 int8 back to back: 107.7 us,
+// 109.1 with two bands, 109.8 with a whole tile per ticket, 115.1 static; A/B knob
+// GASKET_WRITE_TICKET_SHIFT)
+template <class G>
+int ticket_shift() {
+    static const int v = [] {
+        const char* e = getenv("GASKET_WRITE_TICKET_SHIFT");
+        return e ? atoi(e) : 0;
+    }();
+    return v < 0 ? 0 : (v > G::LB ? G::LB : v);
+}
+
+std::mutex g_wq_mu;
+std::map<std::pair<int, cudaStream_t>, uint32_t*> g_wq;
+
+// The ticket counters of the dynamic schedule, one pair per (device, stream) so launches
+// on different streams never share one; nullptr (the static schedule) while a stream is
+// being captured before its pair exists, or if allocation fails.
+uint32_t* work_queue(cudaStream_t s) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_wq_mu);
+    auto it = g_wq.find({dev, s});
+    if (it != g_wq.end()) return it->second;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    uint32_t* q = nullptr;
+    if (cudaMalloc(&q, 2 * sizeof(uint32_t)) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    if (cudaMemset(q, 0, 2 * sizeof(uint32_t)) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(q);
+        return nullptr;
+    }
+    g_wq[{dev, s}] = q;
+    return q;
+}
+
 template <int C, bool ZERO, bool COUNT = false>
 cudaError_t launch_c(const LaunchArgs& a, int q) {
     using G = WGeo<C>;
@@ -463,7 +561,9 @@ cudaError_t launch_c(const LaunchArgs& a, int q) {
                    : gran == 1        ? gasket_write_rows<C, ZERO, 1, COUNT>
                    : gran == 2        ? gasket_write_rows<C, ZERO, 2, COUNT>
                                       : gasket_write_rows<C, ZERO, 3, COUNT>;
-        kr<<<(unsigned)blocks, 256, 0, a.stream>>>(reinterpret_cast<uint8_t*>(a.grid), a.n, a.param);
+        // (zero background: the static schedule -- 55 vs 75 us with tickets at n=2^16 int8)
+        uint32_t* wq = (ZERO || (a.flags & GM_FLAG_STATIC_SCHEDULE)) ? nullptr : work_queue(a.stream);
+        kr<<<(unsigned)blocks, 256, 0, a.stream>>>(reinterpret_cast<uint8_t*>(a.grid), a.n, a.param, wq);
         note_launch();
         return cudaGetLastError();
     }
@@ -487,8 +587,11 @@ cudaError_t launch_c(const LaunchArgs& a, int q) {
     // fewer pages at a time (n=2^16 int8 zero background, back to back: 59.6 us vs 71.6
     // with 2-8 CTAs per SM; general: 114.6 vs 117.3; scripts/write_ab.py)
     const uint64_t blocks = std::min<uint64_t>((uint64_t)sm_count(), ((u_hi - u_lo) * 32 + 255) / 256);
+    // tickets for the general store mode (n=2^16 int8 107.7 vs 115.1 us back to back, 2^17 314 vs 334);
+    // the zero-background pass keeps the static round-robin (60.5 vs 78 us with tickets)
+    uint32_t* wq = (ZERO || (a.flags & GM_FLAG_STATIC_SCHEDULE)) ? nullptr : work_queue(a.stream);
     kern<<<(unsigned)blocks, 256, 0, a.stream>>>(reinterpret_cast<uint8_t*>(a.grid), a.n, q, (uint32_t)u_lo,
-                                                 (uint32_t)u_hi, a.param);
+                                                 (uint32_t)u_hi, a.param, wq, ticket_shift<G>());
     note_launch();
     return cudaGetLastError();
 }

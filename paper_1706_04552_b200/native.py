@@ -33,6 +33,7 @@ FLAG_FOUR_STEPS = 16777216
 FLAG_SIX_STEPS = 33554432
 FLAG_ZERO_BACKGROUND, FLAG_GRID_ROWS = 67108864, 536870912
 FLAG_WRITE_HALVES, FLAG_WRITE_LINES, FLAG_WRITE_SWEEP = 134217728, 268435456, 1073741824
+FLAG_STATIC_SCHEDULE = 4096  # write pass only (the stencil reads the same bit as FLAG_STAGES2)
 
 
 class GmCfg(ctypes.Structure):

@@ -780,7 +780,7 @@ class _TiledCollective:
     values are scattered into this rank's rings, and the rank's own ring copies run as
     one gm_copy_cells."""
 
-    def __init__(self, plan, rank, entries, dtype, group=None, loopback=None) -> None:
+    def __init__(self, plan, rank, entries, dtype, group=None, loopback=None, device: str = "cuda") -> None:
         self.plan, self.rank, self.group, self.loopback = plan, rank, group, loopback
         W = plan.world
         # per source rank o: its unique cells read by other ranks, in a fixed order
@@ -792,7 +792,7 @@ class _TiledCollective:
         self.width = max([1] + [len(v) for v in sends])
         srcs, dsts = entries[rank]
         local = (dsts >> 56) == rank
-        dev = torch.device("cuda")
+        dev = torch.device(device)
         self.send_idx = torch.from_numpy(sends[rank]).to(dev)
         self.local_src = torch.from_numpy(srcs[local]).to(dev)
         self.local_dst = torch.from_numpy(dsts[local] & ((1 << 56) - 1)).to(dev)

@@ -99,19 +99,34 @@ def _peer_worker(rank, world, port, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
-    n = 256
+    n, level = 1024, 3
     ok = True
-    for depth in (1, 2, 6):
-        plan = P.PartitionPlan(n, 2, world, eight=True, depth=depth)
+    try:
         init = oracle.fill_hash(n, np.int8, 9, 0)
-        ca = P.PartitionedCA(plan, rank, torch.from_numpy(init).cuda(), 2, 1, group=dist.group.WORLD, halo="peer",
-                             fused=True)
-        for _ in range(2):
-            ca.step()
-        torch.cuda.synchronize()
-        mask = ca.owned_mask().cpu().numpy()
-        ok &= bool(np.array_equal(ca.a.cpu().numpy()[mask], steps(init, 2, 1, 2 * depth)[mask]))
-        ca.close()
+        for depth in (1, 2, 6):
+            want = steps(init, 2, 1, 2 * depth)
+            plan = P.PartitionPlan(n, level, world, eight=True, depth=depth)
+            # dense layout, exchange fused into the step kernel
+            ca = P.PartitionedCA(plan, rank, torch.from_numpy(init).cuda(), 2, 1, group=dist.group.WORLD,
+                                 halo="peer", fused=True)
+            for _ in range(2):
+                ca.step()
+            torch.cuda.synchronize()
+            mask = ca.owned_mask().cpu().numpy()
+            ok &= bool(np.array_equal(ca.a.cpu().numpy()[mask], want[mask]))
+            ca.close()
+            # tiled storage, per-entry destinations in the fused epilogue
+            tc = P.TiledCA(plan, rank, 2, 1, init=torch.from_numpy(init).cuda(), group=dist.group.WORLD,
+                           halo="peer", fused=True)
+            for _ in range(2):
+                tc.step()
+            got = torch.from_numpy(init.copy()).cuda()
+            tc.store_dense(got)
+            ok &= bool(np.array_equal(got.cpu().numpy()[mask], want[mask]))
+            tc.close()
+    except Exception as e:  # report instead of leaving the parent waiting
+        print(f"rank {rank}: {e!r}", flush=True)
+        ok = False
     dist.destroy_process_group()
     q.put((rank, ok))
 
@@ -124,7 +139,7 @@ def main_part():
     ps = [ctx.Process(target=_peer_worker, args=(r, 2, 29611, q)) for r in range(2)]
     for p in ps:
         p.start()
-    res = dict(q.get(timeout=600) for _ in ps)
+    res = dict(q.get(timeout=900) for _ in ps)
     for p in ps:
         p.join()
     print(f"sanitize part (2 processes, fused peer epilogue): {'ok' if all(res.values()) else res}", flush=True)

@@ -32,6 +32,10 @@ VARIANTS = (
     ("gridrows-zero-halves", Z | native.FLAG_GRID_ROWS | native.FLAG_WRITE_HALVES),
     ("gridrows-zero-lines", Z | native.FLAG_GRID_ROWS | native.FLAG_WRITE_LINES),
     ("gridrows-zero-v8", Z | native.FLAG_GRID_ROWS | native.FLAG_WRITE_LINES | native.FLAG_WRITE_HALVES),
+    ("lambda-static", native.FLAG_STATIC_SCHEDULE),
+    ("gridrows-zero-static", Z | native.FLAG_GRID_ROWS | native.FLAG_STATIC_SCHEDULE),
+    ("lambda-zero-static", Z | native.FLAG_DIGIT_ORDER | native.FLAG_STATIC_SCHEDULE),
+    ("lambda-zero-dyn", Z | native.FLAG_DIGIT_ORDER),
     ("sweep", native.FLAG_WRITE_SWEEP),
     ("sweep-zero", Z | native.FLAG_WRITE_SWEEP),
     ("hostrows-zero", Z | native.FLAG_HOST_ROWS | native.FLAG_EXPLICIT_RMW | native.FLAG_WHOLE_LINES),

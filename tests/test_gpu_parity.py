@@ -624,6 +624,34 @@ def test_pin_cache_registers_once_and_releases(gpu, monkeypatch):
     assert dev.pinned.pinned_bytes() == 0
 
 
+def test_mapped_staged_stencil_misaligned_host_grids(gpu, oracle, monkeypatch):
+    """The staged neighbour-sum path (masked snapshot -> kernel -> write-back) on host grids
+    16..112 bytes past a 64-byte boundary (the host-aligned windows of snapshot.cu):
+    == the oracle step, the bytes around the array untouched."""
+    monkeypatch.setenv("GASKET_HOST_TRANSPORT", "mapped")
+    S = gpu.geometry.IntraStrategy
+    for dtype in (np.int8, np.int16, np.int32):
+        c = np.dtype(dtype).itemsize
+        for n in (128 // c, 4 * (128 // c), 512):
+            nbytes = n * n * c
+            for shift in (16, 32, 48, 80, 112):
+                for kind in (1, 2):
+                    raw = np.zeros(nbytes + 512, dtype=np.uint8)
+                    base = (-raw.ctypes.data) % 128 + 128 + shift
+                    raw[:] = 0x5A
+                    g = raw[base:base + nbytes].view(dtype).reshape(n, n)
+                    g0 = oracle.fill_hash(n, dtype, 11 + shift, 0)
+                    g[...] = g0
+                    want = g0.copy()
+                    oracle.run_bounding_box(want, g0, 1, kind, 5)
+                    gpu.backends.run_block_space(g, g, 64 if n >= 64 else n, (n // min(64, n)).bit_length() - 1,
+                                                 S.TUNED, kind=kind, param=5)
+                    assert np.array_equal(g, want), (np.dtype(dtype).name, n, shift, kind)
+                    assert (raw[:base] == 0x5A).all() and (raw[base + nbytes:] == 0x5A).all(), (n, shift, "guard")
+                    del g
+    gpu.device.pinned.clear()
+
+
 @pytest.mark.parametrize("dtype", [np.int8, np.int16, np.int32])
 def test_mapped_write_misaligned_host_grids(gpu, oracle, monkeypatch, dtype):
     """The mapped write pass on host grids that do not start on a 128-byte boundary (a

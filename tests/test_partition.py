@@ -443,3 +443,28 @@ def test_tiled_peer_memory_processes(gpu, world, depth, kind, fused):
         p.join(timeout=300)
         assert p.exitcode == 0
     assert all(out[r] for r in range(world)), dict(out)
+
+
+@pytest.mark.parametrize("world,depth", [(2, 1), (4, 2), (8, 6), (3, 4)])
+def test_tiled_collective_and_peer_move_the_same_cells(world, depth):
+    """The all_gather layout of the tiled collective path (unique sends per owner, the
+    receivers' gathered positions, own ring copies) delivers exactly the copies the peer
+    path's per-entry destinations make: the same (destination rank, cell) <- (owner, cell)
+    pairs, nothing more, nothing less."""
+    plan = P.PartitionPlan(1 << 12, 4, world, eight=True, depth=depth)
+    ent = P.tiled_exchange(plan, 1)
+    peer = set()
+    for o, (src, dst) in enumerate(ent):
+        for a, b in zip(src.tolist(), dst.tolist()):
+            peer.add((b >> 56, b & ((1 << 56) - 1), o, a))
+    coll = set()
+    colls = [P._TiledCollective(plan, r, ent, torch.int8, device="cpu") for r in range(world)]
+    sends = [c.send_idx.numpy() for c in colls]
+    for r, c in enumerate(colls):
+        for pos, cell in zip(c.recv_pos.tolist(), c.recv_idx.tolist()):
+            o, slot = divmod(pos, c.width)
+            coll.add((r, cell, o, int(sends[o][slot])))
+        for a, b in zip(c.local_src.tolist(), c.local_dst.tolist()):
+            coll.add((r, b, r, a))
+        assert c.width == colls[0].width  # one fixed-size all_gather
+    assert coll == peer and len(peer) > 0
