@@ -231,8 +231,12 @@ def _traffic_from_profiles(workload: str) -> tuple[float | None, str | None]:
         return None, None
 
 
-def _make_step(workload: str, grid, src, rho: int, flags: int):
-    from paper_1706_04552_b200 import backends
+def _make_step(workload: str, grid, src, rho: int, flags: int, edge=None):
+    """One timed step.  Write pass: backends.run_block_space(grid, grid, ...).  CA step:
+    ping-pong between two buffers that agree off the gasket -- through gm_ca_run with the
+    static left-edge cache when `edge` is given (the CA driver's single step, ca.CARunner),
+    else through the drop-in backends.run_block_space(..., flags=DST_FROM_SRC)."""
+    from paper_1706_04552_b200 import backends, device, native
     from paper_1706_04552_b200.geometry import IntraStrategy
 
     r, _, kind, _, _ = WORKLOADS[workload]
@@ -243,12 +247,16 @@ def _make_step(workload: str, grid, src, rho: int, flags: int):
     def step():
         if kind == 0:
             backends.run_block_space(grid, grid, rho, r_b, IntraStrategy.TUNED, kind=0, param=1)
+            return
+        # CA ping-pong: read bufs[i], write bufs[1-i]; both agree off the gasket
+        i = state["i"]
+        if edge is not None:
+            native.call("gm_ca_run", bufs[1 - i].data_ptr(), bufs[i].data_ptr(), 1 << r, grid.element_size(), kind,
+                        1, 1, edge.data_ptr(), 0, device.stream_handle())
         else:
-            # CA ping-pong: read bufs[i], write bufs[1-i]; both agree off the gasket
-            i = state["i"]
             backends.run_block_space(bufs[1 - i], bufs[i], rho, r_b, IntraStrategy.TUNED, kind=kind, param=1,
                                      flags=flags)
-            state["i"] = 1 - i
+        state["i"] = 1 - i
 
     return step
 
@@ -628,31 +636,41 @@ def run_ours(args) -> None:
             step = lambda: (part.compute(), part.finish())  # noqa: E731  (no peers: nothing to exchange)
         else:
             step = part.step  # (tiled, one rank: the blocks' own ring copies every round)
-        grid = src = None
+        grid = src = edge = None
     else:
         grid = torch.zeros((n, n), dtype=tdt, device="cuda")
-        src = None
+        src = edge = None
         flags = 0
         if kind != 0:
             src = device.fill_hash(n, tdt, 1 + rank, 0)
             grid.copy_(src)
             flags = native.FLAG_DST_FROM_SRC
-        step = _make_step(workload, grid, src, rho, flags)
+            if c in (1, 2, 4):  # the CA driver's step: static left-edge cache (edge.cu)
+                edge = torch.empty(native.ca_edge_bytes(n, c), dtype=torch.uint8, device="cuda")
+                native.call("gm_ca_edge_build", edge.data_ptr(), src.data_ptr(), n, c, -1, 0, 0, None, 0,
+                            device.stream_handle())
+        step = _make_step(workload, grid, src, rho, flags, edge=edge)
+    torch.cuda.synchronize()
+    t_warm = time.perf_counter()
     for _ in range(args.warmup):
         flusher()
         step()
     torch.cuda.synchronize()
+    t_warm = (time.perf_counter() - t_warm) / max(1, args.warmup)
+    # the same steps for ~60 ms right before the timed region, so that the clock sampler sees
+    # the GPU under this load (the timed region itself lasts only milliseconds).  A fixed step
+    # count, the same on every rank: each step of a partitioned run is a collective / a peer
+    # epoch, so ranks must run exactly as many steps as each other
+    busy_steps = int(_max_over_ranks(float(min(2000, max(8, int(0.06 / max(t_warm, 1e-6)) + 1))), world))
 
     _barrier(world)
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        # the same steps for ~60 ms right before the timed region, so that the clock sampler
-        # sees the GPU under this load (the timed region itself lasts only milliseconds)
-        t_busy = time.perf_counter() + 0.06
-        while time.perf_counter() < t_busy:
-            for _ in range(8):
-                step()
-            torch.cuda.synchronize()
+        for i in range(busy_steps):
+            step()
+            if i % 8 == 7:
+                torch.cuda.synchronize()
+        torch.cuda.synchronize()
         _barrier(world)
         t_wall0 = time.perf_counter()
         per = _time_b2b(step, args.steps)
@@ -712,6 +730,21 @@ def run_ours(args) -> None:
         line["roofline"]["pattern_ceiling"] = {
             "us": fl, "frac": fl * 1e-3 / statistics.fmean(ms),
             "note": "the same DRAM accesses in address order (scripts/probe_rmw.cu); frac = ceiling / measured"}
+    if part is None and kind != 0 and edge is not None:
+        # the same CA step through the drop-in call (no edge cache): the reference-shaped launch
+        drop = _make_step(workload, grid, src, rho, flags)
+        for _ in range(3):
+            drop()
+        ms_drop = _time_b2b(drop, args.steps)
+        line["config"]["step"] = ("CA step src -> dst through gm_ca_run (ca.CARunner's single step) with the static "
+                                  "left-edge cache (edge.cu), ping-pong buffers")
+        line["drop_in_step"] = {"ms_per_step": ms_drop, "cells_per_s": cells / (ms_drop * 1e-3),
+                                "frac": alg_bytes / (ms_drop * 1e-3) / 1e9 / peak,
+                                "api": "backends.run_block_space(dst, src, ..., flags=FLAG_DST_FROM_SRC), no edge cache"}
+        line["roofline"]["edge_cache_note"] = (
+            "the CA step stages the off-gasket cells left of member tiles whose left neighbour tile holds no gasket "
+            "cell from a dense cache built once per run, so it reads fewer DRAM lines than the single-launch "
+            "sector model counts; frac keeps the single-launch bytes (drop_in_step.frac: the same bytes, no cache)")
     if part is not None:
         line["config"]["halo_bytes_per_step"] = part.halo_bytes_per_step if world > 1 else 0
         line["config"]["halo"] = (args.halo if world > 1 else "none (one rank)")
@@ -732,7 +765,7 @@ def run_ours(args) -> None:
             part.close()
         line["config"]["subgasket_ranges"] = part.plan.ranges
         del part
-    del grid, src
+    del grid, src, edge
     torch.cuda.empty_cache()
     if rank == 0 and world == 1 and not workload.startswith("part"):
         if not args.no_sweep and kind == 0:

@@ -206,6 +206,25 @@ int gm_ca_step2(void* grid, const void* src, int64_t n, int32_t cell_bytes, int3
  * grid <- step^steps(src), same preconditions. */
 int gm_ca_steps(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
                 int32_t steps, int32_t flags, void* stream);
+/* CA runs with a static left-edge cache (edge.cu, no reference
+ * counterpart).  Off-gasket cells never change in a CA run (backends.py:155-156), so
+ * the 16-byte chunks left of the rows of every member tile whose left neighbour tile
+ * holds no gasket cell -- one sparse DRAM line per row otherwise -- are gathered once
+ * into a dense cache and staged from there by every step.
+ * gm_ca_edge_bytes: the cache size for the tiles of the level-`level` sub-gaskets
+ * [sg_begin, sg_end) (level < 0: the whole gasket).  gm_ca_edge_build: fill it from
+ * `src` (dense n x n, or the tiled blocks of gm_run_part_tiled when sg_off != NULL).
+ * gm_ca_run: `steps` (1, 2, 4 or 6) CA steps src -> grid with the CA ping-pong
+ * preconditions of gm_ca_steps (grid == src off the gasket) and the cache built from a
+ * buffer that agrees with src off the gasket (edge = NULL: no cache; the fused 2/4/6-step
+ * kernels, bound by arithmetic rather than staging, read the grid either way); flags:
+ * GM_FLAG_* kernel variants (0: the defaults). */
+int gm_ca_edge_bytes(int64_t n, int32_t cell_bytes, int32_t level, uint32_t sg_begin, uint32_t sg_end,
+                     int64_t* bytes);
+int gm_ca_edge_build(void* edge, const void* src, int64_t n, int32_t cell_bytes, int32_t level, uint32_t sg_begin,
+                     uint32_t sg_end, const int64_t* sg_off, int64_t pitch, void* stream);
+int gm_ca_run(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param, int32_t steps,
+              const void* edge, int32_t flags, void* stream);
 /* Peer-memory halo exchange of the partitioned CA (peer.cu).
  * gm_dev_alloc/free: plain cudaMalloc'd buffers (allocation bases, so they can be
  * exported); gm_ipc_get_handle writes a 64-byte cudaIpcMemHandle_t; gm_ipc_open_handle
@@ -240,13 +259,16 @@ int gm_peer_halo_put_to(const void* mine, const uint64_t* peers, const int64_t* 
  * gm_run_part_tiled: `steps` (1, 2, 4 or 6) CA steps src -> grid over the rank's blocks
  * (one step: whole-sector blend from src; the blocks of src and grid agree off the gasket);
  * epilogue/wait/signal: the fused peer exchange of gm_run_part_peer (NULL: none; the
- * descriptor's didx then lists per-entry destinations, gm_peer_halo_put_to's format).
+ * descriptor's didx then lists per-entry destinations, gm_peer_halo_put_to's format);
+ * edge: the rank's static left-edge cache (gm_ca_edge_build over the same blocks; used by
+ * one-step launches; NULL: none).
  * gm_copy_cells: dst[dst_idx[i]] = src[src_idx[i]] (cell indices).  gm_fill_hash_window:
  * the synthetic grid's cells [x0, x0+w) x [y0, y0+h) (0 outside n x n) into a pitched
  * block. */
 int gm_run_part_tiled(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
                       int32_t steps, int32_t level, uint32_t sg_begin, uint32_t sg_end, const int64_t* sg_off,
-                      int64_t pitch, void* epilogue, uint64_t wait_epoch, uint64_t signal_epoch, void* stream);
+                      int64_t pitch, void* epilogue, uint64_t wait_epoch, uint64_t signal_epoch, const void* edge,
+                      void* stream);
 int gm_copy_cells(void* dst, const void* src, int32_t cell_bytes, const int64_t* dst_idx, const int64_t* src_idx,
                   int64_t count, void* stream);
 int gm_fill_hash_window(void* out, int64_t pitch, int64_t n, int32_t cell_bytes, int64_t x0, int64_t y0, int64_t w,

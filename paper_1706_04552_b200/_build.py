@@ -18,7 +18,7 @@ LIB_DIR = PKG / "_lib"
 AB_BUILD = os.environ.get("GASKET_AB_BUILD", "") == "1"
 LIB = LIB_DIR / ("libgasket_b200_ab.so" if AB_BUILD else "libgasket_b200.so")
 SOURCES = ["literal.cu", "tuned.cu", "stream.cu", "write.cu", "stencil2.cu", "stencil_tb.cu", "hostrows.cu",
-           "maps.cu", "capi.cu", "peer.cu", "snapshot.cu"]
+           "maps.cu", "capi.cu", "peer.cu", "snapshot.cu", "edge.cu"]
 AB_SOURCES = ["stencil.cu", "stencil_tma.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",

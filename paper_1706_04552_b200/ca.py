@@ -14,6 +14,13 @@ the per-step Python/ctypes launch cost for long runs.
 with one fused launch (``gm_ca_steps``, stencil_tb.cu): state t is read once, the
 intermediate states live only in shared memory, state t+T is written once -- 1/T
 of the DRAM traffic per step.  Results are bit-identical to single steps.
+
+``edge_cache=True`` (default): the off-gasket cells left of every member tile whose
+left neighbour tile holds no gasket cell are gathered once into a dense cache
+(``gm_ca_edge_build``, edge.cu) and every step stages them from there instead of
+fetching one sparse DRAM line per tile row (a third of an 8-neighbour step's line
+reads at n=2^17).  The cache is taken from the initial state: like the ping-pong
+itself it relies on nobody changing off-gasket cells of the buffers between steps.
 """
 
 from __future__ import annotations
@@ -27,7 +34,7 @@ from .geometry import FractalSpec, IntraStrategy
 
 class CARunner:
     def __init__(self, grid: torch.Tensor, kind: int = backends.KERNEL_NEIGHBOR_SUM8, param: int = 1,
-                 rho: int = 64, use_graph: bool = True, temporal: int = 6) -> None:
+                 rho: int = 64, use_graph: bool = True, temporal: int = 6, edge_cache: bool = True) -> None:
         device.require_cuda()
         if not device.is_device(grid):
             raise TypeError("CARunner works on a CUDA grid tensor")
@@ -48,15 +55,30 @@ class CARunner:
             self.temporal = 4  # a 6-cell cone outgrows the 4-cell halo chunk of 4-byte cells
         self._graph = None
         self.steps_done = 0
+        # tiled kernels (1-, 2-, 4-byte cells, at least one 128-byte tile, <= 2^15 tiles per edge)
+        c = grid.element_size()
+        self._tiled = c in (1, 2, 4) and n * c >= 128 and n // (128 // c) <= (1 << 15)
+        self.edge = None
+        if edge_cache and self._tiled:
+            self.edge = torch.empty(native.ca_edge_bytes(n, c), dtype=torch.uint8, device=grid.device)
+            native.call("gm_ca_edge_build", self.edge.data_ptr(), grid.data_ptr(), n, c, -1, 0, 0, None, 0,
+                        device.stream_handle())
+
+    def _edge_ptr(self):
+        return self.edge.data_ptr() if self.edge is not None else None
 
     def _step(self, dst: torch.Tensor, src: torch.Tensor) -> None:
-        backends.run_block_space(dst, src, self.spec.rho, self.spec.r_b, IntraStrategy.TUNED, kind=self.kind,
-                                 param=self.param, flags=native.FLAG_DST_FROM_SRC)
+        if self._tiled:
+            native.call("gm_ca_run", dst.data_ptr(), src.data_ptr(), self.spec.n, dst.element_size(), self.kind,
+                        int(np.int32(self.param)), 1, self._edge_ptr(), 0, device.stream_handle())
+        else:
+            backends.run_block_space(dst, src, self.spec.rho, self.spec.r_b, IntraStrategy.TUNED, kind=self.kind,
+                                     param=self.param, flags=native.FLAG_DST_FROM_SRC)
 
     def _fused(self, dst: torch.Tensor, src: torch.Tensor, steps: int) -> None:
         """`steps` (2, 4 or 6) steps src -> dst (the intermediate states never leave the SM)."""
-        native.call("gm_ca_steps", dst.data_ptr(), src.data_ptr(), self.spec.n, dst.element_size(), self.kind,
-                    int(np.int32(self.param)), steps, 0, device.stream_handle())
+        native.call("gm_ca_run", dst.data_ptr(), src.data_ptr(), self.spec.n, dst.element_size(), self.kind,
+                    int(np.int32(self.param)), steps, self._edge_ptr(), 0, device.stream_handle())
 
     def _single(self) -> None:
         src, dst = self.bufs[self.cur], self.bufs[1 - self.cur]
@@ -137,9 +159,9 @@ class CARunner:
 
 
 def run_ca(grid: torch.Tensor, steps: int, kind: int = backends.KERNEL_NEIGHBOR_SUM8, param: int = 1,
-           use_graph: bool = True, temporal: int = 6) -> torch.Tensor:
+           use_graph: bool = True, temporal: int = 6, edge_cache: bool = True) -> torch.Tensor:
     """`steps` CA steps starting from `grid`; the final state is copied back into `grid`."""
-    runner = CARunner(grid, kind, param, use_graph=use_graph, temporal=temporal)
+    runner = CARunner(grid, kind, param, use_graph=use_graph, temporal=temporal, edge_cache=edge_cache)
     out = runner.run(steps)
     if out.data_ptr() != grid.data_ptr():
         grid.copy_(out)

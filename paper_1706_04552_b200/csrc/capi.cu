@@ -404,6 +404,88 @@ int gm_ca_steps(void* grid, const void* src, int64_t n, int32_t cell_bytes, int3
     return cuda_rc(e, "fused multi-step CA launch");
 }
 
+namespace {
+// the launch descriptor of a CA run: n, cells, kind, the sub-gasket range (level < 0: all)
+int ca_args(gm::LaunchArgs& a, const char* who, void* grid, const void* src, int64_t n, int32_t cell_bytes,
+            int32_t kind, int32_t param, int32_t level, uint32_t sg_begin, uint32_t sg_end, const int64_t* sg_off,
+            int64_t pitch, void* stream) {
+    gm_cfg_t c{};
+    c.n = n;
+    c.rho = 1;
+    c.mapping = GM_MAP_LAMBDA;
+    c.strategy = GM_STRAT_TUNED;
+    c.kind = kind;
+    c.cell_bytes = cell_bytes;
+    c.param = param;
+    if (int rc = check_common(n, cell_bytes, 1, kind)) return rc;
+    if (cell_bytes != 1 && cell_bytes != 2 && cell_bytes != 4) return fail(GM_EINVAL, "%s: 1-, 2- or 4-byte cells", who);
+    if (n * cell_bytes < 128) return fail(GM_EINVAL, "%s: the grid must be at least one 128-byte tile wide", who);
+    if (level >= 0) {
+        uint64_t nsg = 1;
+        for (int i = 0; i < level; ++i) nsg *= 3;
+        if ((n >> level) * cell_bytes < 128) return fail(GM_EINVAL, "partition level %d too deep", level);
+        if (sg_begin > sg_end || sg_end > nsg)
+            return fail(GM_EINVAL, "sub-gasket range [%u, %u) outside [0, %llu)", sg_begin, sg_end, (unsigned long long)nsg);
+    }
+    if (sg_off != nullptr && (pitch % 32 != 0 || level < 0)) return fail(GM_EINVAL, "%s: bad tiled layout", who);
+    a = make_args(&c, grid, src, nullptr, nullptr, 0, stream);
+    a.part_level = level;
+    a.sg_begin = sg_begin;
+    a.sg_end = sg_end;
+    a.sg_off = sg_off;
+    a.pitch = sg_off != nullptr ? pitch : 0;
+    return GM_OK;
+}
+}  // namespace
+
+int gm_ca_edge_bytes(int64_t n, int32_t cell_bytes, int32_t level, uint32_t sg_begin, uint32_t sg_end, int64_t* bytes) {
+    if (!bytes) return fail(GM_EINVAL, "gm_ca_edge_bytes: null output");
+    gm::LaunchArgs a{};
+    if (int rc = ca_args(a, "gm_ca_edge_bytes", nullptr, nullptr, n, cell_bytes, GM_KIND_NSUM8, 1, level, sg_begin,
+                         sg_end, nullptr, 0, nullptr))
+        return rc;
+    *bytes = gm::edge_cache_bytes(a);
+    if (*bytes == 0 && n * cell_bytes >= 128)
+        return fail(GM_EINVAL, "gm_ca_edge_bytes: more than 2^15 tiles per edge");
+    return GM_OK;
+}
+
+int gm_ca_edge_build(void* edge, const void* src, int64_t n, int32_t cell_bytes, int32_t level, uint32_t sg_begin,
+                     uint32_t sg_end, const int64_t* sg_off, int64_t pitch, void* stream) {
+    if (!edge || !src) return fail(GM_EINVAL, "gm_ca_edge_build: null buffer");
+    gm::LaunchArgs a{};
+    if (int rc = ca_args(a, "gm_ca_edge_build", nullptr, src, n, cell_bytes, GM_KIND_NSUM8, 1, level, sg_begin, sg_end,
+                         sg_off, pitch, stream))
+        return rc;
+    const cudaError_t e = gm::launch_edge_build(a, reinterpret_cast<uint8_t*>(edge));
+    if (e == cudaErrorNotSupported) {
+        cudaGetLastError();
+        return fail(GM_EINVAL, "gm_ca_edge_build: more than 2^15 tiles per edge");
+    }
+    return cuda_rc(e, "edge cache build");
+}
+
+int gm_ca_run(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param, int32_t steps,
+              const void* edge, int32_t flags, void* stream) {
+    if (steps != 1 && steps != 2 && steps != 4 && steps != 6) return fail(GM_EINVAL, "gm_ca_run: steps must be 1, 2, 4 or 6");
+    if (kind != GM_KIND_NSUM4 && kind != GM_KIND_NSUM8) return fail(GM_EINVAL, "gm_ca_run: kind must be NSUM4 or NSUM8");
+    if (!grid || !src || src == grid) return fail(GM_EINVAL, "gm_ca_run needs distinct grid and src buffers");
+    gm::LaunchArgs a{};
+    if (int rc = ca_args(a, "gm_ca_run", grid, src, n, cell_bytes, kind, param, -1, 0, 0, nullptr, 0, stream)) return rc;
+    a.flags = (flags & ~GM_FLAG_DST_FROM_SRC) | (steps == 1 ? GM_FLAG_DST_FROM_SRC : 0);
+    // the single-step kernel stages from the cache; the fused kernels are bound by their
+    // arithmetic, not staging (n=2^17 NSUM8 with the cache: 1 step 436 -> 406 us, 2/4/6
+    // steps 1-2% slower), so they read the grid
+    a.edge = steps == 1 ? reinterpret_cast<const uint8_t*>(edge) : nullptr;
+    const cudaError_t e = steps == 1 ? gm::launch_stencil_v2(a) : gm::launch_stencil_tb(a, steps);
+    if (e == cudaErrorNotSupported) {
+        cudaGetLastError();
+        return fail(GM_EINVAL, "gm_ca_run: no tiled kernel for these cells (6 steps: 1- or 2-byte cells; <= 2^15 tiles "
+                               "per edge)");
+    }
+    return cuda_rc(e, "CA launch");
+}
+
 int gm_dev_alloc(int64_t bytes, void** out) {
     if (bytes <= 0 || !out) return fail(GM_EINVAL, "gm_dev_alloc: bad size/out");
     return cuda_rc(cudaMalloc(out, (size_t)bytes), "cudaMalloc");
@@ -467,7 +549,8 @@ int gm_fill_hash_window(void* out, int64_t pitch, int64_t n, int32_t cell_bytes,
 
 int gm_run_part_tiled(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
                       int32_t steps, int32_t level, uint32_t sg_begin, uint32_t sg_end, const int64_t* sg_off,
-                      int64_t pitch, void* epilogue, uint64_t wait_epoch, uint64_t signal_epoch, void* stream) {
+                      int64_t pitch, void* epilogue, uint64_t wait_epoch, uint64_t signal_epoch, const void* edge,
+                      void* stream) {
     if (steps != 1 && steps != 2 && steps != 4 && steps != 6)
         return fail(GM_EINVAL, "gm_run_part_tiled: steps must be 1, 2, 4 or 6");
     gm_cfg_t c{};
@@ -501,6 +584,7 @@ int gm_run_part_tiled(void* grid, const void* src, int64_t n, int32_t cell_bytes
     a.peer_epi = epilogue;
     a.wait_epoch = epilogue ? wait_epoch : 0;
     a.signal_epoch = epilogue ? signal_epoch : 0;
+    a.edge = steps == 1 ? reinterpret_cast<const uint8_t*>(edge) : nullptr;  // (see gm_ca_run)
     const cudaError_t e = steps == 1 ? gm::launch_stencil_v2(a) : gm::launch_stencil_tb(a, steps);
     if (e == cudaErrorNotSupported) {
         cudaGetLastError();

@@ -38,7 +38,17 @@ struct LaunchArgs {
     // bytes of those blocks.  nullptr = the dense n x n layout (pitch n * cell_bytes).
     const int64_t* sg_off = nullptr;
     int64_t pitch = 0;
+    // static left-edge cache of a CA run (gm_ca_edge_build, edge.cu): for tile #i of the
+    // launch's tile range whose left neighbour tile is not a gasket tile, the 16-byte chunk
+    // left of each of its TT rows at edge + (i * TT + row) * 16; nullptr = read the grid
+    const uint8_t* edge = nullptr;
 };
+
+// The left neighbour of member tile (bx, by) holds no gasket cell (so its cells never
+// change in a CA run: backends.py:155-156) and lies inside the grid.
+__host__ __device__ inline bool left_static(uint32_t bx, uint32_t by) {
+    return bx > 0 && ((bx - 1) & ~by) != 0;
+}
 
 // row pitch in bytes of a launch's buffers
 inline int64_t row_pitch(const LaunchArgs& a) { return a.pitch > 0 ? a.pitch : a.n * a.cell_bytes; }
@@ -86,6 +96,8 @@ cudaError_t launch_stencil_tma(const LaunchArgs& a);
 cudaError_t launch_stencil_v2(const LaunchArgs& a);
 cudaError_t launch_stencil_tb2(const LaunchArgs& a);
 cudaError_t launch_stencil_tb(const LaunchArgs& a, int steps);  // steps = 2, 4 or 6
+cudaError_t launch_edge_build(const LaunchArgs& a, uint8_t* edge);  // edge.cu
+int64_t edge_cache_bytes(const LaunchArgs& a);                   // edge.cu (0: no tiled kernel)
 cudaError_t launch_snapshot_stencil(void* snap, const void* grid, int64_t n, int cell_bytes, cudaStream_t s);
 cudaError_t launch_writeback_tiles(void* out, const void* dst, const void* snap, int64_t n, int cell_bytes, cudaStream_t s);
 cudaError_t launch_host_rows_copyback(void* out, const void* dst, const void* snap, int64_t n, int cell_bytes,

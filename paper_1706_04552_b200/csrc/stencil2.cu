@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
                                                              const uint32_t* __restrict__ order, PeerEpilogue* epi,
                                                              uint64_t wait_epoch, uint64_t signal_epoch,
                                                              const int64_t* __restrict__ sg_off, int64_t pitch,
-                                                             uint32_t per) {
+                                                             uint32_t per, const uint8_t* __restrict__ edge) {
     using S = T2<C>;
     peer_prologue_wait(epi, wait_epoch);  // partitioned CA with the fused exchange only
     constexpr bool EIGHT = KIND == KIND_NSUM8;
@@ -240,6 +240,13 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
         const uint8_t* srct = src + tile_off(idx);
         const uint8_t* base = srct + (y0 - 1) * rowstride + x0 * C - 16;  // staged (row 0, chunk 0)
         const bool interior = y0 > 0 && y0 + S::TT < n && x0 > 0 && x0 + S::TT < n;
+        // a static left edge (CA runs, edge.cu): the left halo chunks of the tile's own rows
+        // come from the dense edge cache instead of one sparse grid line each
+        const bool ls = edge != nullptr && order != nullptr && left_static(bx, by);  // (cache: order-table index)
+        const uint8_t* ecol = edge + (ls ? (int64_t)(first + idx * step - tile_lo) * S::TT * 16 - 16 : 0);  // + j*16
+        auto from_edge = [&](uint32_t c) {  // chunk 0 of staged row j = tile row j-1 in [0, TT)
+            return ls && (c & 0x0f000000u) == 0 && ((c >> 16) & 0xffu) - 1u < (uint32_t)S::TT;
+        };
         if (interior) {
             for (int i = threadIdx.x; i < nch; i += S::THREADS) {
                 const uint32_t c = chunks[i];
@@ -249,7 +256,8 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
                 } else {
                     go = (int64_t)((c >> 16) & 0xffu) * rowstride + (int64_t)((c >> 24) & 15u) * 16;
                 }
-                if (fetch256) cp_async16_256(sb + (c & 0xffffu), base + go, 16);
+                if (from_edge(c)) cp_async16(sb + (c & 0xffffu), ecol + ((c >> 16) & 0xffu) * 16, 16, true);
+                else if (fetch256) cp_async16_256(sb + (c & 0xffffu), base + go, 16);
                 else cp_async16(sb + (c & 0xffffu), base + go, 16, fetch_line || (fetch_mixed && (c >> 28)));
             }
         } else {
@@ -259,8 +267,9 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
                 const int64_t y = y0 + j - 1;
                 const int64_t xb = x0 * C + (qq - 1) * 16;
                 const bool in = y >= 0 && y < n && xb >= 0 && xb < rowbytes;
-                cp_async16(sb + (c & 0xffffu), in ? srct + y * rowstride + xb : src, in ? 16 : 0,
-                           fetch_line || (fetch_mixed && (c >> 28)));
+                if (from_edge(c)) cp_async16(sb + (c & 0xffffu), ecol + j * 16, 16, true);
+                else cp_async16(sb + (c & 0xffffu), in ? srct + y * rowstride + xb : src, in ? 16 : 0,
+                                fetch_line || (fetch_mixed && (c >> 28)));
             }
         }
     };
@@ -348,7 +357,7 @@ cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
                                                           a.part_level, a.param, a.flags, order,
                                                           reinterpret_cast<PeerEpilogue*>(a.peer_epi), a.wait_epoch,
                                                           a.signal_epoch, a.sg_off, row_pitch(a),
-                                                          tiles_per_subgasket(a, r_t));
+                                                          tiles_per_subgasket(a, r_t), a.edge);
     note_launch();
     return cudaGetLastError();
 }

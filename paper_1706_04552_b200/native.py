@@ -93,10 +93,13 @@ _SIGS = {
     "gm_peer_halo_put": [_vp, _vp, _vp, _i64, _i32, _vp, _i32, _i32, _u64, _vp],
     "gm_peer_halo_put_to": [_vp, _vp, _vp, _vp, _i64, _i32, _vp, _i32, _i32, _u64, _vp],
     "gm_run_part_tiled": [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, ctypes.c_uint32, ctypes.c_uint32, _vp, _i64,
-                          _vp, _u64, _u64, _vp],
+                          _vp, _u64, _u64, _vp, _vp],
     "gm_copy_cells": [_vp, _vp, _i32, _vp, _vp, _i64, _vp],
     "gm_fill_hash_window": [_vp, _i64, _i64, _i32, _i64, _i64, _i64, _i64, _u64, _i32, _vp],
     "gm_peer_halo_wait": [_vp, _i32, _i32, _u64, _u64, _vp, _vp],
+    "gm_ca_edge_bytes": [_i64, _i32, _i32, ctypes.c_uint32, ctypes.c_uint32, ctypes.POINTER(ctypes.c_int64)],
+    "gm_ca_edge_build": [_vp, _vp, _i64, _i32, _i32, ctypes.c_uint32, ctypes.c_uint32, _vp, _i64, _vp],
+    "gm_ca_run": [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _i32, _vp],
 }
 
 # Every symbol include/gasket_b200.h declares (checked by tests/test_native_abi.py).
@@ -153,6 +156,13 @@ def launch_count() -> int:
 
 def version() -> str:
     return lib().gm_version().decode()
+
+
+def ca_edge_bytes(n: int, cell_bytes: int, level: int = -1, sg_begin: int = 0, sg_end: int = 0) -> int:
+    """Size of the static left-edge cache of a CA run (gm_ca_edge_bytes)."""
+    out = ctypes.c_int64(0)
+    check(lib().gm_ca_edge_bytes(n, cell_bytes, level, sg_begin, sg_end, ctypes.byref(out)))
+    return int(out.value)
 
 
 def tile_order(q: int, level: int = 0):

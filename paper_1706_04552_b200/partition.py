@@ -681,8 +681,10 @@ class TiledCA:
 
     def __init__(self, plan: "PartitionPlan", rank: int, kind: int, param: int = 1, dtype=torch.int8,
                  init: Optional[torch.Tensor] = None, seed: Optional[int] = None, group=None,
-                 loopback: Optional["LoopbackGroup"] = None, halo: str = "collective", fused: bool = False) -> None:
+                 loopback: Optional["LoopbackGroup"] = None, halo: str = "collective", fused: bool = False,
+                 edge_cache: bool = True) -> None:
         from . import device as dev
+        from . import native
 
         dev.require_cuda()
         self.plan, self.rank, self.kind, self.param = plan, rank, kind, param
@@ -709,6 +711,13 @@ class TiledCA:
             raise ValueError("pass the initial state: a dense grid (init) or a synthetic seed")
         self.b.copy_(self.a)  # both buffers agree off the gasket (rings included)
         self.lo, self.hi = L.lo, L.hi
+        # the static left-edge cache of the rank's tiles (edge.cu; one-step launches use it)
+        self.edge = None
+        if edge_cache and plan.depth == 1 and self.hi > self.lo:
+            self.edge = torch.empty(native.ca_edge_bytes(plan.n, c, plan.level, self.lo, self.hi), dtype=torch.uint8,
+                                    device="cuda")
+            native.call("gm_ca_edge_build", self.edge.data_ptr(), self.a.data_ptr(), plan.n, c, plan.level, self.lo,
+                        self.hi, self.sg_off.data_ptr(), L.pitch, dev.stream_handle())
         self.fused = bool(fused)
         if halo == "peer":
             self.peer = PeerHaloExchange(plan, rank, self._dbufs, group=group, entries=entries[rank])
@@ -726,7 +735,8 @@ class TiledCA:
 
         native.call("gm_run_part_tiled", self.b.data_ptr(), self.a.data_ptr(), self.plan.n, self.a.element_size(),
                     self.kind, int(np.int32(self.param)), self.plan.depth, self.plan.level, self.lo, self.hi,
-                    self.sg_off.data_ptr(), self.layout.pitch, epi, wait, signal, dev.stream_handle())
+                    self.sg_off.data_ptr(), self.layout.pitch, epi, wait, signal,
+                    self.edge.data_ptr() if self.edge is not None else None, dev.stream_handle())
 
     def compute(self) -> None:
         if self.hi > self.lo:
@@ -757,7 +767,7 @@ class TiledCA:
 
     @property
     def storage_bytes(self) -> int:
-        return 2 * self.layout.nbytes
+        return 2 * self.layout.nbytes + (self.edge.numel() if self.edge is not None else 0)
 
     def store_dense(self, dense: torch.Tensor) -> None:
         torch.cuda.synchronize()

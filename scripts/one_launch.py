@@ -3,6 +3,7 @@
 
     python scripts/one_launch.py stencil17 FLAGS [reps]
     python scripts/one_launch.py write16 FLAGS [reps]
+    python scripts/one_launch.py castep17 FLAGS [reps]   (gm_ca_run, one step, edge cache)
 """
 
 import sys
@@ -23,7 +24,18 @@ def main():
     n = 1 << r
     flush = device.L2Flusher()
     T = IntraStrategy.TUNED
-    if wl.startswith("ca"):
+    if wl.startswith("castep"):
+        # castep17: one CA step through gm_ca_run with the static left-edge cache (edge.cu)
+        from paper_1706_04552_b200 import native
+        kind = 1 if "nsum4" in wl else 2
+        src = device.fill_hash(n, torch.int8, 1, 0)
+        dst = src.clone()
+        edge = torch.empty(native.ca_edge_bytes(n, 1), dtype=torch.uint8, device="cuda")
+        native.call("gm_ca_edge_build", edge.data_ptr(), src.data_ptr(), n, 1, -1, 0, 0, None, 0,
+                    device.stream_handle())
+        fn = lambda: native.call("gm_ca_run", dst.data_ptr(), src.data_ptr(), n, 1, kind, 1, 1,  # noqa: E731
+                                 edge.data_ptr(), flags, device.stream_handle())
+    elif wl.startswith("ca"):
         from paper_1706_04552_b200 import native
         kind = 1 if "nsum4" in wl else 2
         src = device.fill_hash(n, torch.int8, 1, 0)

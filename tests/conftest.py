@@ -58,3 +58,20 @@ def gpu():
 
     gm.native.lib()  # fails loudly if the sm_100a library is missing
     return gm
+
+
+@pytest.fixture(autouse=True)
+def _release_gpu_memory(request):
+    """After every GPU test, hand the cached device memory back to the driver: the
+    BASELINE-size cases allocate up to ~130 GB, and later tests that start their own
+    processes on the same GPU (tests/test_bench_multirank.py) must find it free."""
+    yield
+    if request.node.get_closest_marker("gpu") is None:
+        return
+    torch = sys.modules.get("torch")
+    if torch is not None and torch.cuda.is_available() and torch.cuda.is_initialized():
+        import gc
+
+        gc.collect()
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()

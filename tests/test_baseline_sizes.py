@@ -132,6 +132,17 @@ def test_n17_int8_ca_exact(gpu, oracle, kind):
         d = src.clone()
         _ca_steps(gpu, d, src, n, kind, steps)
         results[steps] = d
+    # the CA steps with the static left-edge cache (edge.cu) give the same cells
+    edge = torch.empty(gpu.native.ca_edge_bytes(n, 1), dtype=torch.uint8, device="cuda")
+    gpu.native.call("gm_ca_edge_build", edge.data_ptr(), src.data_ptr(), n, 1, -1, 0, 0, None, 0,
+                    gpu.device.stream_handle())
+    t = src.clone()
+    for steps in (1, 2, 6):
+        gpu.native.call("gm_ca_run", t.data_ptr(), src.data_ptr(), n, 1, kind, 1, steps, edge.data_ptr(), 0,
+                        gpu.device.stream_handle())
+        assert gpu.device.count_mismatch(t, results[steps]) == 0, ("edge cache", steps)
+    del t, edge
+    torch.cuda.empty_cache()
     torch.cuda.synchronize()
     bad = band_mismatches(gpu, oracle, results, n, np.int8, seed, 0, kind, 1, band_rows=4096)
     assert bad == {s: 0 for s in results}, bad

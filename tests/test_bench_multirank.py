@@ -5,6 +5,7 @@ GPU); the 8-GPU command is scripts/part18_8gpu.sh."""
 
 import json
 import os
+import signal
 import socket
 import subprocess
 import sys
@@ -26,14 +27,38 @@ def _port() -> int:
                                                    ("peer-fused", 1, "tiled"), ("peer-fused", 6, "tiled"),
                                                    ("collective", 2, "dense")])
 def test_bench_two_ranks_part15(gpu, halo, temporal, storage):
-    env = dict(os.environ, GASKET_BENCH_SHARED_GPU="1", OMP_NUM_THREADS="1")
+    env = dict(os.environ, GASKET_BENCH_SHARED_GPU="1", OMP_NUM_THREADS="1", PYTHONFAULTHANDLER="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), str(ROOT / "bench.py"), "--gpus", "2",
            "--steps", "4", "--warmup", "3", "--workload", "part15", "--halo", halo, "--temporal", str(temporal),
            "--storage", storage]
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
-    assert out.returncode == 0, out.stderr[-3000:]
-    line = json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][-1])
+    # on a hang every rank gets SIGABRT (faulthandler prints where it waits) instead of the
+    # test blocking the suite
+    p = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True, env=env, cwd=ROOT)
+    try:
+        stdout, stderr = p.communicate(timeout=240)
+    except subprocess.TimeoutExpired:
+        # torchrun starts its workers in sessions of their own: signal every descendant
+        import psutil
+
+        procs = psutil.Process(p.pid).children(recursive=True) + [psutil.Process(p.pid)]
+        for q in procs:
+            try:
+                q.send_signal(signal.SIGABRT)
+            except psutil.NoSuchProcess:
+                pass
+        try:
+            stdout, stderr = p.communicate(timeout=30)
+        except subprocess.TimeoutExpired:
+            for q in procs:
+                try:
+                    q.kill()
+                except psutil.NoSuchProcess:
+                    pass
+            stdout, stderr = p.communicate()
+        pytest.fail(f"multi-rank bench hung (240 s); tracebacks:\n{stderr[-8000:]}")
+    assert p.returncode == 0, stderr[-3000:]
+    line = json.loads([x for x in stdout.splitlines() if x.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["gpu_launches"] > 0
     assert line["config"]["storage"] == storage and line["config"]["halo"] == halo
     if storage == "tiled":

@@ -385,6 +385,51 @@ def test_fused_steps_vs_oracle(gpu, oracle, dtype, steps):
 
 
 @pytest.mark.parametrize("dtype", [np.int8, np.int16, np.int32])
+@pytest.mark.parametrize("steps", [1, 2, 4, 6])
+def test_ca_run_edge_cache_vs_oracle(gpu, oracle, dtype, steps):
+    """gm_ca_run with the static left-edge cache (edge.cu) == the same run without it ==
+    that many oracle steps, every cell: grid-edge tiles, interior tiles whose left
+    neighbour tile is (not) a gasket tile, both kinds, both background modes."""
+    from paper_1706_04552_b200 import device, native
+
+    c = np.dtype(dtype).itemsize
+    if steps == 6 and c == 4:
+        return  # (the 6-cell cone outgrows a 4-cell halo chunk: gm_ca_run raises, as gm_ca_steps)
+    n0 = 128 // c
+    for n in (n0, 2 * n0, 8 * n0, 1 << 12):
+        for mode in (0, 1):
+            init = oracle.fill_hash(n, dtype, 51 + mode, mode)
+            src = torch.from_numpy(init.copy()).cuda()
+            edge = torch.empty(native.ca_edge_bytes(n, c), dtype=torch.uint8, device="cuda")
+            native.call("gm_ca_edge_build", edge.data_ptr(), src.data_ptr(), n, c, -1, 0, 0, None, 0,
+                        device.stream_handle())
+            for kind in (1, 2):
+                want = _oracle_steps(oracle, init, kind, -3, steps)
+                for e in (None, edge.data_ptr()):
+                    dst = src.clone()
+                    native.call("gm_ca_run", dst.data_ptr(), src.data_ptr(), n, c, kind, -3, steps, e, 0,
+                                device.stream_handle())
+                    assert np.array_equal(dst.cpu().numpy(), want), (np.dtype(dtype).name, n, mode, kind, e is None)
+
+
+def test_ca_run_rejects_bad_arguments(gpu):
+    from paper_1706_04552_b200 import device, native
+
+    g = torch.zeros((256, 256), dtype=torch.int8, device="cuda")
+    h = g.clone()
+    s = device.stream_handle()
+    for steps in (0, 3, 8):
+        with pytest.raises(ValueError):
+            native.call("gm_ca_run", g.data_ptr(), h.data_ptr(), 256, 1, 2, 1, steps, None, 0, s)
+    with pytest.raises(ValueError):  # CONST is not a CA step
+        native.call("gm_ca_run", g.data_ptr(), h.data_ptr(), 256, 1, 0, 1, 1, None, 0, s)
+    with pytest.raises(ValueError):  # src must not alias grid
+        native.call("gm_ca_run", g.data_ptr(), g.data_ptr(), 256, 1, 2, 1, 1, None, 0, s)
+    with pytest.raises(ValueError):  # 8-byte cells have no tiled kernel
+        native.call("gm_ca_run", g.data_ptr(), h.data_ptr(), 32, 8, 2, 1, 1, None, 0, s)
+
+
+@pytest.mark.parametrize("dtype", [np.int8, np.int16, np.int32])
 def test_dst_from_src_variants(gpu, oracle, dtype):
     """GM_FLAG_DST_FROM_SRC (grid == snapshot off the gasket: engine.launch / CA
     ping-pong) through every stencil kernel variant, including edge tiles."""

@@ -70,3 +70,19 @@ def test_product_never_imports_the_oracle():
                 assert all(not a.name.split(".")[0] == "oracle" for a in node.names), path
             elif isinstance(node, ast.ImportFrom):
                 assert (node.module or "").split(".")[0] != "oracle", path
+
+
+def test_ca_edge_bytes_host_only():
+    """The static left-edge cache size (gm_ca_edge_bytes: no CUDA call): 16 bytes per row
+    of every member tile of the launch's tile range."""
+    from paper_1706_04552_b200 import native
+
+    assert native.ca_edge_bytes(1 << 17, 1) == 3**10 * 128 * 16
+    assert native.ca_edge_bytes(128, 1) == 128 * 16
+    assert native.ca_edge_bytes(1 << 12, 4) == 3**7 * 32 * 16
+    # a partitioned launch: level-2 sub-gaskets [1, 3) of n=2^12 int8 (27 tiles each)
+    assert native.ca_edge_bytes(1 << 12, 1, 2, 1, 3) == 2 * 27 * 128 * 16
+    with pytest.raises(ValueError):
+        native.ca_edge_bytes(64, 1)  # narrower than a tile
+    with pytest.raises(ValueError):
+        native.ca_edge_bytes(1 << 12, 8)
