@@ -15,8 +15,9 @@
 // sparse lines.  Results are unchanged by construction (the same bytes land in the same
 // shared-memory slots); rows -1 and TT of the staged window still come from the grid,
 // since the tiles above-left and below-left may be gasket tiles.  n=2^17 int8, one step:
-// NSUM8 436 -> 406 us, NSUM4 431 -> 397 us.  (The fused 2/4/6-step kernel, bound by its
-// arithmetic, gained nothing from it and does not use it.)
+// NSUM8 436 -> 406 us, NSUM4 431 -> 397 us with the same 3-deep staging ring; the lighter
+// staging then lets a 2-deep ring with 4 CTAs per SM win: 378 / 368 us (stencil2.cu).  (The
+// fused 2/4/6-step kernel, bound by its arithmetic, gained nothing and does not use it.)
 #include "launch.h"
 
 namespace gm {

@@ -49,9 +49,10 @@ def main():
     native.call("gm_ca_edge_build", edge.data_ptr(), src.data_ptr(), n, 1, -1, 0, 0, None, 0, s)
     cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
     FH, FM, F256, S2 = native.FLAG_FETCH_HALF, native.FLAG_FETCH_MIXED, native.FLAG_FETCH256, native.FLAG_STAGES2
-    variants = [("grid", None, 0), ("edge", edge.data_ptr(), 0), ("edge+mixed", edge.data_ptr(), FH | FM),
-                ("edge+half", edge.data_ptr(), FH), ("edge+256", edge.data_ptr(), F256),
-                ("edge+stages2", edge.data_ptr(), S2), ("grid+mixed", None, FH | FM)]
+    E = edge.data_ptr()
+    variants = [("grid", None, 0), ("edge", E, 0), ("grid+stages2", None, S2), ("edge+stages2", E, S2),
+                ("edge+stages2+256", E, S2 | F256), ("edge+stages2+mixed", E, S2 | FH | FM),
+                ("edge (again)", E, 0), ("edge+stages2 (again)", E, S2)]
     for kind in (2, 1):
         for steps in ((1,) if which == "single" else (1, 2, 6)):
             for name, e, fl in (variants if steps == 1 else variants[:2]):
@@ -63,7 +64,7 @@ def main():
                 else:
                     native.call("gm_count_equal", dst.data_ptr(), ref.data_ptr(), n * n, 1, cnt.data_ptr(), s)
                     extra = f"  differing words vs grid: {int(cnt.item())}"
-                print(f"nsum{4 * kind} steps={steps} {name:13s}: flushed mean {m:8.1f} us min {mn:8.1f} us, "
+                print(f"nsum{4 * kind} steps={steps} {name:20s}: flushed mean {m:8.1f} us min {mn:8.1f} us, "
                       f"b2b {b2b:8.1f} us, per step {b2b / steps:7.1f} us{extra}", flush=True)
 
 

@@ -16,7 +16,7 @@ ncu)
   timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 60 --csv --log-file gpurun_out/$TAG/launches_write16.csv python bench.py --steps 20 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1; echo ncu_rc=$?
   timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 40 --csv --log-file gpurun_out/$TAG/launches_stencil17.csv python bench.py --workload stencil17 --steps 10 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1; echo ncu2_rc=$? ;;
 ncufull)
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:lambda_stream -s 3 -c 1 -o gpurun_out/$TAG/prof_write16 python bench.py --steps 2 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1; echo ncuf_rc=$?
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:gasket_write -s 3 -c 1 -o gpurun_out/$TAG/prof_write16 python bench.py --steps 2 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1; echo ncuf_rc=$?
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:stencil_v2 -s 3 -c 1 -o gpurun_out/$TAG/prof_stencil17 python bench.py --workload stencil17 --steps 2 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1; echo ncuf2_rc=$? ;;
 probe)
   ./scripts/probe_stride > gpurun_out/$TAG/probe_stride.txt 2>&1; echo probe_rc=$? ;;
@@ -37,7 +37,7 @@ profile)
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --csv --log-file gpurun_out/$TAG/probe_partial_ncu.csv ./scripts/probe_partial > /dev/null 2>&1
   timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"lambda|stencil|l2_flush|fill_hash" -c 60 --csv --log-file gpurun_out/$TAG/launches_write16.csv python bench.py --steps 20 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1
   timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"lambda|stencil|l2_flush|fill_hash" -c 40 --csv --log-file gpurun_out/$TAG/launches_stencil17.csv python bench.py --workload stencil17 --steps 10 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:lambda_stream -s 3 -c 1 -o gpurun_out/$TAG/prof_write16 python bench.py --steps 2 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:gasket_write -s 3 -c 1 -o gpurun_out/$TAG/prof_write16 python bench.py --steps 2 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:stencil_v2 -s 2 -c 1 -o gpurun_out/$TAG/prof_stencil17 python bench.py --workload stencil17 --steps 2 --warmup 3 --no-sweep --no-e2e --no-cpu > /dev/null 2>&1
   echo profile_done ;;
 nsweep)

@@ -20,7 +20,7 @@ from paper_1706_04552_b200.geometry import IntraStrategy  # noqa: E402
 def main():
     wl, flags = sys.argv[1], int(sys.argv[2], 0)
     reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
-    r = int(wl.replace("x4", "")[-2:])
+    r = int(wl.replace("x4", "").replace("x6", "")[-2:])
     n = 1 << r
     flush = device.L2Flusher()
     T = IntraStrategy.TUNED
@@ -40,7 +40,7 @@ def main():
         kind = 1 if "nsum4" in wl else 2
         src = device.fill_hash(n, torch.int8, 1, 0)
         dst = src.clone()
-        steps = 4 if wl.endswith("x4") else 2  # ca17 / ca17x4: 2 or 4 fused steps (gm_ca_steps)
+        steps = 6 if wl.endswith("x6") else 4 if wl.endswith("x4") else 2  # ca17 / ca17x4 / ca17x6 (gm_ca_steps)
         fn = lambda: native.call("gm_ca_steps", dst.data_ptr(), src.data_ptr(), n, 1, kind, 1, steps,  # noqa: E731
                                  flags, device.stream_handle())
     elif wl.startswith("stencil"):
