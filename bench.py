@@ -961,7 +961,7 @@ def main() -> None:
                          "rank (dense)")
     ap.add_argument("--r-min", type=int, default=8)
     ap.add_argument("--r-max", type=int, default=18)
-    ap.add_argument("--nsweep-out", default="profiles/r1_nsweep.csv")
+    ap.add_argument("--nsweep-out", default="gpurun_out/nsweep.csv")
     args = ap.parse_args()
     if args.nsweep:
         run_nsweep(args)

@@ -31,6 +31,7 @@
 // of V rows.  Work lists are host-precomputed (tile-independent supersets).
 // Arithmetic: the split-lane SIMD of stencil_common.cuh.  Results are bit-identical
 // to T single steps (tests/test_gpu_parity.py).
+#include <algorithm>
 #include <map>
 #include <mutex>
 #include <set>
@@ -79,7 +80,12 @@ struct TB {
     static constexpr int SROWS = TT + 2 * T;   // state t rows -T .. TT+T-1
     static constexpr int IROWS = TT + 2 * T - 2;  // odd-phase results, rows -(T-1) .. TT+T-2
     static constexpr int SH_S = T, SH_I = T - 1;  // buffer row = tile row + SH
-    static constexpr int SBUF = SROWS * PITCH + SKEW_BYTES;
+    // S slots are whole multiples of 128 bytes and I starts 32 bytes past one (IOFF): a word of
+    // S and the same tile word in I (one row lower, SH_I = SH_S - 1) then sit in the same
+    // bank, so the even phases' mixed S/I loads keep the conflict pattern of the odd phases
+    // (sbuf - ibuf + PITCH == 0 mod 128)
+    static constexpr int SBUF = (SROWS * PITCH + SKEW_BYTES + 127) / 128 * 128;
+    static constexpr int IOFF = 32;
     static constexpr int IBUF = IROWS * PITCH + SKEW_BYTES;
     static constexpr int NTOUCH = 9 * SC;
     // 4/3 threads per touched sector: the store pass uses the first NTOUCH, the work
@@ -210,7 +216,7 @@ __global__ void __launch_bounds__(TB<C, T>::THREADS)
     peer_prologue_wait(epi, wait_epoch);  // partitioned CA with the fused exchange only
     constexpr bool EIGHT = KIND == KIND_NSUM8;
     extern __shared__ __align__(128) uint8_t smem[];
-    uint8_t* ibuf = smem + NST * S::SBUF;
+    uint8_t* ibuf = smem + NST * S::SBUF + S::IOFF;
     // work lists: staged chunks as j * 16 + q (S row j, chunk q); runs as t0 * 64 + k
     // (first tile row, word k); ring words as (r + T) * 64 + k (tile row r, word k)
     uint16_t* slist = reinterpret_cast<uint16_t*>(ibuf + S::IBUF);
@@ -371,6 +377,39 @@ __global__ void __launch_bounds__(TB<C, T>::THREADS)
 }
 
 // ---- host: the work lists (tile-independent supersets) ----------------------
+
+// Reorder the list segment [b, e) of `v` so that the entries one warp instruction serves
+// together fall on distinct shared-memory banks where the bank histogram allows: blocks of
+// `blk` consecutive entries (the first block `first` entries long: where the segment starts
+// inside a warp's 32 items), each filled round-robin over the keys with the most entries
+// left.  Entries are independent work items (no order inside a list), so only the bank
+// pattern changes (ncu, n=2^17 NSUM8, T = 6: 212 M shared wavefronts for 84 M ideal, most of
+// it 2.5-way conflicts of the phases' loads/stores and 4.8-way of the staging copies).
+template <class Key>
+void spread_banks(std::vector<uint32_t>& v, size_t b, size_t e, Key key, int nkeys, int blk, int first) {
+    std::vector<std::vector<uint32_t>> by(nkeys);
+    for (size_t i = b; i < e; ++i) by[key(v[i])].push_back(v[i]);
+    for (auto& q : by) std::reverse(q.begin(), q.end());  // (pop_back keeps the original order per key)
+    std::vector<int> order(nkeys);
+    size_t left = e - b, o = b;
+    int size = first > 0 ? first : blk;
+    while (left) {
+        int cnt = 0;
+        while (cnt < size && left) {
+            for (int k = 0; k < nkeys; ++k) order[k] = k;
+            std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return by[x].size() > by[y].size(); });
+            for (int k : order) {
+                if (cnt == size || by[k].empty()) break;
+                v[o++] = by[k].back();
+                by[k].pop_back();
+                ++cnt;
+                --left;
+            }
+        }
+        size = blk;
+    }
+}
+
 struct TbLists {
     uint16_t* lists = nullptr;  // [staged chunks | the tile's runs | ring words of phases 1..T]
     TbCounts cnt;
@@ -437,16 +476,27 @@ void build_lists(bool eight, int T, std::vector<uint32_t>& out, TbCounts& cnt) {
             if (any) out.push_back((uint32_t)((r + T) * 16 + q));
         }
     cnt.ns = (int)out.size();
+    // (the staging copies keep their row-major order: a cp.async fills shared memory once per
+    // global sector it reads, so chunks of one row side by side beat any bank-aware order)
+    auto roff = [&](int idx) { return idx * PITCH + 16 * ((idx - T + 8) >> 2); };  // row_off<T>: S row idx
     // the tile's gasket words, one entry per aligned run of V rows (every phase: every
     // N_p, p < T, holds all their cells)
     for (int t0 = 0; t0 < TT; t0 += V)
         for (int w = 0; w < TT / V; ++w)
             if (((w * V) & ~t0) == 0) out.push_back((uint32_t)(t0 * 64 + w + 4));
     cnt.ni = (int)out.size() - cnt.ns;
+    // the runs: 32-bit loads/stores at word k of the run's rows; the bank of an entry is that
+    // of its first word in S (I has the same pattern shifted)
+    auto bank = [&](int r, int k) { return ((roff(r + T) >> 2) + k) & 31; };  // tile row r, word k
+    spread_banks(out, cnt.ns, out.size(), [&](uint32_t c) { return bank((int)(c >> 6), (int)(c & 63u)); }, 32, 32, 0);
     cnt.ring[0] = 0;
     for (int p = 1; p <= MAX_T; ++p) {
+        const size_t b0 = out.size();
         if (p <= T)
             for (auto [r, k] : ring[p]) out.push_back((uint32_t)((r + T) * 64 + k));
+        // phase p's ring items follow the runs in the same thread loop: item ni + i
+        spread_banks(out, b0, out.size(), [&](uint32_t c) { return bank((int)(c >> 6) - T, (int)(c & 63u)); }, 32, 32,
+                     (32 - cnt.ni % 32) % 32);
         cnt.ring[p] = (int)out.size() - cnt.ns - cnt.ni;
     }
 }
@@ -488,7 +538,7 @@ cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
     if (order != nullptr) order += lo;
     if (L == nullptr || order == nullptr) return cudaErrorMemoryAllocation;
     const int entries = L->cnt.ns + L->cnt.ni + L->cnt.ring[T];
-    const size_t smem = (size_t)NST * S::SBUF + S::IBUF + 2 * (size_t)entries;
+    const size_t smem = (size_t)NST * S::SBUF + S::IOFF + S::IBUF + 2 * (size_t)entries;
     auto* kern = stencil_tb<C, KIND, T, NST>;
     ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
     int dev = 0, sms = 148, per_sm = 1;
