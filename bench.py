@@ -361,6 +361,53 @@ def _sweep(r: int, dtype, flusher, budget_s: float = 3.0) -> dict:
             "summary": summary, "useful_thread_fraction": useful}
 
 
+def _stencil_vs_bb(r: int, tdt, kind: int, flusher, budget_s: float = 2.0) -> dict:
+    """BASELINE config 3's "lambda vs BB" for the neighbour-sum step: the paper's
+    bounding-box kernel (and its block-exit variant) against the paper-literal lambda
+    strategies and the tuned lambda step, every one a full step dst <- step(src)
+    (backends.run_bounding_box / run_block_space, flushed launches)."""
+    import torch
+
+    from paper_1706_04552_b200 import backends, device
+    from paper_1706_04552_b200.geometry import IntraStrategy
+
+    n = 1 << r
+    src = device.fill_hash(n, tdt, 1, 0)
+    dst = src.clone()
+
+    def timed(fn) -> float:
+        fn()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        fn()
+        torch.cuda.synchronize()
+        one = time.perf_counter() - t0
+        reps = int(max(2, min(10, budget_s / max(one, 1e-6))))
+        return statistics.fmean(_time_steps(fn, flusher, reps))
+
+    row = {}
+    for rho in (16, 32):
+        r_b = r - (rho.bit_length() - 1)
+        row[f"bb rho={rho}"] = timed(lambda: backends.run_bounding_box(dst, src, rho, kind, 1))
+        row[f"bb-exit rho={rho}"] = timed(lambda: backends.run_bounding_box(dst, src, rho, kind, 1, early_exit=True))
+        for st in (IntraStrategy.SUBBOX, IntraStrategy.TABLE):
+            lx, ly = backends.local_cell_arrays(st, rho) if st == IntraStrategy.TABLE else (None, None)
+            row[f"lambda {st.value} rho={rho}"] = timed(
+                lambda: backends.run_block_space(dst, src, rho, r_b, st, lx, ly, kind=kind, param=1))
+    row["lambda tuned"] = timed(lambda: backends.run_block_space(dst, src, 64, r - 6, IntraStrategy.TUNED, kind=kind,
+                                                                 param=1))
+    del src, dst
+    torch.cuda.empty_cache()
+    bb = min(v for k, v in row.items() if k.startswith("bb rho"))
+    bbx = min(v for k, v in row.items() if k.startswith("bb"))
+    lit = min(v for k, v in row.items() if k.startswith("lambda") and "tuned" not in k)
+    return {"ms": {k: round(v, 4) for k, v in row.items()},
+            "speedup_paper_literal_best_vs_best": bb / lit,
+            "speedup_tuned_lambda_vs_best_bb_paper": bb / row["lambda tuned"],
+            "speedup_tuned_lambda_vs_best_bb_any": bbx / row["lambda tuned"],
+            "note": "single launches after an L2 flush, the drop-in semantics (off-gasket cells of dst kept)"}
+
+
 def _multi_step(r: int, tdt, kind: int, flusher, steps: int = 48) -> dict:
     """The multi-step CA driver (ca.CARunner): single-step launches vs 2 or 4 fused steps
     per launch (temporal blocking, stencil_tb.cu), CUDA graphs, L2 flushed once before
@@ -774,6 +821,8 @@ def run_ours(args) -> None:
             line["zero_background"] = _zero_background(r, tdt, flusher, steps=args.steps)
         if kind != 0 and c in (1, 2, 4):
             line["multi_step"] = _multi_step(r, tdt, kind, flusher)
+        if kind != 0 and not args.no_sweep:
+            line["lambda_vs_bb"] = _stencil_vs_bb(r, tdt, kind, flusher)
         if not args.no_e2e:
             line["e2e"] = _e2e(workload, rho, steps=max(3, min(args.steps, 10)))
         if not args.no_cpu:

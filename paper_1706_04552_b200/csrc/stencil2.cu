@@ -365,10 +365,11 @@ cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
 template <int C, int KIND>
 cudaError_t launch_kind(const LaunchArgs& a, int r_t) {
     // ring depth: GM_FLAG_STAGES2 / default 3 (byte cells; 2-byte and 4-byte tiles are smaller: 4).
-    // With the static edge cache (CA runs) byte cells take the 2-deep ring: 4 instead of 3 CTAs
-    // per SM pay off once the sparse left-halo lines are gone (n=2^17 NSUM8 378 vs 406 us,
-    // NSUM4 368 vs 397; without the cache the 2-deep ring is slower, 499 vs 438 us)
-    if ((a.flags & GM_FLAG_STAGES2) || (C == 1 && a.edge != nullptr)) return launch_ck<C, KIND, 2>(a, r_t);
+    // With the static edge cache (CA runs) the 2-deep ring: more CTAs per SM pay off once the
+    // sparse left-halo lines are gone (n=2^17 NSUM8 int8 378 vs 406 us, 4 vs 3 CTAs per SM;
+    // n=2^16 NSUM4 int16 191 vs 227 us, int32 273 vs 317 us); without the cache the 2-deep
+    // ring is slower (int8 499 vs 438 us)
+    if ((a.flags & GM_FLAG_STAGES2) || a.edge != nullptr) return launch_ck<C, KIND, 2>(a, r_t);
     if constexpr (C == 1) return launch_ck<C, KIND, 3>(a, r_t);
     else return launch_ck<C, KIND, 4>(a, r_t);
 }
