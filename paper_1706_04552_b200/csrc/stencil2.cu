@@ -321,8 +321,11 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
 #pragma unroll
                 for (int i = 0; i < 8; ++i) out[i] = (out[i] & wmask[i]) | (w[1][i + 1] & ~wmask[i]);
             } else {  // off-gasket cells from the grid itself (still a whole-sector write)
+                // read with the 64-byte fetch hint: only this tile touches the line, so the rest
+                // of a 128-byte fetch is wasted (n=2^17 NSUM8 571 vs 586 us; byte-masked stores
+                // of the gasket cells instead, with the L2's sector fill: 704 us)
                 uint32_t old[8];
-                ld_sector(gp, fetch_line, v8, old);
+                ld_sector(gp, false, v8, old);
 #pragma unroll
                 for (int i = 0; i < 8; ++i) out[i] = (out[i] & wmask[i]) | (old[i] & ~wmask[i]);
             }
