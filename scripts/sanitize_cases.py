@@ -4,7 +4,8 @@ racecheck, synccheck):  compute-sanitizer --tool T python scripts/sanitize_cases
 
   (default)  write pass (every schedule, both store modes), paper-literal lambda / BB
              (incl. the vectorised BB), stencil v2 (NSUM4/8, 1/2/4-byte cells, whole-sector
-             blend), the fused CA kernel (T = 2, 4, 6), the masked snapshot + staged
+             blend), the CA step with the static edge cache, the fused CA kernel (T = 2, 4, 6),
+             the masked snapshot + staged
              host write-back, lambda maps, coverage
   part       the partitioned CA with the peer-memory halo fused into the step kernel, two
              processes on the one GPU (CUDA IPC)
@@ -68,6 +69,16 @@ def main_cases():
                 g = torch.from_numpy(src.copy()).cuda()
                 backends.run_block_space(g, torch.from_numpy(src).cuda(), 64, 3, S.TUNED, kind=kind, param=3, flags=fl)
                 bad += not np.array_equal(g.cpu().numpy(), want)
+            # the CA step with the static left-edge cache (edge.cu: build + 2-deep staging ring)
+            s_d = torch.from_numpy(src.copy()).cuda()
+            c = s_d.element_size()
+            edge = torch.empty(native.ca_edge_bytes(n, c), dtype=torch.uint8, device="cuda")
+            native.call("gm_ca_edge_build", edge.data_ptr(), s_d.data_ptr(), n, c, -1, 0, 0, None, 0,
+                        device.stream_handle())
+            d_d = s_d.clone()
+            native.call("gm_ca_run", d_d.data_ptr(), s_d.data_ptr(), n, c, kind, 3, 1, edge.data_ptr(), 0,
+                        device.stream_handle())
+            bad += not np.array_equal(d_d.cpu().numpy(), want)
             for T in (2, 4, 6):
                 if T == 6 and dt == np.int32:
                     continue
