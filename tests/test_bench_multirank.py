@@ -23,22 +23,14 @@ def _port() -> int:
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("halo,temporal,storage", [("collective", 1, "tiled"), ("peer", 6, "tiled"),
-                                                   ("peer-fused", 1, "tiled"), ("peer-fused", 6, "tiled"),
-                                                   ("collective", 2, "dense")])
-def test_bench_two_ranks_part15(gpu, halo, temporal, storage):
+def _run_two_ranks(args: list[str]) -> dict:
     env = dict(os.environ, GASKET_BENCH_SHARED_GPU="1", OMP_NUM_THREADS="1", PYTHONFAULTHANDLER="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", str(_port()), str(ROOT / "bench.py"), "--gpus", "2",
-           "--steps", "4", "--warmup", "3", "--workload", "part15", "--halo", halo, "--temporal", str(temporal),
-           "--storage", storage]
-    # on a hang every rank gets SIGABRT (faulthandler prints where it waits) instead of the
-    # test blocking the suite
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), str(ROOT / "bench.py"), "--gpus", "2", *args]
     p = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True, env=env, cwd=ROOT)
     try:
         stdout, stderr = p.communicate(timeout=240)
     except subprocess.TimeoutExpired:
-        # torchrun starts its workers in sessions of their own: signal every descendant
         import psutil
 
         procs = psutil.Process(p.pid).children(recursive=True) + [psutil.Process(p.pid)]
@@ -58,7 +50,23 @@ def test_bench_two_ranks_part15(gpu, halo, temporal, storage):
             stdout, stderr = p.communicate()
         pytest.fail(f"multi-rank bench hung (240 s); tracebacks:\n{stderr[-8000:]}")
     assert p.returncode == 0, stderr[-3000:]
-    line = json.loads([x for x in stdout.splitlines() if x.startswith("{")][-1])
+    return json.loads([x for x in stdout.splitlines() if x.startswith("{")][-1])
+
+
+def test_bench_two_ranks_write16(gpu):
+    """The default workload at N=2 (the driver's scaling run): one independent n=2^16 grid per
+    rank, weak scaling, the job's e2e from every rank's own host grid."""
+    line = _run_two_ranks(["--steps", "5", "--warmup", "3"])
+    assert line["n_gpus"] == 2 and line["scaling"] == "weak" and line["value"] > 0 and line["gpu_launches"] > 0
+    assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] > 0
+
+
+@pytest.mark.parametrize("halo,temporal,storage", [("collective", 1, "tiled"), ("peer", 6, "tiled"),
+                                                   ("peer-fused", 1, "tiled"), ("peer-fused", 6, "tiled"),
+                                                   ("collective", 2, "dense")])
+def test_bench_two_ranks_part15(gpu, halo, temporal, storage):
+    line = _run_two_ranks(["--steps", "4", "--warmup", "3", "--workload", "part15", "--halo", halo, "--temporal",
+                           str(temporal), "--storage", storage])
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["gpu_launches"] > 0
     assert line["config"]["storage"] == storage and line["config"]["halo"] == halo
     if storage == "tiled":
