@@ -196,14 +196,11 @@ __global__ void __launch_bounds__(256) gasket_write(uint8_t* __restrict__ grid, 
     const uint32_t js = (uint32_t)(lane & ~7) * 4u / C;                            // first cell of its sector
     const uint32_t v = splat_w<C>(param, lane);
     const uint64_t inv = lambda_lane_reciprocal(lane);
-    // units come 1 << tshift per ticket (consecutive bands of one tile) when the queue is there;
-    // lane 0 requests the next ticket one unit ahead, so its round trip overlaps this unit's
-    // stores instead of stalling the warp between units
-    uint32_t u = u_lo + warp, u_end = u + 1, pend = 0;
+    // units come 1 << tshift per ticket (consecutive bands of one tile) when the queue is there
+    uint32_t u = u_lo + warp, u_end = u + 1;
     if (wq != nullptr) {
         u = u_lo + (grab(wq, lane, 1u) << tshift);
         u_end = u + (1u << tshift);
-        if (lane == 0 && u < u_hi) pend = atomicAdd(wq, 1u);
     }
     for (;;) {
         if (u >= u_hi) break;
@@ -231,9 +228,8 @@ __global__ void __launch_bounds__(256) gasket_write(uint8_t* __restrict__ grid, 
         }
         if (wq != nullptr) {
             if (++u == u_end) {
-                u = u_lo + (__shfl_sync(0xffffffffu, pend, 0) << tshift);
+                u = u_lo + (grab(wq, lane, 1u) << tshift);
                 u_end = u + (1u << tshift);
-                if (lane == 0 && u < u_hi) pend = atomicAdd(wq, 1u);
             }
         } else {
             u += nwarps;
