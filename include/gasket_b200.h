@@ -225,6 +225,15 @@ int gm_ca_edge_build(void* edge, const void* src, int64_t n, int32_t cell_bytes,
                      uint32_t sg_end, const int64_t* sg_off, int64_t pitch, void* stream);
 int gm_ca_run(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param, int32_t steps,
               const void* edge, int32_t flags, void* stream);
+/* In-place neighbour-sum launch with engine.launch's snapshot semantics (engine.py:201:
+ * every cell reads the pre-launch state) without a grid-sized snapshot (edge.cu): each
+ * tile stages its window before it writes, so only the <= 5 border cells per member tile
+ * that neighbouring tiles read can change under them; those are copied into `border`
+ * (gm_border_bytes bytes, device memory, one per stream) and patched into the staged
+ * windows.  kind NSUM4 / NSUM8; 1-, 2- or 4-byte cells, n >= one 128-byte tile. */
+int gm_border_bytes(int64_t n, int32_t cell_bytes, int64_t* bytes);
+int gm_run_inplace(void* grid, void* border, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
+                   void* stream);
 /* Peer-memory halo exchange of the partitioned CA (peer.cu).
  * gm_dev_alloc/free: plain cudaMalloc'd buffers (allocation bases, so they can be
  * exported); gm_ipc_get_handle writes a 64-byte cudaIpcMemHandle_t; gm_ipc_open_handle

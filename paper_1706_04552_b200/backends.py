@@ -133,13 +133,17 @@ def _same_array(a: Any, b: Any) -> bool:
             and a.shape == b.shape and a.strides == b.strides)
 
 
-def _run(grid: Any, src: Any, kind: int, launch, *, mapped_ok: bool) -> None:
+def _run(grid: Any, src: Any, kind: int, launch, *, mapped_ok: bool, inplace: Optional[Any] = None) -> None:
     """Route one launch: device tensors directly, numpy through a host transport.
 
     ``launch(grid_ptr, src_ptr, n, cell_bytes, stream, extra_flags)`` issues the C-ABI call.
     In the mapped (zero-copy) transport the kernel is asked for whole-sector
     writes (``FLAG_EXPLICIT_RMW``): PCIe cannot carry byte-masked partial lines
-    efficiently, so partial sectors are read, blended and written back whole."""
+    efficiently, so partial sectors are read, blended and written back whole.
+
+    ``inplace(grid)``: the in-place form of a neighbour-sum launch whose src is the grid
+    itself (device.run_inplace, the tuned kernel only); otherwise such a launch reads a
+    masked snapshot of the grid (engine.py:201)."""
     device.require_cuda()
     n = device.check_square(grid)
     c = device.cell_bytes_of(grid)
@@ -157,7 +161,14 @@ def _run(grid: Any, src: Any, kind: int, launch, *, mapped_ok: bool) -> None:
             if not device.is_device(src):
                 src_dev = torch.from_numpy(np.ascontiguousarray(src)).to(grid.device, non_blocking=True)
             elif _shares_memory(src, grid):
+                if (inplace is not None and src.data_ptr() == grid.data_ptr() and src.stride() == grid.stride()
+                        and device.inplace_ok(n, c)):
+                    inplace(grid)  # engine.py:201's semantics, the snapshot reduced to tile borders
+                    return
                 src_dev = device.stencil_snapshot(grid)  # engine.py:201's snapshot, masked
+                # the grid and its snapshot agree off the gasket: stencils may blend from src
+                launch(device.data_ptr(grid), device.data_ptr(src_dev), n, c, stream, native.FLAG_DST_FROM_SRC)
+                return
             else:
                 device.check_square(src, "src")
         launch(device.data_ptr(grid), device.data_ptr(src_dev) if reads_src else 0, n, c, stream, 0)
@@ -273,7 +284,10 @@ def run_block_space(grid, src, rho: int, r_b: int, strategy, local_x: Optional[n
         native.call("gm_run_block_space", gp, sp, n, c, int(rho), int(r_b), tag, tx, ty, ntab, kind, p,
                     int(flags) | extra_flags, stream)
 
-    _run(grid, src, kind, launch, mapped_ok=(tag == STRAT_TUNED))
+    inplace = None
+    if tag == STRAT_TUNED and kind in (KERNEL_NEIGHBOR_SUM, KERNEL_NEIGHBOR_SUM8):
+        inplace = lambda g: device.run_inplace(g, kind, p)  # noqa: E731
+    _run(grid, src, kind, launch, mapped_ok=(tag == STRAT_TUNED), inplace=inplace)
 
 
 __all__ = [

@@ -486,6 +486,34 @@ int gm_ca_run(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_
     return cuda_rc(e, "CA launch");
 }
 
+int gm_border_bytes(int64_t n, int32_t cell_bytes, int64_t* bytes) {
+    if (!bytes) return fail(GM_EINVAL, "gm_border_bytes: null output");
+    gm::LaunchArgs a{};
+    if (int rc = ca_args(a, "gm_border_bytes", nullptr, nullptr, n, cell_bytes, GM_KIND_NSUM8, 1, -1, 0, 0, nullptr, 0,
+                         nullptr))
+        return rc;
+    *bytes = gm::border_bytes(n, cell_bytes);
+    return GM_OK;
+}
+
+int gm_run_inplace(void* grid, void* border, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param,
+                   void* stream) {
+    if (kind != GM_KIND_NSUM4 && kind != GM_KIND_NSUM8) return fail(GM_EINVAL, "gm_run_inplace: kind must be NSUM4 or NSUM8");
+    if (!grid || !border || border == grid) return fail(GM_EINVAL, "gm_run_inplace: needs the grid and a border buffer");
+    gm::LaunchArgs a{};
+    if (int rc = ca_args(a, "gm_run_inplace", grid, grid, n, cell_bytes, kind, param, -1, 0, 0, nullptr, 0, stream))
+        return rc;
+    a.flags = GM_FLAG_DST_FROM_SRC;  // off-gasket cells come from the staged window (the grid itself)
+    a.border = reinterpret_cast<const uint8_t*>(border);
+    cudaError_t e = gm::launch_border_snapshot(reinterpret_cast<uint8_t*>(border), grid, n, cell_bytes, a.stream);
+    if (e == cudaSuccess) e = gm::launch_stencil_v2(a);
+    if (e == cudaErrorNotSupported) {
+        cudaGetLastError();
+        return fail(GM_EINVAL, "gm_run_inplace: no tiled kernel for these cells (<= 2^15 tiles per edge)");
+    }
+    return cuda_rc(e, "in-place neighbour-sum launch");
+}
+
 int gm_dev_alloc(int64_t bytes, void** out) {
     if (bytes <= 0 || !out) return fail(GM_EINVAL, "gm_dev_alloc: bad size/out");
     return cuda_rc(cudaMalloc(out, (size_t)bytes), "cudaMalloc");

@@ -42,6 +42,10 @@ struct LaunchArgs {
     // launch's tile range whose left neighbour tile is not a gasket tile, the 16-byte chunk
     // left of each of its TT rows at edge + (i * TT + row) * 16; nullptr = read the grid
     const uint8_t* edge = nullptr;
+    // in-place neighbour-sum launch (src == grid): the pre-launch border cells of every
+    // member tile (launch_border_snapshot, edge.cu); the tuned stencil patches its staged
+    // window from there.  nullptr = src is a separate pre-launch state.
+    const uint8_t* border = nullptr;
 };
 
 // The left neighbour of member tile (bx, by) holds no gasket cell (so its cells never
@@ -98,6 +102,8 @@ cudaError_t launch_stencil_tb2(const LaunchArgs& a);
 cudaError_t launch_stencil_tb(const LaunchArgs& a, int steps);  // steps = 2, 4 or 6
 cudaError_t launch_edge_build(const LaunchArgs& a, uint8_t* edge);  // edge.cu
 int64_t edge_cache_bytes(const LaunchArgs& a);                   // edge.cu (0: no tiled kernel)
+int64_t border_bytes(int64_t n, int cell_bytes);                  // edge.cu
+cudaError_t launch_border_snapshot(uint8_t* border, const void* grid, int64_t n, int cell_bytes, cudaStream_t s);
 cudaError_t launch_snapshot_stencil(void* snap, const void* grid, int64_t n, int cell_bytes, cudaStream_t s);
 cudaError_t launch_writeback_tiles(void* out, const void* dst, const void* snap, int64_t n, int cell_bytes, cudaStream_t s);
 cudaError_t launch_host_rows_copyback(void* out, const void* dst, const void* snap, int64_t n, int cell_bytes,

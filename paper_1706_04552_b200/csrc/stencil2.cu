@@ -103,7 +103,8 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
                                                              const uint32_t* __restrict__ order, PeerEpilogue* epi,
                                                              uint64_t wait_epoch, uint64_t signal_epoch,
                                                              const int64_t* __restrict__ sg_off, int64_t pitch,
-                                                             uint32_t per, const uint8_t* __restrict__ edge) {
+                                                             uint32_t per, const uint8_t* __restrict__ edge,
+                                                             const uint8_t* __restrict__ border) {
     using S = T2<C>;
     peer_prologue_wait(epi, wait_epoch);  // partitioned CA with the fused exchange only
     constexpr bool EIGHT = KIND == KIND_NSUM8;
@@ -287,6 +288,36 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
         // n=2^17 NSUM8 427 vs 436 us, NSUM4 430 vs 451 us with the entry loaded a tile ahead
         stage(idx + NST - 1, order_v(idx + NST - 1));
         cp_async_commit();
+        if (border != nullptr) {
+            // in-place launch (src aliases grid; edge.cu): the neighbouring tiles' gasket cells
+            // this tile reads may already hold new values -- put their pre-launch values into
+            // the staged window (8 reader positions; a patch with the old value is always right)
+            if (threadIdx.x < 8) {
+                uint32_t bx, by;
+                tile_xy(first + idx * step, bx, by);
+                constexpr int TT = S::TT;
+                const int p = threadIdx.x;
+                int px, py, ox, oy, sl;
+                switch (p) {
+                case 0: px = -1; py = -1; ox = -1; oy = -1; sl = 4; break;
+                case 1: px = 0; py = -1; ox = 0; oy = -1; sl = 2; break;
+                case 2: px = 1; py = -1; ox = 0; oy = -1; sl = 3; break;
+                case 3: px = -1; py = TT - 1; ox = -1; oy = 0; sl = 4; break;
+                case 4: px = 0; py = TT; ox = 0; oy = 1; sl = 0; break;
+                case 5: px = TT; py = TT - 2; ox = 1; oy = 0; sl = 1; break;
+                case 6: px = TT; py = TT - 1; ox = 1; oy = 0; sl = 2; break;
+                default: px = TT; py = TT; ox = 1; oy = 1; sl = 0; break;
+                }
+                const int64_t ntx = n / TT, tx = (int64_t)bx + ox, ty = (int64_t)by + oy;
+                if (tx >= 0 && ty >= 0 && tx < ntx && ty < ntx && (tx & ~ty) == 0) {
+                    uint8_t* d = smem + (idx % NST) * S::BUF + (py + 1) * PITCH + 16 + px * C;
+                    const uint8_t* b = border + ((ty * ntx + tx) * 8 + sl) * C;
+#pragma unroll
+                    for (int k = 0; k < C; ++k) d[k] = b[k];
+                }
+            }
+            __syncthreads();
+        }
         if (active) {
             uint32_t bx, by;
             tile_xy(first + idx * step, bx, by);
@@ -360,7 +391,7 @@ cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
                                                           a.part_level, a.param, a.flags, order,
                                                           reinterpret_cast<PeerEpilogue*>(a.peer_epi), a.wait_epoch,
                                                           a.signal_epoch, a.sg_off, row_pitch(a),
-                                                          tiles_per_subgasket(a, r_t), a.edge);
+                                                          tiles_per_subgasket(a, r_t), a.edge, a.border);
     note_launch();
     return cudaGetLastError();
 }

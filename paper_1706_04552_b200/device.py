@@ -141,6 +141,25 @@ def staged_writeback_ok(n: int, c: int) -> bool:
     return n * c >= 256 if c == 8 else True
 
 
+def inplace_ok(n: int, c: int) -> bool:
+    """Grids the in-place neighbour-sum launch covers (gm_run_inplace: the tuned tile
+    stencil on 1/2/4-byte cells, a power-of-two edge of at least one 128-byte tile)."""
+    return c in (1, 2, 4) and tile_staging_ok(n, c)
+
+
+def run_inplace(grid: torch.Tensor, kind: int, param: int) -> None:
+    """engine.launch's neighbour-sum semantics on a device grid (every cell reads the
+    pre-launch state, engine.py:201) in place: gm_run_inplace snapshots only the <= 5
+    border cells per member tile that neighbouring tiles read (edge.cu) instead of the
+    grid.  The border buffer is per stream, like the snapshot scratch."""
+    n = int(grid.shape[0])
+    c = grid.element_size()
+    key = f"border:{torch.cuda.current_stream(grid.device).cuda_stream}"
+    border = scratch.get(key, native.border_bytes(n, c), torch.uint8, grid.device)
+    native.call("gm_run_inplace", grid.data_ptr(), border.data_ptr(), n, c, int(kind), int(np.int32(param)),
+                stream_handle())
+
+
 def stencil_snapshot(grid: torch.Tensor) -> torch.Tensor:
     """engine.launch's pre-launch copy of a neighbour-sum launch (engine.py:201), on the
     device and masked: only the cells a one-step stencil over the gasket reads are

@@ -100,6 +100,8 @@ _SIGS = {
     "gm_ca_edge_bytes": [_i64, _i32, _i32, ctypes.c_uint32, ctypes.c_uint32, ctypes.POINTER(ctypes.c_int64)],
     "gm_ca_edge_build": [_vp, _vp, _i64, _i32, _i32, ctypes.c_uint32, ctypes.c_uint32, _vp, _i64, _vp],
     "gm_ca_run": [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _i32, _vp],
+    "gm_border_bytes": [_i64, _i32, ctypes.POINTER(ctypes.c_int64)],
+    "gm_run_inplace": [_vp, _vp, _i64, _i32, _i32, _i32, _vp],
 }
 
 # Every symbol include/gasket_b200.h declares (checked by tests/test_native_abi.py).
@@ -162,6 +164,13 @@ def ca_edge_bytes(n: int, cell_bytes: int, level: int = -1, sg_begin: int = 0, s
     """Size of the static left-edge cache of a CA run (gm_ca_edge_bytes)."""
     out = ctypes.c_int64(0)
     check(lib().gm_ca_edge_bytes(n, cell_bytes, level, sg_begin, sg_end, ctypes.byref(out)))
+    return int(out.value)
+
+
+def border_bytes(n: int, cell_bytes: int) -> int:
+    """Size of the border-cell buffer of an in-place neighbour-sum launch (gm_border_bytes)."""
+    out = ctypes.c_int64(0)
+    check(lib().gm_border_bytes(n, cell_bytes, ctypes.byref(out)))
     return int(out.value)
 
 

@@ -1,6 +1,8 @@
 #!/usr/bin/env python
 """engine.launch NEIGHBOR_SUM on a device grid, snapshot included (engine.py:201):
-the masked snapshot (device.stencil_snapshot) vs the full grid copy the reference takes.
+the in-place launch with a border-cell snapshot (what engine.launch runs for the tuned
+strategy), the masked snapshot (device.stencil_snapshot) and the full grid copy the
+reference takes.
     python scripts/time_engine_launch.py [r] [K]      (default n = 2^16 int32, the reference's dtype)"""
 import statistics
 import sys
@@ -57,7 +59,11 @@ def main():
         s = device.stencil_snapshot(g)
         backends.run_block_space(g, s, rho, spec.r_b, IntraStrategy.TUNED, kind=1, param=1, flags=2)
 
-    for name, fn in (("full grid copy + launch", full_copy), ("engine.launch (masked snapshot)", masked),
+    def inplace():  # src = grid: the tuned kernel in place with the border-cell snapshot (gm_run_inplace)
+        backends.run_block_space(g, g, rho, spec.r_b, IntraStrategy.TUNED, kind=1, param=1)
+
+    for name, fn in (("full grid copy + launch", full_copy), ("engine.launch", masked),
+                     ("in place (border snapshot)", inplace),
                      ("masked snapshot + launch", snapshot_launch), ("masked snapshot only", snapshot_only),
                      ("launch only", kernel_only)):
         print(f"n=2^{r} int32 NSUM4  {name:34s} {timed(fn, flush, k):8.3f} ms", flush=True)

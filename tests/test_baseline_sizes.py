@@ -141,6 +141,10 @@ def test_n17_int8_ca_exact(gpu, oracle, kind):
         gpu.native.call("gm_ca_run", t.data_ptr(), src.data_ptr(), n, 1, kind, 1, steps, edge.data_ptr(), 0,
                         gpu.device.stream_handle())
         assert gpu.device.count_mismatch(t, results[steps]) == 0, ("edge cache", steps)
+    # the in-place launch (src = grid: engine.launch semantics with a border snapshot only)
+    t.copy_(src)
+    gpu.backends.run_block_space(t, t, 64, 11, S.TUNED, kind=kind, param=1)
+    assert gpu.device.count_mismatch(t, results[1]) == 0, "in-place"
     del t, edge
     torch.cuda.empty_cache()
     torch.cuda.synchronize()

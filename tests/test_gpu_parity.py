@@ -412,6 +412,49 @@ def test_ca_run_edge_cache_vs_oracle(gpu, oracle, dtype, steps):
                     assert np.array_equal(dst.cpu().numpy(), want), (np.dtype(dtype).name, n, mode, kind, e is None)
 
 
+@pytest.mark.parametrize("dtype", [np.int8, np.int16, np.int32])
+def test_inplace_neighbour_sum_vs_oracle(gpu, oracle, dtype):
+    """A neighbour-sum launch whose src is the grid (engine.launch semantics, engine.py:201)
+    through the tuned kernel runs in place with a snapshot of the tiles' border cells only
+    (gm_run_inplace): every cell equals the oracle's step from the pre-launch grid --
+    grid-edge tiles, n from one tile to 2^12, both kinds, both background modes, and
+    repeated launches (each reading the previous launch's result)."""
+    be, S = gpu.backends, gpu.geometry.IntraStrategy
+    c = np.dtype(dtype).itemsize
+    n0 = 128 // c
+    for n in (n0, 2 * n0, 8 * n0, 1 << 12):
+        for mode in (0, 1):
+            init = oracle.fill_hash(n, dtype, 61 + mode, mode)
+            for kind in (1, 2):
+                g = torch.from_numpy(init.copy()).cuda()
+                want = init.copy()
+                rho = min(64, n)
+                for _ in range(3):
+                    be.run_block_space(g, g, rho, (n // rho).bit_length() - 1, S.TUNED, kind=kind, param=-7)
+                    nxt = want.copy()
+                    oracle.run_bounding_box(nxt, want, 1, kind, -7)
+                    want = nxt
+                    assert np.array_equal(g.cpu().numpy(), want), (np.dtype(dtype).name, n, mode, kind)
+
+
+def test_engine_launch_device_inplace_int32(gpu, oracle):
+    """engine.launch NEIGHBOR_SUM on an int32 device grid (the reference's entry point):
+    tuned (in place, border snapshot) and SUBBOX (masked snapshot) == the oracle."""
+    from paper_1706_04552_b200 import engine
+    from paper_1706_04552_b200.geometry import FractalSpec, IntraStrategy
+
+    n = 1 << 11
+    init = oracle.fill_hash(n, np.int32, 5, 0)
+    want = init.copy()
+    oracle.run_bounding_box(want, init, 1, 1, 3)
+    for strat, rho in ((IntraStrategy.TUNED, 32), (IntraStrategy.SUBBOX, 16)):
+        g = torch.from_numpy(init.copy()).cuda()
+        cfg = engine.LaunchConfig(spec=FractalSpec(n=n, rho=rho), mapping=engine.Mapping.BLOCK_SPACE, strategy=strat,
+                                  kernel=engine.CellKernel(engine.KernelKind.NEIGHBOR_SUM, 3))
+        engine.launch(cfg, g)
+        assert np.array_equal(g.cpu().numpy(), want), strat
+
+
 def test_ca_run_rejects_bad_arguments(gpu):
     from paper_1706_04552_b200 import device, native
 

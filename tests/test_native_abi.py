@@ -86,3 +86,13 @@ def test_ca_edge_bytes_host_only():
         native.ca_edge_bytes(64, 1)  # narrower than a tile
     with pytest.raises(ValueError):
         native.ca_edge_bytes(1 << 12, 8)
+
+
+def test_border_bytes_host_only():
+    """The in-place launch's border buffer: 8 cells per tile of the tile grid."""
+    from paper_1706_04552_b200 import native
+
+    assert native.border_bytes(1 << 17, 1) == (1 << 10) ** 2 * 8
+    assert native.border_bytes(1 << 16, 4) == (1 << 11) ** 2 * 8 * 4
+    with pytest.raises(ValueError):
+        native.border_bytes(64, 1)
