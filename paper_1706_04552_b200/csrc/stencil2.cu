@@ -402,8 +402,10 @@ cudaError_t launch_kind(const LaunchArgs& a, int r_t) {
     // With the static edge cache (CA runs) the 2-deep ring: more CTAs per SM pay off once the
     // sparse left-halo lines are gone (n=2^17 NSUM8 int8 378 vs 406 us, 4 vs 3 CTAs per SM;
     // n=2^16 NSUM4 int16 191 vs 227 us, int32 273 vs 317 us); without the cache the 2-deep
-    // ring is slower (int8 499 vs 438 us)
-    if ((a.flags & GM_FLAG_STAGES2) || a.edge != nullptr) return launch_ck<C, KIND, 2>(a, r_t);
+    // ring is slower (int8 499 vs 438 us).  The in-place launch (border patches, one more
+    // barrier per tile) also prefers it: n=2^16 int32 NSUM4 364 vs 479 us, n=2^17 int8 NSUM8
+    // 472 vs 535 us
+    if ((a.flags & GM_FLAG_STAGES2) || a.edge != nullptr || a.border != nullptr) return launch_ck<C, KIND, 2>(a, r_t);
     if constexpr (C == 1) return launch_ck<C, KIND, 3>(a, r_t);
     else return launch_ck<C, KIND, 4>(a, r_t);
 }

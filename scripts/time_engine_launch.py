@@ -32,7 +32,7 @@ def timed(fn, flush, k):
 
 
 def main():
-    r = int(sys.argv[1]) if len(sys.argv) > 1 else 16
+    r = int(sys.argv[1]) if len(sys.argv) > 1 else 16  # (int32: three grids, so r <= 16 on one B200)
     k = int(sys.argv[2]) if len(sys.argv) > 2 else 10
     n, rho = 1 << r, 32
     flush = device.L2Flusher()
