@@ -156,6 +156,13 @@ int gm_coverage_blocks(const int64_t* bx, const int64_t* by, int64_t nblocks, co
                        const int32_t* ly, int32_t nlocal, int32_t rho, int64_t n, uint32_t* counts,
                        void* stream);
 
+/* engine.py:252-258, the comparison leg of the coverage audit, on the device: over the
+ * n*n uint32 counters of gm_coverage, totals[0] = duplicates (count above membership),
+ * totals[1] = misses (gasket cells with count 0); the first `cap` linear indices y*n + x of
+ * each go to dup_idx / miss_idx in no particular order.  totals: device, 2 entries. */
+int gm_coverage_check(const uint32_t* counts, int64_t n, unsigned long long* totals, int64_t* dup_idx,
+                      int64_t* miss_idx, int64_t cap, void* stream);
+
 /* blockmap.py:123-166 on the device.  Maps coordinates (cx, cy) (e.g. from
  * gm_map_rectangle, row-major omega order) of nblocks blocks onto the edge-n_b
  * gasket; owner must be n_b*n_b int64 scratch.  Writes result[0] = first bad

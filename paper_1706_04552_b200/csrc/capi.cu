@@ -25,6 +25,8 @@ cudaError_t launch_bijection(const int64_t*, const int64_t*, int64_t, int64_t, i
 cudaError_t launch_coverage_blocks(const int64_t*, const int64_t*, int64_t, const int32_t*, const int32_t*, int, int,
                                    int64_t, uint32_t*, cudaStream_t);
 cudaError_t launch_fill_hash(void*, int64_t, int, uint64_t, int, cudaStream_t);
+cudaError_t launch_coverage_check(const uint32_t*, int64_t, unsigned long long*, int64_t*, int64_t*, int64_t,
+                                  cudaStream_t);
 cudaError_t launch_checksum(const void*, int64_t, int, uint64_t*, cudaStream_t);
 cudaError_t launch_count_equal(const void*, const void*, int64_t, unsigned long long*, cudaStream_t);
 cudaError_t launch_l2_flush(const void*, int64_t, uint64_t*, cudaStream_t);
@@ -273,6 +275,15 @@ int gm_coverage_blocks(const int64_t* bx, const int64_t* by, int64_t nblocks, co
     return cuda_rc(gm::launch_coverage_blocks(bx, by, nblocks, lx, ly, nlocal, rho, n, counts,
                                               reinterpret_cast<cudaStream_t>(stream)),
                    "coverage_blocks");
+}
+
+int gm_coverage_check(const uint32_t* counts, int64_t n, unsigned long long* totals, int64_t* dup_idx,
+                      int64_t* miss_idx, int64_t cap, void* stream) {
+    if (!counts || !totals || (cap > 0 && (!dup_idx || !miss_idx)) || cap < 0)
+        return fail(GM_EINVAL, "gm_coverage_check: bad buffers");
+    if (!pow2(n) || n < 2) return fail(GM_EINVAL, "gm_coverage_check: edge must be a power of two >= 2");
+    return cuda_rc(gm::launch_coverage_check(counts, n, totals, dup_idx, miss_idx, cap,
+                                             reinterpret_cast<cudaStream_t>(stream)), "coverage check");
 }
 
 int gm_bijection_check(const int64_t* cx, const int64_t* cy, int64_t nblocks, int64_t n_b, int64_t* owner,

@@ -287,6 +287,49 @@ cudaError_t launch_bijection(const int64_t* cx, const int64_t* cy, int64_t nbloc
     return cudaGetLastError();
 }
 
+// The comparison leg of verify_coverage (engine.py:252-258): one pass over the counters,
+// cell (x, y) a gasket cell iff x & (n-1-y) == 0; duplicates = counts above membership
+// (count > 1 on the gasket, > 0 off it), misses = gasket cells with count 0.  totals[0/1]
+// count them; the first `cap` of each (in no particular order: the caller sorts) have their
+// linear index y*n + x written to dup_idx / miss_idx.
+__global__ void coverage_check_kernel(const uint4* __restrict__ counts, int64_t n, int lgn,
+                                      unsigned long long* __restrict__ totals, int64_t* __restrict__ dup_idx,
+                                      int64_t* __restrict__ miss_idx, int64_t cap) {
+    const int64_t nvec = (n * n) >> 2;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
+        const uint4 c4 = __ldcs(counts + v);
+        const uint32_t cs[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int64_t i = (v << 2) + k;
+            const int64_t y = i >> lgn, x = i & (n - 1);
+            const uint32_t mem = (x & (n - 1 - y)) == 0 ? 1u : 0u;
+            if (cs[k] > mem) {
+                const unsigned long long p = atomicAdd(totals, 1ull);
+                if ((int64_t)p < cap) dup_idx[p] = i;
+            } else if (mem && cs[k] == 0) {
+                const unsigned long long p = atomicAdd(totals + 1, 1ull);
+                if ((int64_t)p < cap) miss_idx[p] = i;
+            }
+        }
+    }
+}
+
+cudaError_t launch_coverage_check(const uint32_t* counts, int64_t n, unsigned long long* totals, int64_t* dup_idx,
+                                  int64_t* miss_idx, int64_t cap, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(totals, 0, 2 * sizeof(unsigned long long), s);
+    if (e) return e;
+    int lgn = 0;
+    while ((int64_t(1) << lgn) < n) ++lgn;
+    if (n * n < 4) {  // (a 1 x 1 grid: one cell, handled as a vector of 4 with 3 pads would overrun)
+        return cudaErrorNotSupported;
+    }
+    coverage_check_kernel<<<grid_for((n * n) >> 2), 256, 0, s>>>(reinterpret_cast<const uint4*>(counts), n, lgn, totals,
+                                                                 dup_idx, miss_idx, cap);
+    note_launch();
+    return cudaGetLastError();
+}
+
 cudaError_t launch_coverage_blocks(const int64_t* bx, const int64_t* by, int64_t nblocks, const int32_t* lx,
                                    const int32_t* ly, int nlocal, int rho, int64_t n, uint32_t* counts, cudaStream_t s) {
     if (nblocks == 0 || nlocal == 0) return cudaSuccess;

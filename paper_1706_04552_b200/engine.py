@@ -260,6 +260,31 @@ def _coverage_counts(config: LaunchConfig, map_fn) -> torch.Tensor:
     return counts
 
 
+def _coverage_compare(counts: torch.Tensor, n: int) -> tuple[list, list]:
+    """Duplicates and misses of the counters (engine.py:252-258), row-major like the
+    reference's np.argwhere: one device pass (gm_coverage_check) that counts them, and a
+    second that collects their indices when there are any -- no n^2 temporaries."""
+    if n == 1:
+        c = int(counts.reshape(-1)[0].item())
+        return ([Coord2(0, 0)] if c > 1 else []), ([Coord2(0, 0)] if c == 0 else [])
+    stream = device.stream_handle()
+    totals = torch.zeros(2, dtype=torch.int64, device="cuda")
+    native.call("gm_coverage_check", counts.data_ptr(), n, totals.data_ptr(), None, None, 0, stream)
+    nd, nm = (int(v) for v in totals.cpu().tolist())
+    if nd == 0 and nm == 0:
+        return [], []
+    cap = max(nd, nm)
+    di = torch.empty(cap, dtype=torch.int64, device="cuda")
+    mi = torch.empty(cap, dtype=torch.int64, device="cuda")
+    native.call("gm_coverage_check", counts.data_ptr(), n, totals.data_ptr(), di.data_ptr(), mi.data_ptr(), cap,
+                stream)
+    out = []
+    for idx, k in ((di, nd), (mi, nm)):
+        lin = torch.sort(idx[:k]).values.cpu().numpy()
+        out.append([Coord2(int(i % n), int(i // n)) for i in lin])
+    return out[0], out[1]
+
+
 def verify_coverage(config: LaunchConfig,
                     map_fn: Optional[Callable[[tuple[int, int], int], MapResult]] = None) -> CoverageReport:
     """Per-cell write counters of the launch shape; duplicates = cells written more
@@ -267,11 +292,6 @@ def verify_coverage(config: LaunchConfig,
     device.require_cuda()
     n = config.spec.n
     counts = _coverage_counts(config, map_fn)
-    idx = torch.arange(n, device="cuda", dtype=torch.int64)
-    member = (idx[None, :] & (n - 1 - idx)[:, None]) == 0
-    over = torch.nonzero(counts.to(torch.int64) > member.to(torch.int64))
-    missed = torch.nonzero(member & (counts == 0))
-    dups = [Coord2(int(x), int(y)) for y, x in over.cpu().tolist()]
-    miss = [Coord2(int(x), int(y)) for y, x in missed.cpu().tolist()]
+    dups, miss = _coverage_compare(counts, n)
     out = counts.cpu().numpy().astype(np.int64) if n <= ORACLE_MAX_EDGE else counts
     return CoverageReport(counts=out, duplicates=dups, misses=miss)

@@ -167,3 +167,32 @@ def test_n18_int8_ca_sampled_bands(gpu, oracle):
     d.copy_(src)
     _ca_steps(gpu, d, src, n, 2, 6)
     assert band_mismatches(gpu, oracle, {6: d}, n, np.int8, seed, 0, 2, 1, bands=bands) == {6: 0}
+
+
+def test_n16_coverage_audit(gpu):
+    """The coverage audit (engine.verify_coverage, engine.py:214-258) at BASELINE config 2's
+    size: the real kernels count every write into n x n uint32 counters (16 GiB) and the
+    comparison runs on the device (gm_coverage_check).  Correct launches are exact; a
+    corrupted map (geometry.corrupted_map_fn, the reference's mutation hook) is caught,
+    its duplicates and misses row-major like np.argwhere."""
+    eng, geo = gpu.engine, gpu.geometry
+    S = geo.IntraStrategy
+    spec = geo.FractalSpec(n=1 << 16, rho=32)
+    for mapping, strat in ((eng.Mapping.BLOCK_SPACE, S.TUNED), (eng.Mapping.BLOCK_SPACE, S.TABLE),
+                           (eng.Mapping.BOUNDING_BOX_EXIT, None)):
+        rep = eng.verify_coverage(eng.LaunchConfig(spec=spec, mapping=mapping, strategy=strat))
+        assert rep.exact and not rep.duplicates and not rep.misses, (mapping, strat)
+        del rep
+        torch.cuda.empty_cache()
+    # one block mapped onto its neighbour's place: that block's cells are missed, the
+    # neighbour's written twice -- the audit finds exactly those, row-major
+    def one_bad(omega, r_b):
+        return geo.map_block((1, 0) if tuple(omega) == (0, 0) else omega, r_b)
+
+    rep = eng.verify_coverage(eng.LaunchConfig(spec=spec, mapping=eng.Mapping.BLOCK_SPACE, strategy=S.SUBBOX), one_bad)
+    good, bad = geo.map_block((0, 0), spec.r_b).coord, geo.map_block((1, 0), spec.r_b).coord
+    cells = [(x, y) for y in range(32) for x in range(32) if (x & ~y) == 0]  # a block's gasket cells
+    want_miss = sorted((good[1] * 32 + y) * spec.n + good[0] * 32 + x for x, y in cells)
+    want_dup = sorted((bad[1] * 32 + y) * spec.n + bad[0] * 32 + x for x, y in cells)
+    assert [c.y * spec.n + c.x for c in rep.misses] == want_miss
+    assert [c.y * spec.n + c.x for c in rep.duplicates] == want_dup
