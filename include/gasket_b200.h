@@ -182,6 +182,19 @@ int gm_snapshot_stencil(void* snap, const void* grid, int64_t n, int32_t cell_by
  * cells from `dst`, the others from `snap`.  out, dst, snap: n*n cells, distinct. */
 int gm_writeback_tiles(void* out, const void* dst, const void* snap, int64_t n, int32_t cell_bytes, void* stream);
 
+/* The staged host path in bands (backends.py: a neighbour-sum launch on a host grid
+ * whose src is the grid): gm_snapshot_stencil / gm_writeback_tiles and the tuned step
+ * (stencil v2) restricted to the tiles [t0, t1) of the whole-grid row-major tile order
+ * (gm_tile_order(q, 0); whole block rows), so that one band's write-back (device -> host)
+ * overlaps the next bands' snapshots (host -> device) on another stream.  The snapshot
+ * of band b+1 must be complete before band b is written back or stepped. */
+int gm_snapshot_stencil_range(void* snap, const void* grid, int64_t n, int32_t cell_bytes, uint32_t t0, uint32_t t1,
+                              void* stream);
+int gm_writeback_tiles_range(void* out, const void* dst, const void* snap, int64_t n, int32_t cell_bytes, uint32_t t0,
+                             uint32_t t1, void* stream);
+int gm_run_tiles(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param, int32_t flags,
+                 uint32_t t0, uint32_t t1, void* stream);
+
 /* Synthetic inputs / checks shared with the CPU oracle (oracle/gasket_oracle.c). */
 int gm_fill_hash(void* buf, int64_t n, int32_t cell_bytes, uint64_t seed, int32_t mode, void* stream);
 int gm_checksum(const void* buf, int64_t count, int32_t cell_bytes, uint64_t* out_dev, void* stream);

@@ -133,7 +133,8 @@ def _same_array(a: Any, b: Any) -> bool:
             and a.shape == b.shape and a.strides == b.strides)
 
 
-def _run(grid: Any, src: Any, kind: int, launch, *, mapped_ok: bool, inplace: Optional[Any] = None) -> None:
+def _run(grid: Any, src: Any, kind: int, launch, *, mapped_ok: bool, inplace: Optional[Any] = None,
+         banded: Optional[Any] = None) -> None:
     """Route one launch: device tensors directly, numpy through a host transport.
 
     ``launch(grid_ptr, src_ptr, n, cell_bytes, stream, extra_flags)`` issues the C-ABI call.
@@ -143,7 +144,8 @@ def _run(grid: Any, src: Any, kind: int, launch, *, mapped_ok: bool, inplace: Op
 
     ``inplace(grid)``: the in-place form of a neighbour-sum launch whose src is the grid
     itself (device.run_inplace, the tuned kernel only); otherwise such a launch reads a
-    masked snapshot of the grid (engine.py:201)."""
+    masked snapshot of the grid (engine.py:201).  ``banded(dst, snap, n, c, t0, t1,
+    stream)``: the tuned step over a tile range, for the banded staged host path."""
     device.require_cuda()
     n = device.check_square(grid)
     c = device.cell_bytes_of(grid)
@@ -189,9 +191,30 @@ def _run(grid: Any, src: Any, kind: int, launch, *, mapped_ok: bool, inplace: Op
         snap = device.scratch.get("host_snap", n * n, tdtype).view(n, n)
         dst = device.scratch.get("host_dst", n * n, tdtype).view(n, n)
         with device.MappedHost(grid) as gptr:
-            native.call("gm_snapshot_stencil", snap.data_ptr(), gptr, n, c, stream)
-            launch(dst.data_ptr(), snap.data_ptr(), n, c, stream, native.FLAG_DST_FROM_SRC)
-            native.call("gm_writeback_tiles", gptr, dst.data_ptr(), snap.data_ptr(), n, c, stream)
+            if banded is not None and c in (1, 2, 4):
+                # in bands of block rows: band b's write-back (device -> host) runs on a side
+                # stream next to band b+2's snapshot (host -> device), the two PCIe directions
+                # at once.  Band b+1's snapshot precedes band b's step and write-back: it holds
+                # the rows band b reads below itself and the pre-launch values band b's
+                # write-back would overwrite.
+                bands = device.staged_bands(n, c)
+                main, side = torch.cuda.current_stream(), device.side_stream()
+                side.wait_stream(main)
+                sh = device.stream_handle(side)
+                native.call("gm_snapshot_stencil_range", snap.data_ptr(), gptr, n, c, *bands[0], stream)
+                for b, (t0, t1) in enumerate(bands):
+                    if b + 1 < len(bands):
+                        native.call("gm_snapshot_stencil_range", snap.data_ptr(), gptr, n, c, *bands[b + 1], stream)
+                    banded(dst.data_ptr(), snap.data_ptr(), n, c, t0, t1, stream)
+                    ev = torch.cuda.Event()
+                    ev.record(main)
+                    side.wait_event(ev)
+                    native.call("gm_writeback_tiles_range", gptr, dst.data_ptr(), snap.data_ptr(), n, c, t0, t1, sh)
+                main.wait_stream(side)
+            else:
+                native.call("gm_snapshot_stencil", snap.data_ptr(), gptr, n, c, stream)
+                launch(dst.data_ptr(), snap.data_ptr(), n, c, stream, native.FLAG_DST_FROM_SRC)
+                native.call("gm_writeback_tiles", gptr, dst.data_ptr(), snap.data_ptr(), n, c, stream)
             torch.cuda.current_stream().synchronize()
         return
     if mode == "mapped" and mapped_ok and not (reads_src and _shares_memory(src, grid)):
@@ -284,10 +307,13 @@ def run_block_space(grid, src, rho: int, r_b: int, strategy, local_x: Optional[n
         native.call("gm_run_block_space", gp, sp, n, c, int(rho), int(r_b), tag, tx, ty, ntab, kind, p,
                     int(flags) | extra_flags, stream)
 
-    inplace = None
+    inplace = banded = None
     if tag == STRAT_TUNED and kind in (KERNEL_NEIGHBOR_SUM, KERNEL_NEIGHBOR_SUM8):
         inplace = lambda g: device.run_inplace(g, kind, p)  # noqa: E731
-    _run(grid, src, kind, launch, mapped_ok=(tag == STRAT_TUNED), inplace=inplace)
+
+        def banded(gp, sp, n, c, t0, t1, stream):
+            native.call("gm_run_tiles", gp, sp, n, c, kind, p, int(flags) | native.FLAG_DST_FROM_SRC, t0, t1, stream)
+    _run(grid, src, kind, launch, mapped_ok=(tag == STRAT_TUNED), inplace=inplace, banded=banded)
 
 
 __all__ = [

@@ -306,6 +306,34 @@ int gm_snapshot_stencil(void* snap, const void* grid, int64_t n, int32_t cell_by
     return cuda_rc(e, "masked snapshot");
 }
 
+int gm_snapshot_stencil_range(void* snap, const void* grid, int64_t n, int32_t cell_bytes, uint32_t t0, uint32_t t1,
+                              void* stream) {
+    if (!snap || !grid || snap == grid) return fail(GM_EINVAL, "gm_snapshot_stencil_range needs distinct buffers");
+    if (n < 1 || t1 < t0) return fail(GM_EINVAL, "gm_snapshot_stencil_range: bad edge or range");
+    if (t0 == t1) return GM_OK;
+    const cudaError_t e =
+        gm::launch_snapshot_stencil(snap, grid, n, cell_bytes, reinterpret_cast<cudaStream_t>(stream), t0, t1);
+    if (e == cudaErrorNotSupported || e == cudaErrorInvalidValue) {
+        cudaGetLastError();
+        return fail(GM_EINVAL, "gm_snapshot_stencil_range: unsupported grid or tile range [%u, %u)", t0, t1);
+    }
+    return cuda_rc(e, "masked snapshot (tile range)");
+}
+
+int gm_writeback_tiles_range(void* out, const void* dst, const void* snap, int64_t n, int32_t cell_bytes, uint32_t t0,
+                             uint32_t t1, void* stream) {
+    if (!out || !dst || !snap || out == dst || out == snap) return fail(GM_EINVAL, "gm_writeback_tiles_range: bad buffers");
+    if (n < 1 || t1 < t0) return fail(GM_EINVAL, "gm_writeback_tiles_range: bad edge or range");
+    if (t0 == t1) return GM_OK;
+    const cudaError_t e =
+        gm::launch_writeback_tiles(out, dst, snap, n, cell_bytes, reinterpret_cast<cudaStream_t>(stream), t0, t1);
+    if (e == cudaErrorNotSupported || e == cudaErrorInvalidValue) {
+        cudaGetLastError();
+        return fail(GM_EINVAL, "gm_writeback_tiles_range: unsupported grid or tile range [%u, %u)", t0, t1);
+    }
+    return cuda_rc(e, "tile write-back (tile range)");
+}
+
 int gm_writeback_tiles(void* out, const void* dst, const void* snap, int64_t n, int32_t cell_bytes, void* stream) {
     if (!out || !dst || !snap || out == dst || out == snap) return fail(GM_EINVAL, "gm_writeback_tiles: bad buffers");
     if (n < 1) return fail(GM_EINVAL, "bad edge");
@@ -523,6 +551,25 @@ int gm_run_inplace(void* grid, void* border, int64_t n, int32_t cell_bytes, int3
         return fail(GM_EINVAL, "gm_run_inplace: no tiled kernel for these cells (<= 2^15 tiles per edge)");
     }
     return cuda_rc(e, "in-place neighbour-sum launch");
+}
+
+int gm_run_tiles(void* grid, const void* src, int64_t n, int32_t cell_bytes, int32_t kind, int32_t param, int32_t flags,
+                 uint32_t t0, uint32_t t1, void* stream) {
+    if (kind != GM_KIND_NSUM4 && kind != GM_KIND_NSUM8) return fail(GM_EINVAL, "gm_run_tiles: kind must be NSUM4 or NSUM8");
+    if (!grid || !src || src == grid) return fail(GM_EINVAL, "gm_run_tiles needs distinct grid and src buffers");
+    if (t1 < t0) return fail(GM_EINVAL, "gm_run_tiles: bad tile range");
+    if (t0 == t1) return GM_OK;
+    gm::LaunchArgs a{};
+    if (int rc = ca_args(a, "gm_run_tiles", grid, src, n, cell_bytes, kind, param, -1, 0, 0, nullptr, 0, stream)) return rc;
+    a.flags = flags & ~GM_FLAG_DIGIT_ORDER;  // (tile ranges refer to the row-major order)
+    a.range_lo = t0;
+    a.range_hi = t1;
+    const cudaError_t e = gm::launch_stencil_v2(a);
+    if (e == cudaErrorNotSupported) {
+        cudaGetLastError();
+        return fail(GM_EINVAL, "gm_run_tiles: no tiled kernel for these cells");
+    }
+    return cuda_rc(e, "tuned step (tile range)");
 }
 
 int gm_dev_alloc(int64_t bytes, void** out) {

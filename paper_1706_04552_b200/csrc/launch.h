@@ -46,6 +46,9 @@ struct LaunchArgs {
     // member tile (launch_border_snapshot, edge.cu); the tuned stencil patches its staged
     // window from there.  nullptr = src is a separate pre-launch state.
     const uint8_t* border = nullptr;
+    // an explicit tile range [range_lo, range_hi) of the whole-grid row-major tile order
+    // (contiguous block rows; the banded staged host path) -- used when range_hi > range_lo
+    uint32_t range_lo = 0, range_hi = 0;
 };
 
 // The left neighbour of member tile (bx, by) holds no gasket cell (so its cells never
@@ -69,6 +72,11 @@ inline uint32_t tiles_per_subgasket(const LaunchArgs& a, int r_t) {
 inline void tile_range(const LaunchArgs& a, int r_t, uint32_t& lo, uint32_t& hi) {
     uint32_t all = 1;
     for (int i = 0; i < r_t; ++i) all *= 3u;
+    if (a.range_hi > a.range_lo) {
+        hi = a.range_hi < all ? a.range_hi : all;
+        lo = a.range_lo < hi ? a.range_lo : hi;
+        return;
+    }
     if (a.part_level < 0 || a.part_level > r_t) { lo = 0; hi = all; return; }
     uint32_t per = 1;
     for (int i = 0; i < r_t - a.part_level; ++i) per *= 3u;
@@ -104,8 +112,11 @@ cudaError_t launch_edge_build(const LaunchArgs& a, uint8_t* edge);  // edge.cu
 int64_t edge_cache_bytes(const LaunchArgs& a);                   // edge.cu (0: no tiled kernel)
 int64_t border_bytes(int64_t n, int cell_bytes);                  // edge.cu
 cudaError_t launch_border_snapshot(uint8_t* border, const void* grid, int64_t n, int cell_bytes, cudaStream_t s);
-cudaError_t launch_snapshot_stencil(void* snap, const void* grid, int64_t n, int cell_bytes, cudaStream_t s);
-cudaError_t launch_writeback_tiles(void* out, const void* dst, const void* snap, int64_t n, int cell_bytes, cudaStream_t s);
+// (t0, t1): a tile range of the whole-grid row-major order; t1 == 0: every member tile
+cudaError_t launch_snapshot_stencil(void* snap, const void* grid, int64_t n, int cell_bytes, cudaStream_t s,
+                                    uint32_t t0 = 0, uint32_t t1 = 0);
+cudaError_t launch_writeback_tiles(void* out, const void* dst, const void* snap, int64_t n, int cell_bytes, cudaStream_t s,
+                                   uint32_t t0 = 0, uint32_t t1 = 0);
 cudaError_t launch_host_rows_copyback(void* out, const void* dst, const void* snap, int64_t n, int cell_bytes,
                                       cudaStream_t s);
 // member tiles of a level-q gasket, row-major inside each level-L sub-gasket (stencil2.cu)

@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(256) writeback_tiles(uint8_t* __restrict__ out
 }  // namespace
 
 cudaError_t launch_writeback_tiles(void* out, const void* dst, const void* snap, int64_t n, int cell_bytes,
-                                   cudaStream_t s) {
+                                   cudaStream_t s, uint32_t t0, uint32_t t1) {
     if (cell_bytes != 1 && cell_bytes != 2 && cell_bytes != 4 && cell_bytes != 8) return cudaErrorNotSupported;
     const int64_t tt = 128 / cell_bytes;
     if (n < tt || (n & (n - 1)) != 0) return cudaErrorNotSupported;
@@ -165,6 +165,11 @@ cudaError_t launch_writeback_tiles(void* out, const void* dst, const void* snap,
     if (order == nullptr) return cudaErrorNotSupported;
     uint32_t ntiles = 1;
     for (int i = 0; i < r_t; ++i) ntiles *= 3u;
+    if (t1 > 0) {  // a range of the row-major order
+        if (t1 > ntiles || t0 >= t1) return t0 == t1 ? cudaSuccess : cudaErrorInvalidValue;
+        order += t0;
+        ntiles = t1 - t0;
+    }
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -180,7 +185,8 @@ cudaError_t launch_writeback_tiles(void* out, const void* dst, const void* snap,
 
 // cudaErrorNotSupported: cell widths other than 1/2/4/8, grids narrower than a tile or
 // with more than 2^15 tiles per edge (the caller then copies the whole grid).
-cudaError_t launch_snapshot_stencil(void* snap, const void* grid, int64_t n, int cell_bytes, cudaStream_t s) {
+cudaError_t launch_snapshot_stencil(void* snap, const void* grid, int64_t n, int cell_bytes, cudaStream_t s,
+                                    uint32_t t0, uint32_t t1) {
     if (cell_bytes != 1 && cell_bytes != 2 && cell_bytes != 4 && cell_bytes != 8) return cudaErrorNotSupported;
     const int64_t tt = 128 / cell_bytes;
     if (n < tt || (n & (n - 1)) != 0) return cudaErrorNotSupported;
@@ -190,6 +196,11 @@ cudaError_t launch_snapshot_stencil(void* snap, const void* grid, int64_t n, int
     if (order == nullptr) return cudaErrorNotSupported;
     uint32_t ntiles = 1;
     for (int i = 0; i < r_t; ++i) ntiles *= 3u;
+    if (t1 > 0) {  // a range of the row-major order
+        if (t1 > ntiles || t0 >= t1) return t0 == t1 ? cudaSuccess : cudaErrorInvalidValue;
+        order += t0;
+        ntiles = t1 - t0;
+    }
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

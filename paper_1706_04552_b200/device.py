@@ -58,6 +58,34 @@ def stream_handle(stream: torch.cuda.Stream | None = None) -> int:
     return int(s.cuda_stream)
 
 
+_SIDE_STREAMS: dict = {}
+
+
+def side_stream(dev: torch.device | None = None) -> torch.cuda.Stream:
+    """A second stream per device (the write-backs of the banded staged host path)."""
+    d = torch.cuda.current_device() if dev is None else torch.device(dev).index
+    st = _SIDE_STREAMS.get(d)
+    if st is None:
+        st = _SIDE_STREAMS[d] = torch.cuda.Stream(device=d)
+    return st
+
+
+def staged_bands(n: int, c: int, nbands: int = 8) -> list[tuple[int, int]]:
+    """Tile ranges [t0, t1) of the whole-grid row-major tile order (gm_tile_order(q, 0))
+    that split the member tiles into about `nbands` bands of whole block rows with about
+    equal tile counts (block row Y holds 2^popcount(Y) member tiles)."""
+    tt = 128 // c
+    q = (n // tt).bit_length() - 1
+    ys = np.arange(1 << q, dtype=np.int64)
+    pc = np.zeros_like(ys)
+    for b in range(q):
+        pc += (ys >> b) & 1
+    cum = np.concatenate([[0], np.cumsum(1 << pc)])  # tiles before block row Y
+    total = int(cum[-1])
+    edges = sorted({int(cum[np.searchsorted(cum, total * k // nbands)]) for k in range(nbands + 1)} | {0, total})
+    return [(a, b) for a, b in zip(edges[:-1], edges[1:]) if b > a]
+
+
 def is_device(a: Any) -> bool:
     return isinstance(a, torch.Tensor) and a.is_cuda
 

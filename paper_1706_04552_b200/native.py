@@ -102,6 +102,9 @@ _SIGS = {
     "gm_ca_run": [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _i32, _vp],
     "gm_border_bytes": [_i64, _i32, ctypes.POINTER(ctypes.c_int64)],
     "gm_coverage_check": [_vp, _i64, _vp, _vp, _vp, _i64, _vp],
+    "gm_snapshot_stencil_range": [_vp, _vp, _i64, _i32, ctypes.c_uint32, ctypes.c_uint32, _vp],
+    "gm_writeback_tiles_range": [_vp, _vp, _vp, _i64, _i32, ctypes.c_uint32, ctypes.c_uint32, _vp],
+    "gm_run_tiles": [_vp, _vp, _i64, _i32, _i32, _i32, _i32, ctypes.c_uint32, ctypes.c_uint32, _vp],
     "gm_run_inplace": [_vp, _vp, _i64, _i32, _i32, _i32, _vp],
 }
 

@@ -668,7 +668,8 @@ def test_engine_launch_neighbour_sum_uses_masked_snapshot(gpu, oracle):
 @pytest.mark.parametrize("pinned", [True, False])
 def test_mapped_staged_neighbour_sum(gpu, oracle, monkeypatch, dtype, pinned):
     """Host-mapped numpy grid, src is the grid (engine.launch semantics): the staged path
-    (masked snapshot -> device kernel -> whole-line write-back, gm_writeback_tiles) ==
+    (masked snapshot -> device kernel -> whole-line write-back, gm_writeback_tiles; for
+    1/2/4-byte cells in bands of block rows on two streams) ==
     the oracle's step, cell for cell, off-gasket cells untouched.  Pinned (torch
     pin_memory) and pageable (plain numpy, registered once by the pin cache) grids;
     int64 covers the grids whose stencil kernel does not store whole sectors (16 <= n <
@@ -676,7 +677,10 @@ def test_mapped_staged_neighbour_sum(gpu, oracle, monkeypatch, dtype, pinned):
     monkeypatch.setenv("GASKET_HOST_TRANSPORT", "mapped")
     S = gpu.geometry.IntraStrategy
     c = np.dtype(dtype).itemsize
-    for n in sorted({128 // c, 2 * (128 // c), 4 * (128 // c), 1 << 12}):
+    sizes = {128 // c, 2 * (128 // c), 4 * (128 // c), 1 << 12}
+    if c == 1:
+        sizes.add(1 << 14)  # (the banded path: 8 bands of whole block rows, 2 streams)
+    for n in sorted(sizes):
         for kind in (1, 2):
             grid0 = oracle.fill_hash(n, dtype, 23 + kind, 0)
             want = grid0.copy()
