@@ -172,9 +172,13 @@ int gm_bijection_check(const int64_t* cx, const int64_t* cy, int64_t nblocks, in
 
 /* The pre-launch snapshot of a neighbour-sum launch (engine.py:201's grid.copy()),
  * masked: copies into `snap` (n*n cells, distinct from grid) only what a one-step
- * stencil over the gasket reads -- each member 128-byte tile's rows -1..TT and one
- * 32-byte sector either side -- at the same positions; other cells of snap are left
- * as they are.  Async on `stream`.  GM_EINVAL for other cell widths, edges that are
+ * stencil over the gasket reads -- each member 128-byte tile's rows -1..TT, the 32-byte
+ * sector left of them, and the sector right of rows TT-2..TT (only tile column TT-1's
+ * gasket cell, at row TT-1, reads further right) -- at the same positions; other cells
+ * of snap are left as they are.  A grid off a 64-byte boundary (a host numpy array, read over PCIe in
+ * host-aligned 64-byte units) gets, per window row, the units covering bytes [-16, 144)
+ * of the tile's line instead: what the tuned stencil and gm_writeback_tiles read (the
+ * staged host path's kernels).  Async on `stream`.  GM_EINVAL for other cell widths, edges that are
  * not a power of two >= 128/cell_bytes, or more than 2^15 tiles per edge. */
 int gm_snapshot_stencil(void* snap, const void* grid, int64_t n, int32_t cell_bytes, void* stream);
 /* The write-back of a staged neighbour-sum launch (host-mapped grids): writes every

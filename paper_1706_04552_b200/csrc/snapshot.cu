@@ -39,20 +39,24 @@ __device__ __forceinline__ uint4 ld16(const uint8_t* p, bool half) {
 constexpr int UNROLL = 8;
 
 // s64 != 0 (a host grid that starts s64 bytes past a 64-byte boundary, e.g. a plain numpy
-// array): each window row is widened to the host-aligned 64-byte units that cover it
-// (PCIe reads whole units; 16 pieces per row instead of 12), so that the write-back can
-// store whole host units too; pieces outside the array are skipped.
+// array): each window row is the three host-aligned 64-byte units covering [-16, 144)
+// (PCIe reads whole units), so that the write-back can store whole host units too; pieces
+// outside the array are skipped.
 __global__ void __launch_bounds__(256) snapshot_tiles(uint8_t* __restrict__ snap, const uint8_t* __restrict__ grid,
                                                       int64_t n, int cell_bytes, const uint32_t* __restrict__ order,
                                                       uint32_t ntiles, uint32_t nb, int s64) {
     const int64_t rowbytes = n * cell_bytes;
     const int64_t total = rowbytes * n;
     const int tt = 128 / cell_bytes;  // tile rows (and cells per row)
-    const int vpr = s64 ? 16 : VEC_PER_ROW;  // pieces per window row
+    // pieces per window row and the first one relative to the tile's line: 64-byte aligned
+    // grids take one 32-byte sector either side (what every stencil kernel may read); host
+    // grids off a 64-byte boundary take the three host units (boundaries at grid offsets g
+    // with (g + s64) % 64 == 0) covering bytes [-16, 144): the tuned stencil's halo chunks
+    // and every byte the write-back of the tile's line stores (the staged path is the tuned
+    // kernel's only) -- one unit per row fewer than covering the 32-byte sectors
+    const int vpr = s64 ? 12 : VEC_PER_ROW;
     const int per_tile = (tt + 2) * vpr;
-    // first piece of a window row relative to the tile's line: -32 aligned, else the host
-    // unit holding byte -32 (unit boundaries at grid offsets g with (g + s64) % 64 == 0)
-    const int64_t lead = s64 ? 32 + ((s64 - 32) & 63) : 32;
+    const int64_t lead = s64 ? 16 + ((s64 - 16) & 63) : 32;
     const int lane = threadIdx.x & 31;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -77,8 +81,19 @@ __global__ void __launch_bounds__(256) snapshot_tiles(uint8_t* __restrict__ snap
                 const int row = i / vpr, q = i - row * vpr;
                 const int64_t y = y0 + row, xb = xb0 + q * 16;
                 const bool lpart = xb < line0, rpart = xb >= line0 + 128;
-                bool skip = i >= per_tile || (row == 0 && up) || (row == tt + 1 && down) || (lpart && left) ||
-                            (rpart && right) || y < 0 || y >= n;
+                // host units (s64 != 0): on the tile's own rows the unit shared with the right
+                // neighbour's window (its first unit is this window's last) is read whole by
+                // that neighbour when it is a member tile (it copies its own rows whole), and
+                // this window's first unit whole by this tile; rows -1 and TT, copied here only
+                // when the tile above / below is not a member, keep all three units
+                const bool shared_right = s64 != 0 && q >= 8 && row >= 1 && row <= tt;
+                // (64-byte aligned grids: the right sector is read by the gasket cells of tile
+                // column TT-1 only, i.e. on window rows tt-1 .. tt+1; its host unit is the
+                // right neighbour's, so on the other rows it is not fetched at all)
+                bool skip = i >= per_tile || (row == 0 && up) || (row == tt + 1 && down) ||
+                            (s64 == 0 ? ((lpart && left) || (rpart && (right || row < tt - 1)))
+                                      : (shared_right && right)) ||
+                            y < 0 || y >= n;
                 if (s64 == 0) {
                     skip = skip || xb < 0 || xb >= rowbytes;
                 } else {  // host units may run into the neighbouring rows: only the array's bytes
@@ -134,7 +149,11 @@ __global__ void __launch_bounds__(256) writeback_tiles(uint8_t* __restrict__ out
                 } else {
                     const int row = i / vpr, q = i - row * vpr;
                     const int64_t f = (y0 + row) * rowbytes + xb0 - s64 + q * 16;
-                    off[k] = (i < per_tile && f >= 0 && f < total) ? f : -1;
+                    // the last unit is also the right neighbour's first: a member neighbour
+                    // stores it (whole, with this line's bytes from dst / snap by the same rule)
+                    const bool shared = q >= 8 && (int64_t)((v & 0xffffu) + 1) * 128 < rowbytes &
+                                                      (((v & 0xffffu) + 1) & ~(v >> 16)) == 0;
+                    off[k] = (i < per_tile && f >= 0 && f < total && !shared) ? f : -1;
                     if (off[k] >= 0) {
                         // the piece's own row, line and sector decide where its bytes come from
                         const int64_t yy = f / rowbytes, col = f - yy * rowbytes;
