@@ -508,26 +508,41 @@ def _zero_background(r: int, tdt, flusher, steps: int = 20) -> dict:
             "bytes": alg, "note": "off-gasket cells must be 0 (opt-in); no DRAM reads"}
 
 
-def _staged_bytes(r: int, c: int) -> tuple[int, int]:
-    """Host bytes of the staged mapped stencil (gm_snapshot_stencil + gm_writeback_tiles):
-    each member tile's rows -1..TT (128-byte line + a 32-byte sector either side, halos a
-    neighbouring member tile covers skipped, grid edges clipped) read, its own TT lines
-    written back."""
+def _staged_bytes(r: int, c: int, s64: int) -> tuple[int, int]:
+    """Host bytes of the staged mapped stencil (gm_snapshot_stencil + gm_writeback_tiles),
+    in the 64-byte units PCIe moves.  Per member tile: its TT rows, plus rows -1 / TT when
+    the tile above / below is not a member.  s64 == 0 (64-byte aligned grid): the line, the
+    unit left of it unless the left tile is a member, the unit right of it on rows TT-2..TT
+    unless the right tile is a member; written back: the TT lines.  s64 != 0 (a numpy grid
+    off a 64-byte boundary): the three host units covering [-16, 144) of each row, less the
+    last on the tile's own rows when the right tile is a member (it reads / writes that
+    unit); written back: the same units of the TT rows."""
     tt = 128 // c
     nb = (1 << r) // tt
-    h2d = ntiles = 0
+    h2d = d2h = 0
+
+    def member(x, y):
+        return 0 <= x < nb and 0 <= y < nb and (x & ~y) == 0
+
     for Y in range(nb):
         X = Y
         while True:  # subsets of Y
-            member = lambda x, y: 0 <= x < nb and 0 <= y < nb and (x & ~y) == 0  # noqa: E731
-            rows = tt + (0 if (Y == 0 or member(X, Y - 1)) else 1) + (0 if (Y == nb - 1 or member(X, Y + 1)) else 1)
-            per_row = 128 + (0 if (X == 0 or member(X - 1, Y)) else 32) + (0 if (X == nb - 1 or member(X + 1, Y)) else 32)
-            h2d += rows * per_row
-            ntiles += 1
+            lm, rm = member(X - 1, Y) or X == 0, member(X + 1, Y) or X == nb - 1
+            extra = int(Y > 0 and not member(X, Y - 1)) + int(Y < nb - 1 and not member(X, Y + 1))
+            if s64 == 0:
+                side = 0 if lm else 64
+                h2d += tt * (128 + side) + (0 if rm else 2 * 64)
+                h2d += int(Y > 0 and not member(X, Y - 1)) * (128 + side)
+                h2d += int(Y < nb - 1 and not member(X, Y + 1)) * (128 + side + (0 if rm else 64))
+                d2h += tt * 128
+            else:
+                own = 128 if (member(X + 1, Y)) else 192
+                h2d += tt * own + extra * 192
+                d2h += tt * own
             if X == 0:
                 break
             X = (X - 1) & Y
-    return h2d, ntiles * tt * 128
+    return h2d, d2h
 
 
 def _e2e(workload: str, rho: int, steps: int, transports: tuple = ("mapped", "mapped-pinned", "copy")) -> dict:
@@ -577,12 +592,14 @@ def _e2e(workload: str, rho: int, steps: int, transports: tuple = ("mapped", "ma
             # schedule): the 64-byte halves holding gasket cells are read (unless all their
             # cells are gasket cells) and written back whole.  Stencils: the staged windows.
             if kind == 0:
+                # (64-byte halves of the grid; on a numpy grid 16 bytes off a 64-byte boundary
+                # the kernel moves the host units covering them instead -- about as many)
                 kh = (64 // c).bit_length() - 1
                 halves = (1 << kh) * 3 ** (r - kh)
                 full = 3 ** (r - kh)  # halves made only of gasket cells need no read
                 h2d, d2h = (halves - full) * 64, halves * 64
             else:
-                h2d, d2h = _staged_bytes(r, c)
+                h2d, d2h = _staged_bytes(r, c, 0 if transport == "mapped-pinned" else 16)
         else:
             h2d = n * n * c
             d2h = n * n * c
