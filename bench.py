@@ -488,7 +488,9 @@ def _zero_background(r: int, tdt, flusher, steps: int = 20) -> dict:
     peak, _ = _peaks()
     alg = R.write_bytes(r, c)
     out = {}
-    for name, flags in (("grid rows (default)", 0), ("lambda tiles", native.FLAG_DIGIT_ORDER),
+    # the default schedule: grid rows for 1- and 2-byte cells, the address sweep for wider ones
+    for name, flags in (("default (grid rows for 1-2-byte cells, address sweep for 4-8)", 0),
+                        ("grid rows", native.FLAG_GRID_ROWS), ("lambda tiles", native.FLAG_DIGIT_ORDER),
                         ("address sweep", native.FLAG_WRITE_SWEEP)):
         def step():
             backends.run_block_space(grid, grid, 32, r - 5, IntraStrategy.TUNED, kind=0, param=1, flags=flags,

@@ -548,8 +548,10 @@ cudaError_t launch_c(const LaunchArgs& a, int q) {
     using G = WGeo<C>;
     // zero background: the grid-row schedule unless lambda tiles (GM_FLAG_DIGIT_ORDER), row-major
     // tiles or the address sweep are asked for (n=2^16 int8: 55.7 us vs 62-64 us for lambda tiles)
-    const bool rows = (a.flags & GM_FLAG_GRID_ROWS) ||
-                      (ZERO && !(a.flags & (GM_FLAG_DIGIT_ORDER | GM_FLAG_ROWMAJOR | GM_FLAG_WRITE_SWEEP)));
+    // (4- and 8-byte cells: the address sweep, 140 vs 154 us back to back at n=2^16 int32)
+    const bool zero_default = ZERO && !(a.flags & (GM_FLAG_DIGIT_ORDER | GM_FLAG_ROWMAJOR | GM_FLAG_WRITE_SWEEP |
+                                                   GM_FLAG_GRID_ROWS));
+    const bool rows = (a.flags & GM_FLAG_GRID_ROWS) || (zero_default && (C < 4 || q > 13));
     if (rows && a.part_level < 0) {
         // 8 CTAs of 256 threads per SM (the row walk wants many rows in flight)
         const uint64_t blocks = std::min<uint64_t>((uint64_t)sm_count() * rows_ctas_per_sm(), ((uint64_t)a.n * 32 + 255) / 256);
@@ -567,7 +569,7 @@ cudaError_t launch_c(const LaunchArgs& a, int q) {
         note_launch();
         return cudaGetLastError();
     }
-    if ((a.flags & GM_FLAG_WRITE_SWEEP) && a.part_level < 0 && !COUNT && q <= 13) {
+    if (((a.flags & GM_FLAG_WRITE_SWEEP) || (zero_default && C >= 4)) && a.part_level < 0 && !COUNT && q <= 13) {
         const uint32_t* pre = sweep_prefix(q, G::TT);
         if (!pre) return cudaErrorMemoryAllocation;
         const unsigned blocks = (unsigned)sm_count() * (unsigned)rows_ctas_per_sm();
