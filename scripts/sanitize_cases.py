@@ -4,8 +4,8 @@ racecheck, synccheck):  compute-sanitizer --tool T python scripts/sanitize_cases
 
   (default)  write pass (every schedule, both store modes), paper-literal lambda / BB
              (incl. the vectorised BB), stencil v2 (NSUM4/8, 1/2/4-byte cells, whole-sector
-             blend), the CA step with the static edge cache, the fused CA kernel (T = 2, 4, 6),
-             the masked snapshot + staged
+             blend), the in-place launch, the CA step with the static edge cache, the fused CA
+             kernel (T = 2, 4, 6), the banded masked snapshot + staged
              host write-back, lambda maps, coverage
   part       the partitioned CA with the peer-memory halo fused into the step kernel, two
              processes on the one GPU (CUDA IPC)
@@ -69,6 +69,10 @@ def main_cases():
                 g = torch.from_numpy(src.copy()).cuda()
                 backends.run_block_space(g, torch.from_numpy(src).cuda(), 64, 3, S.TUNED, kind=kind, param=3, flags=fl)
                 bad += not np.array_equal(g.cpu().numpy(), want)
+            # the in-place launch (src is the grid: border snapshot + patched staging windows)
+            g_ip = torch.from_numpy(src.copy()).cuda()
+            backends.run_block_space(g_ip, g_ip, 64, 3, S.TUNED, kind=kind, param=3)
+            bad += not np.array_equal(g_ip.cpu().numpy(), want)
             # the CA step with the static left-edge cache (edge.cu: build + 2-deep staging ring)
             s_d = torch.from_numpy(src.copy()).cuda()
             c = s_d.element_size()
