@@ -166,3 +166,25 @@ def test_launch_config_validation():
 
     with pytest.raises(ValueError, match="block-space launches need an intra-block strategy"):
         engine.LaunchConfig(spec=G.FractalSpec(8, 2), mapping=engine.Mapping.BLOCK_SPACE)
+
+
+def test_staged_bands_cover_whole_block_rows():
+    """The banded staged host path's tile ranges (device.staged_bands): consecutive, covering
+    every member tile of the row-major order exactly once, each a run of whole block rows
+    (block row Y holds 2^popcount(Y) tiles), about equal in size."""
+    import numpy as np
+
+    from paper_1706_04552_b200 import device, native
+
+    for n, c in ((128, 1), (256, 1), (1 << 12, 1), (1 << 12, 2), (1 << 11, 4), (1 << 17, 1)):
+        q = (n // (128 // c)).bit_length() - 1
+        bands = device.staged_bands(n, c)
+        assert bands[0][0] == 0 and bands[-1][1] == 3**q
+        assert all(a[1] == b[0] for a, b in zip(bands, bands[1:]))
+        starts = set(np.concatenate([[0], np.cumsum([1 << bin(y).count("1") for y in range(1 << q)])]).tolist())
+        assert all(t0 in starts and t1 in starts for t0, t1 in bands)
+        if q >= 5:
+            _, by = native.tile_order(q, 0)
+            assert np.all(np.diff(by) >= 0)  # the row-major order: block rows ascending
+            sizes = [t1 - t0 for t0, t1 in bands]
+            assert len(bands) >= 4 and max(sizes) <= 2 * 3**q / len(bands)
