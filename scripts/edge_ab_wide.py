@@ -1,7 +1,6 @@
 #!/usr/bin/env python
 """CA step with the static left-edge cache on 2- and 4-byte cells: the default staging ring
 (4 deep) vs the 2-deep one (GM_FLAG_STAGES2), and no cache.  python scripts/edge_ab_wide.py"""
-import statistics
 import sys
 from pathlib import Path
 
