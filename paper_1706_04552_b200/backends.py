@@ -254,15 +254,14 @@ def run_bounding_box(grid, src, rho: int, kind: int, param: int, backend: str = 
     """backends.py:225-231: identity map over n_b x n_b blocks of rho x rho threads,
     each thread testing x & (n-1-y) (``early_exit``: whole tiles off the gasket exit first).
 
-    ``vectorized`` (write pass only): the bounding box written like the tuned lambda
-    kernels -- one lane per 16-byte segment of all n x n cells, the same membership test
-    and the same vectorised stores -- the competent BB baseline of the lambda-vs-BB
-    speed-up (rho does not shape this launch)."""
+    ``vectorized``: the bounding box written like the tuned lambda kernels, the competent
+    BB baseline of the lambda-vs-BB speed-up (rho does not shape this launch) -- the write
+    pass as one lane per 16-byte segment of all n x n cells with the tuned kernels' stores,
+    neighbour sums as the tuned tile stencil over every tile of the grid, tiles off the
+    gasket exiting after one membership test."""
     resolve_backend(backend)
     p = _param32(param)
     kind = int(kind)
-    if vectorized and kind != KERNEL_CONST:
-        raise ValueError("the vectorised bounding box runs the write pass (KERNEL_CONST) only")
     variant = 2 if vectorized else (1 if early_exit else 0)
 
     def launch(gp, sp, n, c, stream, extra_flags):

@@ -176,8 +176,8 @@ int gm_run_bounding_box(void* grid, const void* src, int64_t n, int32_t cell_byt
     gm_cfg_t c{};
     c.n = n;
     c.rho = rho;
-    if (early_exit == 2 && kind != GM_KIND_CONST)
-        return fail(GM_EINVAL, "the vectorised bounding box runs the write pass (kind %d) only", GM_KIND_CONST);
+    if (early_exit == 2 && kind == GM_KIND_COUNT)
+        return fail(GM_EINVAL, "the vectorised bounding box has no coverage-counting form");
     c.mapping = early_exit == 2 ? GM_MAP_BB_VEC : early_exit ? GM_MAP_BB_EXIT : GM_MAP_BB;
     c.strategy = GM_STRAT_SUBBOX;
     c.kind = kind;

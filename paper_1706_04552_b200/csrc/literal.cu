@@ -176,8 +176,11 @@ template <int C>
 static cudaError_t launch_lambda_c(const LaunchArgs& a) { GM_DISPATCH_KIND(launch_lambda_t, C, a) }
 
 cudaError_t launch_literal(const LaunchArgs& a) {
-    if (a.mapping == MAP_BB_VEC) {  // grids under one 16-byte segment per row: the literal bounding box
-        const cudaError_t e = launch_bb_vector(a);
+    if (a.mapping == MAP_BB_VEC) {
+        // the bounding box written like the tuned kernels: the write pass over 16-byte segments
+        // (write.cu), neighbour sums as the tuned tile stencil over every tile of the grid
+        // (stencil2.cu); grids those do not cover take the literal bounding box
+        const cudaError_t e = (a.kind == KIND_NSUM4 || a.kind == KIND_NSUM8) ? launch_stencil_v2(a) : launch_bb_vector(a);
         if (e != cudaErrorNotSupported) return e;
         cudaGetLastError();
     }

@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
                                                              uint64_t wait_epoch, uint64_t signal_epoch,
                                                              const int64_t* __restrict__ sg_off, int64_t pitch,
                                                              uint32_t per, const uint8_t* __restrict__ edge,
-                                                             const uint8_t* __restrict__ border) {
+                                                             const uint8_t* __restrict__ border, int bb_lg) {
     using S = T2<C>;
     peer_prologue_wait(epi, wait_epoch);  // partitioned CA with the fused exchange only
     constexpr bool EIGHT = KIND == KIND_NSUM8;
@@ -202,8 +202,13 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
     // table `order` = member tiles row-major within each level-L sub-gasket, so that
     // concurrently running CTAs stage horizontally adjacent tiles (same DRAM pages)
     const bool chunked = (flags & GM_FLAG_CHUNKED) != 0;
+    // bb_lg >= 0: the bounding box at tile granularity (GM_MAP_BB_VEC) -- tile index i covers
+    // every tile of the 2^bb_lg x 2^bb_lg tile grid, and tiles off the gasket exit
     auto tile_xy = [&](uint32_t tile, uint32_t& bx, uint32_t& by) {
-        if (order == nullptr) {
+        if (bb_lg >= 0) {
+            bx = tile & ((1u << bb_lg) - 1u);
+            by = tile >> bb_lg;
+        } else if (order == nullptr) {
             lambda_digit_order(tile, tab, bx, by);
         } else {
             const uint32_t v = __ldg(order + tile);
@@ -230,8 +235,9 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
     auto stage = [&](uint32_t idx, uint32_t v) {  // stage this CTA's tile #idx into ring slot idx % NST
         if (idx >= count || probe_noload) return;
         uint32_t bx, by;
-        if (order == nullptr) {
-            lambda_digit_order(first + idx * step, tab, bx, by);
+        if (bb_lg >= 0 || order == nullptr) {
+            tile_xy(first + idx * step, bx, by);
+            if (bb_lg >= 0 && (bx & ~by) != 0) return;  // (bounding box: a tile off the gasket)
         } else {
             bx = v & 0xffffu;
             by = v >> 16;
@@ -318,9 +324,9 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
             }
             __syncthreads();
         }
-        if (active) {
-            uint32_t bx, by;
-            tile_xy(first + idx * step, bx, by);
+        uint32_t bx, by;
+        tile_xy(first + idx * step, bx, by);
+        if (active && (bb_lg < 0 || (bx & ~by) == 0)) {
             const int64_t x0 = (int64_t)bx * S::TT, y0 = (int64_t)by * S::TT;
             const uint8_t* b = smem + (idx % NST) * S::BUF;
             const uint32_t* up = reinterpret_cast<const uint32_t*>(b + t * PITCH);  // staged row t = tile row t-1
@@ -372,6 +378,11 @@ cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
     using S = T2<C>;
     uint32_t lo, hi;
     tile_range(a, r_t, lo, hi);
+    const int bb_lg = a.mapping == MAP_BB_VEC ? r_t : -1;  // bounding box: every tile of the grid
+    if (bb_lg >= 0) {
+        lo = 0;
+        hi = 1u << (2 * r_t);
+    }
     if (hi == lo) return cudaSuccess;
     const uint32_t ntiles = hi - lo;
     const size_t smem = (size_t)NST * S::BUF + (NST == 2 ? 8 : 4) * S::ROWS * CHUNKS;
@@ -385,13 +396,14 @@ cudaError_t launch_ck(const LaunchArgs& a, int r_t) {
     if (blocks > ntiles) blocks = ntiles;
     if (getenv("GASKET_DEBUG_OCC")) fprintf(stderr, "stencil_v2<C=%d,K=%d,NST=%d>: %d CTAs/SM, smem %zu\n", C, KIND, NST, per_sm, smem);
     const uint32_t* order = nullptr;
-    if (!(a.flags & GM_FLAG_DIGIT_ORDER)) order = rowmajor_table(r_t, order_level(a, r_t));
+    if (!(a.flags & GM_FLAG_DIGIT_ORDER) && bb_lg < 0) order = rowmajor_table(r_t, order_level(a, r_t));
     kern<<<(unsigned)blocks, S::THREADS, smem, a.stream>>>(reinterpret_cast<uint8_t*>(a.grid),
                                                           reinterpret_cast<const uint8_t*>(a.src), a.n, lo, hi, r_t,
                                                           a.part_level, a.param, a.flags, order,
                                                           reinterpret_cast<PeerEpilogue*>(a.peer_epi), a.wait_epoch,
                                                           a.signal_epoch, a.sg_off, row_pitch(a),
-                                                          tiles_per_subgasket(a, r_t), a.edge, a.border);
+                                                          tiles_per_subgasket(a, r_t), bb_lg < 0 ? a.edge : nullptr,
+                                                          bb_lg < 0 ? a.border : nullptr, bb_lg);
     note_launch();
     return cudaGetLastError();
 }

@@ -37,7 +37,7 @@ class Mapping(enum.Enum):
     BOUNDING_BOX = "bb"
     BLOCK_SPACE = "blockspace"
     BOUNDING_BOX_EXIT = "bb-exit"  # BB whose off-gasket tiles exit before any per-thread test
-    BOUNDING_BOX_VEC = "bb-vec"  # BB over 16-byte segments with the tuned kernels' stores (write pass)
+    BOUNDING_BOX_VEC = "bb-vec"  # BB written like the tuned kernels (16-byte segments / every tile of the grid)
 
 
 class KernelKind(enum.Enum):

@@ -455,6 +455,29 @@ def test_engine_launch_device_inplace_int32(gpu, oracle):
         assert np.array_equal(g.cpu().numpy(), want), strat
 
 
+@pytest.mark.parametrize("dtype", [np.int8, np.int16, np.int32, np.int64])
+def test_vectorised_bounding_box_neighbour_sums(gpu, oracle, dtype):
+    """run_bounding_box(vectorized=True) for neighbour sums -- the tuned tile stencil over
+    every tile of the grid, tiles off the gasket exiting (8-byte cells and narrow grids: the
+    literal bounding box) -- == the oracle, with the drop-in semantics (grid keeps its
+    off-gasket cells) and on src aliasing grid."""
+    be = gpu.backends
+    c = np.dtype(dtype).itemsize
+    for n in sorted({16, 128 // c, 4 * (128 // c), 1 << 11}):
+        grid0 = oracle.fill_hash(n, dtype, 71, 0)
+        src = oracle.fill_hash(n, dtype, 72, 0)
+        for kind in (1, 2):
+            want = _oracle_result(oracle, grid0, src, 8, kind, -2)
+            g = _to_dev(grid0)
+            be.run_bounding_box(g, _to_dev(src), min(32, n), kind, -2, vectorized=True)
+            assert np.array_equal(g.cpu().numpy(), want), (np.dtype(dtype).name, n, kind)
+            # src is the grid: engine.launch semantics (the snapshot path)
+            want_a = _oracle_result(oracle, grid0, grid0, 8, kind, -2)
+            g = _to_dev(grid0)
+            be.run_bounding_box(g, g, min(32, n), kind, -2, vectorized=True)
+            assert np.array_equal(g.cpu().numpy(), want_a), (np.dtype(dtype).name, n, kind, "alias")
+
+
 def test_ca_run_rejects_bad_arguments(gpu):
     from paper_1706_04552_b200 import device, native
 
