@@ -324,9 +324,10 @@ __global__ void __launch_bounds__(T2<C>::THREADS) stencil_v2(uint8_t* __restrict
             }
             __syncthreads();
         }
-        uint32_t bx, by;
-        tile_xy(first + idx * step, bx, by);
-        if (active && (bb_lg < 0 || (bx & ~by) == 0)) {
+        if (active) {
+            uint32_t bx, by;
+            tile_xy(first + idx * step, bx, by);
+            if (bb_lg >= 0 && (bx & ~by) != 0) continue;  // (bounding box: a tile off the gasket)
             const int64_t x0 = (int64_t)bx * S::TT, y0 = (int64_t)by * S::TT;
             const uint8_t* b = smem + (idx % NST) * S::BUF;
             const uint32_t* up = reinterpret_cast<const uint32_t*>(b + t * PITCH);  // staged row t = tile row t-1
