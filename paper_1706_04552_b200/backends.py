@@ -188,8 +188,9 @@ def _run(grid: Any, src: Any, kind: int, launch, *, mapped_ok: bool, inplace: Op
         # run the tuned kernel there, write the tiles' own lines back whole -- the host
         # sees whole-line traffic for the dilated gasket instead of 16-byte pieces
         tdtype = device._torch_dtype(grid.dtype)
-        snap = device.scratch.get("host_snap", n * n, tdtype).view(n, n)
-        dst = device.scratch.get("host_dst", n * n, tdtype).view(n, n)
+        # (scratch per stream: host calls made from several threads on their own streams)
+        snap = device.scratch.get(f"host_snap:{stream}", n * n, tdtype).view(n, n)
+        dst = device.scratch.get(f"host_dst:{stream}", n * n, tdtype).view(n, n)
         with device.MappedHost(grid) as gptr:
             if banded is not None and c in (1, 2, 4):
                 # in bands of block rows: band b's write-back (device -> host) runs on a side
@@ -229,7 +230,7 @@ def _run(grid: Any, src: Any, kind: int, launch, *, mapped_ok: bool, inplace: Op
         return
 
     tdtype = device._torch_dtype(grid.dtype)
-    dev_grid = device.scratch.get("host_grid", n * n, tdtype).view(n, n)
+    dev_grid = device.scratch.get(f"host_grid:{stream}", n * n, tdtype).view(n, n)
     host_grid = torch.from_numpy(grid)
     dev_grid.copy_(host_grid, non_blocking=True)
     src_ptr = 0
@@ -237,7 +238,7 @@ def _run(grid: Any, src: Any, kind: int, launch, *, mapped_ok: bool, inplace: Op
         if _shares_memory(src, grid):
             dev_src = device.stencil_snapshot(dev_grid)
         else:
-            dev_src = device.scratch.get("host_src", n * n, tdtype).view(n, n)
+            dev_src = device.scratch.get(f"host_src:{stream}", n * n, tdtype).view(n, n)
             dev_src.copy_(torch.from_numpy(np.ascontiguousarray(src)), non_blocking=True)
         src_ptr = dev_src.data_ptr()
     launch(dev_grid.data_ptr(), src_ptr, n, c, stream, 0)

@@ -22,8 +22,8 @@ def main():
     grid[:] = device.fill_hash(n, torch.int8, 1, 0).cpu().numpy()
     backends.run_block_space(grid, grid, 64, r - 6, IntraStrategy.TUNED, kind=2, param=1)  # registers the array
     s = device.stream_handle()
-    snap = device.scratch.get("host_snap", n * n, torch.int8).view(n, n)
-    dst = device.scratch.get("host_dst", n * n, torch.int8).view(n, n)
+    snap = device.scratch.get(f"host_snap:{s}", n * n, torch.int8).view(n, n)
+    dst = device.scratch.get(f"host_dst:{s}", n * n, torch.int8).view(n, n)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     parts = {"snapshot": [], "kernel": [], "writeback": []}
     with device.MappedHost(grid) as gptr:
