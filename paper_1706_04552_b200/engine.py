@@ -191,11 +191,13 @@ def launch(config: LaunchConfig, grid, backend: Optional[str] = None) -> WorkMet
     plan = prepare(config, backend)
     neighbour = config.kernel.kind is not KernelKind.CONST
     if neighbour:
-        # engine.py:201 (src = grid.copy()).  On the device the launch gets src = grid and
-        # the backend keeps the semantics: the tuned kernel runs in place with a snapshot of
-        # the tiles' border cells only (device.run_inplace), the other strategies read a
-        # masked snapshot of the cells they read (device.stencil_snapshot)
-        src = grid if isinstance(grid, torch.Tensor) else grid.copy()
+        # engine.py:201 (src = grid.copy()).  The launch gets src = grid and the backend keeps
+        # the semantics: on the device the tuned kernel runs in place with a snapshot of the
+        # tiles' border cells only (device.run_inplace), the other strategies read a masked
+        # snapshot of the cells they read (device.stencil_snapshot); a host grid takes the
+        # staged path (masked snapshot over PCIe, device step, write-back) instead of a
+        # grid-sized host copy
+        src = grid
         # grid and its snapshot agree off the gasket: stencils may blend from src
         plan.flags |= native.FLAG_DST_FROM_SRC
     else:

@@ -687,6 +687,30 @@ def test_engine_launch_neighbour_sum_uses_masked_snapshot(gpu, oracle):
             assert np.array_equal(g.cpu().numpy(), want), (n, rho, strat)
 
 
+@pytest.mark.parametrize("transport", ["mapped", "copy"])
+def test_engine_launch_neighbour_sum_host_grid(gpu, oracle, monkeypatch, transport):
+    """engine.launch NEIGHBOR_SUM on an int32 numpy grid: src is the grid itself and the
+    backend keeps engine.py:201's snapshot semantics (the staged path for the tuned
+    kernel, a device snapshot otherwise) -- the oracle's step for every mapping."""
+    monkeypatch.setenv("GASKET_HOST_TRANSPORT", transport)
+    eng = gpu.engine
+    from paper_1706_04552_b200.geometry import FractalSpec
+
+    S = gpu.geometry.IntraStrategy
+    for n, rho in ((256, 8), (1024, 16)):
+        init = oracle.fill_hash(n, np.int32, 15, 0)
+        want = init.copy()
+        oracle.run_bounding_box(want, init, 1, oracle.KIND_NSUM4, 2)
+        spec = FractalSpec(n=n, rho=rho)
+        for mapping, strat in ((eng.Mapping.BLOCK_SPACE, S.TUNED), (eng.Mapping.BLOCK_SPACE, S.TABLE),
+                               (eng.Mapping.BOUNDING_BOX, None)):
+            g = init.copy()
+            cfg = eng.LaunchConfig(spec=spec, mapping=mapping, strategy=strat,
+                                   kernel=eng.CellKernel(eng.KernelKind.NEIGHBOR_SUM, 2))
+            eng.launch(cfg, g)
+            assert np.array_equal(g, want), (transport, n, mapping, strat)
+
+
 @pytest.mark.parametrize("dtype", [np.int8, np.int16, np.int32, np.int64])
 @pytest.mark.parametrize("pinned", [True, False])
 def test_mapped_staged_neighbour_sum(gpu, oracle, monkeypatch, dtype, pinned):
